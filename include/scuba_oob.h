@@ -1,0 +1,172 @@
+/*
+ * scuba_oob.h -- C ABI of the B200 engine for the per-access OOB
+ * satisfiability check of arXiv 2601.21552 ("scuba-mini" reference).
+ *
+ * The reference hot path is the pure-Python bounded-integer solver
+ *   scuba_mini.solver.solve(variables, constraints, timeout_s)
+ *     /root/reference/pkg/src/scuba_mini/solver.py:363-382
+ * bound by name into the analyzer (analyzer.py:32) and called once per query
+ * at analyzer.py:163 (partition-layout checks) and analyzer.py:211 (access
+ * checks).  Its siblings propagate() (solver.py:264-280) and check_model()
+ * (solver.py:319-328) are public API pinned by the reference tests.
+ *
+ * This header replaces those three functions with batched, caller-allocates
+ * entry points.  A "batch" is n independent queries (one ConstraintSet each,
+ * constraint_gen.py:65-73) in flat arrays; all offsets are per query so that
+ * queries can be sliced or sharded without rewriting indices.
+ *
+ * Semantics preserved exactly:
+ *   - variable order = list order (drives branching and model order);
+ *   - divisor side constraints appended in reference order (solver.py:345);
+ *   - any lo > hi  => UNSAT without search (solver.py:374);
+ *   - timeout_s <= 0 => TIMEOUT for every query that reaches search;
+ *   - the SAT model is the reference's first model (same DFS, same
+ *     propagation schedule, same 10**18 clamp and 10 000-pass cap);
+ *   - C truncating division; division/modulo by zero falsifies.
+ *
+ * Threading: every entry point is reentrant; the library keeps no pointer to
+ * caller memory after return.  Device buffers are library-owned and pooled
+ * per device (oob_release() frees them).
+ */
+#ifndef SCUBA_OOB_H
+#define SCUBA_OOB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Two's-complement 128-bit integer, little-endian words. Python ints of the
+ * reference are arbitrary precision; the engine is exact for every query whose
+ * intermediate magnitudes fit in 126 bits (checked per query on the host;
+ * queries beyond that get OOB_ERROR, never a silent wrong answer). */
+typedef struct {
+    uint64_t lo;
+    int64_t hi;
+} oob_i128;
+
+/* Term node opcodes (solver.py:32-49: Lit, VarRef, BinE op in + - * / %). */
+enum {
+    OOB_NODE_LIT = 0,
+    OOB_NODE_VAR = 1,
+    OOB_NODE_ADD = 2,
+    OOB_NODE_SUB = 3,
+    OOB_NODE_MUL = 4,
+    OOB_NODE_DIV = 5,
+    OOB_NODE_MOD = 6
+};
+
+/* Relations, in the order of solver.py:26 RELS = ("<", "<=", "=", ">=", ">"). */
+enum {
+    OOB_REL_LT = 0,
+    OOB_REL_LE = 1,
+    OOB_REL_EQ = 2,
+    OOB_REL_GE = 3,
+    OOB_REL_GT = 4
+};
+
+/* Verdict codes (solver.py:69-84 Sat / Unsat / Timeout). */
+enum {
+    OOB_UNSAT = 0,
+    OOB_SAT = 1,
+    OOB_TIMEOUT = 2,
+    OOB_ERROR = 3 /* query outside the exact regime / capacity; see last_error */
+};
+
+/* Return status of every entry point. */
+enum {
+    OOB_OK = 0,
+    OOB_E_INVALID = 1, /* malformed batch (unknown op/rel, bad index) -> ValueError */
+    OOB_E_CUDA = 2,    /* CUDA runtime error or no device                          */
+    OOB_E_RANGE = 3,   /* some query exceeds the exact 126-bit regime              */
+    OOB_E_NOMEM = 4
+};
+
+/*
+ * Flat batch.  For query q:
+ *   variables   [var_begin[q], var_begin[q+1])   domains var_lo/var_hi
+ *   constraints [con_begin[q], con_begin[q+1])   rel + lhs/rhs root node
+ *   nodes       [node_begin[q], node_begin[q+1]) op + operands
+ *   literals    [lit_begin[q], lit_begin[q+1])
+ * Node, variable and literal indices stored in con_lhs/con_rhs/node_a/node_b
+ * are RELATIVE to the query's own ranges.  Nodes form a DAG in topological
+ * order: a binary node's children have smaller indices than the node.
+ *   LIT: node_a = literal index          VAR: node_a = variable index
+ *   ADD..MOD: node_a = left child node,  node_b = right child node
+ */
+typedef struct {
+    int64_t n_queries;
+    const int64_t* var_begin;  /* n+1 */
+    const oob_i128* var_lo;
+    const oob_i128* var_hi;
+    const int64_t* con_begin;  /* n+1 */
+    const uint8_t* con_rel;
+    const int32_t* con_lhs;
+    const int32_t* con_rhs;
+    const int64_t* node_begin; /* n+1 */
+    const uint8_t* node_op;
+    const int32_t* node_a;
+    const int32_t* node_b;
+    const int64_t* lit_begin;  /* n+1 */
+    const oob_i128* lits;
+} oob_batch;
+
+typedef struct {
+    double timeout_s;     /* per-query wall-clock budget (solver.py:366); <=0 => TIMEOUT */
+    int64_t node_budget;  /* >0: TIMEOUT after this many DFS nodes (deterministic) */
+    int32_t n_gpus;       /* devices to shard over; 0 = all visible               */
+    int32_t device;       /* first device ordinal                                 */
+    int32_t flags;        /* OOB_F_* below                                        */
+    int32_t reserved;
+} oob_options;
+
+enum {
+    OOB_F_NO_SORT = 1,   /* keep input order on device (testing the scheduler) */
+    OOB_F_SEQUENTIAL = 2 /* one DFS node at a time per query (no frontier
+                            parallelism; same results, used by parity tests)  */
+};
+
+/* Results (caller-allocated; optional arrays may be NULL). */
+typedef struct {
+    int8_t* verdict;     /* n: OOB_UNSAT / OOB_SAT / OOB_TIMEOUT / OOB_ERROR        */
+    oob_i128* model;     /* var_begin[n] entries: SAT model at the query's var range */
+    int64_t* nodes;      /* n, optional: DFS nodes visited (reference _search calls) */
+    int64_t* passes;     /* n, optional: propagation passes (one _Narrower each)     */
+    double* elapsed_s;   /* n, optional: device time spent on the query            */
+} oob_result;
+
+/* Batched solve(): replaces solver.py:363-416 (solve + _search). */
+int oob_solve_batch(const oob_batch* batch, const oob_options* opt,
+                    oob_result* out);
+
+/* Batched propagate(domains, constraints): replaces solver.py:264-280.
+ * Domains are var_lo/var_hi; constraints are used AS GIVEN (propagate() adds
+ * no side constraints).  status[q] = 1 and out_lo/out_hi narrowed, or
+ * status[q] = 0 for the reference's None (contradiction). */
+int oob_propagate_batch(const oob_batch* batch, const oob_options* opt,
+                        oob_i128* out_lo, oob_i128* out_hi, int8_t* status);
+
+/* Batched check_model(constraints, model): replaces solver.py:319-328.
+ * model has var_begin[n] entries; ok[q] = 1 iff every constraint holds. */
+int oob_check_model_batch(const oob_batch* batch, const oob_options* opt,
+                          const oob_i128* model, int8_t* ok);
+
+/* Number of divisor side constraints solve() appends for query q
+ * (solver.py:334-357); lets callers size buffers / audit the host compiler. */
+int oob_side_constraint_count(const oob_batch* batch, int64_t* counts);
+
+/* Last error message of the calling thread ("" if none). */
+const char* oob_last_error(void);
+/* Visible CUDA devices (0 when none). */
+int oob_device_count(void);
+/* Library build identification. */
+const char* oob_version(void);
+/* Free pooled device buffers on every device. */
+void oob_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCUBA_OOB_H */
