@@ -1,0 +1,167 @@
+"""ctypes binding of libscuba_oob.so (include/scuba_oob.h).
+
+There is no CPU fallback: if the shared library is missing, or a batch reaches
+search with no CUDA device visible, the call raises.  The library is built
+in-tree by `python -m paper_2601_21552_b200.build` (or __graft_entry__.build()).
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "libscuba_oob.so"
+
+OOB_OK, OOB_E_INVALID, OOB_E_CUDA, OOB_E_RANGE, OOB_E_NOMEM = 0, 1, 2, 3, 4
+UNSAT, SAT, TIMEOUT, ERROR = 0, 1, 2, 3
+
+F_NO_SORT = 1
+F_SEQUENTIAL = 2
+
+
+class EngineError(RuntimeError):
+    """The GPU engine could not decide a batch (no device, capacity, range)."""
+
+
+class oob_options(ctypes.Structure):
+    _fields_ = [
+        ("timeout_s", ctypes.c_double),
+        ("node_budget", ctypes.c_int64),
+        ("n_gpus", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class oob_result(ctypes.Structure):
+    _fields_ = [
+        ("verdict", ctypes.c_void_p),
+        ("model", ctypes.c_void_p),
+        ("nodes", ctypes.c_void_p),
+        ("passes", ctypes.c_void_p),
+        ("elapsed_s", ctypes.c_void_p),
+    ]
+
+
+EXPORTS = (
+    "oob_solve_batch",
+    "oob_propagate_batch",
+    "oob_check_model_batch",
+    "oob_side_constraint_count",
+    "oob_last_error",
+    "oob_device_count",
+    "oob_version",
+    "oob_release",
+)
+
+_lib = None
+
+
+def lib():
+    """Load the engine library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA engine first "
+            "(python -m paper_2601_21552_b200.build); there is no CPU fallback")
+    L = ctypes.CDLL(str(LIB_PATH))
+    vp = ctypes.c_void_p
+    L.oob_solve_batch.argtypes = [vp, vp, vp]
+    L.oob_solve_batch.restype = ctypes.c_int
+    L.oob_propagate_batch.argtypes = [vp, vp, vp, vp, vp]
+    L.oob_propagate_batch.restype = ctypes.c_int
+    L.oob_check_model_batch.argtypes = [vp, vp, vp, vp]
+    L.oob_check_model_batch.restype = ctypes.c_int
+    L.oob_side_constraint_count.argtypes = [vp, vp]
+    L.oob_side_constraint_count.restype = ctypes.c_int
+    L.oob_last_error.restype = ctypes.c_char_p
+    L.oob_device_count.restype = ctypes.c_int
+    L.oob_version.restype = ctypes.c_char_p
+    L.oob_release.restype = None
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return lib().oob_last_error().decode()
+
+
+def check(rc: int, what: str):
+    if rc == OOB_OK:
+        return
+    msg = last_error()
+    if rc == OOB_E_INVALID:
+        raise ValueError(f"{what}: {msg}")
+    raise EngineError(f"{what} failed (status {rc}): {msg}")
+
+
+def device_count() -> int:
+    return int(lib().oob_device_count())
+
+
+def options(timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0):
+    o = oob_options()
+    o.timeout_s = float(timeout_s)
+    o.node_budget = int(node_budget)
+    o.n_gpus = int(n_gpus)
+    o.device = int(device)
+    o.flags = int(flags)
+    return o
+
+
+def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0):
+    """Run oob_solve_batch on a FlatBatch -> dict of numpy result arrays."""
+    n = fb.n
+    out = {
+        "verdict": np.full(n, -1, dtype=np.int8),
+        "model": np.zeros((max(fb.n_vars_total, 1), 2), dtype=np.int64),
+        "nodes": np.zeros(n, dtype=np.int64),
+        "passes": np.zeros(n, dtype=np.int64),
+        "elapsed": np.zeros(n, dtype=np.float64),
+    }
+    r = oob_result(out["verdict"].ctypes.data, out["model"].ctypes.data,
+                   out["nodes"].ctypes.data, out["passes"].ctypes.data,
+                   out["elapsed"].ctypes.data)
+    cb = fb.as_c()
+    o = options(timeout_s, node_budget, n_gpus, device, flags)
+    rc = lib().oob_solve_batch(ctypes.byref(cb), ctypes.byref(o), ctypes.byref(r))
+    out["status"] = rc
+    out["error"] = last_error() if rc else ""
+    return out
+
+
+def propagate_flat(fb, device=0):
+    V = max(fb.n_vars_total, 1)
+    lo = np.zeros((V, 2), dtype=np.int64)
+    hi = np.zeros((V, 2), dtype=np.int64)
+    st = np.zeros(fb.n, dtype=np.int8)
+    cb = fb.as_c()
+    o = options(device=device, n_gpus=1)
+    rc = lib().oob_propagate_batch(ctypes.byref(cb), ctypes.byref(o), lo.ctypes.data,
+                                   hi.ctypes.data, st.ctypes.data)
+    check(rc, "oob_propagate_batch")
+    return lo, hi, st
+
+
+def check_model_flat(fb, model_words, device=0):
+    ok = np.zeros(fb.n, dtype=np.int8)
+    m = np.ascontiguousarray(model_words, dtype=np.int64)
+    cb = fb.as_c()
+    o = options(device=device, n_gpus=1)
+    rc = lib().oob_check_model_batch(ctypes.byref(cb), ctypes.byref(o), m.ctypes.data,
+                                     ok.ctypes.data)
+    check(rc, "oob_check_model_batch")
+    return ok
+
+
+def side_counts(fb):
+    c = np.zeros(fb.n, dtype=np.int64)
+    cb = fb.as_c()
+    check(lib().oob_side_constraint_count(ctypes.byref(cb), c.ctypes.data),
+          "oob_side_constraint_count")
+    return c

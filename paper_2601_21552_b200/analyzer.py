@@ -1,0 +1,109 @@
+"""Plugging the B200 engine into the reference analyzer.
+
+The reference analyzer binds `solve` by name (`from .solver import ... solve`,
+/root/reference/pkg/src/scuba_mini/analyzer.py:32) and calls it once per
+query at analyzer.py:163 (partition-layout checks) and analyzer.py:211 (access
+checks).  Two integrations, both leaving the reference front end untouched:
+
+* `install(analyzer_module)` -- replace that binding with the GPU `solve`
+  (one device call per query; simplest, launch-latency bound).
+
+* `analyze_batched(analyze, *args)` -- two-pass record/replay.  Constraint
+  generation never depends on an earlier verdict (analyzer.py:160-243), so
+  pass 1 runs the analysis with a recording stub, ONE GPU batch decides every
+  recorded query, and pass 2 re-runs the analysis replaying the verdicts in
+  call order.  Diagnostics are identical to the reference's because verdicts
+  and models are.
+"""
+from __future__ import annotations
+
+import contextlib
+
+from .solver import solve_batch
+from .terms import query_to_json
+
+
+def _types(analyzer_module):
+    return (analyzer_module.Sat, analyzer_module.Unsat, analyzer_module.Timeout)
+
+
+@contextlib.contextmanager
+def installed(analyzer_module):
+    """Context manager: analyzer_module.solve -> the GPU engine."""
+    types = _types(analyzer_module)
+    saved = analyzer_module.solve
+
+    def gpu_solve(variables, constraints, timeout_s=30.0):
+        return solve_batch([(variables, constraints)], timeout_s, verdict_types=types)[0]
+
+    analyzer_module.solve = gpu_solve
+    try:
+        yield gpu_solve
+    finally:
+        analyzer_module.solve = saved
+
+
+def install(analyzer_module):
+    """Permanently bind the GPU engine into the analyzer module."""
+    types = _types(analyzer_module)
+
+    def gpu_solve(variables, constraints, timeout_s=30.0):
+        return solve_batch([(variables, constraints)], timeout_s, verdict_types=types)[0]
+
+    analyzer_module.solve = gpu_solve
+    return gpu_solve
+
+
+class _Recorder:
+    def __init__(self, unsat):
+        self.calls = []
+        self._unsat = unsat
+
+    def __call__(self, variables, constraints, timeout_s=30.0):
+        self.calls.append((variables, constraints, float(timeout_s)))
+        return self._unsat()
+
+
+def decide_calls(calls, types, **engine_kw):
+    """One GPU batch per distinct timeout value; verdicts in call order."""
+    verdicts = [None] * len(calls)
+    by_timeout = {}
+    for i, (_, _, t) in enumerate(calls):
+        by_timeout.setdefault(t, []).append(i)
+    for t, idx in by_timeout.items():
+        vs = solve_batch([(calls[i][0], calls[i][1]) for i in idx], t,
+                         verdict_types=types, **engine_kw)
+        for i, v in zip(idx, vs):
+            verdicts[i] = v
+    return verdicts
+
+
+def analyze_batched(analyzer_module, analyze, *args, stats=None, **kwargs):
+    """Run `analyze(*args, **kwargs)` (e.g. analyzer_module.analyze_source)
+    with all of its solver queries decided in one GPU batch."""
+    types = _types(analyzer_module)
+    saved = analyzer_module.solve
+    rec = _Recorder(types[1])
+    analyzer_module.solve = rec
+    try:
+        analyze(*args, **kwargs)
+    finally:
+        analyzer_module.solve = saved
+    verdicts = decide_calls(rec.calls, types)
+    it = iter(range(len(verdicts)))
+
+    def replay(variables, constraints, timeout_s=30.0):
+        i = next(it)
+        want = rec.calls[i]
+        if query_to_json(variables, constraints) != query_to_json(want[0], want[1]):
+            raise RuntimeError("analysis is not deterministic between passes")
+        return verdicts[i]
+
+    analyzer_module.solve = replay
+    try:
+        result = analyze(*args, **kwargs)
+    finally:
+        analyzer_module.solve = saved
+    if stats is not None:
+        stats["queries"] = len(rec.calls)
+    return result

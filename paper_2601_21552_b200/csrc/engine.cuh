@@ -1,0 +1,402 @@
+// engine.cuh -- device-side exact emulation of the reference solver
+// (/root/reference/pkg/src/scuba_mini/solver.py:112-416) for sm_100a.
+//
+// One lane owns one query at a time.  Everything a lane touches repeatedly
+// lives in a per-warp scratch slab laid out [index][32 lanes] (lane-minor), so
+// when the lanes of a warp run structurally identical queries in lockstep --
+// the host sorts queries by structure class -- every scratch access of the
+// warp is one coalesced 128-byte line per 4-byte word, and every code word is
+// a single broadcast load shared by the whole warp.
+//
+// Exactness: the host proves, per query, a bound B on the magnitude of every
+// intermediate value the reference algorithm can produce (forward intervals at
+// the declared domains, narrowing targets including the 10**18 clamp, exact
+// model evaluation).  Queries with B < 2^62 run on int64, B < 2^125 on
+// __int128; plain two's-complement arithmetic is then exact.
+#pragma once
+#include <cstdint>
+
+#include "format.h"
+
+namespace oob {
+
+template <typename T>
+struct Arith {
+    static constexpr T INF = (T)1000000000000000000LL;  // _INF = 10**18 (solver.py:23)
+    __device__ static inline T mn(T a, T b) { return a < b ? a : b; }
+    __device__ static inline T mx(T a, T b) { return a > b ? a : b; }
+    // C division truncates toward zero: exactly tdiv/tmod (solver.py:94-102).
+    __device__ static inline T tdiv(T a, T b) { return a / b; }
+    __device__ static inline T tmod(T a, T b) { return a % b; }
+    // Python floor division a // b
+    __device__ static inline T fdiv(T a, T b) {
+        T q = a / b;
+        T r = a - q * b;
+        return (r != 0 && ((r < 0) != (b < 0))) ? q - 1 : q;
+    }
+    // _ceil_div (solver.py:105-106): -((-a) // b)
+    __device__ static inline T ceil_div(T a, T b) { return -fdiv(-a, b); }
+};
+
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <typename T>
+struct Lane {
+    using A = Arith<T>;
+    // lane-minor scratch views (element i of this lane is p[i * 32])
+    T* env_lo;
+    T* env_hi;
+    T* val_lo;
+    T* val_hi;
+    T* lit;
+    T* fr_mid;
+    T* fr_hi;
+    T* tr_lo;
+    T* tr_hi;
+    uint32_t* stamp;
+    uint32_t* fr_pick;
+    uint32_t* fr_mark;
+    uint32_t* tr_var;
+    const SlabGeom* g;
+    // current query
+    const uint32_t* cons;  // ncon constraint words
+    const uint32_t* code;  // ncode node words
+    uint32_t nv, ncon, ncode, nlit;
+    // search state
+    uint32_t depth, trail_len, seg;
+    bool dirty;     // a variable changed since the current constraint's top-level eval
+    bool changed;   // the current pass changed a domain (_Narrower.changed)
+    int err;
+
+    __device__ __forceinline__ T& E(T* p, uint32_t i) const { return p[(size_t)i * 32]; }
+    __device__ __forceinline__ uint32_t& U(uint32_t* p, uint32_t i) const { return p[(size_t)i * 32]; }
+
+    __device__ __forceinline__ static uint32_t op_of(uint32_t w) { return w & 7u; }
+    __device__ __forceinline__ static uint32_t arg_of(uint32_t w) { return w >> 3; }
+    __device__ __forceinline__ uint32_t size_of(uint32_t i) const {
+        uint32_t w = __ldg(code + i);
+        return op_of(w) >= NODE_ADD ? arg_of(w) : 1u;
+    }
+
+    // ----- _eval_iv over a postfix range (solver.py:112-149) ------------------
+    // Computes val[j] for every node of the subtree rooted at `root`; false if
+    // any node of it has no non-trapping value (the reference's None).
+    __device__ bool eval_subtree(uint32_t root) {
+        uint32_t start = root + 1 - size_of(root);
+        for (uint32_t j = start; j <= root; ++j) {
+            uint32_t w = __ldg(code + j);
+            uint32_t op = op_of(w);
+            T lo, hi;
+            if (op == NODE_LIT) {
+                lo = hi = E(lit, arg_of(w));
+            } else if (op == NODE_VAR) {
+                lo = E(env_lo, arg_of(w));
+                hi = E(env_hi, arg_of(w));
+                if (lo > hi) return false;
+            } else {
+                uint32_t R = j - 1;
+                uint32_t L = R - size_of(R);
+                T l0 = E(val_lo, L), l1 = E(val_hi, L), r0 = E(val_lo, R), r1 = E(val_hi, R);
+                if (op == NODE_ADD) {
+                    lo = l0 + r0;
+                    hi = l1 + r1;
+                } else if (op == NODE_SUB) {
+                    lo = l0 - r1;
+                    hi = l1 - r0;
+                } else if (op == NODE_MUL) {
+                    T k0 = l0 * r0, k1 = l0 * r1, k2 = l1 * r0, k3 = l1 * r1;
+                    lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
+                    hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
+                } else {
+                    T d0 = A::mx(r0, (T)1), d1 = r1;
+                    if (d0 > d1) return false;
+                    if (op == NODE_DIV) {
+                        T k0 = l0 / d0, k1 = l0 / d1, k2 = l1 / d0, k3 = l1 / d1;
+                        lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
+                        hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
+                    } else {  // NODE_MOD
+                        T m = d1 - 1;
+                        if (l0 >= 0) {
+                            lo = 0;
+                            hi = A::mn(l1, m);
+                        } else if (l1 <= 0) {
+                            lo = A::mx(l0, -m);
+                            hi = 0;
+                        } else {
+                            lo = A::mx(l0, -m);
+                            hi = A::mn(l1, m);
+                        }
+                    }
+                }
+            }
+            E(val_lo, j) = lo;
+            E(val_hi, j) = hi;
+        }
+        return true;
+    }
+
+    // ----- domain update with trail logging -----------------------------------
+    __device__ __forceinline__ bool set_dom(uint32_t v, T lo, T hi) {
+        if (depth > 0 && U(stamp, v) != seg) {
+            if (trail_len >= g->trail_cap) {
+                err = ERR_TRAIL;
+                return false;
+            }
+            U(tr_var, trail_len) = v;
+            E(tr_lo, trail_len) = E(env_lo, v);
+            E(tr_hi, trail_len) = E(env_hi, v);
+            ++trail_len;
+            U(stamp, v) = seg;
+        }
+        E(env_lo, v) = lo;
+        E(env_hi, v) = hi;
+        return true;
+    }
+
+    // ----- _Narrower.narrow (solver.py:159-226), explicit pre-order stack ------
+    __device__ bool narrow(uint32_t root, T t0, T t1) {
+        constexpr int NS = 40;
+        uint32_t sn[NS];
+        T s0[NS], s1[NS];
+        int sp = 0;
+        sn[0] = root;
+        s0[0] = t0;
+        s1[0] = t1;
+        sp = 1;
+        while (sp > 0) {
+            --sp;
+            uint32_t i = sn[sp];
+            T a = s0[sp], b = s1[sp];
+            if (a > b) return false;                                   // :161-162
+            uint32_t w = __ldg(code + i);
+            uint32_t op = op_of(w);
+            if (op == NODE_LIT) {                                      // :163-164
+                T v = E(lit, arg_of(w));
+                if (!(a <= v && v <= b)) return false;
+                continue;
+            }
+            if (op == NODE_VAR) {                                      // :165-173
+                uint32_t v = arg_of(w);
+                T lo = E(env_lo, v), hi = E(env_hi, v);
+                T nlo = A::mx(lo, a), nhi = A::mn(hi, b);
+                if (nlo > nhi) return false;
+                if (nlo != lo || nhi != hi) {
+                    if (!set_dom(v, nlo, nhi)) return false;
+                    changed = true;
+                    dirty = true;
+                }
+                continue;
+            }
+            uint32_t R = i - 1;                                        // :174-177
+            uint32_t L = R - size_of(R);
+            if (dirty) {
+                if (!eval_subtree(L) || !eval_subtree(R)) return false;
+            }
+            T l0 = E(val_lo, L), l1 = E(val_hi, L), r0 = E(val_lo, R), r1 = E(val_hi, R);
+            if (sp + 2 > NS) {
+                err = ERR_STACK;
+                return false;
+            }
+            if (op == NODE_ADD) {                                      // :181-185
+                sn[sp] = R; s0[sp] = a - l1; s1[sp] = b - l0; ++sp;
+                sn[sp] = L; s0[sp] = a - r1; s1[sp] = b - r0; ++sp;
+            } else if (op == NODE_SUB) {                               // :186-190
+                sn[sp] = R; s0[sp] = l0 - b; s1[sp] = l1 - a; ++sp;
+                sn[sp] = L; s0[sp] = a + r0; s1[sp] = b + r1; ++sp;
+            } else if (op == NODE_MUL) {                               // :191-216
+                if (l0 < 0 || r0 < 0) continue;
+                if (b < 0) return false;
+                T t0n = A::mx(a, (T)0);
+                T lo_l = -A::INF, hi_l = A::INF, lo_r = -A::INF, hi_r = A::INF;
+                if (t0n > 0) {
+                    if (r1 == 0 || l1 == 0) return false;
+                    lo_l = A::ceil_div(t0n, r1);
+                    lo_r = A::ceil_div(t0n, l1);
+                }
+                if (r0 > 0) hi_l = A::fdiv(b, r0);
+                if (l0 > 0) hi_r = A::fdiv(b, l0);
+                sn[sp] = R; s0[sp] = lo_r; s1[sp] = hi_r; ++sp;
+                sn[sp] = L; s0[sp] = lo_l; s1[sp] = hi_l; ++sp;
+            } else if (op == NODE_DIV) {                               // :217-223
+                uint32_t rw = __ldg(code + R);
+                if (op_of(rw) == NODE_LIT) {
+                    T c = E(lit, arg_of(rw));
+                    if (c >= 1) {
+                        T lo_req = a > 0 ? a * c : a * c - (c - 1);
+                        T hi_req = b >= 0 ? b * c + (c - 1) : b * c;
+                        sn[sp] = L; s0[sp] = lo_req; s1[sp] = hi_req; ++sp;
+                    }
+                }
+            }
+            // NODE_MOD: forward-only (:224-225)
+        }
+        return true;
+    }
+
+    // ----- _propagate_constraint (solver.py:229-261) ---------------------------
+    __device__ bool propagate_constraint(uint32_t k) {
+        uint32_t w = __ldg(cons + k);
+        uint32_t rel = w & 7u;
+        uint32_t lr = (w >> 3) & 0x3FFFu;
+        uint32_t rr = w >> 17;
+        dirty = false;
+        if (!eval_subtree(lr) || !eval_subtree(rr)) return false;
+        T l0 = E(val_lo, lr), l1 = E(val_hi, lr), r0 = E(val_lo, rr), r1 = E(val_hi, rr);
+        T a0, a1, b0, b1;
+        switch (rel) {
+        case REL_LT: a0 = -A::INF; a1 = r1 - 1; b0 = l0 + 1; b1 = A::INF; break;
+        case REL_LE: a0 = -A::INF; a1 = r1; b0 = l0; b1 = A::INF; break;
+        case REL_EQ: a0 = b0 = A::mx(l0, r0); a1 = b1 = A::mn(l1, r1); break;
+        case REL_GE: a0 = r0; a1 = A::INF; b0 = -A::INF; b1 = l1; break;
+        default:     a0 = r0 + 1; a1 = A::INF; b0 = -A::INF; b1 = l1 - 1; break;
+        }
+        return narrow(lr, a0, a1) && narrow(rr, b0, b1);
+    }
+
+    // ----- propagate (solver.py:264-280), in place ----------------------------
+    // returns 1 ok, 0 contradiction, -1 deadline, -2 error
+    __device__ int propagate(int64_t& passes, uint64_t deadline) {
+        for (int pass = 0; pass < PASS_CAP; ++pass) {
+            if (deadline && global_ns() > deadline) return -1;
+            ++passes;
+            changed = false;
+            for (uint32_t k = 0; k < ncon; ++k) {
+                if (!propagate_constraint(k)) return err ? -2 : 0;
+            }
+            if (!changed) break;
+        }
+        return 1;
+    }
+
+    // ----- _eval_exact / check_model (solver.py:286-328) ----------------------
+    // Exact evaluation of every constraint at the point env_lo (val_lo holds
+    // the node values).  Division/modulo by zero falsifies (:301-302).
+    __device__ bool check_point(const T* point) {
+        for (uint32_t k = 0; k < ncon; ++k) {
+            uint32_t w = __ldg(cons + k);
+            uint32_t rel = w & 7u;
+            uint32_t lr = (w >> 3) & 0x3FFFu;
+            uint32_t rr = w >> 17;
+            T vv[2];
+            uint32_t roots[2] = {lr, rr};
+            for (int s = 0; s < 2; ++s) {
+                uint32_t root = roots[s];
+                uint32_t start = root + 1 - size_of(root);
+                for (uint32_t j = start; j <= root; ++j) {
+                    uint32_t cw = __ldg(code + j);
+                    uint32_t op = op_of(cw);
+                    T x;
+                    if (op == NODE_LIT) {
+                        x = E(lit, arg_of(cw));
+                    } else if (op == NODE_VAR) {
+                        x = point[(size_t)arg_of(cw) * 32];
+                    } else {
+                        uint32_t R = j - 1;
+                        uint32_t L = R - size_of(R);
+                        T a = E(val_lo, L), b = E(val_lo, R);
+                        if (op == NODE_ADD) x = a + b;
+                        else if (op == NODE_SUB) x = a - b;
+                        else if (op == NODE_MUL) x = a * b;
+                        else {
+                            if (b == 0) return false;
+                            x = op == NODE_DIV ? a / b : a % b;
+                        }
+                    }
+                    E(val_lo, j) = x;
+                }
+                vv[s] = E(val_lo, root);
+            }
+            T a = vv[0], b = vv[1];
+            bool ok;
+            switch (rel) {
+            case REL_LT: ok = a < b; break;
+            case REL_LE: ok = a <= b; break;
+            case REL_EQ: ok = a == b; break;
+            case REL_GE: ok = a >= b; break;
+            default: ok = a > b; break;
+            }
+            if (!ok) return false;
+        }
+        return true;
+    }
+
+    __device__ void undo_to(uint32_t mark) {
+        while (trail_len > mark) {
+            --trail_len;
+            uint32_t v = U(tr_var, trail_len);
+            E(env_lo, v) = E(tr_lo, trail_len);
+            E(env_hi, v) = E(tr_hi, trail_len);
+        }
+    }
+
+    // ----- solve / _search (solver.py:363-416), iterative DFS ------------------
+    // returns verdict; env_lo holds the model on SAT.
+    __device__ int search(int64_t& nodes, int64_t& passes, uint64_t deadline, int64_t budget) {
+        depth = 0;
+        trail_len = 0;
+        for (;;) {
+            // ---- visit a node (_search body) ----
+            if ((deadline && global_ns() > deadline) || (budget > 0 && nodes >= budget))
+                return VERDICT_TIMEOUT;                                // :391-392
+            ++nodes;
+            int pr = propagate(passes, deadline);                      // :393
+            if (pr == -1) return VERDICT_TIMEOUT;
+            if (pr == -2) return VERDICT_ERROR;
+            bool dead = (pr == 0);
+            if (!dead) {
+                // smallest unresolved domain, ties by declaration order (:397-404)
+                int pick = -1;
+                T best = 0;
+                for (uint32_t v = 0; v < nv; ++v) {
+                    T lo = E(env_lo, v), hi = E(env_hi, v);
+                    if (lo < hi) {
+                        T size = hi - lo + 1;
+                        if (pick < 0 || size < best) {
+                            pick = (int)v;
+                            best = size;
+                        }
+                    }
+                }
+                if (pick < 0) {                                        // leaf (:405-407)
+                    if (check_point(env_lo)) return VERDICT_SAT;
+                    dead = true;
+                } else {                                               // split (:408-415)
+                    if (depth >= g->depth_cap) {
+                        err = ERR_DEPTH;
+                        return VERDICT_ERROR;
+                    }
+                    T lo = E(env_lo, pick), hi = E(env_hi, pick);
+                    T mid = (lo + hi) >> 1;  // floor((lo+hi)/2) in two's complement
+                    U(fr_pick, depth) = (uint32_t)pick;
+                    U(fr_mark, depth) = trail_len;
+                    E(fr_mid, depth) = mid;
+                    E(fr_hi, depth) = hi;
+                    ++depth;
+                    ++seg;
+                    if (!set_dom((uint32_t)pick, lo, mid)) return VERDICT_ERROR;
+                    continue;
+                }
+            }
+            // ---- backtrack ----
+            for (;;) {
+                if (depth == 0) return VERDICT_UNSAT;
+                uint32_t f = depth - 1;
+                uint32_t pk = U(fr_pick, f);
+                undo_to(U(fr_mark, f));
+                if (!(pk & 0x80000000u)) {
+                    U(fr_pick, f) = pk | 0x80000000u;
+                    ++seg;
+                    if (!set_dom(pk, E(fr_mid, f) + 1, E(fr_hi, f))) return VERDICT_ERROR;
+                    break;
+                }
+                depth = f;
+            }
+        }
+    }
+};
+
+}  // namespace oob

@@ -1,0 +1,96 @@
+// format.h -- device-resident layout of a compiled query batch.
+//
+// The host compiler (host.cpp) turns the caller's flat oob_batch into:
+//
+//   code[]   u32 structure words, one block per STRUCTURE CLASS (queries whose
+//            constraint/term shapes are identical share one block):
+//              ncon constraint words   rel | lroot << 3 | rroot << 17
+//              ncode node words        op | arg << 3
+//            Nodes are laid out per constraint side as a contiguous postfix
+//            segment (the DAG is expanded to a tree), so the subtree of node i
+//            is [i - size(i) + 1, i], its right child is i - 1 and its left
+//            child is i - 1 - size(i - 1).  arg = variable index (VAR), literal
+//            slot (LIT, one slot per occurrence), or subtree size (binary op).
+//   data[]   per query: nv (lo, hi) domain pairs then nlit literal slots, each
+//            value W bytes (8 for the int64 regime, 16 for int128), 16-byte
+//            aligned per query.
+//   qdesc[]  per scheduled query (sorted by class, then by cost estimate):
+//            where its code block and data block are and where results go.
+#pragma once
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define OOB_HD __host__ __device__
+#else
+#define OOB_HD
+#endif
+
+namespace oob {
+
+enum : uint32_t {
+    NODE_LIT = 0,
+    NODE_VAR = 1,
+    NODE_ADD = 2,
+    NODE_SUB = 3,
+    NODE_MUL = 4,
+    NODE_DIV = 5,
+    NODE_MOD = 6
+};
+enum : uint32_t { REL_LT = 0, REL_LE = 1, REL_EQ = 2, REL_GE = 3, REL_GT = 4 };
+enum : int { VERDICT_UNSAT = 0, VERDICT_SAT = 1, VERDICT_TIMEOUT = 2, VERDICT_ERROR = 3 };
+
+constexpr int PASS_CAP = 10000;          // _PASS_CAP (solver.py:24)
+constexpr uint32_t MAX_CODE = 16383;     // 14-bit node ids in constraint words
+constexpr uint32_t MAX_TREE_DEPTH = 32;  // bounded pre-order narrowing stack
+
+struct QDesc {
+    uint32_t code_off;   // u32 index of the class's constraint words in code[]
+    uint32_t nv_ncon;    // nv | ncon << 16
+    uint32_t ncode_nlit; // ncode | nlit << 16
+    uint32_t out_q;      // index of the query in the caller's batch
+    uint64_t data_off;   // int64-word index of the query's data in data[]
+    uint64_t out_v;      // caller var_begin[out_q] (model offset, in vars)
+};
+static_assert(sizeof(QDesc) == 32, "QDesc is two int4 words");
+
+OOB_HD inline uint32_t con_word(uint32_t rel, uint32_t l, uint32_t r) {
+    return rel | (l << 3) | (r << 17);
+}
+OOB_HD inline uint32_t node_word(uint32_t op, uint32_t arg) { return op | (arg << 3); }
+
+// Per-launch geometry of the scratch slab (host-computed; see format.h).
+struct SlabGeom {
+    uint32_t maxv, maxcode, maxlit, depth_cap, trail_cap;
+    // word offsets (in units of T) of each array inside one warp's slab
+    uint64_t o_env_lo, o_env_hi, o_val_lo, o_val_hi, o_lit, o_fr_mid, o_fr_hi, o_tr_lo, o_tr_hi;
+    // u32-word offsets inside the u32 part of the slab
+    uint64_t o_stamp, o_fr_pick, o_fr_mark, o_tr_var;
+    uint64_t slab_T_words, slab_u32_words;  // per-warp sizes
+};
+
+struct LaunchArgs {
+    const QDesc* qdesc;       // per scheduled query
+    const uint32_t* code;     // structure words (constraints + nodes), per class
+    const int64_t* data;      // per query domains + literals (W/8 words per value)
+    uint32_t n;               // scheduled queries
+    uint32_t* next;           // work counter (persistent scheduling)
+    void* slab_T;             // T-typed scratch, n_warps * slab_T_words
+    uint32_t* slab_u32;       // u32 scratch, n_warps * slab_u32_words
+    SlabGeom g;
+    // outputs (indexed by QDesc::out_q / out_v)
+    int8_t* verdict;
+    int64_t* model;           // int128 words, 2 per var
+    int64_t* nodes;
+    int64_t* passes;
+    float* elapsed;
+    int8_t* err;              // per query error reason (0 = none)
+    // options
+    uint64_t timeout_ns;      // 0 => unlimited
+    int64_t node_budget;      // >0 => deterministic budget
+    int mode;                 // MODE_SOLVE / MODE_PROPAGATE / MODE_CHECK
+};
+
+enum { MODE_SOLVE = 0, MODE_PROPAGATE = 1, MODE_CHECK = 2 };
+enum { ERR_NONE = 0, ERR_DEPTH = 1, ERR_TRAIL = 2, ERR_STACK = 3 };
+
+}  // namespace oob

@@ -1,0 +1,860 @@
+// host.cpp -- C ABI (include/scuba_oob.h), query compiler and multi-GPU driver.
+//
+// Pipeline of one oob_solve_batch() call:
+//   1. compile  : validate each query of the flat batch, append the divisor
+//                 side constraints (solver.py:334-357), expand each constraint
+//                 side to a postfix segment, prove the 126-bit (or 62-bit)
+//                 magnitude bound, and dedup the code into structure classes;
+//   2. schedule : sort by (regime, class, cost) and deal 32-query tiles
+//                 round-robin over the devices (queries are independent; no
+//                 collective: SURVEY.md 8(e));
+//   3. run      : one host thread per device -- H2D, persistent kernel, D2H --
+//                 and a capacity retry for queries whose DFS outgrew the
+//                 default scratch (deeper stack / longer trail);
+//   4. scatter  : verdicts, models, counters back to the caller's arrays.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/scuba_oob.h"
+#include "format.h"
+
+namespace oob {
+cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
+}
+
+using namespace oob;
+using i128 = __int128;
+
+// ============================================================================
+// errors
+// ============================================================================
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+static i128 from_w(oob_i128 w) { return (i128)(((unsigned __int128)(uint64_t)w.hi << 64) | w.lo); }
+
+// ============================================================================
+// 1. compile
+// ============================================================================
+namespace {
+
+enum Regime : int8_t { R_IMMEDIATE = 0, R_W64 = 1, R_W128 = 2, R_RANGE = 3 };
+
+struct QView {
+    int nv, ncon, nn, nl;
+    const oob_i128 *vlo, *vhi, *lits;
+    const uint8_t* rel;
+    const int32_t *lhs, *rhs;
+    const uint8_t* op;
+    const int32_t *na, *nb;
+};
+
+QView view_of(const oob_batch* b, int64_t q) {
+    QView v;
+    int64_t vb = b->var_begin[q], cb = b->con_begin[q], nb = b->node_begin[q], lb = b->lit_begin[q];
+    v.nv = (int)(b->var_begin[q + 1] - vb);
+    v.ncon = (int)(b->con_begin[q + 1] - cb);
+    v.nn = (int)(b->node_begin[q + 1] - nb);
+    v.nl = (int)(b->lit_begin[q + 1] - lb);
+    v.vlo = b->var_lo + vb;
+    v.vhi = b->var_hi + vb;
+    v.lits = b->lits + lb;
+    v.rel = b->con_rel + cb;
+    v.lhs = b->con_lhs + cb;
+    v.rhs = b->con_rhs + cb;
+    v.op = b->node_op + nb;
+    v.na = b->node_a + nb;
+    v.nb = b->node_b + nb;
+    return v;
+}
+
+std::string validate(const oob_batch* b, int64_t q) {
+    if (b->var_begin[q + 1] < b->var_begin[q] || b->con_begin[q + 1] < b->con_begin[q] ||
+        b->node_begin[q + 1] < b->node_begin[q] || b->lit_begin[q + 1] < b->lit_begin[q])
+        return "decreasing offsets";
+    QView v = view_of(b, q);
+    if (v.nv > 65535 || v.ncon > 65535) return "more than 65535 variables or constraints";
+    for (int i = 0; i < v.nn; i++) {
+        int op = v.op[i];
+        if (op > OOB_NODE_MOD) return "unknown operator code " + std::to_string(op);
+        if (op == OOB_NODE_LIT && (v.na[i] < 0 || v.na[i] >= v.nl)) return "literal index out of range";
+        if (op == OOB_NODE_VAR && (v.na[i] < 0 || v.na[i] >= v.nv)) return "undeclared variable index";
+        if (op >= OOB_NODE_ADD && (v.na[i] < 0 || v.na[i] >= i || v.nb[i] < 0 || v.nb[i] >= i))
+            return "operand node not before its parent";
+    }
+    for (int k = 0; k < v.ncon; k++) {
+        if (v.rel[k] > OOB_REL_GT) return "unknown relation code " + std::to_string(v.rel[k]);
+        if (v.lhs[k] < 0 || v.lhs[k] >= v.nn || v.rhs[k] < 0 || v.rhs[k] >= v.nn)
+            return "constraint root out of range";
+    }
+    return "";
+}
+
+// structural equality of two input terms (dataclass equality in the reference)
+bool same_term(const QView& v, int x, int y) {
+    if (x == y) return true;
+    if (v.op[x] != v.op[y]) return false;
+    if (v.op[x] == OOB_NODE_LIT) return from_w(v.lits[v.na[x]]) == from_w(v.lits[v.na[y]]);
+    if (v.op[x] == OOB_NODE_VAR) return v.na[x] == v.na[y];
+    return same_term(v, v.na[x], v.na[y]) && same_term(v, v.nb[x], v.nb[y]);
+}
+
+// _collect_divisors (solver.py:334-342): pre-order, structural dedup
+void collect_divisors(const QView& v, int e, std::vector<int>& out) {
+    int op = v.op[e];
+    if (op < OOB_NODE_ADD) return;
+    if (op == OOB_NODE_DIV || op == OOB_NODE_MOD) {
+        int r = v.nb[e];
+        bool lit_ok = v.op[r] == OOB_NODE_LIT && from_w(v.lits[v.na[r]]) >= 1;
+        if (!lit_ok) {
+            bool seen = false;
+            for (int d : out) seen = seen || same_term(v, d, r);
+            if (!seen) out.push_back(r);
+        }
+    }
+    collect_divisors(v, v.na[e], out);
+    collect_divisors(v, v.nb[e], out);
+}
+
+// checked 128-bit arithmetic for the bound proof
+struct Chk {
+    bool ovf = false;
+    i128 add(i128 a, i128 b) { i128 r; if (__builtin_add_overflow(a, b, &r)) ovf = true; return r; }
+    i128 sub(i128 a, i128 b) { i128 r; if (__builtin_sub_overflow(a, b, &r)) ovf = true; return r; }
+    i128 mul(i128 a, i128 b) { i128 r; if (__builtin_mul_overflow(a, b, &r)) ovf = true; return r; }
+};
+inline i128 iabs(i128 a) { return a < 0 ? -a : a; }
+inline i128 imax(i128 a, i128 b) { return a > b ? a : b; }
+inline i128 imin(i128 a, i128 b) { return a < b ? a : b; }
+
+const i128 INF_R = (i128)1000000000000000000LL;
+// Regime limits.  Every intermediate value is bounded by B (forward
+// intervals F, exact values G, narrowing targets T, literals); domain
+// arithmetic (hi - lo + 1, lo + hi) additionally needs 2*Dmax + 1.
+const i128 I64MAX = (i128)INT64_MAX;
+const i128 D64MAX = ((i128)1 << 62) - 1;
+const i128 D128MAX = ((i128)1 << 126) - 1;
+
+struct Compiled {
+    int8_t regime = R_IMMEDIATE;
+    int8_t immediate = OOB_UNSAT;
+    uint32_t nv = 0, ncon = 0, ncode = 0, nlit = 0;
+    std::vector<uint32_t> words;  // ncon constraint words + ncode node words
+    std::vector<i128> lits;       // per literal slot
+    double cost = 0;
+    std::string why;              // reason for R_RANGE
+};
+
+struct Emitter {
+    const QView& v;
+    std::vector<uint32_t> code;
+    std::vector<i128>& lits;
+    int max_depth = 0;
+    Emitter(const QView& vv, std::vector<i128>& l) : v(vv), lits(l) {}
+    // returns the postfix index of the emitted subtree root
+    uint32_t emit(int e, int depth) {
+        max_depth = std::max(max_depth, depth);
+        int op = v.op[e];
+        if (op == OOB_NODE_LIT) {
+            lits.push_back(from_w(v.lits[v.na[e]]));
+            code.push_back(node_word(NODE_LIT, (uint32_t)(lits.size() - 1)));
+        } else if (op == OOB_NODE_VAR) {
+            code.push_back(node_word(NODE_VAR, (uint32_t)v.na[e]));
+        } else {
+            size_t start = code.size();
+            emit(v.na[e], depth + 1);
+            emit(v.nb[e], depth + 1);
+            code.push_back(node_word((uint32_t)op, (uint32_t)(code.size() + 1 - start)));
+        }
+        return (uint32_t)(code.size() - 1);
+    }
+    uint32_t emit_lit(i128 value) {
+        lits.push_back(value);
+        code.push_back(node_word(NODE_LIT, (uint32_t)(lits.size() - 1)));
+        return (uint32_t)(code.size() - 1);
+    }
+};
+
+inline uint32_t w_op(uint32_t w) { return w & 7u; }
+inline uint32_t w_arg(uint32_t w) { return w >> 3; }
+
+// Bound proof over the expanded code (see engine.cuh header).  Returns the
+// largest magnitude any intermediate value can reach, or -1 on overflow.
+i128 prove_bound(const std::vector<uint32_t>& code, const std::vector<std::pair<uint32_t, uint32_t>>& cons,
+                 const std::vector<uint8_t>& rels, const std::vector<i128>& dlo,
+                 const std::vector<i128>& dhi, const std::vector<i128>& lits) {
+    Chk c;
+    size_t n = code.size();
+    std::vector<i128> flo(n), fhi(n), gm(n);
+    std::vector<char> none(n, 0);
+    i128 B = 0;
+    for (size_t i = 0; i < dlo.size(); i++) B = imax(B, imax(iabs(dlo[i]), iabs(dhi[i])));
+    for (i128 l : lits) B = imax(B, iabs(l));
+    auto size_of = [&](uint32_t i) { return w_op(code[i]) >= NODE_ADD ? w_arg(code[i]) : 1u; };
+    // forward intervals F (exactly _eval_iv at the declared domains) and exact
+    // magnitude bounds G, postfix order
+    for (size_t j = 0; j < n; j++) {
+        uint32_t w = code[j], op = w_op(w);
+        if (op == NODE_LIT) {
+            flo[j] = fhi[j] = lits[w_arg(w)];
+            gm[j] = iabs(flo[j]);
+            continue;
+        }
+        if (op == NODE_VAR) {
+            flo[j] = dlo[w_arg(w)];
+            fhi[j] = dhi[w_arg(w)];
+            if (flo[j] > fhi[j]) none[j] = 1;
+            gm[j] = imax(iabs(flo[j]), iabs(fhi[j]));
+            continue;
+        }
+        uint32_t R = (uint32_t)j - 1, L = R - size_of(R);
+        i128 gl = gm[L], gr = gm[R];
+        switch (op) {
+        case NODE_ADD: case NODE_SUB: gm[j] = c.add(gl, gr); break;
+        case NODE_MUL: gm[j] = c.mul(gl, gr); break;
+        case NODE_DIV: gm[j] = gl; break;
+        default: gm[j] = imin(gl, gr); break;
+        }
+        if (none[L] || none[R]) { none[j] = 1; continue; }
+        i128 l0 = flo[L], l1 = fhi[L], r0 = flo[R], r1 = fhi[R];
+        if (op == NODE_ADD) { flo[j] = c.add(l0, r0); fhi[j] = c.add(l1, r1); }
+        else if (op == NODE_SUB) { flo[j] = c.sub(l0, r1); fhi[j] = c.sub(l1, r0); }
+        else if (op == NODE_MUL) {
+            i128 k[4] = {c.mul(l0, r0), c.mul(l0, r1), c.mul(l1, r0), c.mul(l1, r1)};
+            flo[j] = imin(imin(k[0], k[1]), imin(k[2], k[3]));
+            fhi[j] = imax(imax(k[0], k[1]), imax(k[2], k[3]));
+        } else {
+            i128 d0 = imax(r0, 1), d1 = r1;
+            if (d0 > d1) { none[j] = 1; continue; }
+            if (op == NODE_DIV) {
+                i128 k[4] = {l0 / d0, l0 / d1, l1 / d0, l1 / d1};
+                flo[j] = imin(imin(k[0], k[1]), imin(k[2], k[3]));
+                fhi[j] = imax(imax(k[0], k[1]), imax(k[2], k[3]));
+            } else {
+                i128 m = d1 - 1;
+                flo[j] = l0 >= 0 ? 0 : imax(l0, -m);
+                fhi[j] = l1 <= 0 ? 0 : imin(l1, m);
+            }
+        }
+        if (c.ovf) return -1;
+    }
+    if (c.ovf) return -1;
+    auto fmag = [&](uint32_t i) -> i128 { return none[i] ? 0 : imax(iabs(flo[i]), iabs(fhi[i])); };
+    for (size_t j = 0; j < n; j++) B = imax(B, imax(fmag((uint32_t)j), gm[j]));
+    // narrowing targets T, top-down from every constraint root.  Root targets
+    // per relation (solver.py:240-259): the one-sided ones are +-INF and the
+    // other side's forward bound +-1; for "=" arithmetic only happens when the
+    // target [max(l0,r0), min(l1,r1)] is non-empty, i.e. inside both sides.
+    std::vector<std::pair<uint32_t, i128>> stack;
+    for (size_t k = 0; k < cons.size(); k++) {
+        i128 fl = fmag(cons[k].first), fr = fmag(cons[k].second), tl, tr;
+        switch (rels[k]) {
+        case OOB_REL_LT: case OOB_REL_GT:
+            tl = imax(INF_R, c.add(fr, 1));
+            tr = imax(INF_R, c.add(fl, 1));
+            break;
+        case OOB_REL_LE: case OOB_REL_GE:
+            tl = imax(INF_R, fr);
+            tr = imax(INF_R, fl);
+            break;
+        default:
+            tl = tr = imin(fl, fr);
+            break;
+        }
+        stack.push_back({cons[k].first, tl});
+        stack.push_back({cons[k].second, tr});
+        while (!stack.empty()) {
+            auto [i, T] = stack.back();
+            stack.pop_back();
+            B = imax(B, T);
+            uint32_t op = w_op(code[i]);
+            if (op < NODE_ADD) continue;
+            uint32_t R = i - 1, L = R - size_of(R);
+            if (op == NODE_ADD || op == NODE_SUB) {
+                stack.push_back({L, c.add(T, fmag(R))});
+                stack.push_back({R, c.add(T, fmag(L))});
+            } else if (op == NODE_MUL) {
+                stack.push_back({L, imax(T, INF_R)});
+                stack.push_back({R, imax(T, INF_R)});
+            } else if (op == NODE_DIV && w_op(code[R]) == NODE_LIT && lits[w_arg(code[R])] >= 1) {
+                i128 cc = lits[w_arg(code[R])];
+                stack.push_back({L, c.add(c.mul(T, cc), cc)});
+            }
+            if (c.ovf) return -1;
+        }
+    }
+    return c.ovf ? -1 : B;
+}
+
+// mode: MODE_SOLVE (side constraints), MODE_PROPAGATE / MODE_CHECK (as given)
+Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s,
+                       const oob_i128* model_in) {
+    Compiled out;
+    QView v = view_of(b, q);
+    out.nv = (uint32_t)v.nv;
+    std::vector<i128> dlo(v.nv), dhi(v.nv);
+    bool empty = false;
+    for (int i = 0; i < v.nv; i++) {
+        if (mode == MODE_CHECK) {
+            dlo[i] = dhi[i] = from_w(model_in[b->var_begin[q] + i]);
+        } else {
+            dlo[i] = from_w(v.vlo[i]);
+            dhi[i] = from_w(v.vhi[i]);
+        }
+        if (dlo[i] > dhi[i]) empty = true;
+        out.cost += (dhi[i] > dlo[i]) ? std::log2((double)(dhi[i] - dlo[i]) + 1.0) : 0.0;
+    }
+    if (mode == MODE_SOLVE) {
+        if (empty) { out.immediate = OOB_UNSAT; return out; }          // solver.py:374-375
+        if (!(timeout_s > 0)) { out.immediate = OOB_TIMEOUT; return out; }  // deadline passed (:391)
+    }
+    // constraint list: user constraints + divisor side constraints (solver.py:371)
+    std::vector<std::pair<int, int>> user;
+    for (int k = 0; k < v.ncon; k++) user.push_back({v.lhs[k], v.rhs[k]});
+    std::vector<int> divs;
+    if (mode == MODE_SOLVE)
+        for (auto& c : user) { collect_divisors(v, c.first, divs); collect_divisors(v, c.second, divs); }
+    Emitter em(v, out.lits);
+    std::vector<std::pair<uint32_t, uint32_t>> roots;
+    std::vector<uint8_t> rels;
+    for (int k = 0; k < v.ncon; k++) {
+        uint32_t l = em.emit(user[k].first, 1);
+        uint32_t r = em.emit(user[k].second, 1);
+        roots.push_back({l, r});
+        rels.push_back(v.rel[k]);
+    }
+    for (int d : divs) {
+        if (v.op[d] == OOB_NODE_LIT) continue;  // solver.py:353-357
+        uint32_t l = em.emit(d, 1);
+        uint32_t r = em.emit_lit(1);
+        roots.push_back({l, r});
+        rels.push_back(OOB_REL_GE);
+    }
+    out.ncon = (uint32_t)roots.size();
+    out.ncode = (uint32_t)em.code.size();
+    out.nlit = (uint32_t)out.lits.size();
+    if (out.ncode > MAX_CODE || out.nlit > 65535 || out.ncon > 65535) {
+        out.regime = R_RANGE;
+        out.why = "expanded query too large (" + std::to_string(out.ncode) + " term nodes)";
+        return out;
+    }
+    if (em.max_depth > (int)MAX_TREE_DEPTH - 2) {
+        out.regime = R_RANGE;
+        out.why = "term nesting deeper than " + std::to_string(MAX_TREE_DEPTH - 2);
+        return out;
+    }
+    i128 B = prove_bound(em.code, roots, rels, dlo, dhi, out.lits);
+    i128 Dmax = 0;
+    for (int i = 0; i < v.nv; i++) Dmax = imax(Dmax, imax(iabs(dlo[i]), iabs(dhi[i])));
+    if (B < 0 || Dmax > D128MAX) {
+        out.regime = R_RANGE;
+        out.why = "intermediate magnitudes exceed the exact 128-bit regime";
+        return out;
+    }
+    out.regime = (B <= I64MAX && Dmax <= D64MAX) ? R_W64 : R_W128;
+    out.words.reserve(out.ncon + out.ncode);
+    for (size_t k = 0; k < roots.size(); k++)
+        out.words.push_back(con_word(rels[k], roots[k].first, roots[k].second));
+    out.words.insert(out.words.end(), em.code.begin(), em.code.end());
+    return out;
+}
+
+// ============================================================================
+// 2./3. device pool, schedule, run
+// ============================================================================
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(bytes, (size_t)1 << 16);
+        want = want + want / 4;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+struct DevicePool {
+    std::mutex mu;
+    DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
+    cudaStream_t stream = nullptr;
+    int sms = 148;
+    int occ[2] = {0, 0};
+    void release_all() {
+        for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
+                          &elapsed, &err})
+            b->release();
+    }
+};
+
+std::mutex g_pools_mu;
+std::vector<std::unique_ptr<DevicePool>> g_pools;
+
+DevicePool* pool_for(int dev) {
+    std::lock_guard<std::mutex> lk(g_pools_mu);
+    if ((int)g_pools.size() <= dev) g_pools.resize(dev + 1);
+    if (!g_pools[dev]) g_pools[dev].reset(new DevicePool());
+    return g_pools[dev].get();
+}
+
+// one device's share of one regime
+struct Job {
+    int dev = 0;
+    int wide = 0;
+    int mode = MODE_SOLVE;
+    std::vector<int64_t> qs;  // caller query ids, in schedule order
+};
+
+struct RunCtx {
+    const oob_batch* b;
+    const oob_options* opt;
+    std::vector<Compiled>* comp;
+    int mode;
+    // outputs (caller arrays, or internal for propagate/check)
+    int8_t* verdict;
+    oob_i128* model;      // SOLVE: lo per var; PROPAGATE: (lo,hi) pairs per var
+    int64_t* nodes;
+    int64_t* passes;
+    double* elapsed;
+    std::vector<int8_t>* errs;
+};
+
+SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t depth_cap, uint32_t trail_cap) {
+    SlabGeom g{};
+    g.maxv = std::max(maxv, 1u);
+    g.maxcode = std::max(maxcode, 1u);
+    g.maxlit = std::max(maxlit, 1u);
+    g.depth_cap = depth_cap;
+    g.trail_cap = trail_cap;
+    uint64_t o = 0;
+    auto put = [&](uint64_t& off, uint64_t count) { off = o; o += count * 32; };
+    put(g.o_env_lo, g.maxv);
+    put(g.o_env_hi, g.maxv);
+    put(g.o_val_lo, g.maxcode);
+    put(g.o_val_hi, g.maxcode);
+    put(g.o_lit, g.maxlit);
+    put(g.o_fr_mid, depth_cap);
+    put(g.o_fr_hi, depth_cap);
+    put(g.o_tr_lo, trail_cap);
+    put(g.o_tr_hi, trail_cap);
+    g.slab_T_words = o;
+    o = 0;
+    put(g.o_stamp, g.maxv);
+    put(g.o_fr_pick, depth_cap);
+    put(g.o_fr_mark, depth_cap);
+    put(g.o_tr_var, trail_cap);
+    g.slab_u32_words = o;
+    return g;
+}
+
+#define CK(x)                                                                                     \
+    do {                                                                                          \
+        cudaError_t e_ = (x);                                                                     \
+        if (e_ != cudaSuccess)                                                                    \
+            return std::string(#x) + ": " + cudaGetErrorString(e_);                              \
+    } while (0)
+
+// Runs `qs` (caller ids) on one device with the given scratch caps.  Writes the
+// per-scheduled-query results into the caller-facing arrays of `rc`.
+std::string run_on_device(RunCtx& rc, int dev, int wide, const std::vector<int64_t>& qs, uint32_t depth_cap,
+                          uint32_t trail_cap, std::vector<int64_t>& retry) {
+    if (qs.empty()) return "";
+    const std::vector<Compiled>& comp = *rc.comp;
+    const oob_batch* b = rc.b;
+    // ---- pack: classes, data, descriptors ----
+    std::unordered_map<std::string, uint32_t> cls;
+    std::vector<uint32_t> code;
+    std::vector<int64_t> data;
+    std::vector<QDesc> qd(qs.size());
+    uint32_t maxv = 1, maxcode = 1, maxlit = 1;
+    uint64_t model_words = 0;
+    std::vector<uint64_t> mo(qs.size());
+    for (size_t i = 0; i < qs.size(); i++) {
+        const Compiled& c = comp[qs[i]];
+        std::string key((const char*)c.words.data(), c.words.size() * 4);
+        key.append((const char*)&c.nv, 4);
+        key.append((const char*)&c.ncon, 4);
+        auto it = cls.find(key);
+        uint32_t off;
+        if (it == cls.end()) {
+            off = (uint32_t)code.size();
+            code.insert(code.end(), c.words.begin(), c.words.end());
+            cls.emplace(std::move(key), off);
+        } else {
+            off = it->second;
+        }
+        QDesc& d = qd[i];
+        d.code_off = off;
+        d.nv_ncon = c.nv | (c.ncon << 16);
+        d.ncode_nlit = c.ncode | (c.nlit << 16);
+        d.out_q = (uint32_t)i;
+        d.data_off = data.size();
+        d.out_v = model_words;
+        mo[i] = model_words;
+        model_words += c.nv;
+        maxv = std::max(maxv, c.nv);
+        maxcode = std::max(maxcode, c.ncode);
+        maxlit = std::max(maxlit, c.nlit);
+        int64_t q = qs[i];
+        int64_t vb = b->var_begin[q];
+        auto push = [&](i128 x) {
+            data.push_back((int64_t)(uint64_t)x);
+            if (wide) data.push_back((int64_t)(x >> 64));
+        };
+        for (uint32_t v = 0; v < c.nv; v++) {
+            if (rc.mode == MODE_CHECK) {
+                i128 m = from_w(rc.model[vb + v]);
+                push(m);
+                push(m);
+            } else {
+                push(from_w(b->var_lo[vb + v]));
+                push(from_w(b->var_hi[vb + v]));
+            }
+        }
+        for (i128 l : c.lits) push(l);
+        if (data.size() & 1) data.push_back(0);
+    }
+    if (code.empty()) code.push_back(0);
+    if (data.empty()) data.resize(2);
+    // ---- device buffers ----
+    DevicePool* P = pool_for(dev);
+    std::lock_guard<std::mutex> lk(P->mu);
+    CK(cudaSetDevice(dev));
+    if (!P->stream) {
+        CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+        CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (!P->occ[wide]) P->occ[wide] = 8;  // 8 x 128-thread blocks per SM (32 warps)
+    const uint32_t n = (uint32_t)qs.size();
+    const uint32_t warps_needed = (n + 31) / 32;
+    uint32_t blocks = std::min<uint32_t>((warps_needed + 3) / 4, (uint32_t)(P->sms * P->occ[wide]));
+    blocks = std::max(blocks, 1u);
+    const uint32_t n_warps = blocks * 4;
+    SlabGeom g = make_geom(maxv, maxcode, maxlit, depth_cap, trail_cap);
+    const size_t tbytes = wide ? 16 : 8;
+    const size_t out_model_words = model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
+    CK(P->qdesc.ensure(qd.size() * sizeof(QDesc)));
+    CK(P->code.ensure(code.size() * 4));
+    CK(P->data.ensure(data.size() * 8));
+    CK(P->slabT.ensure((size_t)n_warps * g.slab_T_words * tbytes));
+    CK(P->slabU.ensure((size_t)n_warps * g.slab_u32_words * 4));
+    CK(P->next.ensure(16));
+    CK(P->verdict.ensure(n));
+    CK(P->err.ensure(n));
+    CK(P->model.ensure(std::max<size_t>(out_model_words, 2) * 8));
+    CK(P->nodes.ensure((size_t)n * 8));
+    CK(P->passes.ensure((size_t)n * 8));
+    CK(P->elapsed.ensure((size_t)n * 4));
+    cudaStream_t s = P->stream;
+    CK(cudaMemcpyAsync(P->qdesc.p, qd.data(), qd.size() * sizeof(QDesc), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(P->code.p, code.data(), code.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(P->data.p, data.data(), data.size() * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(P->next.p, 0, 4, s));
+    LaunchArgs a{};
+    a.qdesc = (const QDesc*)P->qdesc.p;
+    a.code = (const uint32_t*)P->code.p;
+    a.data = (const int64_t*)P->data.p;
+    a.n = n;
+    a.next = (uint32_t*)P->next.p;
+    a.slab_T = P->slabT.p;
+    a.slab_u32 = (uint32_t*)P->slabU.p;
+    a.g = g;
+    a.verdict = (int8_t*)P->verdict.p;
+    a.err = (int8_t*)P->err.p;
+    a.model = (int64_t*)P->model.p;
+    a.nodes = (int64_t*)P->nodes.p;
+    a.passes = (int64_t*)P->passes.p;
+    a.elapsed = (float*)P->elapsed.p;
+    double t = rc.opt ? rc.opt->timeout_s : 30.0;
+    a.timeout_ns = (rc.mode == MODE_SOLVE && t > 0 && t < 1e9) ? (uint64_t)(t * 1e9) : 0;
+    a.node_budget = rc.opt ? rc.opt->node_budget : 0;
+    a.mode = rc.mode;
+    CK(launch_solve(a, wide, (int)blocks, s));
+    std::vector<int8_t> verdict(n), err(n);
+    std::vector<int64_t> nodes(n), passes(n), mw(std::max<size_t>(out_model_words, 2));
+    std::vector<float> el(n);
+    CK(cudaMemcpyAsync(verdict.data(), P->verdict.p, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(err.data(), P->err.p, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(nodes.data(), P->nodes.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(passes.data(), P->passes.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(el.data(), P->elapsed.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    if (out_model_words)
+        CK(cudaMemcpyAsync(mw.data(), P->model.p, out_model_words * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    // ---- scatter ----
+    for (uint32_t i = 0; i < n; i++) {
+        int64_t q = qs[i];
+        if (err[i] == ERR_DEPTH || err[i] == ERR_TRAIL) {
+            retry.push_back(q);
+            continue;
+        }
+        (*rc.errs)[q] = err[i];
+        rc.verdict[q] = verdict[i];
+        if (rc.nodes) rc.nodes[q] = nodes[i];
+        if (rc.passes) rc.passes[q] = passes[i];
+        if (rc.elapsed) rc.elapsed[q] = el[i];
+        int64_t vb = b->var_begin[q];
+        uint32_t nv = comp[q].nv;
+        if (rc.mode == MODE_SOLVE && verdict[i] == VERDICT_SAT && rc.model) {
+            for (uint32_t v = 0; v < nv; v++) {
+                rc.model[vb + v].lo = (uint64_t)mw[2 * (mo[i] + v)];
+                rc.model[vb + v].hi = mw[2 * (mo[i] + v) + 1];
+            }
+        } else if (rc.mode == MODE_PROPAGATE && rc.model) {
+            for (uint32_t v = 0; v < nv; v++) {
+                rc.model[2 * (vb + v)].lo = (uint64_t)mw[4 * (mo[i] + v)];
+                rc.model[2 * (vb + v)].hi = mw[4 * (mo[i] + v) + 1];
+                rc.model[2 * (vb + v) + 1].lo = (uint64_t)mw[4 * (mo[i] + v) + 2];
+                rc.model[2 * (vb + v) + 1].hi = mw[4 * (mo[i] + v) + 3];
+            }
+        }
+    }
+    return "";
+}
+
+std::string run_jobs(RunCtx& rc, std::vector<Job>& jobs) {
+    std::vector<std::string> errs(jobs.size());
+    std::vector<std::thread> th;
+    for (size_t j = 0; j < jobs.size(); j++) {
+        th.emplace_back([&, j]() {
+            Job& jb = jobs[j];
+            uint32_t depth_cap = 128, trail_cap = 1024;
+            std::vector<int64_t> qs = jb.qs;
+            for (int round = 0; round < 5 && !qs.empty(); round++) {
+                std::vector<int64_t> retry;
+                std::string e = run_on_device(rc, jb.dev, jb.wide, qs, depth_cap, trail_cap, retry);
+                if (!e.empty()) {
+                    errs[j] = e;
+                    return;
+                }
+                qs.swap(retry);
+                depth_cap *= 4;
+                trail_cap *= 8;
+            }
+            for (int64_t q : qs) {  // still out of scratch after the last retry
+                rc.verdict[q] = OOB_ERROR;
+                (*rc.errs)[q] = ERR_DEPTH;
+            }
+        });
+    }
+    for (auto& t : th) t.join();
+    for (auto& e : errs)
+        if (!e.empty()) return e;
+    return "";
+}
+
+int visible_devices() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// Common driver of the three batched entry points.
+int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i128* model_in, oob_i128* model_out,
+          int8_t* verdict, int64_t* nodes, int64_t* passes, double* elapsed) {
+    g_last_error.clear();
+    if (!b || b->n_queries < 0) return fail(OOB_E_INVALID, "null or negative batch");
+    oob_options opt{};
+    opt.timeout_s = 30.0;
+    if (opt_in) opt = *opt_in;
+    const int64_t n = b->n_queries;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int64_t q = 0; q < n; q++) {
+        std::string why = validate(b, q);
+        if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
+    }
+    std::vector<Compiled> comp(n);
+    {
+        unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        if (n < 2048) nt = 1;
+        std::vector<std::thread> th;
+        std::atomic<int64_t> next{0};
+        for (unsigned t = 0; t < nt; t++)
+            th.emplace_back([&]() {
+                for (;;) {
+                    int64_t q0 = next.fetch_add(256);
+                    if (q0 >= n) break;
+                    for (int64_t q = q0; q < std::min(n, q0 + 256); q++)
+                        comp[q] = compile_query(b, q, mode, opt.timeout_s, model_in);
+                }
+            });
+        for (auto& t : th) t.join();
+    }
+    double host_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<int8_t> errs(n, 0);
+    std::string range_msg;
+    std::vector<int64_t> reg[2];
+    for (int64_t q = 0; q < n; q++) {
+        const Compiled& c = comp[q];
+        if (c.regime == R_IMMEDIATE) {
+            verdict[q] = c.immediate;
+            if (nodes) nodes[q] = 0;
+            if (passes) passes[q] = 0;
+            if (elapsed) elapsed[q] = std::max(host_s / std::max<int64_t>(n, 1), 1e-9);
+        } else if (c.regime == R_RANGE) {
+            verdict[q] = OOB_ERROR;
+            if (range_msg.empty()) range_msg = "query " + std::to_string(q) + ": " + c.why;
+        } else {
+            reg[c.regime == R_W128].push_back(q);
+        }
+    }
+    int ndev = visible_devices();
+    if ((reg[0].size() + reg[1].size()) > 0 && ndev == 0)
+        return fail(OOB_E_CUDA, "no CUDA device visible: the OOB engine has no CPU fallback");
+    int first = std::max(0, opt.device);
+    int want = opt.n_gpus > 0 ? opt.n_gpus : ndev - first;
+    want = std::max(1, std::min(want, ndev - first));
+    if (first >= ndev && (reg[0].size() + reg[1].size()) > 0)
+        return fail(OOB_E_CUDA, "device ordinal out of range");
+    std::vector<Job> jobs;
+    for (int w = 0; w < 2; w++) {
+        auto& qs = reg[w];
+        if (qs.empty()) continue;
+        if (!(opt.flags & OOB_F_NO_SORT)) {
+            // class-major, cost-minor: a 32-query tile is (nearly) one class
+            std::unordered_map<std::string, uint32_t> cid;
+            std::vector<uint32_t> key(n, 0);
+            for (int64_t q : qs) {
+                const Compiled& c = comp[q];
+                std::string k((const char*)c.words.data(), c.words.size() * 4);
+                k.append((const char*)&c.nv, 4);
+                auto it = cid.emplace(std::move(k), (uint32_t)cid.size()).first;
+                key[q] = it->second;
+            }
+            std::stable_sort(qs.begin(), qs.end(), [&](int64_t x, int64_t y) {
+                if (key[x] != key[y]) return key[x] < key[y];
+                return comp[x].cost > comp[y].cost;
+            });
+        }
+        std::vector<Job> dj(want);
+        for (int d = 0; d < want; d++) {
+            dj[d].dev = first + d;
+            dj[d].wide = w;
+            dj[d].mode = mode;
+        }
+        for (size_t i = 0; i < qs.size(); i++) dj[(i / 32) % want].qs.push_back(qs[i]);
+        for (auto& j : dj)
+            if (!j.qs.empty()) jobs.push_back(std::move(j));
+    }
+    RunCtx rc;
+    rc.b = b;
+    rc.opt = &opt;
+    rc.comp = &comp;
+    rc.mode = mode;
+    rc.verdict = verdict;
+    rc.model = mode == MODE_CHECK ? const_cast<oob_i128*>(model_in) : model_out;
+    rc.nodes = nodes;
+    rc.passes = passes;
+    rc.elapsed = elapsed;
+    rc.errs = &errs;
+    // jobs of different regimes on one device run back to back inside its lock
+    std::string e = run_jobs(rc, jobs);
+    if (!e.empty()) return fail(OOB_E_CUDA, e);
+    for (int64_t q = 0; q < n; q++) {
+        if (errs[q] != ERR_NONE && range_msg.empty())
+            range_msg = "query " + std::to_string(q) + ": search outgrew the device scratch (error " +
+                        std::to_string(errs[q]) + ")";
+    }
+    if (!range_msg.empty()) return fail(OOB_E_RANGE, range_msg);
+    return OOB_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int oob_solve_batch(const oob_batch* batch, const oob_options* opt, oob_result* out) {
+    if (!out || !out->verdict) return fail(OOB_E_INVALID, "result arrays missing");
+    return drive(batch, opt, MODE_SOLVE, nullptr, out->model, out->verdict, out->nodes, out->passes,
+                 out->elapsed_s);
+}
+
+int oob_propagate_batch(const oob_batch* batch, const oob_options* opt, oob_i128* out_lo, oob_i128* out_hi,
+                        int8_t* status) {
+    if (!batch || !out_lo || !out_hi || !status) return fail(OOB_E_INVALID, "null argument");
+    int64_t V = batch->var_begin[batch->n_queries];
+    std::vector<oob_i128> pairs((size_t)std::max<int64_t>(V, 1) * 2);
+    std::vector<int8_t> verdict(batch->n_queries);
+    int rc = drive(batch, opt, MODE_PROPAGATE, nullptr, pairs.data(), verdict.data(), nullptr, nullptr, nullptr);
+    if (rc != OOB_OK) return rc;
+    for (int64_t q = 0; q < batch->n_queries; q++) {
+        status[q] = verdict[q] == OOB_SAT ? 1 : 0;
+        for (int64_t v = batch->var_begin[q]; v < batch->var_begin[q + 1]; v++) {
+            out_lo[v] = pairs[2 * v];
+            out_hi[v] = pairs[2 * v + 1];
+        }
+    }
+    return OOB_OK;
+}
+
+int oob_check_model_batch(const oob_batch* batch, const oob_options* opt, const oob_i128* model, int8_t* ok) {
+    if (!batch || !model || !ok) return fail(OOB_E_INVALID, "null argument");
+    std::vector<int8_t> verdict(batch->n_queries);
+    int rc = drive(batch, opt, MODE_CHECK, model, nullptr, verdict.data(), nullptr, nullptr, nullptr);
+    if (rc != OOB_OK) return rc;
+    for (int64_t q = 0; q < batch->n_queries; q++) ok[q] = verdict[q] == OOB_SAT ? 1 : 0;
+    return OOB_OK;
+}
+
+int oob_side_constraint_count(const oob_batch* b, int64_t* counts) {
+    g_last_error.clear();
+    if (!b || !counts) return fail(OOB_E_INVALID, "null argument");
+    for (int64_t q = 0; q < b->n_queries; q++) {
+        std::string why = validate(b, q);
+        if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
+        QView v = view_of(b, q);
+        std::vector<int> divs;
+        for (int k = 0; k < v.ncon; k++) {
+            collect_divisors(v, v.lhs[k], divs);
+            collect_divisors(v, v.rhs[k], divs);
+        }
+        int64_t c = 0;
+        for (int d : divs) c += v.op[d] != OOB_NODE_LIT;
+        counts[q] = c;
+    }
+    return OOB_OK;
+}
+
+const char* oob_last_error(void) { return g_last_error.c_str(); }
+
+int oob_device_count(void) { return visible_devices(); }
+
+const char* oob_version(void) { return "scuba-oob-b200 0.1 (sm_100a)"; }
+
+void oob_release(void) {
+    std::lock_guard<std::mutex> lk(g_pools_mu);
+    for (auto& p : g_pools) {
+        if (!p) continue;
+        std::lock_guard<std::mutex> lk2(p->mu);
+        p->release_all();
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+"""Shared test plumbing: the `gpu` marker, golden fixtures, import paths."""
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+REF_SRC = Path("/root/reference/pkg/src")
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+GOLDEN_SETS = ("corpus_m1048576", "corpus_m64", "crafted", "random_solver", "random_accept")
+VCODE = {"unsat": 0, "sat": 1, "timeout": 2}
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+
+
+def load_golden(name: str) -> list:
+    with open(GOLDEN / f"{name}.jsonl") as f:
+        return [json.loads(line) for line in f]
+
+
+def reference_available() -> bool:
+    return (REF_SRC / "scuba_mini" / "solver.py").exists()
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return {name: load_golden(name) for name in GOLDEN_SETS}
+
+
+def has_gpu() -> bool:
+    try:
+        from paper_2601_21552_b200 import _lib
+        return _lib.device_count() > 0
+    except Exception:
+        return False
+
+
+@pytest.fixture(scope="session")
+def gpu():
+    if not has_gpu():
+        pytest.fail("GPU test run without a visible CUDA device / engine library")
+    return True
