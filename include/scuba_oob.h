@@ -122,9 +122,7 @@ typedef struct {
 } oob_options;
 
 enum {
-    OOB_F_NO_SORT = 1,   /* keep input order on device (testing the scheduler) */
-    OOB_F_SEQUENTIAL = 2 /* one DFS node at a time per query (no frontier
-                            parallelism; same results, used by parity tests)  */
+    OOB_F_NO_SORT = 1 /* keep input order on device (testing the scheduler) */
 };
 
 /* Results (caller-allocated; optional arrays may be NULL). */
@@ -155,6 +153,31 @@ int oob_check_model_batch(const oob_batch* batch, const oob_options* opt,
 /* Number of divisor side constraints solve() appends for query q
  * (solver.py:334-357); lets callers size buffers / audit the host compiler. */
 int oob_side_constraint_count(const oob_batch* batch, int64_t* counts);
+
+/*
+ * Plans: compile and upload a batch once, then run the decision kernels on
+ * device-resident records as often as needed (benchmarks, repeated checking).
+ * The caller keeps `batch` alive until oob_plan_destroy().
+ *   oob_plan_run      launches every device's kernels; *device_ms = the max
+ *                     over devices of the CUDA-event time on the engine stream
+ *   oob_plan_results  device->host copy + scatter (same contract as
+ *                     oob_solve_batch's results)
+ *   oob_plan_info     [0] queries on devices  [1] record bytes (descriptors +
+ *                     class code + per-query data)  [2] result bytes
+ *                     [3] structure classes  [4] device jobs  [5] kernel
+ *                     launches per run  [6] queries in the int128 regime
+ *                     [7] host compile time (us)
+ */
+typedef struct oob_plan oob_plan;
+int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** plan);
+int oob_plan_run(oob_plan* plan, float* device_ms);
+int oob_plan_results(oob_plan* plan, oob_result* out);
+int oob_plan_info(const oob_plan* plan, int64_t info[8]);
+void oob_plan_destroy(oob_plan* plan);
+
+/* Diagnostics: host-side evaluation of the 256-bit regime arithmetic
+ * (op 0 + 1 - 2 * 3 / 4 % 5 < 6 >>1; 4 little-endian words each). */
+int oob_selftest_i256(int op, const int64_t* a, const int64_t* b, int64_t* out);
 
 /* Last error message of the calling thread ("" if none). */
 const char* oob_last_error(void);

@@ -20,7 +20,7 @@ _lib = None
 
 
 def build(force: bool = False) -> Path:
-    if force or not LIB.exists() or LIB.stat().st_mtime < (HERE / "oob_oracle.c").stat().st_mtime:
+    if force or not LIB.exists() or LIB.stat().st_mtime < (HERE / "oob_oracle.cpp").stat().st_mtime:
         subprocess.check_call(["make", "-s", "-C", str(HERE)])
     return LIB
 

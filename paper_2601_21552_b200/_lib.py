@@ -18,8 +18,6 @@ OOB_OK, OOB_E_INVALID, OOB_E_CUDA, OOB_E_RANGE, OOB_E_NOMEM = 0, 1, 2, 3, 4
 UNSAT, SAT, TIMEOUT, ERROR = 0, 1, 2, 3
 
 F_NO_SORT = 1
-F_SEQUENTIAL = 2
-
 
 class EngineError(RuntimeError):
     """The GPU engine could not decide a batch (no device, capacity, range)."""
@@ -55,6 +53,11 @@ EXPORTS = (
     "oob_device_count",
     "oob_version",
     "oob_release",
+    "oob_plan_create",
+    "oob_plan_run",
+    "oob_plan_results",
+    "oob_plan_info",
+    "oob_plan_destroy",
 )
 
 _lib = None
@@ -83,6 +86,16 @@ def lib():
     L.oob_device_count.restype = ctypes.c_int
     L.oob_version.restype = ctypes.c_char_p
     L.oob_release.restype = None
+    L.oob_plan_create.argtypes = [vp, vp, vp]
+    L.oob_plan_create.restype = ctypes.c_int
+    L.oob_plan_run.argtypes = [vp, vp]
+    L.oob_plan_run.restype = ctypes.c_int
+    L.oob_plan_results.argtypes = [vp, vp]
+    L.oob_plan_results.restype = ctypes.c_int
+    L.oob_plan_info.argtypes = [vp, vp]
+    L.oob_plan_info.restype = ctypes.c_int
+    L.oob_plan_destroy.argtypes = [vp]
+    L.oob_plan_destroy.restype = None
     _lib = L
     return L
 
@@ -165,3 +178,58 @@ def side_counts(fb):
     check(lib().oob_side_constraint_count(ctypes.byref(cb), c.ctypes.data),
           "oob_side_constraint_count")
     return c
+
+
+class Plan:
+    """oob_plan_*: compile + upload once, run kernels on HBM-resident records."""
+
+    INFO = ("queries", "record_bytes", "result_bytes", "classes", "jobs",
+            "launches_per_run", "wide_queries", "compile_us")
+
+    def __init__(self, fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0):
+        self.fb = fb                     # keeps the batch arrays alive
+        self._cb = fb.as_c()
+        self._opt = options(timeout_s, node_budget, n_gpus, device, flags)
+        self._p = ctypes.c_void_p()
+        check(lib().oob_plan_create(ctypes.byref(self._cb), ctypes.byref(self._opt),
+                                    ctypes.byref(self._p)), "oob_plan_create")
+
+    def run(self) -> float:
+        ms = ctypes.c_float()
+        check(lib().oob_plan_run(self._p, ctypes.byref(ms)), "oob_plan_run")
+        return float(ms.value)
+
+    def info(self) -> dict:
+        a = np.zeros(8, dtype=np.int64)
+        check(lib().oob_plan_info(self._p, a.ctypes.data), "oob_plan_info")
+        return dict(zip(self.INFO, (int(x) for x in a)))
+
+    def results(self) -> dict:
+        fb = self.fb
+        n = fb.n
+        out = {
+            "verdict": np.full(n, -1, dtype=np.int8),
+            "model": np.zeros((max(fb.n_vars_total, 1), 2), dtype=np.int64),
+            "nodes": np.zeros(n, dtype=np.int64),
+            "passes": np.zeros(n, dtype=np.int64),
+            "elapsed": np.zeros(n, dtype=np.float64),
+        }
+        r = oob_result(out["verdict"].ctypes.data, out["model"].ctypes.data,
+                       out["nodes"].ctypes.data, out["passes"].ctypes.data,
+                       out["elapsed"].ctypes.data)
+        rc = lib().oob_plan_results(self._p, ctypes.byref(r))
+        if rc not in (OOB_OK, OOB_E_RANGE):
+            check(rc, "oob_plan_results")
+        out["status"] = rc
+        return out
+
+    def close(self):
+        if self._p:
+            lib().oob_plan_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

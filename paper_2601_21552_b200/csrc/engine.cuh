@@ -17,12 +17,13 @@
 #include <cstdint>
 
 #include "format.h"
+#include "wide.cuh"
 
 namespace oob {
 
 template <typename T>
 struct Arith {
-    static constexpr T INF = (T)1000000000000000000LL;  // _INF = 10**18 (solver.py:23)
+    __device__ static inline T inf() { return T(1000000000000000000LL); }  // _INF = 10**18 (solver.py:23)
     __device__ static inline T mn(T a, T b) { return a < b ? a : b; }
     __device__ static inline T mx(T a, T b) { return a > b ? a : b; }
     // C division truncates toward zero: exactly tdiv/tmod (solver.py:94-102).
@@ -211,7 +212,7 @@ struct Lane {
                 if (l0 < 0 || r0 < 0) continue;
                 if (b < 0) return false;
                 T t0n = A::mx(a, (T)0);
-                T lo_l = -A::INF, hi_l = A::INF, lo_r = -A::INF, hi_r = A::INF;
+                T lo_l = -A::inf(), hi_l = A::inf(), lo_r = -A::inf(), hi_r = A::inf();
                 if (t0n > 0) {
                     if (r1 == 0 || l1 == 0) return false;
                     lo_l = A::ceil_div(t0n, r1);
@@ -248,11 +249,11 @@ struct Lane {
         T l0 = E(val_lo, lr), l1 = E(val_hi, lr), r0 = E(val_lo, rr), r1 = E(val_hi, rr);
         T a0, a1, b0, b1;
         switch (rel) {
-        case REL_LT: a0 = -A::INF; a1 = r1 - 1; b0 = l0 + 1; b1 = A::INF; break;
-        case REL_LE: a0 = -A::INF; a1 = r1; b0 = l0; b1 = A::INF; break;
+        case REL_LT: a0 = -A::inf(); a1 = r1 - 1; b0 = l0 + 1; b1 = A::inf(); break;
+        case REL_LE: a0 = -A::inf(); a1 = r1; b0 = l0; b1 = A::inf(); break;
         case REL_EQ: a0 = b0 = A::mx(l0, r0); a1 = b1 = A::mn(l1, r1); break;
-        case REL_GE: a0 = r0; a1 = A::INF; b0 = -A::INF; b1 = l1; break;
-        default:     a0 = r0 + 1; a1 = A::INF; b0 = -A::INF; b1 = l1 - 1; break;
+        case REL_GE: a0 = r0; a1 = A::inf(); b0 = -A::inf(); b1 = l1; break;
+        default:     a0 = r0 + 1; a1 = A::inf(); b0 = -A::inf(); b1 = l1 - 1; break;
         }
         return narrow(lr, a0, a1) && narrow(rr, b0, b1);
     }

@@ -29,6 +29,7 @@
 
 #include "../../include/scuba_oob.h"
 #include "format.h"
+#include "wide.cuh"
 
 namespace oob {
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
@@ -54,7 +55,7 @@ static i128 from_w(oob_i128 w) { return (i128)(((unsigned __int128)(uint64_t)w.h
 // ============================================================================
 namespace {
 
-enum Regime : int8_t { R_IMMEDIATE = 0, R_W64 = 1, R_W128 = 2, R_RANGE = 3 };
+enum Regime : int8_t { R_IMMEDIATE = 0, R_W64 = 1, R_W128 = 2, R_W256 = 3, R_RANGE = 4 };
 
 struct QView {
     int nv, ncon, nn, nl;
@@ -302,6 +303,61 @@ i128 prove_bound(const std::vector<uint32_t>& code, const std::vector<std::pair<
     return c.ovf ? -1 : B;
 }
 
+// Conservative magnitude bound in double precision (used when the exact
+// 128-bit proof overflows): |x + y| <= |x| + |y|, |x * y| <= |x||y|,
+// |tdiv(a, d)| <= |a|, |a % d| <= min(|a|, |d|); targets as in prove_bound.
+// Relative rounding error is far below the 2^250 vs 2^255 margin.
+double prove_bound_mag(const std::vector<uint32_t>& code, const std::vector<std::pair<uint32_t, uint32_t>>& cons,
+                       const std::vector<uint8_t>& rels, const std::vector<i128>& dlo, const std::vector<i128>& dhi,
+                       const std::vector<i128>& lits) {
+    auto mag = [](i128 v) { return (double)(v < 0 ? -(long double)v : (long double)v); };
+    size_t n = code.size();
+    std::vector<double> m(n);
+    double B = 0;
+    auto size_of = [&](uint32_t i) { return w_op(code[i]) >= NODE_ADD ? w_arg(code[i]) : 1u; };
+    for (size_t j = 0; j < n; j++) {
+        uint32_t w = code[j], op = w_op(w);
+        if (op == NODE_LIT) m[j] = mag(lits[w_arg(w)]);
+        else if (op == NODE_VAR) m[j] = std::max(mag(dlo[w_arg(w)]), mag(dhi[w_arg(w)]));
+        else {
+            uint32_t R = (uint32_t)j - 1, L = R - size_of(R);
+            if (op == NODE_ADD || op == NODE_SUB) m[j] = m[L] + m[R];
+            else if (op == NODE_MUL) m[j] = m[L] * m[R];
+            else if (op == NODE_DIV) m[j] = m[L];
+            else m[j] = std::min(m[L], m[R]);
+        }
+        B = std::max(B, m[j]);
+    }
+    const double INF_D = 1e18;
+    std::vector<std::pair<uint32_t, double>> st;
+    for (size_t k = 0; k < cons.size(); k++) {
+        double fl = m[cons[k].first], fr = m[cons[k].second], tl, tr;
+        if (rels[k] == OOB_REL_EQ) tl = tr = std::min(fl, fr);
+        else { tl = std::max(INF_D, fr + 1); tr = std::max(INF_D, fl + 1); }
+        st.push_back({cons[k].first, tl});
+        st.push_back({cons[k].second, tr});
+        while (!st.empty()) {
+            auto [i, T] = st.back();
+            st.pop_back();
+            B = std::max(B, T);
+            uint32_t op = w_op(code[i]);
+            if (op < NODE_ADD) continue;
+            uint32_t R = i - 1, L = R - size_of(R);
+            if (op == NODE_ADD || op == NODE_SUB) {
+                st.push_back({L, T + m[R]});
+                st.push_back({R, T + m[L]});
+            } else if (op == NODE_MUL) {
+                st.push_back({L, std::max(T, INF_D)});
+                st.push_back({R, std::max(T, INF_D)});
+            } else if (op == NODE_DIV && w_op(code[R]) == NODE_LIT && lits[w_arg(code[R])] >= 1) {
+                double cc = mag(lits[w_arg(code[R])]);
+                st.push_back({L, T * cc + cc});
+            }
+        }
+    }
+    return B;
+}
+
 // mode: MODE_SOLVE (side constraints), MODE_PROPAGATE / MODE_CHECK (as given)
 Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s,
                        const oob_i128* model_in) {
@@ -362,12 +418,20 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
     i128 B = prove_bound(em.code, roots, rels, dlo, dhi, out.lits);
     i128 Dmax = 0;
     for (int i = 0; i < v.nv; i++) Dmax = imax(Dmax, imax(iabs(dlo[i]), iabs(dhi[i])));
-    if (B < 0 || Dmax > D128MAX) {
+    if (Dmax > D128MAX) {
         out.regime = R_RANGE;
-        out.why = "intermediate magnitudes exceed the exact 128-bit regime";
+        out.why = "domain bounds exceed the 128-bit wire format";
         return out;
     }
-    out.regime = (B <= I64MAX && Dmax <= D64MAX) ? R_W64 : R_W128;
+    if (B >= 0) {
+        out.regime = (B <= I64MAX && Dmax <= D64MAX) ? R_W64 : R_W128;
+    } else if (prove_bound_mag(em.code, roots, rels, dlo, dhi, out.lits) < 1.8e75) {  // < 2^250
+        out.regime = R_W256;
+    } else {
+        out.regime = R_RANGE;
+        out.why = "intermediate magnitudes exceed the exact 256-bit regime";
+        return out;
+    }
     out.words.reserve(out.ncon + out.ncode);
     for (size_t k = 0; k < roots.size(); k++)
         out.words.push_back(con_word(rels[k], roots[k].first, roots[k].second));
@@ -399,8 +463,8 @@ struct DevicePool {
     std::mutex mu;
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
     cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int sms = 148;
-    int occ[2] = {0, 0};
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err})
@@ -418,22 +482,14 @@ DevicePool* pool_for(int dev) {
     return g_pools[dev].get();
 }
 
-// one device's share of one regime
-struct Job {
-    int dev = 0;
-    int wide = 0;
-    int mode = MODE_SOLVE;
-    std::vector<int64_t> qs;  // caller query ids, in schedule order
-};
-
 struct RunCtx {
     const oob_batch* b;
-    const oob_options* opt;
+    oob_options opt;
     std::vector<Compiled>* comp;
     int mode;
     // outputs (caller arrays, or internal for propagate/check)
     int8_t* verdict;
-    oob_i128* model;      // SOLVE: lo per var; PROPAGATE: (lo,hi) pairs per var
+    oob_i128* model;      // SOLVE: lo per var; PROPAGATE: (lo,hi) pairs; CHECK: input model
     int64_t* nodes;
     int64_t* passes;
     double* elapsed;
@@ -475,52 +531,78 @@ SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t de
             return std::string(#x) + ": " + cudaGetErrorString(e_);                              \
     } while (0)
 
-// Runs `qs` (caller ids) on one device with the given scratch caps.  Writes the
-// per-scheduled-query results into the caller-facing arrays of `rc`.
-std::string run_on_device(RunCtx& rc, int dev, int wide, const std::vector<int64_t>& qs, uint32_t depth_cap,
-                          uint32_t trail_cap, std::vector<int64_t>& retry) {
-    if (qs.empty()) return "";
-    const std::vector<Compiled>& comp = *rc.comp;
-    const oob_batch* b = rc.b;
-    // ---- pack: classes, data, descriptors ----
-    std::unordered_map<std::string, uint32_t> cls;
-    std::vector<uint32_t> code;
-    std::vector<int64_t> data;
-    std::vector<QDesc> qd(qs.size());
+constexpr uint32_t DEPTH_CAP0 = 128, TRAIL_CAP0 = 1024;
+constexpr int BLOCKS_PER_SM = 8;  // 8 x 128 threads = 32 warps per SM
+
+// One device's share of one regime: packed device records + launch geometry.
+struct DevJob {
+    int dev = 0;
+    int wide = 0;
+    std::vector<int64_t> qs;     // caller query ids, in schedule order
+    std::vector<uint64_t> mo;    // device-local model offset (vars) per scheduled query
+    std::vector<uint32_t> code;  // class code blocks
+    std::vector<int64_t> data;   // per query domains + literal slots
+    std::vector<QDesc> qd;
     uint32_t maxv = 1, maxcode = 1, maxlit = 1;
     uint64_t model_words = 0;
-    std::vector<uint64_t> mo(qs.size());
-    for (size_t i = 0; i < qs.size(); i++) {
-        const Compiled& c = comp[qs[i]];
+    uint32_t n_classes = 0;
+    uint32_t blocks = 1;
+    SlabGeom g{};
+    LaunchArgs a{};
+    size_t out_model_words = 0;
+    bool staged = false;
+    float last_ms = 0;
+
+    uint64_t record_bytes() const {  // algorithmic input bytes of one launch
+        return qd.size() * sizeof(QDesc) + code.size() * 4 + data.size() * 8;
+    }
+};
+
+void pack(const RunCtx& rc, DevJob& j) {
+    const std::vector<Compiled>& comp = *rc.comp;
+    const oob_batch* b = rc.b;
+    std::unordered_map<std::string, uint32_t> cls;
+    j.code.clear();
+    j.data.clear();
+    j.qd.assign(j.qs.size(), QDesc{});
+    j.mo.assign(j.qs.size(), 0);
+    j.model_words = 0;
+    for (size_t i = 0; i < j.qs.size(); i++) {
+        const Compiled& c = comp[j.qs[i]];
         std::string key((const char*)c.words.data(), c.words.size() * 4);
         key.append((const char*)&c.nv, 4);
         key.append((const char*)&c.ncon, 4);
         auto it = cls.find(key);
         uint32_t off;
         if (it == cls.end()) {
-            off = (uint32_t)code.size();
-            code.insert(code.end(), c.words.begin(), c.words.end());
+            off = (uint32_t)j.code.size();
+            j.code.insert(j.code.end(), c.words.begin(), c.words.end());
             cls.emplace(std::move(key), off);
         } else {
             off = it->second;
         }
-        QDesc& d = qd[i];
+        QDesc& d = j.qd[i];
         d.code_off = off;
         d.nv_ncon = c.nv | (c.ncon << 16);
         d.ncode_nlit = c.ncode | (c.nlit << 16);
         d.out_q = (uint32_t)i;
-        d.data_off = data.size();
-        d.out_v = model_words;
-        mo[i] = model_words;
-        model_words += c.nv;
-        maxv = std::max(maxv, c.nv);
-        maxcode = std::max(maxcode, c.ncode);
-        maxlit = std::max(maxlit, c.nlit);
-        int64_t q = qs[i];
+        d.data_off = j.data.size();
+        d.out_v = j.model_words;
+        j.mo[i] = j.model_words;
+        j.model_words += c.nv;
+        j.maxv = std::max(j.maxv, c.nv);
+        j.maxcode = std::max(j.maxcode, c.ncode);
+        j.maxlit = std::max(j.maxlit, c.nlit);
+        int64_t q = j.qs[i];
         int64_t vb = b->var_begin[q];
         auto push = [&](i128 x) {
-            data.push_back((int64_t)(uint64_t)x);
-            if (wide) data.push_back((int64_t)(x >> 64));
+            j.data.push_back((int64_t)(uint64_t)x);
+            if (j.wide >= 1) j.data.push_back((int64_t)(x >> 64));
+            if (j.wide == 2) {
+                int64_t s = x < 0 ? -1 : 0;
+                j.data.push_back(s);
+                j.data.push_back(s);
+            }
         };
         for (uint32_t v = 0; v < c.nv; v++) {
             if (rc.mode == MODE_CHECK) {
@@ -533,45 +615,47 @@ std::string run_on_device(RunCtx& rc, int dev, int wide, const std::vector<int64
             }
         }
         for (i128 l : c.lits) push(l);
-        if (data.size() & 1) data.push_back(0);
+        while (j.data.size() & (j.wide == 2 ? 3 : 1)) j.data.push_back(0);
     }
-    if (code.empty()) code.push_back(0);
-    if (data.empty()) data.resize(2);
-    // ---- device buffers ----
-    DevicePool* P = pool_for(dev);
-    std::lock_guard<std::mutex> lk(P->mu);
-    CK(cudaSetDevice(dev));
+    j.n_classes = (uint32_t)cls.size();
+    if (j.code.empty()) j.code.push_back(0);
+    if (j.data.empty()) j.data.resize(2);
+}
+
+// allocate + upload the packed records of `j` into pool P (caller holds P->mu)
+std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap, uint32_t trail_cap) {
+    CK(cudaSetDevice(j.dev));
     if (!P->stream) {
         CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
-        CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaEventCreate(&P->ev0));
+        CK(cudaEventCreate(&P->ev1));
+        CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, j.dev));
     }
-    if (!P->occ[wide]) P->occ[wide] = 8;  // 8 x 128-thread blocks per SM (32 warps)
-    const uint32_t n = (uint32_t)qs.size();
+    const uint32_t n = (uint32_t)j.qs.size();
     const uint32_t warps_needed = (n + 31) / 32;
-    uint32_t blocks = std::min<uint32_t>((warps_needed + 3) / 4, (uint32_t)(P->sms * P->occ[wide]));
-    blocks = std::max(blocks, 1u);
-    const uint32_t n_warps = blocks * 4;
-    SlabGeom g = make_geom(maxv, maxcode, maxlit, depth_cap, trail_cap);
-    const size_t tbytes = wide ? 16 : 8;
-    const size_t out_model_words = model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
-    CK(P->qdesc.ensure(qd.size() * sizeof(QDesc)));
-    CK(P->code.ensure(code.size() * 4));
-    CK(P->data.ensure(data.size() * 8));
-    CK(P->slabT.ensure((size_t)n_warps * g.slab_T_words * tbytes));
-    CK(P->slabU.ensure((size_t)n_warps * g.slab_u32_words * 4));
+    j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + 3) / 4, (uint32_t)(P->sms * BLOCKS_PER_SM)));
+    const uint32_t n_warps = j.blocks * 4;
+    j.g = make_geom(j.maxv, j.maxcode, j.maxlit, depth_cap, trail_cap);
+    const size_t tbytes = j.wide == 2 ? 32 : (j.wide ? 16 : 8);
+    j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
+    CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
+    CK(P->code.ensure(j.code.size() * 4));
+    CK(P->data.ensure(j.data.size() * 8));
+    CK(P->slabT.ensure((size_t)n_warps * j.g.slab_T_words * tbytes));
+    CK(P->slabU.ensure((size_t)n_warps * j.g.slab_u32_words * 4));
     CK(P->next.ensure(16));
     CK(P->verdict.ensure(n));
     CK(P->err.ensure(n));
-    CK(P->model.ensure(std::max<size_t>(out_model_words, 2) * 8));
+    CK(P->model.ensure(std::max<size_t>(j.out_model_words, 2) * 8));
     CK(P->nodes.ensure((size_t)n * 8));
     CK(P->passes.ensure((size_t)n * 8));
     CK(P->elapsed.ensure((size_t)n * 4));
     cudaStream_t s = P->stream;
-    CK(cudaMemcpyAsync(P->qdesc.p, qd.data(), qd.size() * sizeof(QDesc), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(P->code.p, code.data(), code.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(P->data.p, data.data(), data.size() * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(P->next.p, 0, 4, s));
-    LaunchArgs a{};
+    CK(cudaMemcpyAsync(P->qdesc.p, j.qd.data(), j.qd.size() * sizeof(QDesc), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(P->code.p, j.code.data(), j.code.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(P->data.p, j.data.data(), j.data.size() * 8, cudaMemcpyHostToDevice, s));
+    LaunchArgs& a = j.a;
+    a = LaunchArgs{};
     a.qdesc = (const QDesc*)P->qdesc.p;
     a.code = (const uint32_t*)P->code.p;
     a.data = (const int64_t*)P->data.p;
@@ -579,32 +663,59 @@ std::string run_on_device(RunCtx& rc, int dev, int wide, const std::vector<int64
     a.next = (uint32_t*)P->next.p;
     a.slab_T = P->slabT.p;
     a.slab_u32 = (uint32_t*)P->slabU.p;
-    a.g = g;
+    a.g = j.g;
     a.verdict = (int8_t*)P->verdict.p;
     a.err = (int8_t*)P->err.p;
     a.model = (int64_t*)P->model.p;
     a.nodes = (int64_t*)P->nodes.p;
     a.passes = (int64_t*)P->passes.p;
     a.elapsed = (float*)P->elapsed.p;
-    double t = rc.opt ? rc.opt->timeout_s : 30.0;
+    double t = rc.opt.timeout_s;
     a.timeout_ns = (rc.mode == MODE_SOLVE && t > 0 && t < 1e9) ? (uint64_t)(t * 1e9) : 0;
-    a.node_budget = rc.opt ? rc.opt->node_budget : 0;
+    a.node_budget = rc.opt.node_budget;
     a.mode = rc.mode;
-    CK(launch_solve(a, wide, (int)blocks, s));
+    j.staged = true;
+    return "";
+}
+
+// kernel launch bracketed by events on the engine's stream
+std::string launch(DevJob& j, DevicePool* P) {
+    CK(cudaSetDevice(j.dev));
+    cudaStream_t s = P->stream;
+    CK(cudaMemsetAsync(P->next.p, 0, 4, s));
+    CK(cudaEventRecord(P->ev0, s));
+    CK(launch_solve(j.a, j.wide, (int)j.blocks, s));
+    CK(cudaEventRecord(P->ev1, s));
+    return "";
+}
+
+std::string kernel_ms(DevJob& j, DevicePool* P) {
+    CK(cudaSetDevice(j.dev));
+    CK(cudaEventSynchronize(P->ev1));
+    CK(cudaEventElapsedTime(&j.last_ms, P->ev0, P->ev1));
+    return "";
+}
+
+// D2H + scatter into the caller arrays; capacity overflows go to `retry`
+std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t>& retry) {
+    CK(cudaSetDevice(j.dev));
+    const uint32_t n = (uint32_t)j.qs.size();
+    cudaStream_t s = P->stream;
     std::vector<int8_t> verdict(n), err(n);
-    std::vector<int64_t> nodes(n), passes(n), mw(std::max<size_t>(out_model_words, 2));
+    std::vector<int64_t> nodes(n), passes(n), mw(std::max<size_t>(j.out_model_words, 2));
     std::vector<float> el(n);
     CK(cudaMemcpyAsync(verdict.data(), P->verdict.p, n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(err.data(), P->err.p, n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(nodes.data(), P->nodes.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(passes.data(), P->passes.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(el.data(), P->elapsed.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
-    if (out_model_words)
-        CK(cudaMemcpyAsync(mw.data(), P->model.p, out_model_words * 8, cudaMemcpyDeviceToHost, s));
+    if (j.out_model_words)
+        CK(cudaMemcpyAsync(mw.data(), P->model.p, j.out_model_words * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    // ---- scatter ----
+    const std::vector<Compiled>& comp = *rc.comp;
+    const oob_batch* b = rc.b;
     for (uint32_t i = 0; i < n; i++) {
-        int64_t q = qs[i];
+        int64_t q = j.qs[i];
         if (err[i] == ERR_DEPTH || err[i] == ERR_TRAIL) {
             retry.push_back(q);
             continue;
@@ -616,48 +727,58 @@ std::string run_on_device(RunCtx& rc, int dev, int wide, const std::vector<int64
         if (rc.elapsed) rc.elapsed[q] = el[i];
         int64_t vb = b->var_begin[q];
         uint32_t nv = comp[q].nv;
+        uint64_t m0 = j.mo[i];
         if (rc.mode == MODE_SOLVE && verdict[i] == VERDICT_SAT && rc.model) {
             for (uint32_t v = 0; v < nv; v++) {
-                rc.model[vb + v].lo = (uint64_t)mw[2 * (mo[i] + v)];
-                rc.model[vb + v].hi = mw[2 * (mo[i] + v) + 1];
+                rc.model[vb + v].lo = (uint64_t)mw[2 * (m0 + v)];
+                rc.model[vb + v].hi = mw[2 * (m0 + v) + 1];
             }
         } else if (rc.mode == MODE_PROPAGATE && rc.model) {
             for (uint32_t v = 0; v < nv; v++) {
-                rc.model[2 * (vb + v)].lo = (uint64_t)mw[4 * (mo[i] + v)];
-                rc.model[2 * (vb + v)].hi = mw[4 * (mo[i] + v) + 1];
-                rc.model[2 * (vb + v) + 1].lo = (uint64_t)mw[4 * (mo[i] + v) + 2];
-                rc.model[2 * (vb + v) + 1].hi = mw[4 * (mo[i] + v) + 3];
+                rc.model[2 * (vb + v)].lo = (uint64_t)mw[4 * (m0 + v)];
+                rc.model[2 * (vb + v)].hi = mw[4 * (m0 + v) + 1];
+                rc.model[2 * (vb + v) + 1].lo = (uint64_t)mw[4 * (m0 + v) + 2];
+                rc.model[2 * (vb + v) + 1].hi = mw[4 * (m0 + v) + 3];
             }
         }
     }
     return "";
 }
 
-std::string run_jobs(RunCtx& rc, std::vector<Job>& jobs) {
+// full run of one job on the device's shared pool, with capacity retries
+std::string run_job(RunCtx& rc, DevJob& job) {
+    uint32_t depth_cap = DEPTH_CAP0, trail_cap = TRAIL_CAP0;
+    DevicePool* P = pool_for(job.dev);
+    std::vector<int64_t> qs = job.qs;
+    for (int round = 0; round < 5 && !qs.empty(); round++) {
+        DevJob j;
+        j.dev = job.dev;
+        j.wide = job.wide;
+        j.qs = qs;
+        pack(rc, j);
+        std::vector<int64_t> retry;
+        {
+            std::lock_guard<std::mutex> lk(P->mu);
+            std::string e = stage(rc, j, P, depth_cap, trail_cap);
+            if (e.empty()) e = launch(j, P);
+            if (e.empty()) e = fetch(rc, j, P, retry);
+            if (!e.empty()) return e;
+        }
+        qs.swap(retry);
+        depth_cap *= 4;
+        trail_cap *= 8;
+    }
+    for (int64_t q : qs) {  // still out of scratch after the last retry
+        rc.verdict[q] = OOB_ERROR;
+        (*rc.errs)[q] = ERR_DEPTH;
+    }
+    return "";
+}
+
+std::string run_jobs(RunCtx& rc, std::vector<DevJob>& jobs) {
     std::vector<std::string> errs(jobs.size());
     std::vector<std::thread> th;
-    for (size_t j = 0; j < jobs.size(); j++) {
-        th.emplace_back([&, j]() {
-            Job& jb = jobs[j];
-            uint32_t depth_cap = 128, trail_cap = 1024;
-            std::vector<int64_t> qs = jb.qs;
-            for (int round = 0; round < 5 && !qs.empty(); round++) {
-                std::vector<int64_t> retry;
-                std::string e = run_on_device(rc, jb.dev, jb.wide, qs, depth_cap, trail_cap, retry);
-                if (!e.empty()) {
-                    errs[j] = e;
-                    return;
-                }
-                qs.swap(retry);
-                depth_cap *= 4;
-                trail_cap *= 8;
-            }
-            for (int64_t q : qs) {  // still out of scratch after the last retry
-                rc.verdict[q] = OOB_ERROR;
-                (*rc.errs)[q] = ERR_DEPTH;
-            }
-        });
-    }
+    for (size_t j = 0; j < jobs.size(); j++) th.emplace_back([&, j]() { errs[j] = run_job(rc, jobs[j]); });
     for (auto& t : th) t.join();
     for (auto& e : errs)
         if (!e.empty()) return e;
@@ -673,21 +794,31 @@ int visible_devices() {
     return n;
 }
 
-// Common driver of the three batched entry points.
-int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i128* model_in, oob_i128* model_out,
-          int8_t* verdict, int64_t* nodes, int64_t* passes, double* elapsed) {
+// Compile + schedule: fills immediate verdicts and returns the device jobs.
+struct Prepared {
+    std::vector<Compiled> comp;
+    std::vector<int8_t> errs;
+    std::vector<DevJob> jobs;
+    std::string range_msg;
+    oob_options opt{};
+    double compile_s = 0;
+};
+
+int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i128* model_in, int8_t* verdict,
+            int64_t* nodes, int64_t* passes, double* elapsed, Prepared& pr) {
     g_last_error.clear();
     if (!b || b->n_queries < 0) return fail(OOB_E_INVALID, "null or negative batch");
-    oob_options opt{};
-    opt.timeout_s = 30.0;
-    if (opt_in) opt = *opt_in;
+    pr.opt.timeout_s = 30.0;
+    if (opt_in) pr.opt = *opt_in;
+    const oob_options& opt = pr.opt;
     const int64_t n = b->n_queries;
     auto t0 = std::chrono::steady_clock::now();
     for (int64_t q = 0; q < n; q++) {
         std::string why = validate(b, q);
         if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
     }
-    std::vector<Compiled> comp(n);
+    std::vector<Compiled>& comp = pr.comp;
+    comp.assign(n, Compiled{});
     {
         unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         if (n < 2048) nt = 1;
@@ -704,34 +835,33 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
             });
         for (auto& t : th) t.join();
     }
-    double host_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    std::vector<int8_t> errs(n, 0);
-    std::string range_msg;
-    std::vector<int64_t> reg[2];
+    pr.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    pr.errs.assign(n, 0);
+    std::vector<int64_t> reg[3];
     for (int64_t q = 0; q < n; q++) {
         const Compiled& c = comp[q];
         if (c.regime == R_IMMEDIATE) {
             verdict[q] = c.immediate;
             if (nodes) nodes[q] = 0;
             if (passes) passes[q] = 0;
-            if (elapsed) elapsed[q] = std::max(host_s / std::max<int64_t>(n, 1), 1e-9);
+            if (elapsed) elapsed[q] = std::max(pr.compile_s / std::max<int64_t>(n, 1), 1e-9);
         } else if (c.regime == R_RANGE) {
             verdict[q] = OOB_ERROR;
-            if (range_msg.empty()) range_msg = "query " + std::to_string(q) + ": " + c.why;
+            if (pr.range_msg.empty()) pr.range_msg = "query " + std::to_string(q) + ": " + c.why;
         } else {
-            reg[c.regime == R_W128].push_back(q);
+            reg[c.regime - R_W64].push_back(q);
         }
     }
     int ndev = visible_devices();
-    if ((reg[0].size() + reg[1].size()) > 0 && ndev == 0)
+    const size_t n_dev_q = reg[0].size() + reg[1].size() + reg[2].size();
+    if (n_dev_q > 0 && ndev == 0)
         return fail(OOB_E_CUDA, "no CUDA device visible: the OOB engine has no CPU fallback");
     int first = std::max(0, opt.device);
+    if (first >= ndev && n_dev_q > 0)
+        return fail(OOB_E_CUDA, "device ordinal out of range");
     int want = opt.n_gpus > 0 ? opt.n_gpus : ndev - first;
     want = std::max(1, std::min(want, ndev - first));
-    if (first >= ndev && (reg[0].size() + reg[1].size()) > 0)
-        return fail(OOB_E_CUDA, "device ordinal out of range");
-    std::vector<Job> jobs;
-    for (int w = 0; w < 2; w++) {
+    for (int w = 0; w < 3; w++) {
         auto& qs = reg[w];
         if (qs.empty()) continue;
         if (!(opt.flags & OOB_F_NO_SORT)) {
@@ -750,37 +880,48 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
                 return comp[x].cost > comp[y].cost;
             });
         }
-        std::vector<Job> dj(want);
+        std::vector<DevJob> dj(want);
         for (int d = 0; d < want; d++) {
             dj[d].dev = first + d;
             dj[d].wide = w;
-            dj[d].mode = mode;
         }
         for (size_t i = 0; i < qs.size(); i++) dj[(i / 32) % want].qs.push_back(qs[i]);
         for (auto& j : dj)
-            if (!j.qs.empty()) jobs.push_back(std::move(j));
+            if (!j.qs.empty()) pr.jobs.push_back(std::move(j));
     }
+    return OOB_OK;
+}
+
+int finish(Prepared& pr, int64_t n) {
+    for (int64_t q = 0; q < n; q++) {
+        if (pr.errs[q] != ERR_NONE && pr.range_msg.empty())
+            pr.range_msg = "query " + std::to_string(q) + ": search outgrew the device scratch (error " +
+                           std::to_string(pr.errs[q]) + ")";
+    }
+    if (!pr.range_msg.empty()) return fail(OOB_E_RANGE, pr.range_msg);
+    return OOB_OK;
+}
+
+// Common driver of the three batched entry points.
+int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i128* model_in, oob_i128* model_out,
+          int8_t* verdict, int64_t* nodes, int64_t* passes, double* elapsed) {
+    Prepared pr;
+    int rc0 = prepare(b, opt_in, mode, model_in, verdict, nodes, passes, elapsed, pr);
+    if (rc0 != OOB_OK) return rc0;
     RunCtx rc;
     rc.b = b;
-    rc.opt = &opt;
-    rc.comp = &comp;
+    rc.opt = pr.opt;
+    rc.comp = &pr.comp;
     rc.mode = mode;
     rc.verdict = verdict;
     rc.model = mode == MODE_CHECK ? const_cast<oob_i128*>(model_in) : model_out;
     rc.nodes = nodes;
     rc.passes = passes;
     rc.elapsed = elapsed;
-    rc.errs = &errs;
-    // jobs of different regimes on one device run back to back inside its lock
-    std::string e = run_jobs(rc, jobs);
+    rc.errs = &pr.errs;
+    std::string e = run_jobs(rc, pr.jobs);
     if (!e.empty()) return fail(OOB_E_CUDA, e);
-    for (int64_t q = 0; q < n; q++) {
-        if (errs[q] != ERR_NONE && range_msg.empty())
-            range_msg = "query " + std::to_string(q) + ": search outgrew the device scratch (error " +
-                        std::to_string(errs[q]) + ")";
-    }
-    if (!range_msg.empty()) return fail(OOB_E_RANGE, range_msg);
-    return OOB_OK;
+    return finish(pr, b->n_queries);
 }
 
 }  // namespace
@@ -839,6 +980,187 @@ int oob_side_constraint_count(const oob_batch* b, int64_t* counts) {
         for (int d : divs) c += v.op[d] != OOB_NODE_LIT;
         counts[q] = c;
     }
+    return OOB_OK;
+}
+
+// ----- plans: compile + upload once, time kernels on device-resident data -----
+struct oob_plan {
+    const oob_batch* b;
+    Prepared pr;
+    std::vector<std::unique_ptr<DevicePool>> pools;  // one private pool per job
+    RunCtx rc;
+    std::vector<int8_t> verdict;
+    std::vector<int64_t> nodes, passes;
+    std::vector<double> elapsed;
+    std::vector<oob_i128> model;
+    int64_t runs = 0;
+};
+
+int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** out) {
+    if (!out) return fail(OOB_E_INVALID, "null plan pointer");
+    std::unique_ptr<oob_plan> p(new oob_plan());
+    p->b = batch;
+    if (!batch) return fail(OOB_E_INVALID, "null batch");
+    int64_t n = batch->n_queries;
+    p->verdict.assign(n, 0);
+    p->nodes.assign(n, 0);
+    p->passes.assign(n, 0);
+    p->elapsed.assign(n, 0);
+    p->model.assign((size_t)std::max<int64_t>(batch->var_begin[n], 1), oob_i128{0, 0});
+    int rc0 = prepare(batch, opt, MODE_SOLVE, nullptr, p->verdict.data(), p->nodes.data(), p->passes.data(),
+                      p->elapsed.data(), p->pr);
+    if (rc0 != OOB_OK) return rc0;
+    RunCtx& rc = p->rc;
+    rc.b = batch;
+    rc.opt = p->pr.opt;
+    rc.comp = &p->pr.comp;
+    rc.mode = MODE_SOLVE;
+    rc.verdict = p->verdict.data();
+    rc.model = p->model.data();
+    rc.nodes = p->nodes.data();
+    rc.passes = p->passes.data();
+    rc.elapsed = p->elapsed.data();
+    rc.errs = &p->pr.errs;
+    for (auto& j : p->pr.jobs) {
+        pack(rc, j);
+        p->pools.emplace_back(new DevicePool());
+        std::string e = stage(rc, j, p->pools.back().get(), DEPTH_CAP0, TRAIL_CAP0);
+        if (!e.empty()) return fail(OOB_E_CUDA, e);
+    }
+    for (size_t k = 0; k < p->pools.size(); k++) {
+        cudaSetDevice(p->pr.jobs[k].dev);
+        if (cudaStreamSynchronize(p->pools[k]->stream) != cudaSuccess)
+            return fail(OOB_E_CUDA, cudaGetErrorString(cudaGetLastError()));
+    }
+    *out = p.release();
+    return OOB_OK;
+}
+
+int oob_plan_run(oob_plan* p, float* device_ms) {
+    if (!p) return fail(OOB_E_INVALID, "null plan");
+    auto& jobs = p->pr.jobs;
+    // jobs sharing a device run back to back: chain their streams with events
+    for (size_t k = 0; k < jobs.size(); k++) {
+        for (size_t m = 0; m < k; m++) {
+            if (jobs[m].dev == jobs[k].dev) {
+                cudaSetDevice(jobs[k].dev);
+                cudaStreamWaitEvent(p->pools[k]->stream, p->pools[m]->ev1, 0);
+            }
+        }
+        std::string e = launch(jobs[k], p->pools[k].get());
+        if (!e.empty()) return fail(OOB_E_CUDA, e);
+    }
+    float worst = 0;
+    std::vector<int> seen;
+    for (size_t k = 0; k < jobs.size(); k++) {
+        std::string e = kernel_ms(jobs[k], p->pools[k].get());
+        if (!e.empty()) return fail(OOB_E_CUDA, e);
+    }
+    // per device: first job's start to last job's end
+    for (size_t k = 0; k < jobs.size(); k++) {
+        int dev = jobs[k].dev;
+        if (std::find(seen.begin(), seen.end(), dev) != seen.end()) continue;
+        seen.push_back(dev);
+        size_t first = k, last = k;
+        for (size_t m = k; m < jobs.size(); m++)
+            if (jobs[m].dev == dev) last = m;
+        float ms = 0;
+        cudaSetDevice(dev);
+        cudaEventElapsedTime(&ms, p->pools[first]->ev0, p->pools[last]->ev1);
+        worst = std::max(worst, ms);
+    }
+    p->runs++;
+    if (device_ms) *device_ms = worst;
+    return OOB_OK;
+}
+
+int oob_plan_results(oob_plan* p, oob_result* out) {
+    if (!p || !out || !out->verdict) return fail(OOB_E_INVALID, "null argument");
+    if (p->runs == 0) {
+        int rc0 = oob_plan_run(p, nullptr);
+        if (rc0 != OOB_OK) return rc0;
+    }
+    RunCtx& rc = p->rc;
+    std::vector<int64_t> retry_all;
+    for (size_t k = 0; k < p->pr.jobs.size(); k++) {
+        std::vector<int64_t> retry;
+        std::string e = fetch(rc, p->pr.jobs[k], p->pools[k].get(), retry);
+        if (!e.empty()) return fail(OOB_E_CUDA, e);
+        if (!retry.empty()) {
+            DevJob rj;
+            rj.dev = p->pr.jobs[k].dev;
+            rj.wide = p->pr.jobs[k].wide;
+            rj.qs = retry;
+            e = run_job(rc, rj);
+            if (!e.empty()) return fail(OOB_E_CUDA, e);
+        }
+    }
+    int64_t n = p->b->n_queries;
+    for (int64_t q = 0; q < n; q++) {
+        out->verdict[q] = p->verdict[q];
+        if (out->nodes) out->nodes[q] = p->nodes[q];
+        if (out->passes) out->passes[q] = p->passes[q];
+        if (out->elapsed_s) out->elapsed_s[q] = p->elapsed[q];
+        if (out->model && p->verdict[q] == OOB_SAT)
+            for (int64_t v = p->b->var_begin[q]; v < p->b->var_begin[q + 1]; v++) out->model[v] = p->model[v];
+    }
+    return finish(p->pr, n);
+}
+
+int oob_plan_info(const oob_plan* p, int64_t info[8]) {
+    if (!p || !info) return fail(OOB_E_INVALID, "null argument");
+    int64_t nq = 0, rec = 0, res = 0, cls = 0, wide = 0;
+    for (auto& j : p->pr.jobs) {
+        nq += (int64_t)j.qs.size();
+        rec += (int64_t)j.record_bytes();
+        res += (int64_t)j.qs.size() * (1 + 1 + 8 + 8 + 4) + (int64_t)j.out_model_words * 8;
+        cls += j.n_classes;
+        if (j.wide) wide += (int64_t)j.qs.size();
+    }
+    info[0] = nq;
+    info[1] = rec;
+    info[2] = res;
+    info[3] = cls;
+    info[4] = (int64_t)p->pr.jobs.size();
+    info[5] = (int64_t)p->pr.jobs.size();  // kernel launches per run
+    info[6] = wide;
+    info[7] = (int64_t)(p->pr.compile_s * 1e6);
+    return OOB_OK;
+}
+
+void oob_plan_destroy(oob_plan* p) {
+    if (!p) return;
+    for (size_t k = 0; k < p->pools.size(); k++) {
+        cudaSetDevice(p->pr.jobs[k].dev);
+        auto& P = p->pools[k];
+        P->release_all();
+        if (P->ev0) cudaEventDestroy(P->ev0);
+        if (P->ev1) cudaEventDestroy(P->ev1);
+        if (P->stream) cudaStreamDestroy(P->stream);
+    }
+    delete p;
+}
+
+// Host-side self-test of the 256-bit regime arithmetic (tests/test_wide.py
+// compares it with Python integers).  op: 0 + 1 - 2 * 3 / 4 % 5 < 6 >>1
+int oob_selftest_i256(int op, const int64_t* a, const int64_t* b, int64_t* out) {
+    i256 x, y;
+    for (int i = 0; i < 4; i++) {
+        x.w[i] = (uint64_t)a[i];
+        y.w[i] = (uint64_t)b[i];
+    }
+    i256 r(0);
+    switch (op) {
+    case 0: r = x + y; break;
+    case 1: r = x - y; break;
+    case 2: r = x * y; break;
+    case 3: r = x / y; break;
+    case 4: r = x % y; break;
+    case 5: r = i256(x < y ? 1 : 0); break;
+    case 6: r = x >> 1; break;
+    default: return fail(OOB_E_INVALID, "unknown self-test op");
+    }
+    for (int i = 0; i < 4; i++) out[i] = (int64_t)r.w[i];
     return OOB_OK;
 }
 

@@ -17,13 +17,23 @@
 
 #include "engine.cuh"
 #include "format.h"
+#include "wide.cuh"
 
 namespace oob {
 
-template <typename T>
-__device__ __forceinline__ void store_i128(int64_t* out, T v) {
+// model / domain output in the caller's int128 wire format (values are
+// within the declared domains, which the wire format bounds to 128 bits)
+__device__ __forceinline__ void store_i128(int64_t* out, long long v) {
+    out[0] = v;
+    out[1] = v < 0 ? -1 : 0;
+}
+__device__ __forceinline__ void store_i128(int64_t* out, __int128 v) {
     out[0] = (int64_t)(uint64_t)v;
-    out[1] = (int64_t)(v >> 63 >> 1);  // sign / high word (valid for int64 and int128)
+    out[1] = (int64_t)(v >> 64);
+}
+__device__ __forceinline__ void store_i128(int64_t* out, const i256& v) {
+    out[0] = (int64_t)v.w[0];
+    out[1] = (int64_t)v.w[1];
 }
 
 template <typename T>
@@ -121,7 +131,9 @@ static cudaError_t launch_impl(const LaunchArgs& a, int blocks, cudaStream_t s) 
     return cudaGetLastError();
 }
 
+// wide: 0 = int64, 1 = __int128, 2 = 256-bit regime
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, cudaStream_t s) {
+    if (wide == 2) return launch_impl<i256>(a, blocks, s);
     return wide ? launch_impl<__int128>(a, blocks, s) : launch_impl<long long>(a, blocks, s);
 }
 

@@ -13,7 +13,8 @@ REF_SRC = Path("/root/reference/pkg/src")
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
-GOLDEN_SETS = ("corpus_m1048576", "corpus_m64", "crafted", "random_solver", "random_accept")
+GOLDEN_SETS = ("corpus_m1048576", "corpus_m64", "crafted", "random_solver", "random_accept",
+               "synth_c3", "synth_c4", "synth_c5s")
 VCODE = {"unsat": 0, "sat": 1, "timeout": 2}
 
 
