@@ -3,16 +3,26 @@
 //
 // One lane owns one query at a time.  Everything a lane touches repeatedly
 // lives in a per-warp scratch slab laid out [index][32 lanes] (lane-minor), so
-// when the lanes of a warp run structurally identical queries in lockstep --
-// the host sorts queries by structure class -- every scratch access of the
-// warp is one coalesced 128-byte line per 4-byte word, and every code word is
-// a single broadcast load shared by the whole warp.
+// when the lanes of a warp run instances of one structure class in lockstep
+// (kernels.cu schedules whole warps per class and advances all lanes one
+// propagation pass at a time) every scratch access of the warp is one
+// coalesced line per word and every code word is a broadcast load.
 //
 // Exactness: the host proves, per query, a bound B on the magnitude of every
 // intermediate value the reference algorithm can produce (forward intervals at
 // the declared domains, narrowing targets including the 10**18 clamp, exact
-// model evaluation).  Queries with B < 2^62 run on int64, B < 2^125 on
-// __int128; plain two's-complement arithmetic is then exact.
+// model evaluation); the query then runs on int64, __int128 or the 256-bit
+// type of wide.cuh, on which plain two's-complement arithmetic is exact.
+//
+// Constraint skipping (exact): a constraint whose last propagation changed
+// nothing and none of whose variables changed since is skipped -- running it
+// again would change nothing and succeed, because narrowing is a function of
+// the current domains only.  Per lane a "clean" bit per constraint is kept;
+// a domain change of variable v clears the bits of every constraint that
+// mentions v (per-class membership masks).  Pass counts, node counts, the
+// order of every effective narrowing and hence verdicts and models are those
+// of the reference.  A DFS child starts from its parent's clean mask minus
+// the constraints of the split variable.
 #pragma once
 #include <cstdint>
 
@@ -26,14 +36,11 @@ struct Arith {
     __device__ static inline T inf() { return T(1000000000000000000LL); }  // _INF = 10**18 (solver.py:23)
     __device__ static inline T mn(T a, T b) { return a < b ? a : b; }
     __device__ static inline T mx(T a, T b) { return a > b ? a : b; }
-    // C division truncates toward zero: exactly tdiv/tmod (solver.py:94-102).
-    __device__ static inline T tdiv(T a, T b) { return a / b; }
-    __device__ static inline T tmod(T a, T b) { return a % b; }
-    // Python floor division a // b
+    // Python floor division a // b (C division truncates: that is tdiv, solver.py:94)
     __device__ static inline T fdiv(T a, T b) {
         T q = a / b;
         T r = a - q * b;
-        return (r != 0 && ((r < 0) != (b < 0))) ? q - 1 : q;
+        return (r != T(0) && ((r < T(0)) != (b < T(0)))) ? q - T(1) : q;
     }
     // _ceil_div (solver.py:105-106): -((-a) // b)
     __device__ static inline T ceil_div(T a, T b) { return -fdiv(-a, b); }
@@ -61,14 +68,18 @@ struct Lane {
     uint32_t* stamp;
     uint32_t* fr_pick;
     uint32_t* fr_mark;
+    uint32_t* fr_clean;  // 4 words per frame
     uint32_t* tr_var;
     const SlabGeom* g;
-    // current query
-    const uint32_t* cons;  // ncon constraint words
-    const uint32_t* code;  // ncode node words
+    // current query (class-uniform within a warp)
+    const uint32_t* cons;    // ncon constraint words
+    const uint32_t* code;    // ncode node words
+    const uint32_t* member;  // 4 words per variable: constraints mentioning it
     uint32_t nv, ncon, ncode, nlit;
+    bool skip;               // constraint skipping enabled (ncon <= 128)
     // search state
     uint32_t depth, trail_len, seg;
+    uint64_t clean0, clean1; // clean bit per constraint (0..63, 64..127)
     bool dirty;     // a variable changed since the current constraint's top-level eval
     bool changed;   // the current pass changed a domain (_Narrower.changed)
     int err;
@@ -81,6 +92,20 @@ struct Lane {
     __device__ __forceinline__ uint32_t size_of(uint32_t i) const {
         uint32_t w = __ldg(code + i);
         return op_of(w) >= NODE_ADD ? arg_of(w) : 1u;
+    }
+
+    __device__ __forceinline__ bool is_clean(uint32_t k) const {
+        if (!skip) return false;
+        return k < 64 ? ((clean0 >> k) & 1ull) : ((clean1 >> (k - 64)) & 1ull);
+    }
+    __device__ __forceinline__ void set_clean(uint32_t k) {
+        if (k < 64) clean0 |= 1ull << k;
+        else if (k < 128) clean1 |= 1ull << (k - 64);
+    }
+    __device__ __forceinline__ void touch(uint32_t v) {
+        const uint32_t* m = member + 4 * v;
+        clean0 &= ~(((uint64_t)__ldg(m + 1) << 32) | __ldg(m));
+        clean1 &= ~(((uint64_t)__ldg(m + 3) << 32) | __ldg(m + 2));
     }
 
     // ----- _eval_iv over a postfix range (solver.py:112-149) ------------------
@@ -113,20 +138,20 @@ struct Lane {
                     lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
                     hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
                 } else {
-                    T d0 = A::mx(r0, (T)1), d1 = r1;
+                    T d0 = A::mx(r0, T(1)), d1 = r1;
                     if (d0 > d1) return false;
                     if (op == NODE_DIV) {
                         T k0 = l0 / d0, k1 = l0 / d1, k2 = l1 / d0, k3 = l1 / d1;
                         lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
                         hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
                     } else {  // NODE_MOD
-                        T m = d1 - 1;
-                        if (l0 >= 0) {
-                            lo = 0;
+                        T m = d1 - T(1);
+                        if (l0 >= T(0)) {
+                            lo = T(0);
                             hi = A::mn(l1, m);
-                        } else if (l1 <= 0) {
+                        } else if (l1 <= T(0)) {
                             lo = A::mx(l0, -m);
-                            hi = 0;
+                            hi = T(0);
                         } else {
                             lo = A::mx(l0, -m);
                             hi = A::mn(l1, m);
@@ -155,19 +180,19 @@ struct Lane {
         }
         E(env_lo, v) = lo;
         E(env_hi, v) = hi;
+        touch(v);
         return true;
     }
 
     // ----- _Narrower.narrow (solver.py:159-226), explicit pre-order stack ------
     __device__ bool narrow(uint32_t root, T t0, T t1) {
-        constexpr int NS = 40;
+        constexpr int NS = (int)MAX_TREE_DEPTH + 2;
         uint32_t sn[NS];
         T s0[NS], s1[NS];
-        int sp = 0;
+        int sp = 1;
         sn[0] = root;
         s0[0] = t0;
         s1[0] = t1;
-        sp = 1;
         while (sp > 0) {
             --sp;
             uint32_t i = sn[sp];
@@ -209,26 +234,26 @@ struct Lane {
                 sn[sp] = R; s0[sp] = l0 - b; s1[sp] = l1 - a; ++sp;
                 sn[sp] = L; s0[sp] = a + r0; s1[sp] = b + r1; ++sp;
             } else if (op == NODE_MUL) {                               // :191-216
-                if (l0 < 0 || r0 < 0) continue;
-                if (b < 0) return false;
-                T t0n = A::mx(a, (T)0);
+                if (l0 < T(0) || r0 < T(0)) continue;
+                if (b < T(0)) return false;
+                T t0n = A::mx(a, T(0));
                 T lo_l = -A::inf(), hi_l = A::inf(), lo_r = -A::inf(), hi_r = A::inf();
-                if (t0n > 0) {
-                    if (r1 == 0 || l1 == 0) return false;
+                if (t0n > T(0)) {
+                    if (r1 == T(0) || l1 == T(0)) return false;
                     lo_l = A::ceil_div(t0n, r1);
                     lo_r = A::ceil_div(t0n, l1);
                 }
-                if (r0 > 0) hi_l = A::fdiv(b, r0);
-                if (l0 > 0) hi_r = A::fdiv(b, l0);
+                if (r0 > T(0)) hi_l = A::fdiv(b, r0);
+                if (l0 > T(0)) hi_r = A::fdiv(b, l0);
                 sn[sp] = R; s0[sp] = lo_r; s1[sp] = hi_r; ++sp;
                 sn[sp] = L; s0[sp] = lo_l; s1[sp] = hi_l; ++sp;
             } else if (op == NODE_DIV) {                               // :217-223
                 uint32_t rw = __ldg(code + R);
                 if (op_of(rw) == NODE_LIT) {
                     T c = E(lit, arg_of(rw));
-                    if (c >= 1) {
-                        T lo_req = a > 0 ? a * c : a * c - (c - 1);
-                        T hi_req = b >= 0 ? b * c + (c - 1) : b * c;
+                    if (c >= T(1)) {
+                        T lo_req = a > T(0) ? a * c : a * c - (c - T(1));
+                        T hi_req = b >= T(0) ? b * c + (c - T(1)) : b * c;
                         sn[sp] = L; s0[sp] = lo_req; s1[sp] = hi_req; ++sp;
                     }
                 }
@@ -249,24 +274,34 @@ struct Lane {
         T l0 = E(val_lo, lr), l1 = E(val_hi, lr), r0 = E(val_lo, rr), r1 = E(val_hi, rr);
         T a0, a1, b0, b1;
         switch (rel) {
-        case REL_LT: a0 = -A::inf(); a1 = r1 - 1; b0 = l0 + 1; b1 = A::inf(); break;
+        case REL_LT: a0 = -A::inf(); a1 = r1 - T(1); b0 = l0 + T(1); b1 = A::inf(); break;
         case REL_LE: a0 = -A::inf(); a1 = r1; b0 = l0; b1 = A::inf(); break;
         case REL_EQ: a0 = b0 = A::mx(l0, r0); a1 = b1 = A::mn(l1, r1); break;
         case REL_GE: a0 = r0; a1 = A::inf(); b0 = -A::inf(); b1 = l1; break;
-        default:     a0 = r0 + 1; a1 = A::inf(); b0 = -A::inf(); b1 = l1 - 1; break;
+        default:     a0 = r0 + T(1); a1 = A::inf(); b0 = -A::inf(); b1 = l1 - T(1); break;
         }
         return narrow(lr, a0, a1) && narrow(rr, b0, b1);
     }
 
-    // ----- propagate (solver.py:264-280), in place ----------------------------
-    // returns 1 ok, 0 contradiction, -1 deadline, -2 error
-    __device__ int propagate(int64_t& passes, uint64_t deadline) {
+    // one constraint inside a pass, with exact skipping; false = contradiction
+    __device__ __forceinline__ bool pass_constraint(uint32_t k) {
+        if (is_clean(k)) return true;
+        bool before = changed;
+        changed = false;
+        bool ok = propagate_constraint(k);
+        if (ok && !changed && skip) set_clean(k);
+        changed = changed || before;
+        return ok;
+    }
+
+    // ----- propagate (solver.py:264-280), in place (aux kernel) ----------------
+    // returns 1 ok, 0 contradiction, -2 error
+    __device__ int propagate(int64_t& passes) {
         for (int pass = 0; pass < PASS_CAP; ++pass) {
-            if (deadline && global_ns() > deadline) return -1;
             ++passes;
             changed = false;
             for (uint32_t k = 0; k < ncon; ++k) {
-                if (!propagate_constraint(k)) return err ? -2 : 0;
+                if (!pass_constraint(k)) return err ? -2 : 0;
             }
             if (!changed) break;
         }
@@ -303,7 +338,7 @@ struct Lane {
                         else if (op == NODE_SUB) x = a - b;
                         else if (op == NODE_MUL) x = a * b;
                         else {
-                            if (b == 0) return false;
+                            if (b == T(0)) return false;
                             x = op == NODE_DIV ? a / b : a % b;
                         }
                     }
@@ -334,68 +369,63 @@ struct Lane {
         }
     }
 
-    // ----- solve / _search (solver.py:363-416), iterative DFS ------------------
-    // returns verdict; env_lo holds the model on SAT.
-    __device__ int search(int64_t& nodes, int64_t& passes, uint64_t deadline, int64_t budget) {
-        depth = 0;
-        trail_len = 0;
+    // ----- DFS steps of _search (solver.py:397-415) ---------------------------
+    // smallest unresolved domain, ties by declaration order (:397-404); -1: leaf
+    __device__ int pick_var() const {
+        int pick = -1;
+        T best = T(0);
+        for (uint32_t v = 0; v < nv; ++v) {
+            T lo = E(env_lo, v), hi = E(env_hi, v);
+            if (lo < hi) {
+                T size = hi - lo + T(1);
+                if (pick < 0 || size < best) {
+                    pick = (int)v;
+                    best = size;
+                }
+            }
+        }
+        return pick;
+    }
+
+    // push a frame and enter the lower half (:408-413); false on capacity error
+    __device__ bool split(uint32_t pick) {
+        if (depth >= g->depth_cap) {
+            err = ERR_DEPTH;
+            return false;
+        }
+        T lo = E(env_lo, pick), hi = E(env_hi, pick);
+        T mid = (lo + hi) >> 1;  // floor((lo + hi) / 2) in two's complement
+        U(fr_pick, depth) = pick;
+        U(fr_mark, depth) = trail_len;
+        E(fr_mid, depth) = mid;
+        E(fr_hi, depth) = hi;
+        uint32_t* c = fr_clean + (size_t)depth * 4 * 32;
+        c[0] = (uint32_t)clean0;
+        c[32] = (uint32_t)(clean0 >> 32);
+        c[64] = (uint32_t)clean1;
+        c[96] = (uint32_t)(clean1 >> 32);
+        ++depth;
+        ++seg;
+        return set_dom(pick, lo, mid);
+    }
+
+    // after a dead node: enter the next upper half (:414-416).  Returns 1 if a
+    // new node is ready, 0 if the search space is exhausted (Unsat), -1 error.
+    __device__ int backtrack() {
         for (;;) {
-            // ---- visit a node (_search body) ----
-            if ((deadline && global_ns() > deadline) || (budget > 0 && nodes >= budget))
-                return VERDICT_TIMEOUT;                                // :391-392
-            ++nodes;
-            int pr = propagate(passes, deadline);                      // :393
-            if (pr == -1) return VERDICT_TIMEOUT;
-            if (pr == -2) return VERDICT_ERROR;
-            bool dead = (pr == 0);
-            if (!dead) {
-                // smallest unresolved domain, ties by declaration order (:397-404)
-                int pick = -1;
-                T best = 0;
-                for (uint32_t v = 0; v < nv; ++v) {
-                    T lo = E(env_lo, v), hi = E(env_hi, v);
-                    if (lo < hi) {
-                        T size = hi - lo + 1;
-                        if (pick < 0 || size < best) {
-                            pick = (int)v;
-                            best = size;
-                        }
-                    }
-                }
-                if (pick < 0) {                                        // leaf (:405-407)
-                    if (check_point(env_lo)) return VERDICT_SAT;
-                    dead = true;
-                } else {                                               // split (:408-415)
-                    if (depth >= g->depth_cap) {
-                        err = ERR_DEPTH;
-                        return VERDICT_ERROR;
-                    }
-                    T lo = E(env_lo, pick), hi = E(env_hi, pick);
-                    T mid = (lo + hi) >> 1;  // floor((lo+hi)/2) in two's complement
-                    U(fr_pick, depth) = (uint32_t)pick;
-                    U(fr_mark, depth) = trail_len;
-                    E(fr_mid, depth) = mid;
-                    E(fr_hi, depth) = hi;
-                    ++depth;
-                    ++seg;
-                    if (!set_dom((uint32_t)pick, lo, mid)) return VERDICT_ERROR;
-                    continue;
-                }
+            if (depth == 0) return 0;
+            uint32_t f = depth - 1;
+            uint32_t pk = U(fr_pick, f);
+            undo_to(U(fr_mark, f));
+            if (!(pk & 0x80000000u)) {
+                U(fr_pick, f) = pk | 0x80000000u;
+                uint32_t* c = fr_clean + (size_t)f * 4 * 32;
+                clean0 = ((uint64_t)c[32] << 32) | c[0];
+                clean1 = ((uint64_t)c[96] << 32) | c[64];
+                ++seg;
+                return set_dom(pk, E(fr_mid, f) + T(1), E(fr_hi, f)) ? 1 : -1;
             }
-            // ---- backtrack ----
-            for (;;) {
-                if (depth == 0) return VERDICT_UNSAT;
-                uint32_t f = depth - 1;
-                uint32_t pk = U(fr_pick, f);
-                undo_to(U(fr_mark, f));
-                if (!(pk & 0x80000000u)) {
-                    U(fr_pick, f) = pk | 0x80000000u;
-                    ++seg;
-                    if (!set_dom(pk, E(fr_mid, f) + 1, E(fr_hi, f))) return VERDICT_ERROR;
-                    break;
-                }
-                depth = f;
-            }
+            depth = f;
         }
     }
 };

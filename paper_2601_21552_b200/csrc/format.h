@@ -58,22 +58,39 @@ OOB_HD inline uint32_t con_word(uint32_t rel, uint32_t l, uint32_t r) {
 }
 OOB_HD inline uint32_t node_word(uint32_t op, uint32_t arg) { return op | (arg << 3); }
 
-// Per-launch geometry of the scratch slab (host-computed; see format.h).
+// Per-launch geometry of the per-warp scratch slab (host-computed).
 struct SlabGeom {
     uint32_t maxv, maxcode, maxlit, depth_cap, trail_cap;
     // word offsets (in units of T) of each array inside one warp's slab
     uint64_t o_env_lo, o_env_hi, o_val_lo, o_val_hi, o_lit, o_fr_mid, o_fr_hi, o_tr_lo, o_tr_hi;
     // u32-word offsets inside the u32 part of the slab
-    uint64_t o_stamp, o_fr_pick, o_fr_mark, o_tr_var;
+    uint64_t o_stamp, o_fr_pick, o_fr_mark, o_fr_clean, o_tr_var;
     uint64_t slab_T_words, slab_u32_words;  // per-warp sizes
 };
+
+// One structure class: its code block (constraint words, node words, then 4
+// membership words per variable) and its slice [q_begin, q_end) of the
+// class-major schedule.
+struct ClassDesc {
+    uint32_t code_off;
+    uint32_t nv_ncon;
+    uint32_t ncode_nlit;
+    uint32_t q_begin;
+    uint32_t q_end;
+    uint32_t pad[3];
+};
+static_assert(sizeof(ClassDesc) == 32, "ClassDesc is two int4 words");
 
 struct LaunchArgs {
     const QDesc* qdesc;       // per scheduled query
     const uint32_t* code;     // structure words (constraints + nodes), per class
     const int64_t* data;      // per query domains + literals (W/8 words per value)
     uint32_t n;               // scheduled queries
-    uint32_t* next;           // work counter (persistent scheduling)
+    uint32_t* next;           // work counter (aux kernel)
+    const ClassDesc* classes; // per structure class
+    uint32_t n_classes;
+    uint32_t* class_next;     // per class work cursor (starts at q_begin)
+    const uint32_t* warp_class;  // starting class of every warp
     void* slab_T;             // T-typed scratch, n_warps * slab_T_words
     uint32_t* slab_u32;       // u32 scratch, n_warps * slab_u32_words
     SlabGeom g;

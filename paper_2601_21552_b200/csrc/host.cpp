@@ -432,10 +432,23 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
         out.why = "intermediate magnitudes exceed the exact 256-bit regime";
         return out;
     }
-    out.words.reserve(out.ncon + out.ncode);
+    out.words.reserve(out.ncon + out.ncode + 4 * out.nv);
     for (size_t k = 0; k < roots.size(); k++)
         out.words.push_back(con_word(rels[k], roots[k].first, roots[k].second));
     out.words.insert(out.words.end(), em.code.begin(), em.code.end());
+    // membership masks for exact constraint skipping: bit k of variable v is
+    // set iff constraint k mentions v (only used when ncon <= 128)
+    std::vector<uint32_t> member((size_t)out.nv * 4, 0);
+    if (out.ncon <= 128) {
+        for (uint32_t k = 0; k < out.ncon; k++) {
+            for (uint32_t root : {roots[k].first, roots[k].second}) {
+                uint32_t sz = w_op(em.code[root]) >= NODE_ADD ? w_arg(em.code[root]) : 1u;
+                for (uint32_t j = root + 1 - sz; j <= root; j++)
+                    if (w_op(em.code[j]) == NODE_VAR) member[4 * w_arg(em.code[j]) + k / 32] |= 1u << (k % 32);
+            }
+        }
+    }
+    out.words.insert(out.words.end(), member.begin(), member.end());
     return out;
 }
 
@@ -462,12 +475,13 @@ struct DevBuf {
 struct DevicePool {
     std::mutex mu;
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
+    DevBuf classes, class_next, class_init, warp_class;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int sms = 148;
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
-                          &elapsed, &err})
+                          &elapsed, &err, &classes, &class_next, &class_init, &warp_class})
             b->release();
     }
 };
@@ -519,6 +533,7 @@ SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t de
     put(g.o_stamp, g.maxv);
     put(g.o_fr_pick, depth_cap);
     put(g.o_fr_mark, depth_cap);
+    put(g.o_fr_clean, (uint64_t)depth_cap * 4);
     put(g.o_tr_var, trail_cap);
     g.slab_u32_words = o;
     return g;
@@ -543,6 +558,8 @@ struct DevJob {
     std::vector<uint32_t> code;  // class code blocks
     std::vector<int64_t> data;   // per query domains + literal slots
     std::vector<QDesc> qd;
+    std::vector<ClassDesc> cls;
+    std::vector<uint32_t> warp_class;
     uint32_t maxv = 1, maxcode = 1, maxlit = 1;
     uint64_t model_words = 0;
     uint32_t n_classes = 0;
@@ -554,35 +571,61 @@ struct DevJob {
     float last_ms = 0;
 
     uint64_t record_bytes() const {  // algorithmic input bytes of one launch
-        return qd.size() * sizeof(QDesc) + code.size() * 4 + data.size() * 8;
+        return qd.size() * sizeof(QDesc) + cls.size() * sizeof(ClassDesc) + code.size() * 4 + data.size() * 8;
     }
 };
 
 void pack(const RunCtx& rc, DevJob& j) {
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
-    std::unordered_map<std::string, uint32_t> cls;
+    // group the job's queries by structure class, keeping their order within
+    // a class (the lockstep kernel runs each warp on one class)
+    std::unordered_map<std::string, uint32_t> cls_of;
+    std::vector<std::vector<int64_t>> members;
+    std::vector<uint32_t> code_off;
     j.code.clear();
+    for (int64_t q : j.qs) {
+        const Compiled& c = comp[q];
+        std::string key((const char*)c.words.data(), c.words.size() * 4);
+        key.append((const char*)&c.nv, 4);
+        key.append((const char*)&c.ncon, 4);
+        auto it = cls_of.find(key);
+        uint32_t id;
+        if (it == cls_of.end()) {
+            id = (uint32_t)members.size();
+            cls_of.emplace(std::move(key), id);
+            members.emplace_back();
+            code_off.push_back((uint32_t)j.code.size());
+            j.code.insert(j.code.end(), c.words.begin(), c.words.end());
+        } else {
+            id = it->second;
+        }
+        members[id].push_back(q);
+    }
+    j.qs.clear();
+    j.cls.clear();
+    for (size_t id = 0; id < members.size(); id++) {
+        const Compiled& c = comp[members[id][0]];
+        ClassDesc cd{};
+        cd.code_off = code_off[id];
+        cd.nv_ncon = c.nv | (c.ncon << 16);
+        cd.ncode_nlit = c.ncode | (c.nlit << 16);
+        cd.q_begin = (uint32_t)j.qs.size();
+        j.qs.insert(j.qs.end(), members[id].begin(), members[id].end());
+        cd.q_end = (uint32_t)j.qs.size();
+        j.cls.push_back(cd);
+    }
+    j.n_classes = (uint32_t)j.cls.size();
     j.data.clear();
     j.qd.assign(j.qs.size(), QDesc{});
     j.mo.assign(j.qs.size(), 0);
     j.model_words = 0;
+    size_t ci = 0;
     for (size_t i = 0; i < j.qs.size(); i++) {
+        while (i >= j.cls[ci].q_end) ci++;
         const Compiled& c = comp[j.qs[i]];
-        std::string key((const char*)c.words.data(), c.words.size() * 4);
-        key.append((const char*)&c.nv, 4);
-        key.append((const char*)&c.ncon, 4);
-        auto it = cls.find(key);
-        uint32_t off;
-        if (it == cls.end()) {
-            off = (uint32_t)j.code.size();
-            j.code.insert(j.code.end(), c.words.begin(), c.words.end());
-            cls.emplace(std::move(key), off);
-        } else {
-            off = it->second;
-        }
         QDesc& d = j.qd[i];
-        d.code_off = off;
+        d.code_off = j.cls[ci].code_off;
         d.nv_ncon = c.nv | (c.ncon << 16);
         d.ncode_nlit = c.ncode | (c.nlit << 16);
         d.out_q = (uint32_t)i;
@@ -617,9 +660,24 @@ void pack(const RunCtx& rc, DevJob& j) {
         for (i128 l : c.lits) push(l);
         while (j.data.size() & (j.wide == 2 ? 3 : 1)) j.data.push_back(0);
     }
-    j.n_classes = (uint32_t)cls.size();
     if (j.code.empty()) j.code.push_back(0);
-    if (j.data.empty()) j.data.resize(2);
+    if (j.data.empty()) j.data.resize(4);
+    if (j.cls.empty()) j.cls.push_back(ClassDesc{});
+}
+
+// starting class of every warp, in proportion to the class sizes
+void assign_warps(DevJob& j, uint32_t n_warps) {
+    j.warp_class.assign(n_warps, 0);
+    uint64_t total = j.qs.size();
+    if (total == 0) return;
+    uint32_t w = 0;
+    for (uint32_t c = 0; c < j.n_classes && w < n_warps; c++) {
+        uint64_t size = j.cls[c].q_end - j.cls[c].q_begin;
+        uint64_t share = std::max<uint64_t>(1, (size * n_warps + total - 1) / total);
+        share = std::min<uint64_t>(share, (size + 31) / 32);
+        for (uint64_t k = 0; k < share && w < n_warps; k++) j.warp_class[w++] = c;
+    }
+    for (uint32_t c = 0; w < n_warps; w++, c = (c + 1) % std::max(1u, j.n_classes)) j.warp_class[w] = c;
 }
 
 // allocate + upload the packed records of `j` into pool P (caller holds P->mu)
@@ -635,6 +693,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     const uint32_t warps_needed = (n + 31) / 32;
     j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + 3) / 4, (uint32_t)(P->sms * BLOCKS_PER_SM)));
     const uint32_t n_warps = j.blocks * 4;
+    assign_warps(j, n_warps);
     j.g = make_geom(j.maxv, j.maxcode, j.maxlit, depth_cap, trail_cap);
     const size_t tbytes = j.wide == 2 ? 32 : (j.wide ? 16 : 8);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
@@ -650,7 +709,19 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->nodes.ensure((size_t)n * 8));
     CK(P->passes.ensure((size_t)n * 8));
     CK(P->elapsed.ensure((size_t)n * 4));
+    CK(P->classes.ensure(j.cls.size() * sizeof(ClassDesc)));
+    CK(P->class_next.ensure(j.cls.size() * 4));
+    CK(P->class_init.ensure(j.cls.size() * 4));
+    CK(P->warp_class.ensure((size_t)n_warps * 4));
     cudaStream_t s = P->stream;
+    {
+        std::vector<uint32_t> init(j.cls.size());
+        for (size_t c = 0; c < j.cls.size(); c++) init[c] = j.cls[c].q_begin;
+        CK(cudaMemcpyAsync(P->classes.p, j.cls.data(), j.cls.size() * sizeof(ClassDesc), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(P->class_init.p, init.data(), init.size() * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(P->warp_class.p, j.warp_class.data(), (size_t)n_warps * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // host vectors above are temporaries
+    }
     CK(cudaMemcpyAsync(P->qdesc.p, j.qd.data(), j.qd.size() * sizeof(QDesc), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(P->code.p, j.code.data(), j.code.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(P->data.p, j.data.data(), j.data.size() * 8, cudaMemcpyHostToDevice, s));
@@ -661,6 +732,10 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.data = (const int64_t*)P->data.p;
     a.n = n;
     a.next = (uint32_t*)P->next.p;
+    a.classes = (const ClassDesc*)P->classes.p;
+    a.n_classes = j.n_classes;
+    a.class_next = (uint32_t*)P->class_next.p;
+    a.warp_class = (const uint32_t*)P->warp_class.p;
     a.slab_T = P->slabT.p;
     a.slab_u32 = (uint32_t*)P->slabU.p;
     a.g = j.g;
@@ -683,6 +758,7 @@ std::string launch(DevJob& j, DevicePool* P) {
     CK(cudaSetDevice(j.dev));
     cudaStream_t s = P->stream;
     CK(cudaMemsetAsync(P->next.p, 0, 4, s));
+    CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s));
     CK(cudaEventRecord(P->ev0, s));
     CK(launch_solve(j.a, j.wide, (int)j.blocks, s));
     CK(cudaEventRecord(P->ev1, s));

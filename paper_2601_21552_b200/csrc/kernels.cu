@@ -1,16 +1,23 @@
 // kernels.cu -- sm_100a kernels of the OOB-query engine.
 //
-//   oob_solve_kernel<T>   K1: exact solve() emulation (solver.py:363-416) with
-//                         K4 (check_model at every leaf, solver.py:405-407)
-//                         fused in; MODE_PROPAGATE runs one root propagate()
-//                         (solver.py:264-280), MODE_CHECK one check_model()
-//                         (solver.py:319-328).
+//   oob_lockstep_kernel<T>  K1: exact solve() emulation (solver.py:363-416)
+//                           with K4 (check_model at every leaf, :405-407)
+//                           fused in.
+//   oob_aux_kernel<T>       one root propagate() (solver.py:264-280) or one
+//                           check_model() (solver.py:319-328) per query.
 //
-// Scheduling: a persistent grid (a multiple of the 148 SMs) whose warps pull
-// tiles of 32 consecutive scheduled queries from one atomic counter; lane i of
-// a warp owns query tile*32+i.  The host schedule is sorted by structure class
-// so a tile is normally 32 instances of one class and its lanes walk the same
-// code words in lockstep (broadcast loads, coalesced lane-minor scratch).
+// Scheduling of K1 (persistent grid, a multiple of the 148 SMs):
+//   * the host groups queries by STRUCTURE CLASS (identical constraint/term
+//     shapes, different domains and literals) and gives every class a work
+//     queue; each warp is assigned a starting class in proportion to the
+//     class sizes and moves to the next non-empty class when its own drains;
+//   * all 32 lanes of a warp run instances of ONE class and advance together
+//     one propagation pass per step: the constraint loop inside a pass is
+//     uniform, so constraint k's code words are broadcast loads and every
+//     lane-minor scratch access is coalesced;
+//   * between passes each lane independently starts a node, splits, leaves a
+//     model, backtracks or finishes; a finished lane immediately takes the
+//     next query of the warp's class (no lane waits for a whole tile).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -37,12 +44,8 @@ __device__ __forceinline__ void store_i128(int64_t* out, const i256& v) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128) oob_solve_kernel(LaunchArgs a) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ __forceinline__ void bind_scratch(Lane<T>& L, const LaunchArgs& a, uint32_t warp, uint32_t lane) {
     const SlabGeom& g = a.g;
-
-    Lane<T> L;
     T* sT = reinterpret_cast<T*>(a.slab_T) + (size_t)warp * g.slab_T_words + lane;
     uint32_t* sU = a.slab_u32 + (size_t)warp * g.slab_u32_words + lane;
     L.env_lo = sT + g.o_env_lo;
@@ -57,77 +60,228 @@ __global__ void __launch_bounds__(128) oob_solve_kernel(LaunchArgs a) {
     L.stamp = sU + g.o_stamp;
     L.fr_pick = sU + g.o_fr_pick;
     L.fr_mark = sU + g.o_fr_mark;
+    L.fr_clean = sU + g.o_fr_clean;
     L.tr_var = sU + g.o_tr_var;
-    L.g = &g;
+    L.g = &a.g;
     L.seg = 0;
+}
+
+template <typename T>
+__device__ __forceinline__ void bind_class(Lane<T>& L, const LaunchArgs& a, const ClassDesc& c) {
+    L.nv = c.nv_ncon & 0xFFFFu;
+    L.ncon = c.nv_ncon >> 16;
+    L.ncode = c.ncode_nlit & 0xFFFFu;
+    L.nlit = c.ncode_nlit >> 16;
+    L.cons = a.code + c.code_off;
+    L.code = L.cons + L.ncon;
+    L.member = L.code + L.ncode;
+    L.skip = L.ncon <= 128;
+}
+
+// stage a query's domains and literal slots into lane-minor scratch
+template <typename T>
+__device__ __forceinline__ void load_query(Lane<T>& L, const LaunchArgs& a, const QDesc& d) {
+    const T* src = reinterpret_cast<const T*>(a.data + d.data_off);
+    for (uint32_t v = 0; v < L.nv; ++v) {
+        L.E(L.env_lo, v) = src[2 * v];
+        L.E(L.env_hi, v) = src[2 * v + 1];
+        L.U(L.stamp, v) = 0xFFFFFFFFu;
+    }
+    for (uint32_t i = 0; i < L.nlit; ++i) L.E(L.lit, i) = src[2 * L.nv + i];
+    L.err = ERR_NONE;
+    L.depth = 0;
+    L.trail_len = 0;
+    L.clean0 = 0;
+    L.clean1 = 0;
+}
+
+enum : int { PH_IDLE = 0, PH_NODE = 1, PH_PASS = 2, PH_DONE = 3 };
+
+template <typename T>
+__global__ void __launch_bounds__(128) oob_lockstep_kernel(LaunchArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned FULL = 0xffffffffu;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    Lane<T> L;
+    bind_scratch(L, a, warp, lane);
+
+    uint32_t c = a.warp_class[warp];
+    ClassDesc cd = a.classes[c];
+    bind_class(L, a, cd);
+
+    int phase = PH_IDLE;
+    uint32_t qi = 0;
+    int64_t nodes = 0, passes = 0;
+    int pin = 0;
+    int verdict = VERDICT_UNSAT;
+    uint64_t t0 = 0, deadline = 0;
+    uint32_t scanned = 0;  // classes found empty in a row
 
     for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(a.next, 32u);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= a.n) break;
-        const uint32_t qi = base + lane;
-        if (qi >= a.n) continue;
-
-        const QDesc d = a.qdesc[qi];
-        L.nv = d.nv_ncon & 0xFFFFu;
-        L.ncon = d.nv_ncon >> 16;
-        L.ncode = d.ncode_nlit & 0xFFFFu;
-        L.nlit = d.ncode_nlit >> 16;
-        L.cons = a.code + d.code_off;
-        L.code = L.cons + L.ncon;
-        L.err = ERR_NONE;
-        L.depth = 0;
-        L.trail_len = 0;
-
-        // stage this query's domains and literal slots into lane-minor scratch
-        const T* src = reinterpret_cast<const T*>(a.data + d.data_off);
-        for (uint32_t v = 0; v < L.nv; ++v) {
-            L.E(L.env_lo, v) = src[2 * v];
-            L.E(L.env_hi, v) = src[2 * v + 1];
-            L.U(L.stamp, v) = 0xFFFFFFFFu;
+        // ---- refill idle lanes from this warp's class queue ----
+        unsigned idle = __ballot_sync(FULL, phase == PH_IDLE);
+        if (idle) {
+            uint32_t base = 0;
+            int leader = __ffs(idle) - 1;
+            if ((int)lane == leader) base = atomicAdd(a.class_next + c, (uint32_t)__popc(idle));
+            base = __shfl_sync(FULL, base, leader);
+            if (phase == PH_IDLE) {
+                uint32_t q = base + __popc(idle & lt_mask);
+                if (q < cd.q_end) {
+                    qi = q;
+                    const QDesc d = a.qdesc[qi];
+                    load_query(L, a, d);
+                    nodes = passes = 0;
+                    t0 = global_ns();
+                    deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
+                    phase = PH_NODE;
+                }
+            }
         }
-        for (uint32_t i = 0; i < L.nlit; ++i) L.E(L.lit, i) = src[2 * L.nv + i];
+        unsigned active = __ballot_sync(FULL, phase != PH_IDLE);
+        if (!active) {
+            // this class is drained for us: move to the next class with work
+            if (++scanned > a.n_classes) break;
+            c = (c + 1 == a.n_classes) ? 0 : c + 1;
+            cd = a.classes[c];
+            bind_class(L, a, cd);
+            continue;
+        }
+        scanned = 0;
 
-        const uint64_t t_start = global_ns();
-        int64_t nodes = 0, passes = 0;
+        // ---- node start (_search, solver.py:391-393) ----
+        if (phase == PH_NODE) {
+            if ((deadline && global_ns() > deadline) || (a.node_budget > 0 && nodes >= a.node_budget)) {
+                verdict = VERDICT_TIMEOUT;
+                phase = PH_DONE;
+            } else {
+                ++nodes;
+                pin = 0;
+                phase = PH_PASS;
+            }
+        }
+        // ---- pass start (propagate, solver.py:271-274) ----
+        const bool in_pass = (phase == PH_PASS);
+        bool dead = false;
+        if (in_pass) {
+            if (deadline && global_ns() > deadline) {
+                verdict = VERDICT_TIMEOUT;
+                phase = PH_DONE;
+            } else {
+                ++passes;
+                ++pin;
+                L.changed = false;
+            }
+        }
+        const bool run = (phase == PH_PASS);
+        // ---- the pass: class-uniform constraint loop (solver.py:275-277) ----
+        for (uint32_t k = 0; k < L.ncon; ++k) {
+            if (run && !dead) {
+                if (!L.pass_constraint(k)) dead = true;
+            }
+        }
+        // ---- pass end ----
+        if (run) {
+            if (dead) {
+                if (L.err) {
+                    verdict = VERDICT_ERROR;
+                    phase = PH_DONE;
+                } else {
+                    int r = L.backtrack();
+                    if (r <= 0) {
+                        verdict = r == 0 ? VERDICT_UNSAT : VERDICT_ERROR;
+                        phase = PH_DONE;
+                    } else {
+                        phase = PH_NODE;
+                    }
+                }
+            } else if (L.changed && pin < PASS_CAP) {
+                // another pass of this node
+            } else {
+                int pick = L.pick_var();
+                if (pick < 0) {                                        // leaf (:405-407)
+                    if (L.check_point(L.env_lo)) {
+                        verdict = VERDICT_SAT;
+                        phase = PH_DONE;
+                    } else {
+                        int r = L.backtrack();
+                        if (r <= 0) {
+                            verdict = r == 0 ? VERDICT_UNSAT : VERDICT_ERROR;
+                            phase = PH_DONE;
+                        } else {
+                            phase = PH_NODE;
+                        }
+                    }
+                } else if (L.split((uint32_t)pick)) {                 // (:408-413)
+                    phase = PH_NODE;
+                } else {
+                    verdict = VERDICT_ERROR;
+                    phase = PH_DONE;
+                }
+            }
+        }
+        // ---- finished lanes publish their result and go idle ----
+        if (phase == PH_DONE) {
+            const QDesc d = a.qdesc[qi];
+            a.verdict[qi] = (int8_t)verdict;
+            a.err[qi] = (int8_t)L.err;
+            a.nodes[qi] = nodes;
+            a.passes[qi] = passes;
+            a.elapsed[qi] = (float)((double)(global_ns() - t0) * 1e-9);
+            if (verdict == VERDICT_SAT) {
+                int64_t* m = a.model + 2 * d.out_v;
+                for (uint32_t v = 0; v < L.nv; ++v) store_i128(m + 2 * v, L.E(L.env_lo, v));
+            }
+            phase = PH_IDLE;
+        }
+    }
+}
+
+// propagate() / check_model() batches: one query per lane, no search
+template <typename T>
+__global__ void __launch_bounds__(128) oob_aux_kernel(LaunchArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    Lane<T> L;
+    bind_scratch(L, a, warp, lane);
+    for (uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x; qi < a.n; qi += gridDim.x * blockDim.x) {
+        (void)warp;
+        const QDesc d = a.qdesc[qi];
+        ClassDesc cd;
+        cd.code_off = d.code_off;
+        cd.nv_ncon = d.nv_ncon;
+        cd.ncode_nlit = d.ncode_nlit;
+        bind_class(L, a, cd);
+        load_query(L, a, d);
+        int64_t passes = 0;
         int verdict;
-        if (a.mode == MODE_SOLVE) {
-            uint64_t deadline = a.timeout_ns ? t_start + a.timeout_ns : 0;
-            verdict = L.search(nodes, passes, deadline, a.node_budget);
-        } else if (a.mode == MODE_PROPAGATE) {
-            int pr = L.propagate(passes, 0);
+        if (a.mode == MODE_PROPAGATE) {
+            int pr = L.propagate(passes);
             verdict = pr == 1 ? VERDICT_SAT : (pr == 0 ? VERDICT_UNSAT : VERDICT_ERROR);
         } else {
             verdict = L.check_point(L.env_lo) ? VERDICT_SAT : VERDICT_UNSAT;
         }
-        const uint64_t t_end = global_ns();
-
         a.verdict[qi] = (int8_t)verdict;
         a.err[qi] = (int8_t)L.err;
-        if (a.nodes) a.nodes[qi] = nodes;
-        if (a.passes) a.passes[qi] = passes;
-        if (a.elapsed) a.elapsed[qi] = (float)((double)(t_end - t_start) * 1e-9);
-        const bool write_lo = (a.mode == MODE_SOLVE && verdict == VERDICT_SAT);
-        const bool write_both = (a.mode == MODE_PROPAGATE);
-        if (write_lo || write_both) {
-            int64_t* m = a.model + 2 * d.out_v * (write_both ? 2 : 1);
+        a.nodes[qi] = 0;
+        a.passes[qi] = passes;
+        a.elapsed[qi] = 0.f;
+        if (a.mode == MODE_PROPAGATE) {
+            int64_t* m = a.model + 4 * d.out_v;
             for (uint32_t v = 0; v < L.nv; ++v) {
-                if (write_both) {
-                    store_i128(m + 4 * v, L.E(L.env_lo, v));
-                    store_i128(m + 4 * v + 2, L.E(L.env_hi, v));
-                } else {
-                    store_i128(m + 2 * v, L.E(L.env_lo, v));
-                }
+                store_i128(m + 4 * v, L.E(L.env_lo, v));
+                store_i128(m + 4 * v + 2, L.E(L.env_hi, v));
             }
         }
     }
 }
 
-// explicit instantiations + launchers (called from host.cpp)
 template <typename T>
 static cudaError_t launch_impl(const LaunchArgs& a, int blocks, cudaStream_t s) {
-    oob_solve_kernel<T><<<blocks, 128, 0, s>>>(a);
+    if (a.mode == MODE_SOLVE) oob_lockstep_kernel<T><<<blocks, 128, 0, s>>>(a);
+    else oob_aux_kernel<T><<<blocks, 128, 0, s>>>(a);
     return cudaGetLastError();
 }
 
