@@ -118,7 +118,9 @@ typedef struct {
     int32_t n_gpus;       /* devices to shard over; 0 = all visible               */
     int32_t device;       /* first device ordinal                                 */
     int32_t flags;        /* OOB_F_* below                                        */
-    int32_t reserved;
+    int32_t heavy_nodes;  /* DFS nodes after which a query moves to the warp-
+                             cooperative frontier kernel; 0 = default (64),
+                             <0 = never (one lane per query throughout)      */
 } oob_options;
 
 enum {

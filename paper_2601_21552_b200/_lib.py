@@ -30,7 +30,7 @@ class oob_options(ctypes.Structure):
         ("n_gpus", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("flags", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("heavy_nodes", ctypes.c_int32),
     ]
 
 
@@ -117,17 +117,18 @@ def device_count() -> int:
     return int(lib().oob_device_count())
 
 
-def options(timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0):
+def options(timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0):
     o = oob_options()
     o.timeout_s = float(timeout_s)
     o.node_budget = int(node_budget)
     o.n_gpus = int(n_gpus)
     o.device = int(device)
     o.flags = int(flags)
+    o.heavy_nodes = int(heavy_nodes)
     return o
 
 
-def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0):
+def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0):
     """Run oob_solve_batch on a FlatBatch -> dict of numpy result arrays."""
     n = fb.n
     out = {
@@ -141,7 +142,7 @@ def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0):
                    out["nodes"].ctypes.data, out["passes"].ctypes.data,
                    out["elapsed"].ctypes.data)
     cb = fb.as_c()
-    o = options(timeout_s, node_budget, n_gpus, device, flags)
+    o = options(timeout_s, node_budget, n_gpus, device, flags, heavy_nodes)
     rc = lib().oob_solve_batch(ctypes.byref(cb), ctypes.byref(o), ctypes.byref(r))
     out["status"] = rc
     out["error"] = last_error() if rc else ""
@@ -186,10 +187,10 @@ class Plan:
     INFO = ("queries", "record_bytes", "result_bytes", "classes", "jobs",
             "launches_per_run", "wide_queries", "compile_us")
 
-    def __init__(self, fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0):
+    def __init__(self, fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0):
         self.fb = fb                     # keeps the batch arrays alive
         self._cb = fb.as_c()
-        self._opt = options(timeout_s, node_budget, n_gpus, device, flags)
+        self._opt = options(timeout_s, node_budget, n_gpus, device, flags, heavy_nodes)
         self._p = ctypes.c_void_p()
         check(lib().oob_plan_create(ctypes.byref(self._cb), ctypes.byref(self._opt),
                                     ctypes.byref(self._p)), "oob_plan_create")

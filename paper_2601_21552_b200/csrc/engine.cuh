@@ -46,6 +46,21 @@ struct Arith {
     __device__ static inline T ceil_div(T a, T b) { return -fdiv(-a, b); }
 };
 
+// model / domain output in the caller's int128 wire format (values are
+// within the declared domains, which the wire format bounds to 128 bits)
+__device__ __forceinline__ void store_i128(int64_t* out, long long v) {
+    out[0] = v;
+    out[1] = v < 0 ? -1 : 0;
+}
+__device__ __forceinline__ void store_i128(int64_t* out, __int128 v) {
+    out[0] = (int64_t)(uint64_t)v;
+    out[1] = (int64_t)(v >> 64);
+}
+__device__ __forceinline__ void store_i128(int64_t* out, const i256& v) {
+    out[0] = (int64_t)v.w[0];
+    out[1] = (int64_t)v.w[1];
+}
+
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -76,6 +91,7 @@ struct Lane {
     const uint32_t* code;    // ncode node words
     const uint32_t* member;  // 4 words per variable: constraints mentioning it
     uint32_t nv, ncon, ncode, nlit;
+    uint32_t vbase;          // first node of the constraint being processed
     bool skip;               // constraint skipping enabled (ncon <= 128)
     // search state
     uint32_t depth, trail_len, seg;
@@ -85,6 +101,10 @@ struct Lane {
     int err;
 
     __device__ __forceinline__ T& E(T* p, uint32_t i) const { return p[(size_t)i * 32]; }
+    // forward-interval cache of the current constraint's nodes (indexed from
+    // the constraint's first node, so it only needs max-constraint-size slots)
+    __device__ __forceinline__ T& VL(uint32_t j) const { return val_lo[(size_t)(j - vbase) * 32]; }
+    __device__ __forceinline__ T& VH(uint32_t j) const { return val_hi[(size_t)(j - vbase) * 32]; }
     __device__ __forceinline__ uint32_t& U(uint32_t* p, uint32_t i) const { return p[(size_t)i * 32]; }
 
     __device__ __forceinline__ static uint32_t op_of(uint32_t w) { return w & 7u; }
@@ -126,7 +146,7 @@ struct Lane {
             } else {
                 uint32_t R = j - 1;
                 uint32_t L = R - size_of(R);
-                T l0 = E(val_lo, L), l1 = E(val_hi, L), r0 = E(val_lo, R), r1 = E(val_hi, R);
+                T l0 = VL(L), l1 = VH(L), r0 = VL(R), r1 = VH(R);
                 if (op == NODE_ADD) {
                     lo = l0 + r0;
                     hi = l1 + r1;
@@ -159,8 +179,8 @@ struct Lane {
                     }
                 }
             }
-            E(val_lo, j) = lo;
-            E(val_hi, j) = hi;
+            VL(j) = lo;
+            VH(j) = hi;
         }
         return true;
     }
@@ -222,7 +242,7 @@ struct Lane {
             if (dirty) {
                 if (!eval_subtree(L) || !eval_subtree(R)) return false;
             }
-            T l0 = E(val_lo, L), l1 = E(val_hi, L), r0 = E(val_lo, R), r1 = E(val_hi, R);
+            T l0 = VL(L), l1 = VH(L), r0 = VL(R), r1 = VH(R);
             if (sp + 2 > NS) {
                 err = ERR_STACK;
                 return false;
@@ -269,9 +289,10 @@ struct Lane {
         uint32_t rel = w & 7u;
         uint32_t lr = (w >> 3) & 0x3FFFu;
         uint32_t rr = w >> 17;
+        vbase = lr + 1 - size_of(lr);
         dirty = false;
         if (!eval_subtree(lr) || !eval_subtree(rr)) return false;
-        T l0 = E(val_lo, lr), l1 = E(val_hi, lr), r0 = E(val_lo, rr), r1 = E(val_hi, rr);
+        T l0 = VL(lr), l1 = VH(lr), r0 = VL(rr), r1 = VH(rr);
         T a0, a1, b0, b1;
         switch (rel) {
         case REL_LT: a0 = -A::inf(); a1 = r1 - T(1); b0 = l0 + T(1); b1 = A::inf(); break;
@@ -283,9 +304,24 @@ struct Lane {
         return narrow(lr, a0, a1) && narrow(rr, b0, b1);
     }
 
-    // one constraint inside a pass, with exact skipping; false = contradiction
+    // lowest constraint index >= k that is not clean (ncon if none)
+    __device__ __forceinline__ uint32_t next_dirty(uint32_t k) const {
+        if (!skip) return k < ncon ? k : ncon;
+        uint64_t d0 = ~clean0, d1 = ~clean1;
+        if (k < 64) {
+            uint64_t m = d0 & (~0ull << k);
+            if (m) return min((uint32_t)__ffsll((long long)m) - 1, ncon);
+            k = 64;
+        }
+        if (k < 128) {
+            uint64_t m = d1 & (~0ull << (k - 64));
+            if (m) return min(64u + (uint32_t)__ffsll((long long)m) - 1, ncon);
+        }
+        return ncon;
+    }
+
+    // one (dirty) constraint inside a pass; false = contradiction
     __device__ __forceinline__ bool pass_constraint(uint32_t k) {
-        if (is_clean(k)) return true;
         bool before = changed;
         changed = false;
         bool ok = propagate_constraint(k);
@@ -300,7 +336,7 @@ struct Lane {
         for (int pass = 0; pass < PASS_CAP; ++pass) {
             ++passes;
             changed = false;
-            for (uint32_t k = 0; k < ncon; ++k) {
+            for (uint32_t k = next_dirty(0); k < ncon; k = next_dirty(k + 1)) {
                 if (!pass_constraint(k)) return err ? -2 : 0;
             }
             if (!changed) break;
@@ -317,6 +353,7 @@ struct Lane {
             uint32_t rel = w & 7u;
             uint32_t lr = (w >> 3) & 0x3FFFu;
             uint32_t rr = w >> 17;
+            vbase = lr + 1 - size_of(lr);
             T vv[2];
             uint32_t roots[2] = {lr, rr};
             for (int s = 0; s < 2; ++s) {
@@ -333,7 +370,7 @@ struct Lane {
                     } else {
                         uint32_t R = j - 1;
                         uint32_t L = R - size_of(R);
-                        T a = E(val_lo, L), b = E(val_lo, R);
+                        T a = VL(L), b = VL(R);
                         if (op == NODE_ADD) x = a + b;
                         else if (op == NODE_SUB) x = a - b;
                         else if (op == NODE_MUL) x = a * b;
@@ -342,9 +379,9 @@ struct Lane {
                             x = op == NODE_DIV ? a / b : a % b;
                         }
                     }
-                    E(val_lo, j) = x;
+                    VL(j) = x;
                 }
-                vv[s] = E(val_lo, root);
+                vv[s] = VL(root);
             }
             T a = vv[0], b = vv[1];
             bool ok;

@@ -60,7 +60,12 @@ OOB_HD inline uint32_t node_word(uint32_t op, uint32_t arg) { return op | (arg <
 
 // Per-launch geometry of the per-warp scratch slab (host-computed).
 struct SlabGeom {
-    uint32_t maxv, maxcode, maxlit, depth_cap, trail_cap;
+    uint32_t maxv, maxcode, maxlit, depth_cap, trail_cap, maxcsize;
+    // shared-memory residency of the hot per-lane state (env, forward-interval
+    // cache of the current constraint, literal slots): bytes per warp, 0 = the
+    // global slab is used instead; offsets in units of T inside the warp's part
+    uint32_t smem_per_warp;
+    uint64_t o_s_env_lo, o_s_env_hi, o_s_val_lo, o_s_val_hi, o_s_lit;
     // word offsets (in units of T) of each array inside one warp's slab
     uint64_t o_env_lo, o_env_hi, o_val_lo, o_val_hi, o_lit, o_fr_mid, o_fr_hi, o_tr_lo, o_tr_hi;
     // u32-word offsets inside the u32 part of the slab
@@ -94,6 +99,17 @@ struct LaunchArgs {
     void* slab_T;             // T-typed scratch, n_warps * slab_T_words
     uint32_t* slab_u32;       // u32 scratch, n_warps * slab_u32_words
     SlabGeom g;
+    // heavy-query hand-off: the lockstep kernel gives up a query after
+    // heavy_nodes DFS nodes and queues it for the frontier kernel
+    uint32_t heavy_nodes;     // 0 = never hand off
+    uint32_t* heavy_count;
+    uint32_t* heavy_list;
+    uint64_t* heavy_t0;       // start time of each scheduled query (ns)
+    uint32_t* heavy_next;     // frontier kernel work cursor
+    // frontier scratch (one region per frontier warp, see frontier.cuh)
+    void* fr_region;
+    uint64_t fr_region_bytes;
+    uint32_t fr_ecap, fr_ucap, fr_logcap;
     // outputs (indexed by QDesc::out_q / out_v)
     int8_t* verdict;
     int64_t* model;           // int128 words, 2 per var

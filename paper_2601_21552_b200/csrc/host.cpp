@@ -32,7 +32,8 @@
 #include "wide.cuh"
 
 namespace oob {
-cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
+cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s);
+cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm);
 }
 
 using namespace oob;
@@ -156,6 +157,7 @@ struct Compiled {
     int8_t regime = R_IMMEDIATE;
     int8_t immediate = OOB_UNSAT;
     uint32_t nv = 0, ncon = 0, ncode = 0, nlit = 0;
+    uint32_t maxcsize = 1;        // largest constraint (lhs + rhs nodes)
     std::vector<uint32_t> words;  // ncon constraint words + ncode node words
     std::vector<i128> lits;       // per literal slot
     double cost = 0;
@@ -432,6 +434,10 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
         out.why = "intermediate magnitudes exceed the exact 256-bit regime";
         return out;
     }
+    for (auto& rt : roots) {
+        uint32_t lsz = w_op(em.code[rt.first]) >= NODE_ADD ? w_arg(em.code[rt.first]) : 1u;
+        out.maxcsize = std::max(out.maxcsize, rt.second + 1 - (rt.first + 1 - lsz));
+    }
     out.words.reserve(out.ncon + out.ncode + 4 * out.nv);
     for (size_t k = 0; k < roots.size(); k++)
         out.words.push_back(con_word(rels[k], roots[k].first, roots[k].second));
@@ -476,12 +482,14 @@ struct DevicePool {
     std::mutex mu;
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
     DevBuf classes, class_next, class_init, warp_class;
+    DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int sms = 148;
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
-                          &elapsed, &err, &classes, &class_next, &class_init, &warp_class})
+                          &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
+                          &heavy_t0, &fr_region})
             b->release();
     }
 };
@@ -489,11 +497,15 @@ struct DevicePool {
 std::mutex g_pools_mu;
 std::vector<std::unique_ptr<DevicePool>> g_pools;
 
-DevicePool* pool_for(int dev) {
+// one pool (buffers + stream) per (device, regime): the int64, int128 and
+// 256-bit jobs of a batch run concurrently on their own streams, so their
+// tails overlap on the device
+DevicePool* pool_for(int dev, int wide) {
     std::lock_guard<std::mutex> lk(g_pools_mu);
-    if ((int)g_pools.size() <= dev) g_pools.resize(dev + 1);
-    if (!g_pools[dev]) g_pools[dev].reset(new DevicePool());
-    return g_pools[dev].get();
+    size_t slot = (size_t)dev * 3 + (size_t)wide;
+    if (g_pools.size() <= slot) g_pools.resize(slot + 1);
+    if (!g_pools[slot]) g_pools[slot].reset(new DevicePool());
+    return g_pools[slot].get();
 }
 
 struct RunCtx {
@@ -510,8 +522,23 @@ struct RunCtx {
     std::vector<int8_t>* errs;
 };
 
-SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t depth_cap, uint32_t trail_cap) {
+constexpr size_t SMEM_WARP_MAX = 48 * 1024;  // hot state per warp kept on chip up to this
+
+SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t depth_cap, uint32_t trail_cap,
+                   uint32_t maxcsize, size_t tbytes) {
     SlabGeom g{};
+    g.maxcsize = std::max(maxcsize, 1u);
+    {
+        uint64_t o = 0;
+        auto sput = [&](uint64_t& off, uint64_t count) { off = o; o += count * 32; };
+        sput(g.o_s_env_lo, std::max(maxv, 1u));
+        sput(g.o_s_env_hi, std::max(maxv, 1u));
+        sput(g.o_s_val_lo, g.maxcsize);
+        sput(g.o_s_val_hi, g.maxcsize);
+        g.o_s_lit = 0;  // literal slots stay in the L1-cached global slab
+        size_t bytes = (size_t)o * tbytes;
+        g.smem_per_warp = bytes <= SMEM_WARP_MAX ? (uint32_t)bytes : 0;
+    }
     g.maxv = std::max(maxv, 1u);
     g.maxcode = std::max(maxcode, 1u);
     g.maxlit = std::max(maxlit, 1u);
@@ -560,10 +587,10 @@ struct DevJob {
     std::vector<QDesc> qd;
     std::vector<ClassDesc> cls;
     std::vector<uint32_t> warp_class;
-    uint32_t maxv = 1, maxcode = 1, maxlit = 1;
+    uint32_t maxv = 1, maxcode = 1, maxlit = 1, maxcsize = 1;
     uint64_t model_words = 0;
     uint32_t n_classes = 0;
-    uint32_t blocks = 1;
+    uint32_t blocks = 1, fblocks = 0;
     SlabGeom g{};
     LaunchArgs a{};
     size_t out_model_words = 0;
@@ -636,6 +663,7 @@ void pack(const RunCtx& rc, DevJob& j) {
         j.maxv = std::max(j.maxv, c.nv);
         j.maxcode = std::max(j.maxcode, c.ncode);
         j.maxlit = std::max(j.maxlit, c.nlit);
+        j.maxcsize = std::max(j.maxcsize, c.maxcsize);
         int64_t q = j.qs[i];
         int64_t vb = b->var_begin[q];
         auto push = [&](i128 x) {
@@ -681,7 +709,19 @@ void assign_warps(DevJob& j, uint32_t n_warps) {
 }
 
 // allocate + upload the packed records of `j` into pool P (caller holds P->mu)
-std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap, uint32_t trail_cap) {
+constexpr uint32_t FR_ECAP = 2048, FR_UCAP = 4096, FR_LOGCAP = 32768;
+constexpr uint32_t HEAVY_NODES_DEFAULT = 64;
+constexpr uint32_t FR_WARPS_PER_SM = 4;
+
+size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
+    size_t b = (size_t)FR_ECAP * 2 * maxv * tbytes + 2 * (size_t)FR_ECAP * tbytes + (size_t)FR_ECAP * 16 +
+               (size_t)FR_LOGCAP * 16 + (size_t)FR_ECAP * 4 * 2 + (size_t)FR_ECAP * 16 + (size_t)FR_UCAP * 4 +
+               (size_t)FR_ECAP * 4 + (size_t)FR_LOGCAP * 8;
+    return (b + 255) & ~(size_t)255;
+}
+
+std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap, uint32_t trail_cap,
+                  bool heavy = true) {
     CK(cudaSetDevice(j.dev));
     if (!P->stream) {
         CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
@@ -690,12 +730,20 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, j.dev));
     }
     const uint32_t n = (uint32_t)j.qs.size();
+    const size_t tbytes = j.wide == 2 ? 32 : (j.wide ? 16 : 8);
+    j.g = make_geom(j.maxv, j.maxcode, j.maxlit, depth_cap, trail_cap, j.maxcsize, tbytes);
+    int per_sm = BLOCKS_PER_SM;
+    CK(kernel_occupancy(j.wide, rc.mode, (size_t)j.g.smem_per_warp * 4, &per_sm));
+    per_sm = std::max(1, per_sm);
     const uint32_t warps_needed = (n + 31) / 32;
-    j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + 3) / 4, (uint32_t)(P->sms * BLOCKS_PER_SM)));
+    j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + 3) / 4, (uint32_t)(P->sms * per_sm)));
     const uint32_t n_warps = j.blocks * 4;
     assign_warps(j, n_warps);
-    j.g = make_geom(j.maxv, j.maxcode, j.maxlit, depth_cap, trail_cap);
-    const size_t tbytes = j.wide == 2 ? 32 : (j.wide ? 16 : 8);
+    // heavy-query hand-off (solve mode): threshold from the options
+    int64_t hn = rc.opt.heavy_nodes;
+    uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
+    j.fblocks = heavy_nodes ? std::min<uint32_t>(j.blocks, (uint32_t)P->sms * FR_WARPS_PER_SM / 4) : 0;
+    const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
     CK(P->code.ensure(j.code.size() * 4));
@@ -713,6 +761,10 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->class_next.ensure(j.cls.size() * 4));
     CK(P->class_init.ensure(j.cls.size() * 4));
     CK(P->warp_class.ensure((size_t)n_warps * 4));
+    CK(P->heavy_count.ensure(16));
+    CK(P->heavy_list.ensure((size_t)n * 4));
+    CK(P->heavy_t0.ensure((size_t)n * 8));
+    if (j.fblocks) CK(P->fr_region.ensure((size_t)j.fblocks * 4 * fr_bytes));
     cudaStream_t s = P->stream;
     {
         std::vector<uint32_t> init(j.cls.size());
@@ -736,6 +788,16 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.n_classes = j.n_classes;
     a.class_next = (uint32_t*)P->class_next.p;
     a.warp_class = (const uint32_t*)P->warp_class.p;
+    a.heavy_nodes = heavy_nodes;
+    a.heavy_count = (uint32_t*)P->heavy_count.p;
+    a.heavy_next = (uint32_t*)P->heavy_count.p + 1;
+    a.heavy_list = (uint32_t*)P->heavy_list.p;
+    a.heavy_t0 = (uint64_t*)P->heavy_t0.p;
+    a.fr_region = j.fblocks ? P->fr_region.p : nullptr;
+    a.fr_region_bytes = fr_bytes;
+    a.fr_ecap = FR_ECAP;
+    a.fr_ucap = FR_UCAP;
+    a.fr_logcap = FR_LOGCAP;
     a.slab_T = P->slabT.p;
     a.slab_u32 = (uint32_t*)P->slabU.p;
     a.g = j.g;
@@ -759,8 +821,9 @@ std::string launch(DevJob& j, DevicePool* P) {
     cudaStream_t s = P->stream;
     CK(cudaMemsetAsync(P->next.p, 0, 4, s));
     CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(P->heavy_count.p, 0, 8, s));
     CK(cudaEventRecord(P->ev0, s));
-    CK(launch_solve(j.a, j.wide, (int)j.blocks, s));
+    CK(launch_solve(j.a, j.wide, (int)j.blocks, (int)j.fblocks, s));
     CK(cudaEventRecord(P->ev1, s));
     return "";
 }
@@ -824,7 +887,7 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t>& re
 // full run of one job on the device's shared pool, with capacity retries
 std::string run_job(RunCtx& rc, DevJob& job) {
     uint32_t depth_cap = DEPTH_CAP0, trail_cap = TRAIL_CAP0;
-    DevicePool* P = pool_for(job.dev);
+    DevicePool* P = pool_for(job.dev, job.wide);
     std::vector<int64_t> qs = job.qs;
     for (int round = 0; round < 5 && !qs.empty(); round++) {
         DevJob j;
@@ -835,7 +898,7 @@ std::string run_job(RunCtx& rc, DevJob& job) {
         std::vector<int64_t> retry;
         {
             std::lock_guard<std::mutex> lk(P->mu);
-            std::string e = stage(rc, j, P, depth_cap, trail_cap);
+            std::string e = stage(rc, j, P, depth_cap, trail_cap, round == 0);
             if (e.empty()) e = launch(j, P);
             if (e.empty()) e = fetch(rc, j, P, retry);
             if (!e.empty()) return e;
@@ -1115,34 +1178,25 @@ int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** o
 int oob_plan_run(oob_plan* p, float* device_ms) {
     if (!p) return fail(OOB_E_INVALID, "null plan");
     auto& jobs = p->pr.jobs;
-    // jobs sharing a device run back to back: chain their streams with events
+    // all jobs are launched back to back on their own streams and overlap
     for (size_t k = 0; k < jobs.size(); k++) {
-        for (size_t m = 0; m < k; m++) {
-            if (jobs[m].dev == jobs[k].dev) {
-                cudaSetDevice(jobs[k].dev);
-                cudaStreamWaitEvent(p->pools[k]->stream, p->pools[m]->ev1, 0);
-            }
-        }
         std::string e = launch(jobs[k], p->pools[k].get());
         if (!e.empty()) return fail(OOB_E_CUDA, e);
     }
-    float worst = 0;
-    std::vector<int> seen;
     for (size_t k = 0; k < jobs.size(); k++) {
         std::string e = kernel_ms(jobs[k], p->pools[k].get());
         if (!e.empty()) return fail(OOB_E_CUDA, e);
     }
-    // per device: first job's start to last job's end
+    // per device: from its first job's start event to the last end event
+    float worst = 0;
     for (size_t k = 0; k < jobs.size(); k++) {
-        int dev = jobs[k].dev;
-        if (std::find(seen.begin(), seen.end(), dev) != seen.end()) continue;
-        seen.push_back(dev);
-        size_t first = k, last = k;
-        for (size_t m = k; m < jobs.size(); m++)
-            if (jobs[m].dev == dev) last = m;
+        size_t first = k;
+        while (first > 0 && jobs[first - 1].dev == jobs[k].dev) first--;
+        for (size_t m = 0; m < jobs.size(); m++)
+            if (jobs[m].dev == jobs[k].dev && m < first) first = m;
         float ms = 0;
-        cudaSetDevice(dev);
-        cudaEventElapsedTime(&ms, p->pools[first]->ev0, p->pools[last]->ev1);
+        cudaSetDevice(jobs[k].dev);
+        cudaEventElapsedTime(&ms, p->pools[first]->ev0, p->pools[k]->ev1);
         worst = std::max(worst, ms);
     }
     p->runs++;
@@ -1198,7 +1252,9 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
     info[2] = res;
     info[3] = cls;
     info[4] = (int64_t)p->pr.jobs.size();
-    info[5] = (int64_t)p->pr.jobs.size();  // kernel launches per run
+    int64_t launches = 0;
+    for (auto& j : p->pr.jobs) launches += 1 + (j.fblocks ? 1 : 0);
+    info[5] = launches;  // kernel launches per run
     info[6] = wide;
     info[7] = (int64_t)(p->pr.compile_s * 1e6);
     return OOB_OK;

@@ -24,35 +24,34 @@
 
 #include "engine.cuh"
 #include "format.h"
+#include "frontier.cuh"
 #include "wide.cuh"
 
 namespace oob {
 
-// model / domain output in the caller's int128 wire format (values are
-// within the declared domains, which the wire format bounds to 128 bits)
-__device__ __forceinline__ void store_i128(int64_t* out, long long v) {
-    out[0] = v;
-    out[1] = v < 0 ? -1 : 0;
-}
-__device__ __forceinline__ void store_i128(int64_t* out, __int128 v) {
-    out[0] = (int64_t)(uint64_t)v;
-    out[1] = (int64_t)(v >> 64);
-}
-__device__ __forceinline__ void store_i128(int64_t* out, const i256& v) {
-    out[0] = (int64_t)v.w[0];
-    out[1] = (int64_t)v.w[1];
-}
+constexpr int THREADS = 128;  // 4 warps per block
+
+extern __shared__ __align__(16) unsigned char oob_smem[];
 
 template <typename T>
 __device__ __forceinline__ void bind_scratch(Lane<T>& L, const LaunchArgs& a, uint32_t warp, uint32_t lane) {
     const SlabGeom& g = a.g;
     T* sT = reinterpret_cast<T*>(a.slab_T) + (size_t)warp * g.slab_T_words + lane;
     uint32_t* sU = a.slab_u32 + (size_t)warp * g.slab_u32_words + lane;
-    L.env_lo = sT + g.o_env_lo;
-    L.env_hi = sT + g.o_env_hi;
-    L.val_lo = sT + g.o_val_lo;
-    L.val_hi = sT + g.o_val_hi;
-    L.lit = sT + g.o_lit;
+    if (g.smem_per_warp) {  // hot state on chip, lane-minor (conflict-free in lockstep)
+        T* s = reinterpret_cast<T*>(oob_smem + (threadIdx.x >> 5) * g.smem_per_warp) + lane;
+        L.env_lo = s + g.o_s_env_lo;
+        L.env_hi = s + g.o_s_env_hi;
+        L.val_lo = s + g.o_s_val_lo;
+        L.val_hi = s + g.o_s_val_hi;
+        L.lit = sT + g.o_lit;
+    } else {
+        L.env_lo = sT + g.o_env_lo;
+        L.env_hi = sT + g.o_env_hi;
+        L.val_lo = sT + g.o_val_lo;
+        L.val_hi = sT + g.o_val_hi;
+        L.lit = sT + g.o_lit;
+    }
     L.fr_mid = sT + g.o_fr_mid;
     L.fr_hi = sT + g.o_fr_hi;
     L.tr_lo = sT + g.o_tr_lo;
@@ -98,7 +97,7 @@ __device__ __forceinline__ void load_query(Lane<T>& L, const LaunchArgs& a, cons
 enum : int { PH_IDLE = 0, PH_NODE = 1, PH_PASS = 2, PH_DONE = 3 };
 
 template <typename T>
-__global__ void __launch_bounds__(128) oob_lockstep_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned FULL = 0xffffffffu;
@@ -152,6 +151,14 @@ __global__ void __launch_bounds__(128) oob_lockstep_kernel(LaunchArgs a) {
         scanned = 0;
 
         // ---- node start (_search, solver.py:391-393) ----
+        if (phase == PH_NODE && a.heavy_nodes && nodes >= a.heavy_nodes) {
+            // a heavy search: hand it to the warp-cooperative frontier kernel
+            // (which restarts it from the root with 32 lanes)
+            uint32_t slot = atomicAdd(a.heavy_count, 1u);
+            a.heavy_list[slot] = qi;
+            a.heavy_t0[qi] = t0;
+            phase = PH_IDLE;
+        }
         if (phase == PH_NODE) {
             if ((deadline && global_ns() > deadline) || (a.node_budget > 0 && nodes >= a.node_budget)) {
                 verdict = VERDICT_TIMEOUT;
@@ -177,10 +184,14 @@ __global__ void __launch_bounds__(128) oob_lockstep_kernel(LaunchArgs a) {
         }
         const bool run = (phase == PH_PASS);
         // ---- the pass: class-uniform constraint loop (solver.py:275-277) ----
-        for (uint32_t k = 0; k < L.ncon; ++k) {
-            if (run && !dead) {
-                if (!L.pass_constraint(k)) dead = true;
-            }
+        // The warp visits, in order, every constraint that is dirty in at
+        // least one lane (clean ones would change nothing, engine.cuh).
+        for (uint32_t k = 0;;) {
+            uint32_t mine = (run && !dead) ? L.next_dirty(k) : 0xFFFFu;
+            uint32_t kk = __reduce_min_sync(FULL, mine);
+            if (kk >= L.ncon) break;
+            if (mine == kk && !L.pass_constraint(kk)) dead = true;
+            k = kk + 1;
         }
         // ---- pass end ----
         if (run) {
@@ -239,9 +250,37 @@ __global__ void __launch_bounds__(128) oob_lockstep_kernel(LaunchArgs a) {
     }
 }
 
+// heavy queries: one warp per query, lanes expand the leftmost pending nodes
+template <typename T>
+__global__ void __launch_bounds__(THREADS) oob_frontier_kernel(LaunchArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    Lane<T> L;
+    bind_scratch(L, a, warp, lane);
+    FrontierRegion<T> R;
+    R.bind((unsigned char*)a.fr_region + (size_t)warp * a.fr_region_bytes, a.g.maxv, a.fr_ecap, a.fr_ucap,
+           a.fr_logcap);
+    const uint32_t n_heavy = *(volatile uint32_t*)a.heavy_count;
+    for (;;) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(a.heavy_next, 1u);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= n_heavy) break;
+        const uint32_t qi = a.heavy_list[idx];
+        const QDesc d = a.qdesc[qi];
+        ClassDesc cd;
+        cd.code_off = d.code_off;
+        cd.nv_ncon = d.nv_ncon;
+        cd.ncode_nlit = d.ncode_nlit;
+        bind_class(L, a, cd);
+        load_query(L, a, d);
+        frontier_query(L, a, R, qi, lane);
+    }
+}
+
 // propagate() / check_model() batches: one query per lane, no search
 template <typename T>
-__global__ void __launch_bounds__(128) oob_aux_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(THREADS) oob_aux_kernel(LaunchArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     Lane<T> L;
@@ -279,16 +318,50 @@ __global__ void __launch_bounds__(128) oob_aux_kernel(LaunchArgs a) {
 }
 
 template <typename T>
-static cudaError_t launch_impl(const LaunchArgs& a, int blocks, cudaStream_t s) {
-    if (a.mode == MODE_SOLVE) oob_lockstep_kernel<T><<<blocks, 128, 0, s>>>(a);
-    else oob_aux_kernel<T><<<blocks, 128, 0, s>>>(a);
+static const void* kernel_ptr(int mode) {
+    return mode == MODE_SOLVE ? (const void*)oob_lockstep_kernel<T> : (const void*)oob_aux_kernel<T>;
+}
+
+template <typename T>
+static cudaError_t launch_impl(const LaunchArgs& a, int blocks, int fblocks, cudaStream_t s) {
+    size_t smem = (size_t)a.g.smem_per_warp * (THREADS / 32);
+    if (a.mode == MODE_SOLVE) {
+        oob_lockstep_kernel<T><<<blocks, THREADS, smem, s>>>(a);
+        if (a.heavy_nodes && fblocks > 0) {
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            oob_frontier_kernel<T><<<fblocks, THREADS, smem, s>>>(a);
+        }
+    } else {
+        oob_aux_kernel<T><<<blocks, THREADS, smem, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
+template <typename T>
+static cudaError_t occupancy_impl(int mode, size_t smem, int* blocks_per_sm) {
+    const void* fn = kernel_ptr<T>(mode);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (mode == MODE_SOLVE) {
+        e = cudaFuncSetAttribute((const void*)oob_frontier_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, THREADS, smem);
+}
+
 // wide: 0 = int64, 1 = __int128, 2 = 256-bit regime
-cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, cudaStream_t s) {
-    if (wide == 2) return launch_impl<i256>(a, blocks, s);
-    return wide ? launch_impl<__int128>(a, blocks, s) : launch_impl<long long>(a, blocks, s);
+cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s) {
+    if (wide == 2) return launch_impl<i256>(a, blocks, fblocks, s);
+    return wide ? launch_impl<__int128>(a, blocks, fblocks, s) : launch_impl<long long>(a, blocks, fblocks, s);
+}
+
+// resident blocks per SM of the kernel for `mode` with `smem` dynamic bytes per block
+cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm) {
+    if (wide == 2) return occupancy_impl<i256>(mode, smem, blocks_per_sm);
+    return wide ? occupancy_impl<__int128>(mode, smem, blocks_per_sm)
+                : occupancy_impl<long long>(mode, smem, blocks_per_sm);
 }
 
 }  // namespace oob

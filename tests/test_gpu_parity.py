@@ -26,19 +26,22 @@ def _by_timeout(recs):
     return groups
 
 
+# heavy_nodes: 0 = default hand-off, -1 = one lane per query throughout,
+# 1 = every query goes through the warp-cooperative frontier kernel
+@pytest.mark.parametrize("heavy", [0, -1, 1])
 @pytest.mark.parametrize("name", GOLDEN_SETS)
-def test_golden_exact(gpu, name):
+def test_golden_exact(gpu, name, heavy):
     recs = load_golden(name)
     for timeout, idx in _by_timeout(recs).items():
         sub = [recs[i] for i in idx if recs[i]["verdict"] != "timeout"]
         if not sub:
             continue
         fb = flatten(sub)
-        out = solve_flat(fb, timeout)
+        out = solve_flat(fb, timeout, heavy_nodes=heavy)
         for q, r in enumerate(sub):
-            assert int(out["verdict"][q]) == VCODE[r["verdict"]], (name, q, r.get("name"))
-            assert int(out["nodes"][q]) == r["nodes"], (name, q, "nodes")
-            assert int(out["passes"][q]) == r["passes"], (name, q, "passes")
+            assert int(out["verdict"][q]) == VCODE[r["verdict"]], (name, heavy, q, r.get("name"))
+            assert int(out["nodes"][q]) == r["nodes"], (name, heavy, q, "nodes")
+            assert int(out["passes"][q]) == r["passes"], (name, heavy, q, "passes")
             if r["verdict"] == "sat":
                 vb, ve = int(fb.var_begin[q]), int(fb.var_begin[q + 1])
                 model = dict(zip(fb.names(q), words_to_ints(out["model"][vb:ve])))
@@ -69,8 +72,23 @@ def test_all_sets_in_one_batch_sorted_and_unsorted(gpu):
     assert np.array_equal(a["model"], b["model"])
 
 
-def test_node_budget_is_deterministic_timeout(gpu):
+@pytest.mark.parametrize("heavy", [0, -1, 1])
+def test_node_budget_is_deterministic_timeout(gpu, heavy):
     recs = [r for r in load_golden("corpus_m1048576") if r["nodes"] > 50]
     fb = flatten(recs)
-    out = solve_flat(fb, 30.0, node_budget=10)
+    out = solve_flat(fb, 30.0, node_budget=10, heavy_nodes=heavy)
     assert (out["verdict"] == _lib.TIMEOUT).all()
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_frontier_matches_sequential_on_synthetic_streams(gpu, cfg):
+    """20K queries of each stream: the frontier path (every query handed off)
+    and the one-lane path agree on every verdict, model and counter."""
+    from paper_2601_21552_b200 import synth
+    fb = synth.generate(cfg, 20000, names=False)
+    a = solve_flat(fb, 30.0, heavy_nodes=-1)
+    b = solve_flat(fb, 30.0, heavy_nodes=1)
+    c = solve_flat(fb, 30.0)
+    for o in (b, c):
+        for k in ("verdict", "nodes", "passes", "model"):
+            assert np.array_equal(a[k], o[k]), k
