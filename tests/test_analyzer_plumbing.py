@@ -1,0 +1,70 @@
+"""Analyzer integration (paper_2601_21552_b200.analyzer) against the real
+reference front end, in THIS container (the reference is absent on the GPU
+box).  The engine call is stood in by the C oracle so the test runs without a
+GPU: it checks the plumbing -- record/replay, flattening of the reference's
+own objects, verdict objects of the reference's classes -- reproduces the
+reference's diagnostics byte for byte on the whole corpus.  The GPU side of
+the same queries is covered by tests/test_gpu_parity.py (corpus golden sets).
+"""
+from __future__ import annotations
+
+import json
+import sys
+
+import pytest
+
+from conftest import GOLDEN, REF_SRC, reference_available
+
+pytestmark = pytest.mark.skipif(not reference_available(), reason="reference not mounted")
+
+
+@pytest.fixture
+def ref(monkeypatch):
+    sys.path.insert(0, str(REF_SRC))
+    import scuba_mini.analyzer as An
+    from oracle import oracle
+    from paper_2601_21552_b200 import _lib
+
+    def oracle_engine(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0):
+        out = oracle.solve_flat(fb, timeout_s, node_budget)
+        out["status"], out["error"] = 0, ""
+        return out
+
+    monkeypatch.setattr(_lib, "solve_flat", oracle_engine)
+    return An
+
+
+@pytest.mark.parametrize("m", [2**20, 64])
+def test_batched_analysis_reproduces_reference_diagnostics(ref, m):
+    from pathlib import Path
+
+    from scuba_mini.analyzer import AnalyzerConfig, analyze_source
+    from scuba_mini.report import render_json_lines
+
+    from paper_2601_21552_b200.analyzer import analyze_batched
+
+    want = json.loads((GOLDEN / "corpus_diags.json").read_text())
+    corpus = Path("/root/reference/pkg/corpus")
+    total = 0
+    for p in sorted(corpus.glob("*/*.mcu")):
+        rel = f"{p.parent.name}/{p.name}"
+        stats = {}
+        res = analyze_batched(ref, analyze_source, p.read_text(), p.name,
+                              AnalyzerConfig(max_domain=m), stats=stats)
+        assert render_json_lines(res.diagnostics) == want[rel][f"m{m}"]["json"], rel
+        assert stats["queries"] == want[rel][f"m{m}"]["n_queries"]
+        total += stats["queries"]
+    assert total == 110
+
+
+def test_installed_solve_replaces_reference_binding(ref):
+    from scuba_mini.analyzer import analyze_source
+    from scuba_mini.report import render_json_lines
+
+    from paper_2601_21552_b200.analyzer import installed
+
+    want = json.loads((GOLDEN / "corpus_diags.json").read_text())
+    src = (REF_SRC.parent / "corpus/figs/sosfilt_intra.mcu").read_text()
+    with installed(ref):
+        res = analyze_source(src, "sosfilt_intra.mcu")
+    assert render_json_lines(res.diagnostics) == want["figs/sosfilt_intra.mcu"]["m1048576"]["json"]
