@@ -31,6 +31,26 @@
 
 namespace oob {
 
+// C truncating division / remainder (tdiv / tmod, solver.py:94-102); the
+// 128-bit software routine is skipped when both operands fit in 64 bits
+template <typename T>
+__device__ __forceinline__ T cdiv(T a, T b) { return a / b; }
+template <typename T>
+__device__ __forceinline__ T cmod(T a, T b) { return a % b; }
+__device__ __forceinline__ bool fits64(__int128 v) { return v == (__int128)(long long)v; }
+template <>
+__device__ __forceinline__ __int128 cdiv<__int128>(__int128 a, __int128 b) {
+    if (fits64(a) && fits64(b) && !((long long)a == (-9223372036854775807LL - 1) && (long long)b == -1))
+        return (__int128)((long long)a / (long long)b);
+    return a / b;
+}
+template <>
+__device__ __forceinline__ __int128 cmod<__int128>(__int128 a, __int128 b) {
+    if (fits64(a) && fits64(b) && !((long long)a == (-9223372036854775807LL - 1) && (long long)b == -1))
+        return (__int128)((long long)a % (long long)b);
+    return a % b;
+}
+
 template <typename T>
 struct Arith {
     __device__ static inline T inf() { return T(1000000000000000000LL); }  // _INF = 10**18 (solver.py:23)
@@ -38,7 +58,7 @@ struct Arith {
     __device__ static inline T mx(T a, T b) { return a > b ? a : b; }
     // Python floor division a // b (C division truncates: that is tdiv, solver.py:94)
     __device__ static inline T fdiv(T a, T b) {
-        T q = a / b;
+        T q = cdiv(a, b);
         T r = a - q * b;
         return (r != T(0) && ((r < T(0)) != (b < T(0)))) ? q - T(1) : q;
     }
@@ -85,6 +105,10 @@ struct Lane {
     uint32_t* fr_mark;
     uint32_t* fr_clean;  // 4 words per frame
     uint32_t* tr_var;
+    uint32_t* st_n;          // narrowing stack (shared memory when it fits)
+    T* st_0;
+    T* st_1;
+    uint32_t st_cap;
     const SlabGeom* g;
     // current query (class-uniform within a warp)
     const uint32_t* cons;    // ncon constraint words
@@ -161,7 +185,7 @@ struct Lane {
                     T d0 = A::mx(r0, T(1)), d1 = r1;
                     if (d0 > d1) return false;
                     if (op == NODE_DIV) {
-                        T k0 = l0 / d0, k1 = l0 / d1, k2 = l1 / d0, k3 = l1 / d1;
+                        T k0 = cdiv(l0, d0), k1 = cdiv(l0, d1), k2 = cdiv(l1, d0), k3 = cdiv(l1, d1);
                         lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
                         hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
                     } else {  // NODE_MOD
@@ -205,18 +229,18 @@ struct Lane {
     }
 
     // ----- _Narrower.narrow (solver.py:159-226), explicit pre-order stack ------
+    // The pre-order stack lives in lane-minor shared memory (st_*), sized by
+    // the host to the deepest term of the job (st_cap entries).
     __device__ bool narrow(uint32_t root, T t0, T t1) {
-        constexpr int NS = (int)MAX_TREE_DEPTH + 2;
-        uint32_t sn[NS];
-        T s0[NS], s1[NS];
+        const int NS = (int)st_cap;
         int sp = 1;
-        sn[0] = root;
-        s0[0] = t0;
-        s1[0] = t1;
+        U(st_n, 0) = root;
+        E(st_0, 0) = t0;
+        E(st_1, 0) = t1;
         while (sp > 0) {
             --sp;
-            uint32_t i = sn[sp];
-            T a = s0[sp], b = s1[sp];
+            uint32_t i = U(st_n, sp);
+            T a = E(st_0, sp), b = E(st_1, sp);
             if (a > b) return false;                                   // :161-162
             uint32_t w = __ldg(code + i);
             uint32_t op = op_of(w);
@@ -248,11 +272,11 @@ struct Lane {
                 return false;
             }
             if (op == NODE_ADD) {                                      // :181-185
-                sn[sp] = R; s0[sp] = a - l1; s1[sp] = b - l0; ++sp;
-                sn[sp] = L; s0[sp] = a - r1; s1[sp] = b - r0; ++sp;
+                U(st_n, sp) = R; E(st_0, sp) = a - l1; E(st_1, sp) = b - l0; ++sp;
+                U(st_n, sp) = L; E(st_0, sp) = a - r1; E(st_1, sp) = b - r0; ++sp;
             } else if (op == NODE_SUB) {                               // :186-190
-                sn[sp] = R; s0[sp] = l0 - b; s1[sp] = l1 - a; ++sp;
-                sn[sp] = L; s0[sp] = a + r0; s1[sp] = b + r1; ++sp;
+                U(st_n, sp) = R; E(st_0, sp) = l0 - b; E(st_1, sp) = l1 - a; ++sp;
+                U(st_n, sp) = L; E(st_0, sp) = a + r0; E(st_1, sp) = b + r1; ++sp;
             } else if (op == NODE_MUL) {                               // :191-216
                 if (l0 < T(0) || r0 < T(0)) continue;
                 if (b < T(0)) return false;
@@ -265,8 +289,8 @@ struct Lane {
                 }
                 if (r0 > T(0)) hi_l = A::fdiv(b, r0);
                 if (l0 > T(0)) hi_r = A::fdiv(b, l0);
-                sn[sp] = R; s0[sp] = lo_r; s1[sp] = hi_r; ++sp;
-                sn[sp] = L; s0[sp] = lo_l; s1[sp] = hi_l; ++sp;
+                U(st_n, sp) = R; E(st_0, sp) = lo_r; E(st_1, sp) = hi_r; ++sp;
+                U(st_n, sp) = L; E(st_0, sp) = lo_l; E(st_1, sp) = hi_l; ++sp;
             } else if (op == NODE_DIV) {                               // :217-223
                 uint32_t rw = __ldg(code + R);
                 if (op_of(rw) == NODE_LIT) {
@@ -274,7 +298,7 @@ struct Lane {
                     if (c >= T(1)) {
                         T lo_req = a > T(0) ? a * c : a * c - (c - T(1));
                         T hi_req = b >= T(0) ? b * c + (c - T(1)) : b * c;
-                        sn[sp] = L; s0[sp] = lo_req; s1[sp] = hi_req; ++sp;
+                        U(st_n, sp) = L; E(st_0, sp) = lo_req; E(st_1, sp) = hi_req; ++sp;
                     }
                 }
             }
@@ -283,12 +307,64 @@ struct Lane {
         return true;
     }
 
+    // ----- leaf fast path: both sides are a variable or a literal ---------------
+    // (most analyzer constraints: geometry ranges, launch equations, bindings,
+    // asserts).  Same semantics as the general path below, without the
+    // forward-interval cache or the narrowing stack.
+    __device__ __forceinline__ bool narrow_leaf(uint32_t w, T a, T b) {
+        if (a > b) return false;                                       // :161-162
+        if (op_of(w) == NODE_LIT) {                                    // :163-164
+            T v = E(lit, arg_of(w));
+            return a <= v && v <= b;
+        }
+        uint32_t v = arg_of(w);                                        // :165-173
+        T lo = E(env_lo, v), hi = E(env_hi, v);
+        T nlo = A::mx(lo, a), nhi = A::mn(hi, b);
+        if (nlo > nhi) return false;
+        if (nlo != lo || nhi != hi) {
+            if (!set_dom(v, nlo, nhi)) return false;
+            changed = true;
+        }
+        return true;
+    }
+
+    __device__ __forceinline__ bool propagate_leaves(uint32_t rel, uint32_t lw, uint32_t rw) {
+        T l0, l1, r0, r1;
+        if (op_of(lw) == NODE_LIT) {
+            l0 = l1 = E(lit, arg_of(lw));
+        } else {
+            l0 = E(env_lo, arg_of(lw));
+            l1 = E(env_hi, arg_of(lw));
+            if (l0 > l1) return false;
+        }
+        if (op_of(rw) == NODE_LIT) {
+            r0 = r1 = E(lit, arg_of(rw));
+        } else {
+            r0 = E(env_lo, arg_of(rw));
+            r1 = E(env_hi, arg_of(rw));
+            if (r0 > r1) return false;
+        }
+        T a0, a1, b0, b1;
+        switch (rel) {
+        case REL_LT: a0 = -A::inf(); a1 = r1 - T(1); b0 = l0 + T(1); b1 = A::inf(); break;
+        case REL_LE: a0 = -A::inf(); a1 = r1; b0 = l0; b1 = A::inf(); break;
+        case REL_EQ: a0 = b0 = A::mx(l0, r0); a1 = b1 = A::mn(l1, r1); break;
+        case REL_GE: a0 = r0; a1 = A::inf(); b0 = -A::inf(); b1 = l1; break;
+        default:     a0 = r0 + T(1); a1 = A::inf(); b0 = -A::inf(); b1 = l1 - T(1); break;
+        }
+        return narrow_leaf(lw, a0, a1) && narrow_leaf(rw, b0, b1);
+    }
+
     // ----- _propagate_constraint (solver.py:229-261) ---------------------------
     __device__ bool propagate_constraint(uint32_t k) {
         uint32_t w = __ldg(cons + k);
         uint32_t rel = w & 7u;
         uint32_t lr = (w >> 3) & 0x3FFFu;
         uint32_t rr = w >> 17;
+        {
+            uint32_t lw = __ldg(code + lr), rw = __ldg(code + rr);
+            if (op_of(lw) < NODE_ADD && op_of(rw) < NODE_ADD) return propagate_leaves(rel, lw, rw);
+        }
         vbase = lr + 1 - size_of(lr);
         dirty = false;
         if (!eval_subtree(lr) || !eval_subtree(rr)) return false;
@@ -376,7 +452,7 @@ struct Lane {
                         else if (op == NODE_MUL) x = a * b;
                         else {
                             if (b == T(0)) return false;
-                            x = op == NODE_DIV ? a / b : a % b;
+                            x = op == NODE_DIV ? cdiv(a, b) : cmod(a, b);
                         }
                     }
                     VL(j) = x;

@@ -65,11 +65,13 @@ struct SlabGeom {
     // cache of the current constraint, literal slots): bytes per warp, 0 = the
     // global slab is used instead; offsets in units of T inside the warp's part
     uint32_t smem_per_warp;
-    uint64_t o_s_env_lo, o_s_env_hi, o_s_val_lo, o_s_val_hi, o_s_lit;
+    uint64_t o_s_env_lo, o_s_env_hi, o_s_val_lo, o_s_val_hi, o_s_lit, o_s_st0, o_s_st1;
+    uint64_t o_s_stn_bytes;  // byte offset of the u32 stack-node slots in the warp's part
+    uint32_t st_cap;         // narrowing stack entries (deepest term + 2)
     // word offsets (in units of T) of each array inside one warp's slab
-    uint64_t o_env_lo, o_env_hi, o_val_lo, o_val_hi, o_lit, o_fr_mid, o_fr_hi, o_tr_lo, o_tr_hi;
+    uint64_t o_env_lo, o_env_hi, o_val_lo, o_val_hi, o_lit, o_fr_mid, o_fr_hi, o_tr_lo, o_tr_hi, o_st0, o_st1;
     // u32-word offsets inside the u32 part of the slab
-    uint64_t o_stamp, o_fr_pick, o_fr_mark, o_fr_clean, o_tr_var;
+    uint64_t o_stamp, o_fr_pick, o_fr_mark, o_fr_clean, o_tr_var, o_stn;
     uint64_t slab_T_words, slab_u32_words;  // per-warp sizes
 };
 

@@ -167,8 +167,9 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
             bool run = prop;
             for (uint32_t kc = 0;;) {
                 uint32_t mine = (run && !dead) ? L.next_dirty(kc) : 0xFFFFu;
+                if (mine >= L.ncon) mine = 0xFFFFu;
                 uint32_t kk = __reduce_min_sync(FULL, mine);
-                if (kk >= L.ncon) break;
+                if (kk == 0xFFFFu) break;
                 if (mine == kk && !L.pass_constraint(kk)) dead = true;
                 kc = kk + 1;
             }

@@ -158,6 +158,7 @@ struct Compiled {
     int8_t immediate = OOB_UNSAT;
     uint32_t nv = 0, ncon = 0, ncode = 0, nlit = 0;
     uint32_t maxcsize = 1;        // largest constraint (lhs + rhs nodes)
+    uint32_t maxdepth = 1;        // deepest term
     std::vector<uint32_t> words;  // ncon constraint words + ncode node words
     std::vector<i128> lits;       // per literal slot
     double cost = 0;
@@ -434,6 +435,7 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
         out.why = "intermediate magnitudes exceed the exact 256-bit regime";
         return out;
     }
+    out.maxdepth = (uint32_t)std::max(1, em.max_depth);
     for (auto& rt : roots) {
         uint32_t lsz = w_op(em.code[rt.first]) >= NODE_ADD ? w_arg(em.code[rt.first]) : 1u;
         out.maxcsize = std::max(out.maxcsize, rt.second + 1 - (rt.first + 1 - lsz));
@@ -525,9 +527,10 @@ struct RunCtx {
 constexpr size_t SMEM_WARP_MAX = 48 * 1024;  // hot state per warp kept on chip up to this
 
 SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t depth_cap, uint32_t trail_cap,
-                   uint32_t maxcsize, size_t tbytes) {
+                   uint32_t maxcsize, uint32_t maxdepth, size_t tbytes) {
     SlabGeom g{};
     g.maxcsize = std::max(maxcsize, 1u);
+    g.st_cap = maxdepth + 2;
     {
         uint64_t o = 0;
         auto sput = [&](uint64_t& off, uint64_t count) { off = o; o += count * 32; };
@@ -535,8 +538,12 @@ SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t de
         sput(g.o_s_env_hi, std::max(maxv, 1u));
         sput(g.o_s_val_lo, g.maxcsize);
         sput(g.o_s_val_hi, g.maxcsize);
+        sput(g.o_s_st0, g.st_cap);
+        sput(g.o_s_st1, g.st_cap);
         g.o_s_lit = 0;  // literal slots stay in the L1-cached global slab
-        size_t bytes = (size_t)o * tbytes;
+        g.o_s_stn_bytes = (size_t)o * tbytes;
+        size_t bytes = g.o_s_stn_bytes + (size_t)g.st_cap * 32 * 4;
+        bytes = (bytes + 15) & ~(size_t)15;
         g.smem_per_warp = bytes <= SMEM_WARP_MAX ? (uint32_t)bytes : 0;
     }
     g.maxv = std::max(maxv, 1u);
@@ -548,13 +555,15 @@ SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t de
     auto put = [&](uint64_t& off, uint64_t count) { off = o; o += count * 32; };
     put(g.o_env_lo, g.maxv);
     put(g.o_env_hi, g.maxv);
-    put(g.o_val_lo, g.maxcode);
-    put(g.o_val_hi, g.maxcode);
+    put(g.o_val_lo, g.maxcsize);
+    put(g.o_val_hi, g.maxcsize);
     put(g.o_lit, g.maxlit);
     put(g.o_fr_mid, depth_cap);
     put(g.o_fr_hi, depth_cap);
     put(g.o_tr_lo, trail_cap);
     put(g.o_tr_hi, trail_cap);
+    put(g.o_st0, g.st_cap);
+    put(g.o_st1, g.st_cap);
     g.slab_T_words = o;
     o = 0;
     put(g.o_stamp, g.maxv);
@@ -562,6 +571,7 @@ SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t de
     put(g.o_fr_mark, depth_cap);
     put(g.o_fr_clean, (uint64_t)depth_cap * 4);
     put(g.o_tr_var, trail_cap);
+    put(g.o_stn, g.st_cap);
     g.slab_u32_words = o;
     return g;
 }
@@ -574,7 +584,8 @@ SlabGeom make_geom(uint32_t maxv, uint32_t maxcode, uint32_t maxlit, uint32_t de
     } while (0)
 
 constexpr uint32_t DEPTH_CAP0 = 128, TRAIL_CAP0 = 1024;
-constexpr int BLOCKS_PER_SM = 8;  // 8 x 128 threads = 32 warps per SM
+constexpr int BLOCKS_PER_SM = 16;
+constexpr uint32_t WARPS_PER_BLOCK = 2;  // kernels.cu THREADS / 32
 
 // One device's share of one regime: packed device records + launch geometry.
 struct DevJob {
@@ -587,7 +598,7 @@ struct DevJob {
     std::vector<QDesc> qd;
     std::vector<ClassDesc> cls;
     std::vector<uint32_t> warp_class;
-    uint32_t maxv = 1, maxcode = 1, maxlit = 1, maxcsize = 1;
+    uint32_t maxv = 1, maxcode = 1, maxlit = 1, maxcsize = 1, maxdepth = 1;
     uint64_t model_words = 0;
     uint32_t n_classes = 0;
     uint32_t blocks = 1, fblocks = 0;
@@ -664,6 +675,7 @@ void pack(const RunCtx& rc, DevJob& j) {
         j.maxcode = std::max(j.maxcode, c.ncode);
         j.maxlit = std::max(j.maxlit, c.nlit);
         j.maxcsize = std::max(j.maxcsize, c.maxcsize);
+        j.maxdepth = std::max(j.maxdepth, c.maxdepth);
         int64_t q = j.qs[i];
         int64_t vb = b->var_begin[q];
         auto push = [&](i128 x) {
@@ -710,7 +722,7 @@ void assign_warps(DevJob& j, uint32_t n_warps) {
 
 // allocate + upload the packed records of `j` into pool P (caller holds P->mu)
 constexpr uint32_t FR_ECAP = 2048, FR_UCAP = 4096, FR_LOGCAP = 32768;
-constexpr uint32_t HEAVY_NODES_DEFAULT = 64;
+constexpr uint32_t HEAVY_NODES_DEFAULT = 32;
 constexpr uint32_t FR_WARPS_PER_SM = 4;
 
 size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
@@ -731,18 +743,19 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     }
     const uint32_t n = (uint32_t)j.qs.size();
     const size_t tbytes = j.wide == 2 ? 32 : (j.wide ? 16 : 8);
-    j.g = make_geom(j.maxv, j.maxcode, j.maxlit, depth_cap, trail_cap, j.maxcsize, tbytes);
+    j.g = make_geom(j.maxv, j.maxcode, j.maxlit, depth_cap, trail_cap, j.maxcsize, j.maxdepth, tbytes);
     int per_sm = BLOCKS_PER_SM;
-    CK(kernel_occupancy(j.wide, rc.mode, (size_t)j.g.smem_per_warp * 4, &per_sm));
+    CK(kernel_occupancy(j.wide, rc.mode, (size_t)j.g.smem_per_warp * WARPS_PER_BLOCK, &per_sm));
     per_sm = std::max(1, per_sm);
     const uint32_t warps_needed = (n + 31) / 32;
-    j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + 3) / 4, (uint32_t)(P->sms * per_sm)));
-    const uint32_t n_warps = j.blocks * 4;
+    j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                                (uint32_t)(P->sms * per_sm)));
+    const uint32_t n_warps = j.blocks * WARPS_PER_BLOCK;
     assign_warps(j, n_warps);
     // heavy-query hand-off (solve mode): threshold from the options
     int64_t hn = rc.opt.heavy_nodes;
     uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
-    j.fblocks = heavy_nodes ? std::min<uint32_t>(j.blocks, (uint32_t)P->sms * FR_WARPS_PER_SM / 4) : 0;
+    j.fblocks = heavy_nodes ? std::min<uint32_t>(j.blocks, (uint32_t)P->sms * FR_WARPS_PER_SM / WARPS_PER_BLOCK) : 0;
     const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
@@ -764,7 +777,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->heavy_count.ensure(16));
     CK(P->heavy_list.ensure((size_t)n * 4));
     CK(P->heavy_t0.ensure((size_t)n * 8));
-    if (j.fblocks) CK(P->fr_region.ensure((size_t)j.fblocks * 4 * fr_bytes));
+    if (j.fblocks) CK(P->fr_region.ensure((size_t)j.fblocks * WARPS_PER_BLOCK * fr_bytes));
     cudaStream_t s = P->stream;
     {
         std::vector<uint32_t> init(j.cls.size());

@@ -29,7 +29,7 @@
 
 namespace oob {
 
-constexpr int THREADS = 128;  // 4 warps per block
+constexpr int THREADS = 64;  // 2 warps per block: fine-grained shared-memory packing
 
 extern __shared__ __align__(16) unsigned char oob_smem[];
 
@@ -45,13 +45,20 @@ __device__ __forceinline__ void bind_scratch(Lane<T>& L, const LaunchArgs& a, ui
         L.val_lo = s + g.o_s_val_lo;
         L.val_hi = s + g.o_s_val_hi;
         L.lit = sT + g.o_lit;
+        L.st_0 = s + g.o_s_st0;
+        L.st_1 = s + g.o_s_st1;
+        L.st_n = reinterpret_cast<uint32_t*>(oob_smem + (threadIdx.x >> 5) * g.smem_per_warp + g.o_s_stn_bytes) + lane;
     } else {
         L.env_lo = sT + g.o_env_lo;
         L.env_hi = sT + g.o_env_hi;
         L.val_lo = sT + g.o_val_lo;
         L.val_hi = sT + g.o_val_hi;
         L.lit = sT + g.o_lit;
+        L.st_0 = sT + g.o_st0;
+        L.st_1 = sT + g.o_st1;
+        L.st_n = sU + g.o_stn;
     }
+    L.st_cap = g.st_cap;
     L.fr_mid = sT + g.o_fr_mid;
     L.fr_hi = sT + g.o_fr_hi;
     L.tr_lo = sT + g.o_tr_lo;
@@ -106,9 +113,10 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
     Lane<T> L;
     bind_scratch(L, a, warp, lane);
 
-    uint32_t c = a.warp_class[warp];
+    uint32_t c = a.warp_class[warp];  // the warp's current class queue (warp-uniform)
     ClassDesc cd = a.classes[c];
     bind_class(L, a, cd);
+    bool drained = false;             // every class queue is empty
 
     int phase = PH_IDLE;
     uint32_t qi = 0;
@@ -116,12 +124,13 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
     int pin = 0;
     int verdict = VERDICT_UNSAT;
     uint64_t t0 = 0, deadline = 0;
-    uint32_t scanned = 0;  // classes found empty in a row
 
     for (;;) {
-        // ---- refill idle lanes from this warp's class queue ----
+        // ---- refill idle lanes from the warp's class queue; when it runs dry
+        // move the queue on to the next class with work (lanes still busy keep
+        // their own class: every lane carries its own code pointers) ----
         unsigned idle = __ballot_sync(FULL, phase == PH_IDLE);
-        if (idle) {
+        while (idle && !drained) {
             uint32_t base = 0;
             int leader = __ffs(idle) - 1;
             if ((int)lane == leader) base = atomicAdd(a.class_next + c, (uint32_t)__popc(idle));
@@ -130,6 +139,7 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
                 uint32_t q = base + __popc(idle & lt_mask);
                 if (q < cd.q_end) {
                     qi = q;
+                    bind_class(L, a, cd);
                     const QDesc d = a.qdesc[qi];
                     load_query(L, a, d);
                     nodes = passes = 0;
@@ -138,17 +148,22 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
                     phase = PH_NODE;
                 }
             }
+            idle = __ballot_sync(FULL, phase == PH_IDLE);
+            if (idle) {  // class c is exhausted: find the next class with work
+                bool found = false;
+                for (uint32_t s = 1; s <= a.n_classes && !found; ++s) {
+                    uint32_t c2 = (c + s) % a.n_classes;
+                    if (*(volatile uint32_t*)(a.class_next + c2) < a.classes[c2].q_end) {
+                        c = c2;
+                        found = true;
+                    }
+                }
+                if (found) cd = a.classes[c];
+                else drained = true;
+            }
         }
         unsigned active = __ballot_sync(FULL, phase != PH_IDLE);
-        if (!active) {
-            // this class is drained for us: move to the next class with work
-            if (++scanned > a.n_classes) break;
-            c = (c + 1 == a.n_classes) ? 0 : c + 1;
-            cd = a.classes[c];
-            bind_class(L, a, cd);
-            continue;
-        }
-        scanned = 0;
+        if (!active) break;
 
         // ---- node start (_search, solver.py:391-393) ----
         if (phase == PH_NODE && a.heavy_nodes && nodes >= a.heavy_nodes) {
@@ -188,8 +203,9 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
         // least one lane (clean ones would change nothing, engine.cuh).
         for (uint32_t k = 0;;) {
             uint32_t mine = (run && !dead) ? L.next_dirty(k) : 0xFFFFu;
+            if (mine >= L.ncon) mine = 0xFFFFu;  // lanes may be on different classes
             uint32_t kk = __reduce_min_sync(FULL, mine);
-            if (kk >= L.ncon) break;
+            if (kk == 0xFFFFu) break;
             if (mine == kk && !L.pass_constraint(kk)) dead = true;
             k = kk + 1;
         }

@@ -68,7 +68,16 @@ W_HD i256 operator-(const i256& a, const i256& b) {
     }
     return r;
 }
+// true iff the value is a sign-extended int64 (the common case once domains
+// have been narrowed): the hot operations below take a 64-bit fast path
+W_HD bool fits64(const i256& a) {
+    uint64_t s = (uint64_t)((int64_t)a.w[0] >> 63);
+    return a.w[1] == s && a.w[2] == s && a.w[3] == s;
+}
+W_HD i256 from64(long long v) { return i256(v); }
+
 W_HD i256 operator*(const i256& a, const i256& b) {  // low 256 bits (two's complement)
+    if (fits64(a) && fits64(b)) return i256::from128((__int128)(long long)a.w[0] * (long long)b.w[0]);
     uint64_t r[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 4; i++) {
@@ -149,12 +158,20 @@ W_HD void udivmod(const i256& n, const i256& d, i256& q, i256& r) {
 
 // C semantics: quotient truncates toward zero, remainder takes the dividend's sign
 W_HD i256 operator/(const i256& a, const i256& b) {
+    if (fits64(a) && fits64(b)) {
+        long long x = (long long)a.w[0], y = (long long)b.w[0];
+        if (!(x == (-9223372036854775807LL - 1) && y == -1)) return i256(x / y);
+    }
     bool na = a.neg(), nb = b.neg();
     i256 q, r;
     udivmod(na ? -a : a, nb ? -b : b, q, r);
     return (na != nb) ? -q : q;
 }
 W_HD i256 operator%(const i256& a, const i256& b) {
+    if (fits64(a) && fits64(b)) {
+        long long x = (long long)a.w[0], y = (long long)b.w[0];
+        if (!(x == (-9223372036854775807LL - 1) && y == -1)) return i256(x % y);
+    }
     bool na = a.neg(), nb = b.neg();
     i256 q, r;
     udivmod(na ? -a : a, nb ? -b : b, q, r);
