@@ -124,7 +124,9 @@ typedef struct {
 } oob_options;
 
 enum {
-    OOB_F_NO_SORT = 1 /* keep input order on device (testing the scheduler) */
+    OOB_F_NO_SORT = 1,   /* keep input order on device (testing the scheduler) */
+    OOB_F_NO_DEMOTE = 2  /* decide wide-regime queries entirely in their proven
+                            regime (no root-phase demotion; testing) */
 };
 
 /* Results (caller-allocated; optional arrays may be NULL). */
@@ -155,6 +157,10 @@ int oob_check_model_batch(const oob_batch* batch, const oob_options* opt,
 /* Number of divisor side constraints solve() appends for query q
  * (solver.py:334-357); lets callers size buffers / audit the host compiler. */
 int oob_side_constraint_count(const oob_batch* batch, int64_t* counts);
+/* Host-only audit of the compiler: the exact-arithmetic regime each query is
+ * decided in (0 immediate verdict, 1 int64, 2 int128, 3 256-bit, 4 out of
+ * range -> OOB_ERROR).  No device is touched. */
+int oob_query_regime(const oob_batch* batch, const oob_options* opt, int8_t* regime);
 
 /*
  * Plans: compile and upload a batch once, then run the decision kernels on

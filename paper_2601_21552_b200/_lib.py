@@ -18,6 +18,7 @@ OOB_OK, OOB_E_INVALID, OOB_E_CUDA, OOB_E_RANGE, OOB_E_NOMEM = 0, 1, 2, 3, 4
 UNSAT, SAT, TIMEOUT, ERROR = 0, 1, 2, 3
 
 F_NO_SORT = 1
+F_NO_DEMOTE = 2
 
 class EngineError(RuntimeError):
     """The GPU engine could not decide a batch (no device, capacity, range)."""
@@ -49,6 +50,7 @@ EXPORTS = (
     "oob_propagate_batch",
     "oob_check_model_batch",
     "oob_side_constraint_count",
+    "oob_query_regime",
     "oob_last_error",
     "oob_device_count",
     "oob_version",
@@ -82,6 +84,8 @@ def lib():
     L.oob_check_model_batch.restype = ctypes.c_int
     L.oob_side_constraint_count.argtypes = [vp, vp]
     L.oob_side_constraint_count.restype = ctypes.c_int
+    L.oob_query_regime.argtypes = [vp, vp, vp]
+    L.oob_query_regime.restype = ctypes.c_int
     L.oob_last_error.restype = ctypes.c_char_p
     L.oob_device_count.restype = ctypes.c_int
     L.oob_version.restype = ctypes.c_char_p
@@ -234,3 +238,13 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def query_regime(fb, timeout_s=30.0):
+    """Per-query exact-arithmetic regime chosen by the host compiler
+    (0 immediate, 1 int64, 2 int128, 3 256-bit, 4 out of range); host only."""
+    out = np.zeros(fb.n, dtype=np.int8)
+    cb = fb.as_c()
+    o = options(timeout_s)
+    check(lib().oob_query_regime(ctypes.byref(cb), ctypes.byref(o), out.ctypes.data), "oob_query_regime")
+    return out

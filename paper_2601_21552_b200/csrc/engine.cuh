@@ -81,6 +81,18 @@ __device__ __forceinline__ void store_i128(int64_t* out, const i256& v) {
     out[1] = (int64_t)v.w[1];
 }
 
+// value conversions between the regimes (the caller has proven the value fits)
+template <typename T>
+__device__ __forceinline__ T from_i128(__int128 v) { return (T)v; }
+template <>
+__device__ __forceinline__ i256 from_i128<i256>(__int128 v) { return i256::from128(v); }
+__device__ __forceinline__ long long low64(long long v) { return v; }
+__device__ __forceinline__ long long low64(__int128 v) { return (long long)v; }
+__device__ __forceinline__ long long low64(const i256& v) { return (long long)v.w[0]; }
+__device__ __forceinline__ __int128 low128(long long v) { return v; }
+__device__ __forceinline__ __int128 low128(__int128 v) { return v; }
+__device__ __forceinline__ __int128 low128(const i256& v) { return v.low128(); }
+
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -471,6 +483,131 @@ struct Lane {
             if (!ok) return false;
         }
         return true;
+    }
+
+    // ----- regime demotion (root kernel) ----------------------------------------
+    // The host proves its regime bound at the DECLARED domains (host.cpp
+    // prove_bound).  Domains only shrink below the current node, and forward
+    // intervals, narrowing targets and exact values are inclusion-monotone, so
+    // the same proof restated at the CURRENT domains bounds every value the
+    // rest of the search can produce.  Returns the narrowest regime that
+    // holds: 0 int64, 1 int128, 2 neither.
+    __device__ static T tabs(T x) { return x < T(0) ? -x : x; }
+    __device__ int fit_regime() {
+        T B = T(0), D = T(0);
+        for (uint32_t v = 0; v < nv; ++v) D = A::mx(D, A::mx(tabs(E(env_lo, v)), tabs(E(env_hi, v))));
+        for (uint32_t i = 0; i < nlit; ++i) B = A::mx(B, tabs(E(lit, i)));
+        const T INF = A::inf();
+        for (uint32_t k = 0; k < ncon; ++k) {
+            uint32_t w = __ldg(cons + k);
+            uint32_t rel = w & 7u, lr = (w >> 3) & 0x3FFFu, rr = w >> 17;
+            uint32_t start = lr + 1 - size_of(lr);
+            vbase = start;
+            // forward intervals F; "no value" (the reference's None) is lo > hi
+            for (uint32_t j = start; j <= rr; ++j) {
+                uint32_t cw = __ldg(code + j), op = op_of(cw);
+                T lo, hi;
+                if (op == NODE_LIT) {
+                    lo = hi = E(lit, arg_of(cw));
+                } else if (op == NODE_VAR) {
+                    lo = E(env_lo, arg_of(cw));
+                    hi = E(env_hi, arg_of(cw));
+                } else {
+                    uint32_t R = j - 1, L = R - size_of(R);
+                    T l0 = VL(L), l1 = VH(L), r0 = VL(R), r1 = VH(R);
+                    lo = T(1);
+                    hi = T(0);
+                    if (l0 <= l1 && r0 <= r1) {
+                        if (op == NODE_ADD) { lo = l0 + r0; hi = l1 + r1; }
+                        else if (op == NODE_SUB) { lo = l0 - r1; hi = l1 - r0; }
+                        else if (op == NODE_MUL) {
+                            T k0 = l0 * r0, k1 = l0 * r1, k2 = l1 * r0, k3 = l1 * r1;
+                            lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
+                            hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
+                        } else {
+                            T d0 = A::mx(r0, T(1)), d1 = r1;
+                            if (d0 <= d1) {
+                                if (op == NODE_DIV) {
+                                    T k0 = cdiv(l0, d0), k1 = cdiv(l0, d1), k2 = cdiv(l1, d0), k3 = cdiv(l1, d1);
+                                    lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
+                                    hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
+                                } else {
+                                    T m = d1 - T(1);
+                                    lo = l0 >= T(0) ? T(0) : A::mx(l0, -m);
+                                    hi = l1 <= T(0) ? T(0) : A::mn(l1, m);
+                                }
+                            }
+                        }
+                    }
+                }
+                VL(j) = lo;
+                VH(j) = hi;
+                if (lo <= hi) B = A::mx(B, A::mx(tabs(lo), tabs(hi)));
+            }
+            // narrowing targets, top-down from both roots
+            auto fmag = [&](uint32_t j) -> T {
+                T lo = VL(j), hi = VH(j);
+                return lo <= hi ? A::mx(tabs(lo), tabs(hi)) : T(0);
+            };
+            T fl = fmag(lr), fr = fmag(rr), tl, tr;
+            if (rel == REL_LT || rel == REL_GT) {
+                tl = A::mx(INF, fr + T(1));
+                tr = A::mx(INF, fl + T(1));
+            } else if (rel == REL_LE || rel == REL_GE) {
+                tl = A::mx(INF, fr);
+                tr = A::mx(INF, fl);
+            } else {
+                tl = tr = A::mn(fl, fr);
+            }
+            int sp = 0;
+            U(st_n, sp) = lr; E(st_0, sp) = tl; ++sp;
+            U(st_n, sp) = rr; E(st_0, sp) = tr; ++sp;
+            while (sp > 0) {
+                --sp;
+                uint32_t i = U(st_n, sp);
+                T t = E(st_0, sp);
+                B = A::mx(B, t);
+                uint32_t cw = __ldg(code + i), op = op_of(cw);
+                if (op < NODE_ADD) continue;
+                uint32_t R = i - 1, L = R - size_of(R);
+                if (sp + 2 > (int)st_cap) return 2;
+                if (op == NODE_ADD || op == NODE_SUB) {
+                    U(st_n, sp) = L; E(st_0, sp) = t + fmag(R); ++sp;
+                    U(st_n, sp) = R; E(st_0, sp) = t + fmag(L); ++sp;
+                } else if (op == NODE_MUL) {
+                    U(st_n, sp) = L; E(st_0, sp) = A::mx(t, INF); ++sp;
+                    U(st_n, sp) = R; E(st_0, sp) = A::mx(t, INF); ++sp;
+                } else if (op == NODE_DIV) {
+                    uint32_t rw = __ldg(code + R);
+                    if (op_of(rw) == NODE_LIT) {
+                        T c = E(lit, arg_of(rw));
+                        if (c >= T(1)) { U(st_n, sp) = L; E(st_0, sp) = t * c + c; ++sp; }
+                    }
+                }
+            }
+            // exact-value magnitudes G (reuse VL: children precede parents)
+            for (uint32_t j = start; j <= rr; ++j) {
+                uint32_t cw = __ldg(code + j), op = op_of(cw);
+                T g;
+                if (op == NODE_LIT) g = tabs(E(lit, arg_of(cw)));
+                else if (op == NODE_VAR) g = A::mx(tabs(E(env_lo, arg_of(cw))), tabs(E(env_hi, arg_of(cw))));
+                else {
+                    uint32_t R = j - 1, L = R - size_of(R);
+                    T gl = VL(L), gr = VL(R);
+                    if (op == NODE_ADD || op == NODE_SUB) g = gl + gr;
+                    else if (op == NODE_MUL) g = gl * gr;
+                    else if (op == NODE_DIV) g = gl;
+                    else g = A::mn(gl, gr);
+                }
+                VL(j) = g;
+                B = A::mx(B, g);
+            }
+        }
+        if (B <= T(0x7FFFFFFFFFFFFFFFLL) && D <= T((long long)((1ull << 62) - 1))) return 0;
+        const __int128 one = 1;
+        if (B <= from_i128<T>((__int128)(~((unsigned __int128)0) >> 1)) && D <= from_i128<T>((one << 126) - 1))
+            return 1;
+        return 2;
     }
 
     __device__ void undo_to(uint32_t mark) {

@@ -88,6 +88,30 @@ struct ClassDesc {
 };
 static_assert(sizeof(ClassDesc) == 32, "ClassDesc is two int4 words");
 
+// Regime demotion (SOLVE mode).  A query whose declared domains need the
+// int128 / 256-bit regime first runs its ROOT node's propagation in that
+// regime (oob_root_kernel); as soon as the bound proof restated at the
+// narrowed domains fits a narrower regime, the query's state is written into
+// a SHADOW entry of that regime's job, which resumes the search there.
+// resume[] word per scheduled query:
+//   0          fresh start from the declared domains
+//   RES_SKIP   not live in this job (shadow not chosen / demoted / finished)
+//   RES_ROOT | [RES_FIX] | passes   resume the root node after `passes`
+//              propagation passes (RES_FIX: the last one changed nothing)
+constexpr uint32_t RES_SKIP = 0xFFFFFFFFu;
+constexpr uint32_t RES_ROOT = 0x80000000u;
+constexpr uint32_t RES_FIX = 0x40000000u;
+constexpr uint32_t RES_PASSES = 0x3FFFFFFFu;
+constexpr uint32_t ROOT_MAX_PASSES = 64;  // root-kernel pass budget before giving up on demotion
+
+struct DemoteTarget {
+    const QDesc* qdesc;     // target job's descriptors (data_off of the shadow)
+    int64_t* data;          // target job's per-query data
+    uint32_t* resume;       // target job's resume words
+    uint64_t* t0;           // target job's per-query start times
+    const uint32_t* slot;   // per entry of THIS job: its shadow's index in the target job
+};
+
 struct LaunchArgs {
     const QDesc* qdesc;       // per scheduled query
     const uint32_t* code;     // structure words (constraints + nodes), per class
@@ -123,9 +147,12 @@ struct LaunchArgs {
     uint64_t timeout_ns;      // 0 => unlimited
     int64_t node_budget;      // >0 => deterministic budget
     int mode;                 // MODE_SOLVE / MODE_PROPAGATE / MODE_CHECK
+    uint32_t* resume;         // per scheduled query (null: all fresh)
+    DemoteTarget dem[2];      // root kernel: [0] int64 job, [1] int128 job (slot null: none)
 };
 
 enum { MODE_SOLVE = 0, MODE_PROPAGATE = 1, MODE_CHECK = 2 };
+constexpr int8_t VERDICT_NONE = -1;  // entry not owned by this job (shadow / demoted)
 enum { ERR_NONE = 0, ERR_DEPTH = 1, ERR_TRAIL = 2, ERR_STACK = 3 };
 
 }  // namespace oob

@@ -81,6 +81,7 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
     const uint32_t ecap = a.fr_ecap, ucap = a.fr_ucap, logcap = a.fr_logcap;
     const uint64_t t0 = a.heavy_t0[qi];
     const uint64_t deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
+    const uint32_t rs = a.resume ? a.resume[qi] : 0u;  // demoted: the root resumes (format.h)
 
     uint32_t nunits = 1, nfree = 0, ebump = 0, nlog = 0;
     if (lane == 0) R.units[0] = UNIT_ROOT;
@@ -108,11 +109,13 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
         const bool has = lane < k;
         uint64_t p0 = 0, p1 = 0;
         uint32_t depth = 0, freed = 0xFFFFFFFFu;
+        bool resumed_root = false;
         if (has) {
             uint32_t u = R.units[nunits - 1 - lane];
             L.depth = 0;  // no trail: every lane owns its node's domains
             L.clean0 = L.clean1 = 0;
             L.err = ERR_NONE;
+            resumed_root = (u == UNIT_ROOT) && (rs & RES_ROOT);
             if (u != UNIT_ROOT) {
                 uint32_t e = u >> 1, half = u & 1;
                 const T* env = R.e_env + (size_t)e * 2 * nv;
@@ -148,8 +151,9 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
         }
         // ---- expand: node start + pass-synchronous propagate() ----
         int outcome = FN_NONE;
-        int64_t my_passes = 0;
-        bool prop = has;
+        int64_t my_passes = resumed_root ? (int64_t)(rs & RES_PASSES) : 0;
+        const int pin0 = (int)my_passes;
+        bool prop = has && !(resumed_root && (rs & RES_FIX));
         if (__any_sync(FULL, has && deadline && global_ns() > deadline)) {
             status = VERDICT_TIMEOUT;
             break;
@@ -157,7 +161,7 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
         bool dead = false;
         for (int pin = 0; __any_sync(FULL, prop); ++pin) {
             if (prop) {
-                if (pin >= PASS_CAP) {
+                if (pin + pin0 >= PASS_CAP) {
                     prop = false;
                 } else {
                     ++my_passes;

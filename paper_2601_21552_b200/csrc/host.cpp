@@ -33,6 +33,7 @@
 
 namespace oob {
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s);
+cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
 cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm);
 }
 
@@ -485,13 +486,14 @@ struct DevicePool {
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
     DevBuf classes, class_next, class_init, warp_class;
     DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
+    DevBuf resume, resume_init, slot64, slot128;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evr = nullptr;
     int sms = 148;
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
-                          &heavy_t0, &fr_region})
+                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128})
             b->release();
     }
 };
@@ -592,6 +594,10 @@ struct DevJob {
     int dev = 0;
     int wide = 0;
     std::vector<int64_t> qs;     // caller query ids, in schedule order
+    std::vector<int64_t> shadows;  // wider-regime queries this job may resume (SOLVE mode)
+    std::vector<uint8_t> is_shadow;  // per scheduled entry
+    std::vector<uint32_t> resume_init;  // per scheduled entry (format.h resume words)
+    std::vector<uint32_t> slot[2];      // wide jobs: per entry, index of its shadow in job[0] / job[1]
     std::vector<uint64_t> mo;    // device-local model offset (vars) per scheduled query
     std::vector<uint32_t> code;  // class code blocks
     std::vector<int64_t> data;   // per query domains + literal slots
@@ -619,10 +625,13 @@ void pack(const RunCtx& rc, DevJob& j) {
     // group the job's queries by structure class, keeping their order within
     // a class (the lockstep kernel runs each warp on one class)
     std::unordered_map<std::string, uint32_t> cls_of;
-    std::vector<std::vector<int64_t>> members;
+    std::vector<std::vector<int64_t>> members;  // entries: query id, or ~id for a shadow
     std::vector<uint32_t> code_off;
     j.code.clear();
-    for (int64_t q : j.qs) {
+    std::vector<int64_t> entries(j.qs);
+    for (int64_t q : j.shadows) entries.push_back(~q);
+    for (int64_t e : entries) {
+        const int64_t q = e < 0 ? ~e : e;
         const Compiled& c = comp[q];
         std::string key((const char*)c.words.data(), c.words.size() * 4);
         key.append((const char*)&c.nv, 4);
@@ -638,18 +647,25 @@ void pack(const RunCtx& rc, DevJob& j) {
         } else {
             id = it->second;
         }
-        members[id].push_back(q);
+        members[id].push_back(e);
     }
     j.qs.clear();
+    j.is_shadow.clear();
+    j.resume_init.clear();
     j.cls.clear();
     for (size_t id = 0; id < members.size(); id++) {
-        const Compiled& c = comp[members[id][0]];
+        const int64_t e0 = members[id][0];
+        const Compiled& c = comp[e0 < 0 ? ~e0 : e0];
         ClassDesc cd{};
         cd.code_off = code_off[id];
         cd.nv_ncon = c.nv | (c.ncon << 16);
         cd.ncode_nlit = c.ncode | (c.nlit << 16);
         cd.q_begin = (uint32_t)j.qs.size();
-        j.qs.insert(j.qs.end(), members[id].begin(), members[id].end());
+        for (int64_t e : members[id]) {
+            j.qs.push_back(e < 0 ? ~e : e);
+            j.is_shadow.push_back(e < 0);
+            j.resume_init.push_back(e < 0 ? RES_SKIP : 0u);
+        }
         cd.q_end = (uint32_t)j.qs.size();
         j.cls.push_back(cd);
     }
@@ -687,6 +703,11 @@ void pack(const RunCtx& rc, DevJob& j) {
                 j.data.push_back(s);
             }
         };
+        if (j.is_shadow[i]) {  // written on the device by the root kernel
+            j.data.resize(j.data.size() + (size_t)(2 * c.nv + c.nlit) * (j.wide == 2 ? 4 : j.wide + 1), 0);
+            while (j.data.size() & (j.wide == 2 ? 3 : 1)) j.data.push_back(0);
+            continue;
+        }
         for (uint32_t v = 0; v < c.nv; v++) {
             if (rc.mode == MODE_CHECK) {
                 i128 m = from_w(rc.model[vb + v]);
@@ -739,6 +760,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
         CK(cudaEventCreate(&P->ev0));
         CK(cudaEventCreate(&P->ev1));
+        CK(cudaEventCreateWithFlags(&P->evr, cudaEventDisableTiming));
         CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, j.dev));
     }
     const uint32_t n = (uint32_t)j.qs.size();
@@ -778,7 +800,16 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->heavy_list.ensure((size_t)n * 4));
     CK(P->heavy_t0.ensure((size_t)n * 8));
     if (j.fblocks) CK(P->fr_region.ensure((size_t)j.fblocks * WARPS_PER_BLOCK * fr_bytes));
+    CK(P->resume.ensure((size_t)n * 4));
+    CK(P->resume_init.ensure((size_t)n * 4));
+    for (int t = 0; t < 2; t++)
+        if (!j.slot[t].empty()) CK((t ? P->slot128 : P->slot64).ensure(j.slot[t].size() * 4));
     cudaStream_t s = P->stream;
+    CK(cudaMemcpyAsync(P->resume_init.p, j.resume_init.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    for (int t = 0; t < 2; t++)
+        if (!j.slot[t].empty())
+            CK(cudaMemcpyAsync((t ? P->slot128 : P->slot64).p, j.slot[t].data(), j.slot[t].size() * 4,
+                               cudaMemcpyHostToDevice, s));
     {
         std::vector<uint32_t> init(j.cls.size());
         for (size_t c = 0; c < j.cls.size(); c++) init[c] = j.cls[c].q_begin;
@@ -824,32 +855,159 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.timeout_ns = (rc.mode == MODE_SOLVE && t > 0 && t < 1e9) ? (uint64_t)(t * 1e9) : 0;
     a.node_budget = rc.opt.node_budget;
     a.mode = rc.mode;
+    a.resume = (uint32_t*)P->resume.p;
     j.staged = true;
     return "";
 }
 
-// kernel launch bracketed by events on the engine's stream
-std::string launch(DevJob& j, DevicePool* P) {
-    CK(cudaSetDevice(j.dev));
-    cudaStream_t s = P->stream;
-    CK(cudaMemsetAsync(P->next.p, 0, 4, s));
-    CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemsetAsync(P->heavy_count.p, 0, 8, s));
-    CK(cudaEventRecord(P->ev0, s));
-    CK(launch_solve(j.a, j.wide, (int)j.blocks, (int)j.fblocks, s));
-    CK(cudaEventRecord(P->ev1, s));
+// ----- device groups: the regime jobs of one device ---------------------------
+// job[w] holds the queries whose proven regime is w (0 int64, 1 int128, 2
+// 256-bit).  In SOLVE mode job[0] also carries a shadow entry for every query
+// of job[1] and job[2], and job[1] one for every query of job[2]: the root
+// kernels of the wide jobs run first and hand demoted queries to their shadows
+// (format.h), then the three lockstep kernels run concurrently on their own
+// streams.
+struct DevGroup {
+    int dev = 0;
+    DevJob job[3];
+    DevicePool* pool[3] = {nullptr, nullptr, nullptr};
+    bool has(int w) const { return !job[w].qs.empty(); }
+};
+
+// shadows + pack + demotion slots of a group (before staging)
+void pack_group(const RunCtx& rc, DevGroup& G) {
+    for (int w = 0; w < 3; w++) {
+        G.job[w].dev = G.dev;
+        G.job[w].wide = w;
+        G.job[w].shadows.clear();
+        G.job[w].slot[0].clear();
+        G.job[w].slot[1].clear();
+    }
+    // the original (own-regime) query lists, before pack() reorders them
+    std::vector<int64_t> own[3];
+    for (int w = 0; w < 3; w++) own[w] = G.job[w].qs;
+    if (rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_DEMOTE)) {
+        for (int w = 1; w < 3; w++)
+            for (int t = 0; t < w; t++)
+                G.job[t].shadows.insert(G.job[t].shadows.end(), own[w].begin(), own[w].end());
+    }
+    for (int w = 0; w < 3; w++)
+        if (!G.job[w].qs.empty() || !G.job[w].shadows.empty()) pack(rc, G.job[w]);
+    if (rc.mode != MODE_SOLVE || (rc.opt.flags & OOB_F_NO_DEMOTE)) return;
+    for (int t = 0; t < 2; t++) {
+        const DevJob& T = G.job[t];
+        if (T.shadows.empty()) continue;
+        std::unordered_map<int64_t, uint32_t> at;
+        at.reserve(T.shadows.size() * 2);
+        for (size_t i = 0; i < T.qs.size(); i++)
+            if (T.is_shadow[i]) at.emplace(T.qs[i], (uint32_t)i);
+        for (int w = t + 1; w < 3; w++) {
+            DevJob& W = G.job[w];
+            if (W.qs.empty()) continue;
+            W.slot[t].resize(W.qs.size());
+            for (size_t i = 0; i < W.qs.size(); i++) W.slot[t][i] = at.at(W.qs[i]);
+        }
+    }
+}
+
+// a job is present when it has own queries or shadows
+inline bool present(const DevJob& j) { return !j.qs.empty(); }
+
+std::string stage_group(const RunCtx& rc, DevGroup& G, uint32_t depth_cap, uint32_t trail_cap, bool heavy) {
+    for (int w = 0; w < 3; w++) {
+        if (!present(G.job[w])) continue;
+        std::string e = stage(rc, G.job[w], G.pool[w], depth_cap, trail_cap, heavy);
+        if (!e.empty()) return e;
+    }
+    // demotion targets of the wide jobs
+    for (int w = 1; w < 3; w++) {
+        if (!present(G.job[w])) continue;
+        LaunchArgs& a = G.job[w].a;
+        for (int t = 0; t < 2; t++) {
+            a.dem[t] = DemoteTarget{};
+            if (t >= w || G.job[w].slot[t].empty()) continue;
+            DevicePool* T = G.pool[t];
+            a.dem[t].qdesc = (const QDesc*)T->qdesc.p;
+            a.dem[t].data = (int64_t*)T->data.p;
+            a.dem[t].resume = (uint32_t*)T->resume.p;
+            a.dem[t].t0 = (uint64_t*)T->heavy_t0.p;
+            a.dem[t].slot = (const uint32_t*)(t ? G.pool[w]->slot128.p : G.pool[w]->slot64.p);
+        }
+    }
     return "";
 }
 
-std::string kernel_ms(DevJob& j, DevicePool* P) {
-    CK(cudaSetDevice(j.dev));
-    CK(cudaEventSynchronize(P->ev1));
-    CK(cudaEventElapsedTime(&j.last_ms, P->ev0, P->ev1));
+// one run of a group: resets, root kernels, then the lockstep kernels
+std::string launch_group(const RunCtx& rc, DevGroup& G) {
+    CK(cudaSetDevice(G.dev));
+    int first = -1;
+    for (int w = 0; w < 3; w++)
+        if (present(G.job[w])) { first = w; break; }
+    if (first < 0) return "";
+    cudaStream_t s0 = G.pool[first]->stream;
+    // every per-run reset on the first stream, so that the root kernels may
+    // write into the other jobs' buffers once it is done
+    for (int w = first; w < 3; w++) {
+        if (!present(G.job[w])) continue;
+        DevicePool* P = G.pool[w];
+        const DevJob& j = G.job[w];
+        const size_t n = j.qs.size();
+        CK(cudaMemsetAsync(P->next.p, 0, 4, s0));
+        CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s0));
+        CK(cudaMemsetAsync(P->heavy_count.p, 0, 8, s0));
+        CK(cudaMemsetAsync(P->verdict.p, 0xFF, n, s0));
+        CK(cudaMemcpyAsync(P->resume.p, P->resume_init.p, n * 4, cudaMemcpyDeviceToDevice, s0));
+    }
+    CK(cudaEventRecord(G.pool[first]->ev0, s0));
+    for (int w = first + 1; w < 3; w++)
+        if (present(G.job[w])) {
+            CK(cudaStreamWaitEvent(G.pool[w]->stream, G.pool[first]->ev0, 0));
+            CK(cudaEventRecord(G.pool[w]->ev0, G.pool[w]->stream));
+        }
+    if (rc.mode == MODE_SOLVE) {
+        for (int w = 2; w >= 1; w--) {
+            if (!present(G.job[w])) continue;
+            DevJob& j = G.job[w];
+            if (!j.slot[0].empty() || !j.slot[1].empty()) {
+                CK(launch_root(j.a, w, (int)j.blocks, G.pool[w]->stream));
+                CK(cudaEventRecord(G.pool[w]->evr, G.pool[w]->stream));
+                for (int t = 0; t < w; t++)
+                    if (present(G.job[t]) && !j.slot[t].empty())
+                        CK(cudaStreamWaitEvent(G.pool[t]->stream, G.pool[w]->evr, 0));
+            }
+        }
+    }
+    for (int w = 2; w >= 0; w--) {
+        if (!present(G.job[w])) continue;
+        DevJob& j = G.job[w];
+        cudaStream_t s = G.pool[w]->stream;
+        CK(launch_solve(j.a, w, (int)j.blocks, (int)j.fblocks, s));
+        CK(cudaEventRecord(G.pool[w]->ev1, s));
+    }
+    return "";
+}
+
+// device time of the last run of a group: first start event to the last end
+std::string group_ms(DevGroup& G, float* ms) {
+    CK(cudaSetDevice(G.dev));
+    *ms = 0;
+    int first = -1;
+    for (int w = 0; w < 3; w++)
+        if (present(G.job[w])) {
+            if (first < 0) first = w;
+            CK(cudaEventSynchronize(G.pool[w]->ev1));
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, G.pool[first]->ev0, G.pool[w]->ev1));
+            G.job[w].last_ms = t;
+            *ms = std::max(*ms, t);
+        }
     return "";
 }
 
 // D2H + scatter into the caller arrays; capacity overflows go to `retry`
-std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t>& retry) {
+// (by the query's own regime).  Entries a job does not own (shadows that were
+// not resumed, queries that were demoted) carry VERDICT_NONE.
+std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> retry[3]) {
     CK(cudaSetDevice(j.dev));
     const uint32_t n = (uint32_t)j.qs.size();
     cudaStream_t s = P->stream;
@@ -867,9 +1025,10 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t>& re
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
     for (uint32_t i = 0; i < n; i++) {
+        if (verdict[i] == VERDICT_NONE) continue;
         int64_t q = j.qs[i];
         if (err[i] == ERR_DEPTH || err[i] == ERR_TRAIL) {
-            retry.push_back(q);
+            retry[comp[q].regime - R_W64].push_back(q);
             continue;
         }
         (*rc.errs)[q] = err[i];
@@ -897,40 +1056,59 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t>& re
     return "";
 }
 
-// full run of one job on the device's shared pool, with capacity retries
-std::string run_job(RunCtx& rc, DevJob& job) {
-    uint32_t depth_cap = DEPTH_CAP0, trail_cap = TRAIL_CAP0;
-    DevicePool* P = pool_for(job.dev, job.wide);
-    std::vector<int64_t> qs = job.qs;
-    for (int round = 0; round < 5 && !qs.empty(); round++) {
-        DevJob j;
-        j.dev = job.dev;
-        j.wide = job.wide;
-        j.qs = qs;
-        pack(rc, j);
-        std::vector<int64_t> retry;
-        {
-            std::lock_guard<std::mutex> lk(P->mu);
-            std::string e = stage(rc, j, P, depth_cap, trail_cap, round == 0);
-            if (e.empty()) e = launch(j, P);
-            if (e.empty()) e = fetch(rc, j, P, retry);
-            if (!e.empty()) return e;
-        }
-        qs.swap(retry);
-        depth_cap *= 4;
-        trail_cap *= 8;
-    }
-    for (int64_t q : qs) {  // still out of scratch after the last retry
-        rc.verdict[q] = OOB_ERROR;
-        (*rc.errs)[q] = ERR_DEPTH;
+std::string fetch_group(RunCtx& rc, DevGroup& G, std::vector<int64_t> retry[3]) {
+    for (int w = 0; w < 3; w++) {
+        if (!present(G.job[w])) continue;
+        std::string e = fetch(rc, G.job[w], G.pool[w], retry);
+        if (!e.empty()) return e;
     }
     return "";
 }
 
-std::string run_jobs(RunCtx& rc, std::vector<DevJob>& jobs) {
-    std::vector<std::string> errs(jobs.size());
+// full run of one device's queries on the shared pools, with capacity retries
+std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
+    uint32_t depth_cap = DEPTH_CAP0, trail_cap = TRAIL_CAP0;
+    DevicePool* pools[3] = {pool_for(dev, 0), pool_for(dev, 1), pool_for(dev, 2)};
+    std::vector<int64_t> cur[3] = {qs[0], qs[1], qs[2]};
+    for (int round = 0; round < 5; round++) {
+        if (cur[0].empty() && cur[1].empty() && cur[2].empty()) return "";
+        DevGroup G;
+        G.dev = dev;
+        for (int w = 0; w < 3; w++) {
+            G.job[w].qs = cur[w];
+            G.pool[w] = pools[w];
+        }
+        pack_group(rc, G);
+        std::vector<int64_t> retry[3];
+        {
+            std::lock_guard<std::mutex> l0(pools[0]->mu), l1(pools[1]->mu), l2(pools[2]->mu);
+            std::string e = stage_group(rc, G, depth_cap, trail_cap, round == 0);
+            if (e.empty()) e = launch_group(rc, G);
+            if (e.empty()) e = fetch_group(rc, G, retry);
+            if (!e.empty()) return e;
+        }
+        for (int w = 0; w < 3; w++) cur[w].swap(retry[w]);
+        depth_cap *= 4;
+        trail_cap *= 8;
+    }
+    for (int w = 0; w < 3; w++)
+        for (int64_t q : cur[w]) {  // still out of scratch after the last retry
+            rc.verdict[q] = OOB_ERROR;
+            (*rc.errs)[q] = ERR_DEPTH;
+        }
+    return "";
+}
+
+struct DevWork {
+    int dev = 0;
+    std::vector<int64_t> qs[3];
+};
+
+std::string run_all(RunCtx& rc, std::vector<DevWork>& work) {
+    std::vector<std::string> errs(work.size());
     std::vector<std::thread> th;
-    for (size_t j = 0; j < jobs.size(); j++) th.emplace_back([&, j]() { errs[j] = run_job(rc, jobs[j]); });
+    for (size_t k = 0; k < work.size(); k++)
+        th.emplace_back([&, k]() { errs[k] = run_group(rc, work[k].dev, work[k].qs); });
     for (auto& t : th) t.join();
     for (auto& e : errs)
         if (!e.empty()) return e;
@@ -950,7 +1128,7 @@ int visible_devices() {
 struct Prepared {
     std::vector<Compiled> comp;
     std::vector<int8_t> errs;
-    std::vector<DevJob> jobs;
+    std::vector<DevWork> work;  // per device: queries by proven regime
     std::string range_msg;
     oob_options opt{};
     double compile_s = 0;
@@ -1013,6 +1191,10 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         return fail(OOB_E_CUDA, "device ordinal out of range");
     int want = opt.n_gpus > 0 ? opt.n_gpus : ndev - first;
     want = std::max(1, std::min(want, ndev - first));
+    if (n_dev_q > 0) {
+        pr.work.resize(want);
+        for (int d = 0; d < want; d++) pr.work[d].dev = first + d;
+    }
     for (int w = 0; w < 3; w++) {
         auto& qs = reg[w];
         if (qs.empty()) continue;
@@ -1032,14 +1214,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
                 return comp[x].cost > comp[y].cost;
             });
         }
-        std::vector<DevJob> dj(want);
-        for (int d = 0; d < want; d++) {
-            dj[d].dev = first + d;
-            dj[d].wide = w;
-        }
-        for (size_t i = 0; i < qs.size(); i++) dj[(i / 32) % want].qs.push_back(qs[i]);
-        for (auto& j : dj)
-            if (!j.qs.empty()) pr.jobs.push_back(std::move(j));
+        for (size_t i = 0; i < qs.size(); i++) pr.work[(i / 32) % want].qs[w].push_back(qs[i]);
     }
     return OOB_OK;
 }
@@ -1071,7 +1246,7 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
     rc.passes = passes;
     rc.elapsed = elapsed;
     rc.errs = &pr.errs;
-    std::string e = run_jobs(rc, pr.jobs);
+    std::string e = run_all(rc, pr.work);
     if (!e.empty()) return fail(OOB_E_CUDA, e);
     return finish(pr, b->n_queries);
 }
@@ -1135,11 +1310,24 @@ int oob_side_constraint_count(const oob_batch* b, int64_t* counts) {
     return OOB_OK;
 }
 
+int oob_query_regime(const oob_batch* b, const oob_options* opt, int8_t* regime) {
+    g_last_error.clear();
+    if (!b || !regime) return fail(OOB_E_INVALID, "null argument");
+    double timeout_s = opt ? opt->timeout_s : 30.0;
+    for (int64_t q = 0; q < b->n_queries; q++) {
+        std::string why = validate(b, q);
+        if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
+        regime[q] = compile_query(b, q, MODE_SOLVE, timeout_s, nullptr).regime;
+    }
+    return OOB_OK;
+}
+
 // ----- plans: compile + upload once, time kernels on device-resident data -----
 struct oob_plan {
     const oob_batch* b;
     Prepared pr;
-    std::vector<std::unique_ptr<DevicePool>> pools;  // one private pool per job
+    std::vector<DevGroup> groups;
+    std::vector<std::unique_ptr<DevicePool>> pools;  // three private pools per group
     RunCtx rc;
     std::vector<int8_t> verdict;
     std::vector<int64_t> nodes, passes;
@@ -1173,43 +1361,42 @@ int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** o
     rc.passes = p->passes.data();
     rc.elapsed = p->elapsed.data();
     rc.errs = &p->pr.errs;
-    for (auto& j : p->pr.jobs) {
-        pack(rc, j);
-        p->pools.emplace_back(new DevicePool());
-        std::string e = stage(rc, j, p->pools.back().get(), DEPTH_CAP0, TRAIL_CAP0);
+    p->groups.resize(p->pr.work.size());
+    for (size_t k = 0; k < p->pr.work.size(); k++) {
+        DevGroup& G = p->groups[k];
+        G.dev = p->pr.work[k].dev;
+        for (int w = 0; w < 3; w++) {
+            G.job[w].qs = p->pr.work[k].qs[w];
+            p->pools.emplace_back(new DevicePool());
+            G.pool[w] = p->pools.back().get();
+        }
+        pack_group(rc, G);
+        std::string e = stage_group(rc, G, DEPTH_CAP0, TRAIL_CAP0, true);
         if (!e.empty()) return fail(OOB_E_CUDA, e);
     }
-    for (size_t k = 0; k < p->pools.size(); k++) {
-        cudaSetDevice(p->pr.jobs[k].dev);
-        if (cudaStreamSynchronize(p->pools[k]->stream) != cudaSuccess)
-            return fail(OOB_E_CUDA, cudaGetErrorString(cudaGetLastError()));
-    }
+    for (auto& G : p->groups)
+        for (int w = 0; w < 3; w++)
+            if (present(G.job[w])) {
+                cudaSetDevice(G.dev);
+                if (cudaStreamSynchronize(G.pool[w]->stream) != cudaSuccess)
+                    return fail(OOB_E_CUDA, cudaGetErrorString(cudaGetLastError()));
+            }
     *out = p.release();
     return OOB_OK;
 }
 
 int oob_plan_run(oob_plan* p, float* device_ms) {
     if (!p) return fail(OOB_E_INVALID, "null plan");
-    auto& jobs = p->pr.jobs;
-    // all jobs are launched back to back on their own streams and overlap
-    for (size_t k = 0; k < jobs.size(); k++) {
-        std::string e = launch(jobs[k], p->pools[k].get());
+    // every device's groups are launched back to back and overlap
+    for (auto& G : p->groups) {
+        std::string e = launch_group(p->rc, G);
         if (!e.empty()) return fail(OOB_E_CUDA, e);
     }
-    for (size_t k = 0; k < jobs.size(); k++) {
-        std::string e = kernel_ms(jobs[k], p->pools[k].get());
-        if (!e.empty()) return fail(OOB_E_CUDA, e);
-    }
-    // per device: from its first job's start event to the last end event
     float worst = 0;
-    for (size_t k = 0; k < jobs.size(); k++) {
-        size_t first = k;
-        while (first > 0 && jobs[first - 1].dev == jobs[k].dev) first--;
-        for (size_t m = 0; m < jobs.size(); m++)
-            if (jobs[m].dev == jobs[k].dev && m < first) first = m;
+    for (auto& G : p->groups) {
         float ms = 0;
-        cudaSetDevice(jobs[k].dev);
-        cudaEventElapsedTime(&ms, p->pools[first]->ev0, p->pools[k]->ev1);
+        std::string e = group_ms(G, &ms);
+        if (!e.empty()) return fail(OOB_E_CUDA, e);
         worst = std::max(worst, ms);
     }
     p->runs++;
@@ -1224,17 +1411,12 @@ int oob_plan_results(oob_plan* p, oob_result* out) {
         if (rc0 != OOB_OK) return rc0;
     }
     RunCtx& rc = p->rc;
-    std::vector<int64_t> retry_all;
-    for (size_t k = 0; k < p->pr.jobs.size(); k++) {
-        std::vector<int64_t> retry;
-        std::string e = fetch(rc, p->pr.jobs[k], p->pools[k].get(), retry);
+    for (auto& G : p->groups) {
+        std::vector<int64_t> retry[3];
+        std::string e = fetch_group(rc, G, retry);
         if (!e.empty()) return fail(OOB_E_CUDA, e);
-        if (!retry.empty()) {
-            DevJob rj;
-            rj.dev = p->pr.jobs[k].dev;
-            rj.wide = p->pr.jobs[k].wide;
-            rj.qs = retry;
-            e = run_job(rc, rj);
+        if (!retry[0].empty() || !retry[1].empty() || !retry[2].empty()) {
+            e = run_group(rc, G.dev, retry);
             if (!e.empty()) return fail(OOB_E_CUDA, e);
         }
     }
@@ -1252,21 +1434,26 @@ int oob_plan_results(oob_plan* p, oob_result* out) {
 
 int oob_plan_info(const oob_plan* p, int64_t info[8]) {
     if (!p || !info) return fail(OOB_E_INVALID, "null argument");
-    int64_t nq = 0, rec = 0, res = 0, cls = 0, wide = 0;
-    for (auto& j : p->pr.jobs) {
-        nq += (int64_t)j.qs.size();
-        rec += (int64_t)j.record_bytes();
-        res += (int64_t)j.qs.size() * (1 + 1 + 8 + 8 + 4) + (int64_t)j.out_model_words * 8;
-        cls += j.n_classes;
-        if (j.wide) wide += (int64_t)j.qs.size();
-    }
+    int64_t nq = 0, rec = 0, res = 0, cls = 0, wide = 0, jobs = 0, launches = 0;
+    for (auto& G : p->groups)
+        for (int w = 0; w < 3; w++) {
+            const DevJob& j = G.job[w];
+            if (!present(j)) continue;
+            int64_t own = 0;
+            for (uint8_t sh : j.is_shadow) own += !sh;
+            nq += own;
+            rec += (int64_t)j.record_bytes();
+            res += (int64_t)j.qs.size() * (1 + 1 + 8 + 8 + 4) + (int64_t)j.out_model_words * 8;
+            cls += j.n_classes;
+            if (w) wide += own;
+            jobs++;
+            launches += 1 + (j.fblocks ? 1 : 0) + ((w && (!j.slot[0].empty() || !j.slot[1].empty())) ? 1 : 0);
+        }
     info[0] = nq;
     info[1] = rec;
     info[2] = res;
     info[3] = cls;
-    info[4] = (int64_t)p->pr.jobs.size();
-    int64_t launches = 0;
-    for (auto& j : p->pr.jobs) launches += 1 + (j.fblocks ? 1 : 0);
+    info[4] = jobs;
     info[5] = launches;  // kernel launches per run
     info[6] = wide;
     info[7] = (int64_t)(p->pr.compile_s * 1e6);
@@ -1275,14 +1462,16 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
 
 void oob_plan_destroy(oob_plan* p) {
     if (!p) return;
-    for (size_t k = 0; k < p->pools.size(); k++) {
-        cudaSetDevice(p->pr.jobs[k].dev);
-        auto& P = p->pools[k];
-        P->release_all();
-        if (P->ev0) cudaEventDestroy(P->ev0);
-        if (P->ev1) cudaEventDestroy(P->ev1);
-        if (P->stream) cudaStreamDestroy(P->stream);
-    }
+    for (auto& G : p->groups)
+        for (int w = 0; w < 3; w++) {
+            cudaSetDevice(G.dev);
+            DevicePool* P = G.pool[w];
+            P->release_all();
+            if (P->ev0) cudaEventDestroy(P->ev0);
+            if (P->ev1) cudaEventDestroy(P->ev1);
+            if (P->evr) cudaEventDestroy(P->evr);
+            if (P->stream) cudaStreamDestroy(P->stream);
+        }
     delete p;
 }
 

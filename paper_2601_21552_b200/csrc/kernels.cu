@@ -101,7 +101,7 @@ __device__ __forceinline__ void load_query(Lane<T>& L, const LaunchArgs& a, cons
     L.clean1 = 0;
 }
 
-enum : int { PH_IDLE = 0, PH_NODE = 1, PH_PASS = 2, PH_DONE = 3 };
+enum : int { PH_IDLE = 0, PH_NODE = 1, PH_PASS = 2, PH_DONE = 3, PH_POST = 4 };
 
 template <typename T>
 __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
@@ -138,18 +138,30 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
             if (phase == PH_IDLE) {
                 uint32_t q = base + __popc(idle & lt_mask);
                 if (q < cd.q_end) {
-                    qi = q;
-                    bind_class(L, a, cd);
-                    const QDesc d = a.qdesc[qi];
-                    load_query(L, a, d);
-                    nodes = passes = 0;
-                    t0 = global_ns();
-                    deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
-                    phase = PH_NODE;
+                    const uint32_t rs = a.resume ? a.resume[q] : 0u;
+                    if (rs != RES_SKIP) {
+                        qi = q;
+                        bind_class(L, a, cd);
+                        const QDesc d = a.qdesc[qi];
+                        load_query(L, a, d);
+                        if (rs & RES_ROOT) {  // demoted: resume the root node (format.h)
+                            nodes = 1;
+                            passes = rs & RES_PASSES;
+                            pin = (int)passes;
+                            t0 = a.heavy_t0[qi];
+                            phase = (rs & RES_FIX) ? PH_POST : PH_PASS;
+                        } else {
+                            nodes = passes = 0;
+                            t0 = global_ns();
+                            phase = PH_NODE;
+                        }
+                        deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
+                    }
                 }
             }
             idle = __ballot_sync(FULL, phase == PH_IDLE);
-            if (idle) {  // class c is exhausted: find the next class with work
+            if (idle && *(volatile uint32_t*)(a.class_next + c) >= cd.q_end) {
+                // class c is exhausted: find the next class with work
                 bool found = false;
                 for (uint32_t s = 1; s <= a.n_classes && !found; ++s) {
                     uint32_t c2 = (c + s) % a.n_classes;
@@ -197,7 +209,14 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
                 L.changed = false;
             }
         }
-        const bool run = (phase == PH_PASS);
+        // a resumed root node whose last pass (in the root kernel) changed
+        // nothing: only the pass-end step remains
+        const bool post = (phase == PH_POST);
+        if (post) {
+            L.changed = false;
+            phase = PH_PASS;
+        }
+        const bool run = (phase == PH_PASS) && !post;
         // ---- the pass: class-uniform constraint loop (solver.py:275-277) ----
         // The warp visits, in order, every constraint that is dirty in at
         // least one lane (clean ones would change nothing, engine.cuh).
@@ -210,7 +229,7 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
             k = kk + 1;
         }
         // ---- pass end ----
-        if (run) {
+        if (run || post) {
             if (dead) {
                 if (L.err) {
                     verdict = VERDICT_ERROR;
@@ -294,6 +313,97 @@ __global__ void __launch_bounds__(THREADS) oob_frontier_kernel(LaunchArgs a) {
     }
 }
 
+// Root phase of the wide regimes (format.h, "regime demotion"): one lane per
+// query runs the root node's propagate() passes (solver.py:264-280 under
+// _search's first call, :393) in the query's proven regime; after passes 1,
+// 2, 4, ... and at the fixpoint it restates the bound proof at the narrowed
+// domains (Lane::fit_regime) and, if a narrower regime holds, hands the
+// query's state to that regime's shadow entry.  A contradiction at the root
+// is the final verdict (Unsat after one node).  Queries that neither die nor
+// demote within ROOT_MAX_PASSES are left to this regime's lockstep kernel,
+// which restarts them from the declared domains.
+template <typename T, int SELF>
+__global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    Lane<T> L;
+    bind_scratch(L, a, warp, lane);
+    for (uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x; qi < a.n; qi += gridDim.x * blockDim.x) {
+        if (a.resume[qi] != 0u) continue;  // a shadow of a wider job's query
+        const QDesc d = a.qdesc[qi];
+        ClassDesc cd;
+        cd.code_off = d.code_off;
+        cd.nv_ncon = d.nv_ncon;
+        cd.ncode_nlit = d.ncode_nlit;
+        bind_class(L, a, cd);
+        load_query(L, a, d);
+        const uint64_t t0 = global_ns();
+        const uint64_t deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
+        uint32_t passes = 0;
+        bool dead = false, fix = false, expired = false;
+        int target = -1;
+        while (passes < ROOT_MAX_PASSES) {
+            if (deadline && global_ns() > deadline) {
+                expired = true;
+                break;
+            }
+            ++passes;
+            L.changed = false;
+            for (uint32_t k = L.next_dirty(0); k < L.ncon; k = L.next_dirty(k + 1)) {
+                if (!L.pass_constraint(k)) {
+                    dead = true;
+                    break;
+                }
+            }
+            if (dead) break;
+            fix = !L.changed;
+            if (fix || (passes & (passes - 1)) == 0) {
+                int r = L.fit_regime();
+                if (r < SELF && a.dem[r].slot) {
+                    target = r;
+                    break;
+                }
+            }
+            if (fix) break;
+        }
+        if (expired || L.err) continue;  // the lockstep kernel redoes it and reports
+        if (dead) {                      // Unsat after the root node (solver.py:393-394)
+            a.verdict[qi] = (int8_t)VERDICT_UNSAT;
+            a.err[qi] = (int8_t)ERR_NONE;
+            a.nodes[qi] = 1;
+            a.passes[qi] = passes;
+            a.elapsed[qi] = (float)((double)(global_ns() - t0) * 1e-9);
+            a.resume[qi] = RES_SKIP;
+            continue;
+        }
+        if (target < 0) continue;
+        const DemoteTarget& tg = a.dem[target];
+        const uint32_t s = tg.slot[qi];
+        int64_t* dst = tg.data + tg.qdesc[s].data_off;
+        if (target == 0) {
+            for (uint32_t v = 0; v < L.nv; ++v) {
+                dst[2 * v] = low64(L.E(L.env_lo, v));
+                dst[2 * v + 1] = low64(L.E(L.env_hi, v));
+            }
+            for (uint32_t i = 0; i < L.nlit; ++i) dst[2 * L.nv + i] = low64(L.E(L.lit, i));
+        } else {
+            auto put = [&](uint32_t at, __int128 x) {
+                dst[2 * at] = (int64_t)(uint64_t)x;
+                dst[2 * at + 1] = (int64_t)(x >> 64);
+            };
+            for (uint32_t v = 0; v < L.nv; ++v) {
+                put(2 * v, low128(L.E(L.env_lo, v)));
+                put(2 * v + 1, low128(L.E(L.env_hi, v)));
+            }
+            for (uint32_t i = 0; i < L.nlit; ++i) put(2 * L.nv + i, low128(L.E(L.lit, i)));
+        }
+        tg.t0[s] = t0;
+        __threadfence();
+        tg.resume[s] = RES_ROOT | (fix ? RES_FIX : 0u) | passes;
+        a.resume[qi] = RES_SKIP;
+    }
+}
+
 // propagate() / check_model() batches: one query per lane, no search
 template <typename T>
 __global__ void __launch_bounds__(THREADS) oob_aux_kernel(LaunchArgs a) {
@@ -365,6 +475,21 @@ static cudaError_t occupancy_impl(int mode, size_t smem, int* blocks_per_sm) {
         if (e != cudaSuccess) return e;
     }
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, THREADS, smem);
+}
+
+// root phase of a wide job (wide = 1 or 2)
+cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s) {
+    size_t smem = (size_t)a.g.smem_per_warp * (THREADS / 32);
+    if (wide == 2) {
+        cudaFuncSetAttribute((const void*)oob_root_kernel<i256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        oob_root_kernel<i256, 2><<<blocks, THREADS, smem, s>>>(a);
+    } else {
+        cudaFuncSetAttribute((const void*)oob_root_kernel<__int128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        oob_root_kernel<__int128, 1><<<blocks, THREADS, smem, s>>>(a);
+    }
+    return cudaGetLastError();
 }
 
 // wide: 0 = int64, 1 = __int128, 2 = 256-bit regime

@@ -27,17 +27,20 @@ def _by_timeout(recs):
 
 
 # heavy_nodes: 0 = default hand-off, -1 = one lane per query throughout,
-# 1 = every query goes through the warp-cooperative frontier kernel
+# 1 = every query goes through the warp-cooperative frontier kernel;
+# flags: 0 = wide-regime queries demote after their root phase, F_NO_DEMOTE =
+# they stay in their proven regime throughout
+@pytest.mark.parametrize("flags", [0, _lib.F_NO_DEMOTE])
 @pytest.mark.parametrize("heavy", [0, -1, 1])
 @pytest.mark.parametrize("name", GOLDEN_SETS)
-def test_golden_exact(gpu, name, heavy):
+def test_golden_exact(gpu, name, heavy, flags):
     recs = load_golden(name)
     for timeout, idx in _by_timeout(recs).items():
         sub = [recs[i] for i in idx if recs[i]["verdict"] != "timeout"]
         if not sub:
             continue
         fb = flatten(sub)
-        out = solve_flat(fb, timeout, heavy_nodes=heavy)
+        out = solve_flat(fb, timeout, heavy_nodes=heavy, flags=flags)
         for q, r in enumerate(sub):
             assert int(out["verdict"][q]) == VCODE[r["verdict"]], (name, heavy, q, r.get("name"))
             assert int(out["nodes"][q]) == r["nodes"], (name, heavy, q, "nodes")
@@ -89,6 +92,7 @@ def test_frontier_matches_sequential_on_synthetic_streams(gpu, cfg):
     a = solve_flat(fb, 30.0, heavy_nodes=-1)
     b = solve_flat(fb, 30.0, heavy_nodes=1)
     c = solve_flat(fb, 30.0)
-    for o in (b, c):
+    d = solve_flat(fb, 30.0, flags=_lib.F_NO_DEMOTE)
+    for o in (b, c, d):
         for k in ("verdict", "nodes", "passes", "model"):
             assert np.array_equal(a[k], o[k]), k
