@@ -128,8 +128,8 @@ struct LaunchArgs {
     // heavy-query hand-off: the lockstep kernel gives up a query after
     // heavy_nodes DFS nodes and queues it for the frontier kernel
     uint32_t heavy_nodes;     // 0 = never hand off
-    uint32_t* heavy_count;
-    uint32_t* heavy_list;
+    uint32_t* heavy_count;    // [0] listed [1] claimed [2] warps past lockstep [3] warps started
+    uint32_t* heavy_list;     // query index + 1 (0 = not yet published)
     uint64_t* heavy_t0;       // start time of each scheduled query (ns)
     uint32_t* heavy_next;     // frontier kernel work cursor
     // frontier scratch (one region per frontier warp, see frontier.cuh)
@@ -148,6 +148,7 @@ struct LaunchArgs {
     int64_t node_budget;      // >0 => deterministic budget
     int mode;                 // MODE_SOLVE / MODE_PROPAGATE / MODE_CHECK
     uint32_t* resume;         // per scheduled query (null: all fresh)
+    uint64_t* timeline;       // debug (SCUBA_OOB_TIMELINE): per entry start, hand-off, frontier start, end (ns)
     DemoteTarget dem[2];      // root kernel: [0] int64 job, [1] int128 job (slot null: none)
 };
 

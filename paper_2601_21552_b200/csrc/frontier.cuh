@@ -302,6 +302,7 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
         a.nodes[qi] = out_nodes;
         a.passes[qi] = out_passes;
         a.elapsed[qi] = (float)((double)(global_ns() - t0) * 1e-9);
+        if (a.timeline) a.timeline[4 * (size_t)qi + 3] = global_ns();
     }
     __syncwarp();
 }

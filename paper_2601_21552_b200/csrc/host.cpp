@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -48,6 +49,33 @@ static thread_local std::string g_last_error;
 static int fail(int code, const std::string& msg) {
     g_last_error = msg;
     return code;
+}
+
+// SCUBA_OOB_TRACE=1: per-phase host timings on stderr (compile, pack, stage,
+// kernels, fetch) -- the engine's only tracing hook
+static bool trace_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("SCUBA_OOB_TRACE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+struct Phase {
+    const char* name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit Phase(const char* n) : name(n) {}
+    ~Phase() {
+        if (trace_on())
+            std::fprintf(stderr, "[oob] %-10s %9.3f ms\n", name,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
+// SCUBA_OOB_TIMELINE=<file>: per-entry device timestamps of every solve run
+// appended to <file> (tools/timeline.py reads it)
+static const char* timeline_path() {
+    static const char* p = std::getenv("SCUBA_OOB_TIMELINE");
+    return (p && *p) ? p : nullptr;
 }
 
 static i128 from_w(oob_i128 w) { return (i128)(((unsigned __int128)(uint64_t)w.hi << 64) | w.lo); }
@@ -163,8 +191,67 @@ struct Compiled {
     std::vector<uint32_t> words;  // ncon constraint words + ncode node words
     std::vector<i128> lits;       // per literal slot
     double cost = 0;
+    uint64_t key = 0;             // structure-class hash (words, nv, ncon)
     std::string why;              // reason for R_RANGE
+    bool same_class(const Compiled& o) const {
+        return key == o.key && nv == o.nv && ncon == o.ncon && words == o.words;
+    }
 };
+
+// 64-bit FNV-1a over the structure words: the structure-class key
+inline uint64_t class_hash(const std::vector<uint32_t>& w, uint32_t nv, uint32_t ncon) {
+    uint64_t h = 1469598103934665603ull ^ ((uint64_t)nv << 32 | ncon);
+    for (uint32_t x : w) {
+        h ^= x;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+// Groups items by structure class.  Returns the class id of every item
+// (ids in order of first appearance) and the representative of each class.
+template <typename GetComp>
+void group_classes(size_t n, GetComp get, std::vector<uint32_t>& cls, std::vector<size_t>& rep) {
+    std::unordered_multimap<uint64_t, uint32_t> seen;
+    cls.resize(n);
+    rep.clear();
+    for (size_t i = 0; i < n; i++) {
+        const Compiled& c = get(i);
+        uint32_t id = UINT32_MAX;
+        auto range = seen.equal_range(c.key);
+        for (auto it = range.first; it != range.second; ++it)
+            if (get(rep[it->second]).same_class(c)) {
+                id = it->second;
+                break;
+            }
+        if (id == UINT32_MAX) {
+            id = (uint32_t)rep.size();
+            rep.push_back(i);
+            seen.emplace(c.key, id);
+        }
+        cls[i] = id;
+    }
+}
+
+template <typename F>
+void parallel_for(size_t n, size_t grain, F f) {
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (n < 2 * grain || nt == 1) {
+        f(0, n);
+        return;
+    }
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; t++)
+        th.emplace_back([&]() {
+            for (;;) {
+                size_t a = next.fetch_add(grain);
+                if (a >= n) break;
+                f(a, std::min(n, a + grain));
+            }
+        });
+    for (auto& t : th) t.join();
+}
 
 struct Emitter {
     const QView& v;
@@ -458,6 +545,7 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
         }
     }
     out.words.insert(out.words.end(), member.begin(), member.end());
+    out.key = class_hash(out.words, out.nv, out.ncon);
     return out;
 }
 
@@ -486,14 +574,14 @@ struct DevicePool {
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
     DevBuf classes, class_next, class_init, warp_class;
     DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
-    DevBuf resume, resume_init, slot64, slot128;
+    DevBuf resume, resume_init, slot64, slot128, timeline;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evr = nullptr;
     int sms = 148;
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
-                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128})
+                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &timeline})
             b->release();
     }
 };
@@ -622,107 +710,105 @@ struct DevJob {
 void pack(const RunCtx& rc, DevJob& j) {
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
-    // group the job's queries by structure class, keeping their order within
-    // a class (the lockstep kernel runs each warp on one class)
-    std::unordered_map<std::string, uint32_t> cls_of;
-    std::vector<std::vector<int64_t>> members;  // entries: query id, or ~id for a shadow
-    std::vector<uint32_t> code_off;
-    j.code.clear();
-    std::vector<int64_t> entries(j.qs);
+    // group the job's entries (own queries, then shadows) by structure class,
+    // keeping their order within a class (the lockstep kernel runs each warp
+    // on one class)
+    std::vector<int64_t> entries(j.qs);  // query id, or ~id for a shadow
     for (int64_t q : j.shadows) entries.push_back(~q);
-    for (int64_t e : entries) {
-        const int64_t q = e < 0 ? ~e : e;
-        const Compiled& c = comp[q];
-        std::string key((const char*)c.words.data(), c.words.size() * 4);
-        key.append((const char*)&c.nv, 4);
-        key.append((const char*)&c.ncon, 4);
-        auto it = cls_of.find(key);
-        uint32_t id;
-        if (it == cls_of.end()) {
-            id = (uint32_t)members.size();
-            cls_of.emplace(std::move(key), id);
-            members.emplace_back();
-            code_off.push_back((uint32_t)j.code.size());
-            j.code.insert(j.code.end(), c.words.begin(), c.words.end());
-        } else {
-            id = it->second;
-        }
-        members[id].push_back(e);
+    auto qid = [](int64_t e) { return e < 0 ? ~e : e; };
+    std::vector<uint32_t> cls;
+    std::vector<size_t> rep;
+    group_classes(entries.size(), [&](size_t i) -> const Compiled& { return comp[qid(entries[i])]; }, cls, rep);
+    const size_t nc = rep.size();
+    std::vector<uint32_t> count(nc + 1, 0);
+    for (uint32_t c : cls) count[c + 1]++;
+    for (size_t c = 0; c < nc; c++) count[c + 1] += count[c];
+    std::vector<int64_t> order(entries.size());
+    {
+        std::vector<uint32_t> at(count.begin(), count.end() - 1);
+        for (size_t i = 0; i < entries.size(); i++) order[at[cls[i]]++] = entries[i];
     }
-    j.qs.clear();
-    j.is_shadow.clear();
-    j.resume_init.clear();
-    j.cls.clear();
-    for (size_t id = 0; id < members.size(); id++) {
-        const int64_t e0 = members[id][0];
-        const Compiled& c = comp[e0 < 0 ? ~e0 : e0];
-        ClassDesc cd{};
-        cd.code_off = code_off[id];
+    j.code.clear();
+    j.cls.assign(nc, ClassDesc{});
+    for (size_t id = 0; id < nc; id++) {
+        const Compiled& c = comp[qid(entries[rep[id]])];
+        ClassDesc& cd = j.cls[id];
+        cd.code_off = (uint32_t)j.code.size();
+        j.code.insert(j.code.end(), c.words.begin(), c.words.end());
         cd.nv_ncon = c.nv | (c.ncon << 16);
         cd.ncode_nlit = c.ncode | (c.nlit << 16);
-        cd.q_begin = (uint32_t)j.qs.size();
-        for (int64_t e : members[id]) {
-            j.qs.push_back(e < 0 ? ~e : e);
-            j.is_shadow.push_back(e < 0);
-            j.resume_init.push_back(e < 0 ? RES_SKIP : 0u);
-        }
-        cd.q_end = (uint32_t)j.qs.size();
-        j.cls.push_back(cd);
+        cd.q_begin = count[id];
+        cd.q_end = count[id + 1];
     }
-    j.n_classes = (uint32_t)j.cls.size();
-    j.data.clear();
-    j.qd.assign(j.qs.size(), QDesc{});
-    j.mo.assign(j.qs.size(), 0);
+    j.n_classes = (uint32_t)nc;
+    const size_t n = order.size();
+    j.qs.resize(n);
+    j.is_shadow.resize(n);
+    j.resume_init.resize(n);
+    j.qd.assign(n, QDesc{});
+    j.mo.assign(n, 0);
+    // data layout: per entry (2 nv + nlit) values of the job's width, padded
+    // to 16 (int64/int128) or 32 bytes (256-bit)
+    const size_t vw = j.wide == 2 ? 4 : (size_t)j.wide + 1;  // int64 words per value
+    const size_t align = j.wide == 2 ? 4 : 2;
+    std::vector<uint64_t> doff(n + 1, 0);
     j.model_words = 0;
     size_t ci = 0;
-    for (size_t i = 0; i < j.qs.size(); i++) {
+    for (size_t i = 0; i < n; i++) {
         while (i >= j.cls[ci].q_end) ci++;
-        const Compiled& c = comp[j.qs[i]];
+        const int64_t e = order[i];
+        const Compiled& c = comp[qid(e)];
+        j.qs[i] = qid(e);
+        j.is_shadow[i] = e < 0;
+        j.resume_init[i] = e < 0 ? RES_SKIP : 0u;
         QDesc& d = j.qd[i];
         d.code_off = j.cls[ci].code_off;
         d.nv_ncon = c.nv | (c.ncon << 16);
         d.ncode_nlit = c.ncode | (c.nlit << 16);
         d.out_q = (uint32_t)i;
-        d.data_off = j.data.size();
+        d.data_off = doff[i];
         d.out_v = j.model_words;
         j.mo[i] = j.model_words;
         j.model_words += c.nv;
+        size_t words = (2 * (size_t)c.nv + c.nlit) * vw;
+        doff[i + 1] = doff[i] + ((words + align - 1) / align) * align;
         j.maxv = std::max(j.maxv, c.nv);
         j.maxcode = std::max(j.maxcode, c.ncode);
         j.maxlit = std::max(j.maxlit, c.nlit);
         j.maxcsize = std::max(j.maxcsize, c.maxcsize);
         j.maxdepth = std::max(j.maxdepth, c.maxdepth);
-        int64_t q = j.qs[i];
-        int64_t vb = b->var_begin[q];
-        auto push = [&](i128 x) {
-            j.data.push_back((int64_t)(uint64_t)x);
-            if (j.wide >= 1) j.data.push_back((int64_t)(x >> 64));
-            if (j.wide == 2) {
-                int64_t s = x < 0 ? -1 : 0;
-                j.data.push_back(s);
-                j.data.push_back(s);
-            }
-        };
-        if (j.is_shadow[i]) {  // written on the device by the root kernel
-            j.data.resize(j.data.size() + (size_t)(2 * c.nv + c.nlit) * (j.wide == 2 ? 4 : j.wide + 1), 0);
-            while (j.data.size() & (j.wide == 2 ? 3 : 1)) j.data.push_back(0);
-            continue;
-        }
-        for (uint32_t v = 0; v < c.nv; v++) {
-            if (rc.mode == MODE_CHECK) {
-                i128 m = from_w(rc.model[vb + v]);
-                push(m);
-                push(m);
-            } else {
-                push(from_w(b->var_lo[vb + v]));
-                push(from_w(b->var_hi[vb + v]));
-            }
-        }
-        for (i128 l : c.lits) push(l);
-        while (j.data.size() & (j.wide == 2 ? 3 : 1)) j.data.push_back(0);
     }
+    j.data.assign(std::max<uint64_t>(doff[n], 4), 0);
+    parallel_for(n, 4096, [&](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; i++) {
+            if (j.is_shadow[i]) continue;  // written on the device by the root kernel
+            const int64_t q = j.qs[i];
+            const Compiled& c = comp[q];
+            int64_t* out = j.data.data() + doff[i];
+            auto put = [&](i128 x) {
+                *out++ = (int64_t)(uint64_t)x;
+                if (vw >= 2) *out++ = (int64_t)(x >> 64);
+                if (vw == 4) {
+                    int64_t sgn = x < 0 ? -1 : 0;
+                    *out++ = sgn;
+                    *out++ = sgn;
+                }
+            };
+            const int64_t vb = b->var_begin[q];
+            for (uint32_t v = 0; v < c.nv; v++) {
+                if (rc.mode == MODE_CHECK) {
+                    i128 m = from_w(rc.model[vb + v]);
+                    put(m);
+                    put(m);
+                } else {
+                    put(from_w(b->var_lo[vb + v]));
+                    put(from_w(b->var_hi[vb + v]));
+                }
+            }
+            for (i128 l : c.lits) put(l);
+        }
+    });
     if (j.code.empty()) j.code.push_back(0);
-    if (j.data.empty()) j.data.resize(4);
     if (j.cls.empty()) j.cls.push_back(ClassDesc{});
 }
 
@@ -743,8 +829,7 @@ void assign_warps(DevJob& j, uint32_t n_warps) {
 
 // allocate + upload the packed records of `j` into pool P (caller holds P->mu)
 constexpr uint32_t FR_ECAP = 2048, FR_UCAP = 4096, FR_LOGCAP = 32768;
-constexpr uint32_t HEAVY_NODES_DEFAULT = 32;
-constexpr uint32_t FR_WARPS_PER_SM = 4;
+constexpr uint32_t HEAVY_NODES_DEFAULT = 16;
 
 size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
     size_t b = (size_t)FR_ECAP * 2 * maxv * tbytes + 2 * (size_t)FR_ECAP * tbytes + (size_t)FR_ECAP * 16 +
@@ -777,7 +862,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     // heavy-query hand-off (solve mode): threshold from the options
     int64_t hn = rc.opt.heavy_nodes;
     uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
-    j.fblocks = heavy_nodes ? std::min<uint32_t>(j.blocks, (uint32_t)P->sms * FR_WARPS_PER_SM / WARPS_PER_BLOCK) : 0;
+    j.fblocks = heavy_nodes ? j.blocks : 0;  // one frontier scratch region per warp of the grid
     const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
@@ -856,6 +941,11 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.node_budget = rc.opt.node_budget;
     a.mode = rc.mode;
     a.resume = (uint32_t*)P->resume.p;
+    a.timeline = nullptr;
+    if (timeline_path() && rc.mode == MODE_SOLVE) {
+        CK(P->timeline.ensure((size_t)n * 32));
+        a.timeline = (uint64_t*)P->timeline.p;
+    }
     j.staged = true;
     return "";
 }
@@ -954,7 +1044,9 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         const size_t n = j.qs.size();
         CK(cudaMemsetAsync(P->next.p, 0, 4, s0));
         CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s0));
-        CK(cudaMemsetAsync(P->heavy_count.p, 0, 8, s0));
+        CK(cudaMemsetAsync(P->heavy_count.p, 0, 16, s0));
+        if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 4, s0));
+        if (j.a.timeline) CK(cudaMemsetAsync(j.a.timeline, 0, n * 32, s0));
         CK(cudaMemsetAsync(P->verdict.p, 0xFF, n, s0));
         CK(cudaMemcpyAsync(P->resume.p, P->resume_init.p, n * 4, cudaMemcpyDeviceToDevice, s0));
     }
@@ -1022,6 +1114,21 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
     if (j.out_model_words)
         CK(cudaMemcpyAsync(mw.data(), P->model.p, j.out_model_words * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (j.a.timeline) {  // records: q, wide, shadow, verdict, nodes, passes, 4 timestamps (int64 each)
+        std::vector<uint64_t> tl((size_t)n * 4);
+        CK(cudaMemcpy(tl.data(), j.a.timeline, (size_t)n * 32, cudaMemcpyDeviceToHost));
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lk(mu);
+        if (FILE* f = std::fopen(timeline_path(), "ab")) {
+            for (uint32_t i = 0; i < n; i++) {
+                int64_t rec[10] = {j.qs[i], j.wide, j.is_shadow[i], verdict[i], nodes[i], passes[i],
+                                   (int64_t)tl[4 * i], (int64_t)tl[4 * i + 1], (int64_t)tl[4 * i + 2],
+                                   (int64_t)tl[4 * i + 3]};
+                std::fwrite(rec, sizeof rec, 1, f);
+            }
+            std::fclose(f);
+        }
+    }
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
     for (uint32_t i = 0; i < n; i++) {
@@ -1078,13 +1185,31 @@ std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
             G.job[w].qs = cur[w];
             G.pool[w] = pools[w];
         }
-        pack_group(rc, G);
+        {
+            Phase ph("pack");
+            pack_group(rc, G);
+        }
         std::vector<int64_t> retry[3];
         {
             std::lock_guard<std::mutex> l0(pools[0]->mu), l1(pools[1]->mu), l2(pools[2]->mu);
-            std::string e = stage_group(rc, G, depth_cap, trail_cap, round == 0);
-            if (e.empty()) e = launch_group(rc, G);
-            if (e.empty()) e = fetch_group(rc, G, retry);
+            std::string e;
+            {
+                Phase ph("stage");
+                e = stage_group(rc, G, depth_cap, trail_cap, round == 0);
+                for (int w = 0; w < 3 && e.empty(); w++)
+                    if (present(G.job[w]) && cudaStreamSynchronize(G.pool[w]->stream) != cudaSuccess)
+                        e = "stage sync failed";
+            }
+            if (e.empty()) {
+                Phase ph("kernels");
+                e = launch_group(rc, G);
+                float ms = 0;
+                if (e.empty()) e = group_ms(G, &ms);
+            }
+            if (e.empty()) {
+                Phase ph("fetch");
+                e = fetch_group(rc, G, retry);
+            }
             if (!e.empty()) return e;
         }
         for (int w = 0; w < 3; w++) cur[w].swap(retry[w]);
@@ -1143,13 +1268,17 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     const oob_options& opt = pr.opt;
     const int64_t n = b->n_queries;
     auto t0 = std::chrono::steady_clock::now();
-    for (int64_t q = 0; q < n; q++) {
-        std::string why = validate(b, q);
-        if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
+    {
+        Phase ph("validate");
+        for (int64_t q = 0; q < n; q++) {
+            std::string why = validate(b, q);
+            if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
+        }
     }
     std::vector<Compiled>& comp = pr.comp;
     comp.assign(n, Compiled{});
     {
+        Phase ph("compile");
         unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         if (n < 2048) nt = 1;
         std::vector<std::thread> th;
@@ -1191,6 +1320,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         return fail(OOB_E_CUDA, "device ordinal out of range");
     int want = opt.n_gpus > 0 ? opt.n_gpus : ndev - first;
     want = std::max(1, std::min(want, ndev - first));
+    Phase ph_sched("schedule");
     if (n_dev_q > 0) {
         pr.work.resize(want);
         for (int d = 0; d < want; d++) pr.work[d].dev = first + d;
@@ -1200,15 +1330,11 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         if (qs.empty()) continue;
         if (!(opt.flags & OOB_F_NO_SORT)) {
             // class-major, cost-minor: a 32-query tile is (nearly) one class
-            std::unordered_map<std::string, uint32_t> cid;
+            std::vector<uint32_t> cls;
+            std::vector<size_t> rep;
+            group_classes(qs.size(), [&](size_t i) -> const Compiled& { return comp[qs[i]]; }, cls, rep);
             std::vector<uint32_t> key(n, 0);
-            for (int64_t q : qs) {
-                const Compiled& c = comp[q];
-                std::string k((const char*)c.words.data(), c.words.size() * 4);
-                k.append((const char*)&c.nv, 4);
-                auto it = cid.emplace(std::move(k), (uint32_t)cid.size()).first;
-                key[q] = it->second;
-            }
+            for (size_t i = 0; i < qs.size(); i++) key[qs[i]] = cls[i];
             std::stable_sort(qs.begin(), qs.end(), [&](int64_t x, int64_t y) {
                 if (key[x] != key[y]) return key[x] < key[y];
                 return comp[x].cost > comp[y].cost;
@@ -1447,7 +1573,7 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
             cls += j.n_classes;
             if (w) wide += own;
             jobs++;
-            launches += 1 + (j.fblocks ? 1 : 0) + ((w && (!j.slot[0].empty() || !j.slot[1].empty())) ? 1 : 0);
+            launches += 1 + ((w && (!j.slot[0].empty() || !j.slot[1].empty())) ? 1 : 0);
         }
     info[0] = nq;
     info[1] = rec;

@@ -103,15 +103,12 @@ __device__ __forceinline__ void load_query(Lane<T>& L, const LaunchArgs& a, cons
 
 enum : int { PH_IDLE = 0, PH_NODE = 1, PH_PASS = 2, PH_DONE = 3, PH_POST = 4 };
 
+// Phase 1 of the solve kernel: lockstep class queues (returns when the warp's
+// lanes are idle and every class queue is drained).
 template <typename T>
-__global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, Lane<T>& L, uint32_t warp, uint32_t lane) {
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << lane) - 1u;
-
-    Lane<T> L;
-    bind_scratch(L, a, warp, lane);
 
     uint32_t c = a.warp_class[warp];  // the warp's current class queue (warp-uniform)
     ClassDesc cd = a.classes[c];
@@ -156,6 +153,7 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
                             phase = PH_NODE;
                         }
                         deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
+                        if (a.timeline) a.timeline[4 * (size_t)qi] = t0;
                     }
                 }
             }
@@ -179,11 +177,14 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
 
         // ---- node start (_search, solver.py:391-393) ----
         if (phase == PH_NODE && a.heavy_nodes && nodes >= a.heavy_nodes) {
-            // a heavy search: hand it to the warp-cooperative frontier kernel
-            // (which restarts it from the root with 32 lanes)
+            // a heavy search: hand it to the warp-cooperative frontier phase
+            // (which restarts it from the root with 32 lanes); the list entry
+            // is published after the start time it carries
             uint32_t slot = atomicAdd(a.heavy_count, 1u);
-            a.heavy_list[slot] = qi;
             a.heavy_t0[qi] = t0;
+            if (a.timeline) a.timeline[4 * (size_t)qi + 1] = global_ns();
+            __threadfence();
+            *(volatile uint32_t*)(a.heavy_list + slot) = qi + 1u;
             phase = PH_IDLE;
         }
         if (phase == PH_NODE) {
@@ -276,6 +277,7 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
             a.nodes[qi] = nodes;
             a.passes[qi] = passes;
             a.elapsed[qi] = (float)((double)(global_ns() - t0) * 1e-9);
+            if (a.timeline) a.timeline[4 * (size_t)qi + 3] = global_ns();
             if (verdict == VERDICT_SAT) {
                 int64_t* m = a.model + 2 * d.out_v;
                 for (uint32_t v = 0; v < L.nv; ++v) store_i128(m + 2 * v, L.E(L.env_lo, v));
@@ -285,23 +287,55 @@ __global__ void __launch_bounds__(THREADS) oob_lockstep_kernel(LaunchArgs a) {
     }
 }
 
-// heavy queries: one warp per query, lanes expand the leftmost pending nodes
+// Phase 2 of the solve kernel: heavy queries, one warp per query, lanes
+// expand the leftmost pending nodes (frontier.cuh).  A warp whose lockstep
+// phase is over claims a scratch region and serves the heavy list, which the
+// lockstep warps still running keep appending to; it leaves once every
+// lockstep warp has finished and the list is exhausted.
 template <typename T>
-__global__ void __launch_bounds__(THREADS) oob_frontier_kernel(LaunchArgs a) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    Lane<T> L;
-    bind_scratch(L, a, warp, lane);
-    FrontierRegion<T> R;
+__device__ __forceinline__ void frontier_phase(const LaunchArgs& a, Lane<T>& L, uint32_t warp, uint32_t lane) {
+    const unsigned FULL = 0xffffffffu;
+    // [0] listed [1] claimed [2] warps past their lockstep phase [3] warps started
+    volatile uint32_t* ctl = a.heavy_count;
+    if (lane == 0) {
+        __threadfence();
+        atomicAdd(a.heavy_count + 2, 1u);
+    }
+    if (!a.heavy_nodes) return;
+    FrontierRegion<T> R;  // one scratch region per warp of the grid
     R.bind((unsigned char*)a.fr_region + (size_t)warp * a.fr_region_bytes, a.g.maxv, a.fr_ecap, a.fr_ucap,
            a.fr_logcap);
-    const uint32_t n_heavy = *(volatile uint32_t*)a.heavy_count;
     for (;;) {
-        uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(a.heavy_next, 1u);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= n_heavy) break;
-        const uint32_t qi = a.heavy_list[idx];
+        int idx = -1;
+        if (lane == 0) {
+            for (;;) {
+                // producers finish appending before they count as done; a
+                // warp that has not started yet serves its own entries later,
+                // so nothing here waits on blocks that are not resident
+                const uint32_t done = ctl[2];
+                const uint32_t started = ctl[3];
+                __threadfence();
+                const uint32_t listed = ctl[0], claimed = ctl[1];
+                if (claimed < listed) {
+                    if (atomicCAS(a.heavy_count + 1, claimed, claimed + 1) == claimed) {
+                        idx = (int)claimed;
+                        break;
+                    }
+                    continue;
+                }
+                if (done >= started) break;  // every started producer is done: the list is final for us
+                __nanosleep(2000);
+            }
+        }
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx < 0) break;
+        uint32_t e = 0;
+        if (lane == 0)
+            while ((e = *(volatile uint32_t*)(a.heavy_list + idx)) == 0u) __nanosleep(100);
+        e = __shfl_sync(FULL, e, 0);
+        __threadfence();
+        const uint32_t qi = e - 1u;
+        if (a.timeline && lane == 0) a.timeline[4 * (size_t)qi + 2] = global_ns();
         const QDesc d = a.qdesc[qi];
         ClassDesc cd;
         cd.code_off = d.code_off;
@@ -311,6 +345,18 @@ __global__ void __launch_bounds__(THREADS) oob_frontier_kernel(LaunchArgs a) {
         load_query(L, a, d);
         frontier_query(L, a, R, qi, lane);
     }
+}
+
+// K1 + K4: the solve kernel (persistent; lockstep phase, then frontier phase)
+template <typename T>
+__global__ void __launch_bounds__(THREADS) oob_solve_kernel(LaunchArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    Lane<T> L;
+    bind_scratch(L, a, warp, lane);
+    if (lane == 0) atomicAdd(a.heavy_count + 3, 1u);
+    lockstep_phase(a, L, warp, lane);
+    frontier_phase(a, L, warp, lane);
 }
 
 // Root phase of the wide regimes (format.h, "regime demotion"): one lane per
@@ -373,6 +419,10 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
             a.nodes[qi] = 1;
             a.passes[qi] = passes;
             a.elapsed[qi] = (float)((double)(global_ns() - t0) * 1e-9);
+            if (a.timeline) {
+                a.timeline[4 * (size_t)qi] = t0;
+                a.timeline[4 * (size_t)qi + 3] = global_ns();
+            }
             a.resume[qi] = RES_SKIP;
             continue;
         }
@@ -445,19 +495,15 @@ __global__ void __launch_bounds__(THREADS) oob_aux_kernel(LaunchArgs a) {
 
 template <typename T>
 static const void* kernel_ptr(int mode) {
-    return mode == MODE_SOLVE ? (const void*)oob_lockstep_kernel<T> : (const void*)oob_aux_kernel<T>;
+    return mode == MODE_SOLVE ? (const void*)oob_solve_kernel<T> : (const void*)oob_aux_kernel<T>;
 }
 
 template <typename T>
 static cudaError_t launch_impl(const LaunchArgs& a, int blocks, int fblocks, cudaStream_t s) {
     size_t smem = (size_t)a.g.smem_per_warp * (THREADS / 32);
+    (void)fblocks;
     if (a.mode == MODE_SOLVE) {
-        oob_lockstep_kernel<T><<<blocks, THREADS, smem, s>>>(a);
-        if (a.heavy_nodes && fblocks > 0) {
-            cudaError_t e = cudaGetLastError();
-            if (e != cudaSuccess) return e;
-            oob_frontier_kernel<T><<<fblocks, THREADS, smem, s>>>(a);
-        }
+        oob_solve_kernel<T><<<blocks, THREADS, smem, s>>>(a);
     } else {
         oob_aux_kernel<T><<<blocks, THREADS, smem, s>>>(a);
     }
@@ -469,11 +515,6 @@ static cudaError_t occupancy_impl(int mode, size_t smem, int* blocks_per_sm) {
     const void* fn = kernel_ptr<T>(mode);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (mode == MODE_SOLVE) {
-        e = cudaFuncSetAttribute((const void*)oob_frontier_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        if (e != cudaSuccess) return e;
-    }
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, THREADS, smem);
 }
 

@@ -11,3 +11,4 @@ heavy = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 fb = synth.generate(cfg, n, names=False)
 plan = _lib.Plan(fb, 30.0, n_gpus=1, device=0, heavy_nodes=heavy)
 print(plan.info(), "ms", plan.run())
+if __import__("os").environ.get("SCUBA_OOB_TIMELINE"): plan.results()
