@@ -128,7 +128,7 @@ struct LaunchArgs {
     // heavy-query hand-off: the lockstep kernel gives up a query after
     // heavy_nodes DFS nodes and queues it for the frontier kernel
     uint32_t heavy_nodes;     // 0 = never hand off
-    uint32_t* heavy_count;    // [0] listed [1] claimed [2] warps past lockstep [3] warps started
+    uint32_t* heavy_count;    // [0] listed [1] claimed
     uint32_t* heavy_list;     // query index + 1 (0 = not yet published)
     uint64_t* heavy_t0;       // start time of each scheduled query (ns)
     uint32_t* heavy_next;     // frontier kernel work cursor

@@ -289,18 +289,15 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, Lane<T>& L, 
 
 // Phase 2 of the solve kernel: heavy queries, one warp per query, lanes
 // expand the leftmost pending nodes (frontier.cuh).  A warp whose lockstep
-// phase is over claims a scratch region and serves the heavy list, which the
-// lockstep warps still running keep appending to; it leaves once every
-// lockstep warp has finished and the list is exhausted.
+// phase is over serves the heavy list until it finds nothing left to claim,
+// then exits (it never spins: an idle resident warp would keep the SMs from
+// the other regimes' kernels).  An entry appended later comes from a warp
+// still in its lockstep phase, which serves the list itself afterwards, so
+// every entry is taken.
 template <typename T>
 __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, Lane<T>& L, uint32_t warp, uint32_t lane) {
     const unsigned FULL = 0xffffffffu;
-    // [0] listed [1] claimed [2] warps past their lockstep phase [3] warps started
-    volatile uint32_t* ctl = a.heavy_count;
-    if (lane == 0) {
-        __threadfence();
-        atomicAdd(a.heavy_count + 2, 1u);
-    }
+    volatile uint32_t* ctl = a.heavy_count;  // [0] listed [1] claimed
     if (!a.heavy_nodes) return;
     FrontierRegion<T> R;  // one scratch region per warp of the grid
     R.bind((unsigned char*)a.fr_region + (size_t)warp * a.fr_region_bytes, a.g.maxv, a.fr_ecap, a.fr_ucap,
@@ -309,22 +306,12 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, Lane<T>& L, 
         int idx = -1;
         if (lane == 0) {
             for (;;) {
-                // producers finish appending before they count as done; a
-                // warp that has not started yet serves its own entries later,
-                // so nothing here waits on blocks that are not resident
-                const uint32_t done = ctl[2];
-                const uint32_t started = ctl[3];
-                __threadfence();
                 const uint32_t listed = ctl[0], claimed = ctl[1];
-                if (claimed < listed) {
-                    if (atomicCAS(a.heavy_count + 1, claimed, claimed + 1) == claimed) {
-                        idx = (int)claimed;
-                        break;
-                    }
-                    continue;
+                if (claimed >= listed) break;
+                if (atomicCAS(a.heavy_count + 1, claimed, claimed + 1) == claimed) {
+                    idx = (int)claimed;
+                    break;
                 }
-                if (done >= started) break;  // every started producer is done: the list is final for us
-                __nanosleep(2000);
             }
         }
         idx = __shfl_sync(FULL, idx, 0);
@@ -354,7 +341,6 @@ __global__ void __launch_bounds__(THREADS) oob_solve_kernel(LaunchArgs a) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     Lane<T> L;
     bind_scratch(L, a, warp, lane);
-    if (lane == 0) atomicAdd(a.heavy_count + 3, 1u);
     lockstep_phase(a, L, warp, lane);
     frontier_phase(a, L, warp, lane);
 }
