@@ -99,8 +99,14 @@ __device__ __forceinline__ uint64_t global_ns() {
     return t;
 }
 
-template <typename T>
+extern __shared__ __align__(16) unsigned char oob_smem[];
+
+// The interpreting lane: one query's search state, driven by the class's code
+// words.  lockstep_phase / frontier_phase (phases.cuh) drive any lane type
+// with this interface; jit_lane.cuh provides the compiled counterpart.
+template <typename TT>
 struct Lane {
+    using T = TT;
     using A = Arith<T>;
     // lane-minor scratch views (element i of this lane is p[i * 32])
     T* env_lo;
@@ -483,6 +489,99 @@ struct Lane {
             if (!ok) return false;
         }
         return true;
+    }
+
+    // ----- the lane interface used by the scheduling phases (phases.cuh) -------
+    __device__ __forceinline__ T get_lo(uint32_t v) const { return E(env_lo, v); }
+    __device__ __forceinline__ T get_hi(uint32_t v) const { return E(env_hi, v); }
+    __device__ __forceinline__ void put_env(uint32_t v, T lo, T hi) {
+        E(env_lo, v) = lo;
+        E(env_hi, v) = hi;
+    }
+    __device__ __forceinline__ uint32_t nvars() const { return nv; }
+    __device__ __forceinline__ bool check_env() { return check_point(env_lo); }
+    // One propagation pass of every lane with run set, warp-synchronously: the
+    // warp visits, in order, every constraint that is dirty in at least one
+    // lane (clean ones would change nothing), so constraint k's code words are
+    // warp-uniform.  Returns true if this lane's pass hit a contradiction.
+    __device__ __forceinline__ bool pass_sync(bool run) {
+        bool dead = false;
+        for (uint32_t k = 0;;) {
+            uint32_t mine = (run && !dead) ? next_dirty(k) : 0xFFFFu;
+            if (mine >= ncon) mine = 0xFFFFu;  // lanes may be on different classes
+            uint32_t kk = __reduce_min_sync(0xffffffffu, mine);
+            if (kk == 0xFFFFu) break;
+            if (mine == kk && !pass_constraint(kk)) dead = true;
+            k = kk + 1;
+        }
+        return dead;
+    }
+
+    // per-warp scratch binding (host-computed SlabGeom)
+    __device__ void bind(const LaunchArgs& a, uint32_t warp, uint32_t lane) {
+        const SlabGeom& gg = a.g;
+        T* sT = reinterpret_cast<T*>(a.slab_T) + (size_t)warp * gg.slab_T_words + lane;
+        uint32_t* sU = a.slab_u32 + (size_t)warp * gg.slab_u32_words + lane;
+        if (gg.smem_per_warp) {  // hot state on chip, lane-minor (conflict-free in lockstep)
+            T* s = reinterpret_cast<T*>(oob_smem + (threadIdx.x >> 5) * gg.smem_per_warp) + lane;
+            env_lo = s + gg.o_s_env_lo;
+            env_hi = s + gg.o_s_env_hi;
+            val_lo = s + gg.o_s_val_lo;
+            val_hi = s + gg.o_s_val_hi;
+            lit = sT + gg.o_lit;
+            st_0 = s + gg.o_s_st0;
+            st_1 = s + gg.o_s_st1;
+            st_n = reinterpret_cast<uint32_t*>(oob_smem + (threadIdx.x >> 5) * gg.smem_per_warp + gg.o_s_stn_bytes) +
+                   lane;
+        } else {
+            env_lo = sT + gg.o_env_lo;
+            env_hi = sT + gg.o_env_hi;
+            val_lo = sT + gg.o_val_lo;
+            val_hi = sT + gg.o_val_hi;
+            lit = sT + gg.o_lit;
+            st_0 = sT + gg.o_st0;
+            st_1 = sT + gg.o_st1;
+            st_n = sU + gg.o_stn;
+        }
+        st_cap = gg.st_cap;
+        fr_mid = sT + gg.o_fr_mid;
+        fr_hi = sT + gg.o_fr_hi;
+        tr_lo = sT + gg.o_tr_lo;
+        tr_hi = sT + gg.o_tr_hi;
+        stamp = sU + gg.o_stamp;
+        fr_pick = sU + gg.o_fr_pick;
+        fr_mark = sU + gg.o_fr_mark;
+        fr_clean = sU + gg.o_fr_clean;
+        tr_var = sU + gg.o_tr_var;
+        g = &a.g;
+        seg = 0;
+    }
+
+    __device__ __forceinline__ void set_class(const LaunchArgs& a, const ClassDesc& c) {
+        nv = c.nv_ncon & 0xFFFFu;
+        ncon = c.nv_ncon >> 16;
+        ncode = c.ncode_nlit & 0xFFFFu;
+        nlit = c.ncode_nlit >> 16;
+        cons = a.code + c.code_off;
+        code = cons + ncon;
+        member = code + ncode;
+        skip = ncon <= 128;
+    }
+
+    // stage a query's domains and literal slots into lane-minor scratch
+    __device__ __forceinline__ void load(const LaunchArgs& a, const QDesc& d) {
+        const T* src = reinterpret_cast<const T*>(a.data + d.data_off);
+        for (uint32_t v = 0; v < nv; ++v) {
+            E(env_lo, v) = src[2 * v];
+            E(env_hi, v) = src[2 * v + 1];
+            U(stamp, v) = 0xFFFFFFFFu;
+        }
+        for (uint32_t i = 0; i < nlit; ++i) E(lit, i) = src[2 * nv + i];
+        err = ERR_NONE;
+        depth = 0;
+        trail_len = 0;
+        clean0 = 0;
+        clean1 = 0;
     }
 
     // ----- regime demotion (root kernel) ----------------------------------------

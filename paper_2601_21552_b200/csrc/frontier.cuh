@@ -72,12 +72,13 @@ __device__ __forceinline__ bool path_le(uint64_t a0, uint64_t a1, uint32_t da, u
 
 enum : int { FN_DEAD = 0, FN_SAT = 1, FN_SPLIT = 2, FN_NONE = 3 };
 
-template <typename T>
-__device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T>& R, uint32_t qi,
+template <typename LaneT>
+__device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typename LaneT::T>& R, uint32_t qi,
                                uint32_t lane) {
+    using T = typename LaneT::T;
     const unsigned FULL = 0xffffffffu;
     const QDesc d = a.qdesc[qi];
-    const uint32_t nv = L.nv;
+    const uint32_t nv = L.nvars();
     const uint32_t ecap = a.fr_ecap, ucap = a.fr_ucap, logcap = a.fr_logcap;
     const uint64_t t0 = a.heavy_t0[qi];
     const uint64_t deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
@@ -119,10 +120,7 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
             if (u != UNIT_ROOT) {
                 uint32_t e = u >> 1, half = u & 1;
                 const T* env = R.e_env + (size_t)e * 2 * nv;
-                for (uint32_t v = 0; v < nv; ++v) {
-                    L.E(L.env_lo, v) = env[2 * v];
-                    L.E(L.env_hi, v) = env[2 * v + 1];
-                }
+                for (uint32_t v = 0; v < nv; ++v) L.put_env(v, env[2 * v], env[2 * v + 1]);
                 const uint32_t* c = R.e_clean + (size_t)e * 4;
                 L.clean0 = ((uint64_t)c[1] << 32) | c[0];
                 L.clean1 = ((uint64_t)c[3] << 32) | c[2];
@@ -136,7 +134,7 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
                     L.set_dom(pick, R.e_mid[e] + T(1), R.e_hi[e]);
                     freed = e;  // both units of e are consumed after this round
                 } else {
-                    L.set_dom(pick, L.E(L.env_lo, pick), R.e_mid[e]);
+                    L.set_dom(pick, L.get_lo(pick), R.e_mid[e]);
                 }
                 depth = pd + 1;
             }
@@ -169,14 +167,7 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
                 }
             }
             bool run = prop;
-            for (uint32_t kc = 0;;) {
-                uint32_t mine = (run && !dead) ? L.next_dirty(kc) : 0xFFFFu;
-                if (mine >= L.ncon) mine = 0xFFFFu;
-                uint32_t kk = __reduce_min_sync(FULL, mine);
-                if (kk == 0xFFFFu) break;
-                if (mine == kk && !L.pass_constraint(kk)) dead = true;
-                kc = kk + 1;
-            }
+            if (L.pass_sync(run && !dead)) dead = true;
             if (run && (dead || !L.changed)) prop = false;
             if (__any_sync(FULL, run && deadline && global_ns() > deadline)) {
                 status = VERDICT_TIMEOUT;
@@ -194,7 +185,7 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
             } else {
                 int pk = L.pick_var();
                 if (pk < 0) {
-                    outcome = L.check_point(L.env_lo) ? FN_SAT : FN_DEAD;
+                    outcome = L.check_env() ? FN_SAT : FN_DEAD;
                 } else {
                     outcome = FN_SPLIT;
                     pick = (uint32_t)pk;
@@ -233,7 +224,7 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
             limit = (uint32_t)j;
             if ((int)lane == j) {
                 int64_t* m = a.model + 2 * d.out_v;
-                for (uint32_t v = 0; v < nv; ++v) store_i128(m + 2 * v, L.E(L.env_lo, v));
+                for (uint32_t v = 0; v < nv; ++v) store_i128(m + 2 * v, L.get_lo(v));
             }
             sat_p0 = __shfl_sync(FULL, p0, j);
             sat_p1 = __shfl_sync(FULL, p1, j);
@@ -252,10 +243,10 @@ __device__ void frontier_query(Lane<T>& L, const LaunchArgs& a, FrontierRegion<T
             uint32_t e = r < nfree ? R.freel[nfree - 1 - r] : ebump + (r - nfree);
             T* env = R.e_env + (size_t)e * 2 * nv;
             for (uint32_t v = 0; v < nv; ++v) {
-                env[2 * v] = L.E(L.env_lo, v);
-                env[2 * v + 1] = L.E(L.env_hi, v);
+                env[2 * v] = L.get_lo(v);
+                env[2 * v + 1] = L.get_hi(v);
             }
-            T lo = L.E(L.env_lo, pick), hi = L.E(L.env_hi, pick);
+            T lo = L.get_lo(pick), hi = L.get_hi(pick);
             R.e_mid[e] = (lo + hi) >> 1;  // floor midpoint (solver.py:409)
             R.e_hi[e] = hi;
             R.e_pick[e] = pick;
