@@ -121,12 +121,17 @@ typedef struct {
     int32_t heavy_nodes;  /* DFS nodes after which a query moves to the warp-
                              cooperative frontier kernel; 0 = default (64),
                              <0 = never (one lane per query throughout)      */
+    int32_t jit_min;      /* structure classes with at least this many queries
+                             in an int64 job run as run-time compiled kernels;
+                             0 = default (SCUBA_OOB_JIT_MIN, else off)        */
 } oob_options;
 
 enum {
     OOB_F_NO_SORT = 1,   /* keep input order on device (testing the scheduler) */
-    OOB_F_NO_DEMOTE = 2  /* decide wide-regime queries entirely in their proven
+    OOB_F_NO_DEMOTE = 2, /* decide wide-regime queries entirely in their proven
                             regime (no root-phase demotion; testing) */
+    OOB_F_NO_JIT = 4     /* interpret every structure class (no run-time
+                            compiled class kernels; testing) */
 };
 
 /* Results (caller-allocated; optional arrays may be NULL). */
@@ -161,6 +166,10 @@ int oob_side_constraint_count(const oob_batch* batch, int64_t* counts);
  * decided in (0 immediate verdict, 1 int64, 2 int128, 3 256-bit, 4 out of
  * range -> OOB_ERROR).  No device is touched. */
 int oob_query_regime(const oob_batch* batch, const oob_options* opt, int8_t* regime);
+/* Run-time specialisation audit: the CUDA source generated for query q's
+ * structure class (written to src, NUL-terminated, truncated to src_cap) and
+ * its NVRTC compile for sm_100a (*compile_ms); no device is touched. */
+int oob_jit_compile(const oob_batch* batch, int64_t q, char* src, int64_t src_cap, double* compile_ms);
 
 /*
  * Plans: compile and upload a batch once, then run the decision kernels on

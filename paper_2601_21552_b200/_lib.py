@@ -19,6 +19,7 @@ UNSAT, SAT, TIMEOUT, ERROR = 0, 1, 2, 3
 
 F_NO_SORT = 1
 F_NO_DEMOTE = 2
+F_NO_JIT = 4
 
 class EngineError(RuntimeError):
     """The GPU engine could not decide a batch (no device, capacity, range)."""
@@ -32,6 +33,7 @@ class oob_options(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("flags", ctypes.c_int32),
         ("heavy_nodes", ctypes.c_int32),
+        ("jit_min", ctypes.c_int32),
     ]
 
 
@@ -51,6 +53,7 @@ EXPORTS = (
     "oob_check_model_batch",
     "oob_side_constraint_count",
     "oob_query_regime",
+    "oob_jit_compile",
     "oob_last_error",
     "oob_device_count",
     "oob_version",
@@ -84,6 +87,10 @@ def lib():
     L.oob_check_model_batch.restype = ctypes.c_int
     L.oob_side_constraint_count.argtypes = [vp, vp]
     L.oob_side_constraint_count.restype = ctypes.c_int
+    L.oob_jit_compile.argtypes = [vp, ctypes.c_int64, ctypes.c_char_p, ctypes.c_int64, vp]
+    L.oob_jit_compile.restype = ctypes.c_int
+    L.oob_host_bench.argtypes = [vp, vp, vp]
+    L.oob_host_bench.restype = ctypes.c_int
     L.oob_query_regime.argtypes = [vp, vp, vp]
     L.oob_query_regime.restype = ctypes.c_int
     L.oob_last_error.restype = ctypes.c_char_p
@@ -121,8 +128,9 @@ def device_count() -> int:
     return int(lib().oob_device_count())
 
 
-def options(timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0):
+def options(timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0, jit_min=0):
     o = oob_options()
+    o.jit_min = int(jit_min)
     o.timeout_s = float(timeout_s)
     o.node_budget = int(node_budget)
     o.n_gpus = int(n_gpus)
@@ -132,7 +140,7 @@ def options(timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_no
     return o
 
 
-def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0):
+def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0, jit_min=0):
     """Run oob_solve_batch on a FlatBatch -> dict of numpy result arrays."""
     n = fb.n
     out = {
@@ -146,7 +154,7 @@ def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, h
                    out["nodes"].ctypes.data, out["passes"].ctypes.data,
                    out["elapsed"].ctypes.data)
     cb = fb.as_c()
-    o = options(timeout_s, node_budget, n_gpus, device, flags, heavy_nodes)
+    o = options(timeout_s, node_budget, n_gpus, device, flags, heavy_nodes, jit_min)
     rc = lib().oob_solve_batch(ctypes.byref(cb), ctypes.byref(o), ctypes.byref(r))
     out["status"] = rc
     out["error"] = last_error() if rc else ""
@@ -191,10 +199,11 @@ class Plan:
     INFO = ("queries", "record_bytes", "result_bytes", "classes", "jobs",
             "launches_per_run", "wide_queries", "compile_us")
 
-    def __init__(self, fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0):
+    def __init__(self, fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0,
+                 jit_min=0):
         self.fb = fb                     # keeps the batch arrays alive
         self._cb = fb.as_c()
-        self._opt = options(timeout_s, node_budget, n_gpus, device, flags, heavy_nodes)
+        self._opt = options(timeout_s, node_budget, n_gpus, device, flags, heavy_nodes, jit_min)
         self._p = ctypes.c_void_p()
         check(lib().oob_plan_create(ctypes.byref(self._cb), ctypes.byref(self._opt),
                                     ctypes.byref(self._p)), "oob_plan_create")
@@ -248,3 +257,23 @@ def query_regime(fb, timeout_s=30.0):
     o = options(timeout_s)
     check(lib().oob_query_regime(ctypes.byref(cb), ctypes.byref(o), out.ctypes.data), "oob_query_regime")
     return out
+
+
+def jit_compile(fb, q: int, cap: int = 1 << 22):
+    """Generated source of query q's structure class and its NVRTC compile
+    time in ms (host only: no device is needed)."""
+    buf = ctypes.create_string_buffer(cap)
+    ms = ctypes.c_double()
+    cb = fb.as_c()
+    check(lib().oob_jit_compile(ctypes.byref(cb), int(q), buf, cap, ctypes.byref(ms)), "oob_jit_compile")
+    return buf.value.decode(), ms.value
+
+
+def host_bench(fb, timeout_s=30.0):
+    """Host pipeline timings without a device: [validate+compile, prepare
+    (compile + schedule), pack] in ms (diagnostics)."""
+    ms = np.zeros(3, dtype=np.float64)
+    cb = fb.as_c()
+    o = options(timeout_s)
+    check(lib().oob_host_bench(ctypes.byref(cb), ctypes.byref(o), ms.ctypes.data), "oob_host_bench")
+    return ms

@@ -24,7 +24,7 @@
 // of the reference.  A DFS child starts from its parent's clean mask minus
 // the constraints of the split variable.
 #pragma once
-#include <cstdint>
+#include "types.h"
 
 #include "format.h"
 #include "wide.cuh"
@@ -38,16 +38,29 @@ __device__ __forceinline__ T cdiv(T a, T b) { return a / b; }
 template <typename T>
 __device__ __forceinline__ T cmod(T a, T b) { return a % b; }
 __device__ __forceinline__ bool fits64(__int128 v) { return v == (__int128)(long long)v; }
+// int64: the 32-bit hardware path when both operands lie in [-(2^31-1), 2^31-1]
+// (no INT32_MIN, so no overflow), the 64-bit software routine otherwise
+__device__ __forceinline__ bool fits31(long long v) { return (unsigned long long)v + 0x7FFFFFFFull <= 0xFFFFFFFEull; }
+template <>
+__device__ __forceinline__ long long cdiv<long long>(long long a, long long b) {
+    if (fits31(a) && fits31(b)) return (long long)((int)a / (int)b);
+    return a / b;
+}
+template <>
+__device__ __forceinline__ long long cmod<long long>(long long a, long long b) {
+    if (fits31(a) && fits31(b)) return (long long)((int)a % (int)b);
+    return a % b;
+}
 template <>
 __device__ __forceinline__ __int128 cdiv<__int128>(__int128 a, __int128 b) {
     if (fits64(a) && fits64(b) && !((long long)a == (-9223372036854775807LL - 1) && (long long)b == -1))
-        return (__int128)((long long)a / (long long)b);
+        return (__int128)cdiv<long long>((long long)a, (long long)b);
     return a / b;
 }
 template <>
 __device__ __forceinline__ __int128 cmod<__int128>(__int128 a, __int128 b) {
     if (fits64(a) && fits64(b) && !((long long)a == (-9223372036854775807LL - 1) && (long long)b == -1))
-        return (__int128)((long long)a % (long long)b);
+        return (__int128)cmod<long long>((long long)a, (long long)b);
     return a % b;
 }
 

@@ -17,7 +17,7 @@
 //   qdesc[]  per scheduled query (sorted by class, then by cost estimate):
 //            where its code block and data block are and where results go.
 #pragma once
-#include <cstdint>
+#include "types.h"
 
 #if defined(__CUDACC__)
 #define OOB_HD __host__ __device__
@@ -78,6 +78,8 @@ struct SlabGeom {
 // One structure class: its code block (constraint words, node words, then 4
 // membership words per variable) and its slice [q_begin, q_end) of the
 // class-major schedule.
+constexpr uint32_t NO_CLASS = 0xFFFFFFFFu;  // warp_class entry of a warp with nothing to do
+
 struct ClassDesc {
     uint32_t code_off;
     uint32_t nv_ncon;

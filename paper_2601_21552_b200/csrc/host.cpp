@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -30,6 +31,7 @@
 
 #include "../../include/scuba_oob.h"
 #include "format.h"
+#include "jit.h"
 #include "wide.cuh"
 
 namespace oob {
@@ -192,10 +194,90 @@ struct Compiled {
     std::vector<i128> lits;       // per literal slot
     double cost = 0;
     uint64_t key = 0;             // structure-class hash (words, nv, ncon)
+    uint32_t cls = UINT32_MAX;    // batch-wide structure class id (prepare)
     std::string why;              // reason for R_RANGE
     bool same_class(const Compiled& o) const {
         return key == o.key && nv == o.nv && ncon == o.ncon && words == o.words;
     }
+};
+
+// Page-locked host blocks, recycled across calls (H2D / D2H at full PCIe /
+// C2C bandwidth without a driver staging copy).  Falls back to pageable
+// memory when no CUDA context can be created (host-only diagnostics).
+struct PinnedPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_;
+    void* acquire(size_t bytes, bool* pinned) {
+        bytes = std::max<size_t>(bytes, 64);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = free_.lower_bound(bytes);
+            if (it != free_.end() && it->first <= 2 * bytes + (1u << 20)) {
+                void* p = it->second;
+                free_.erase(it);
+                *pinned = true;
+                return p;
+            }
+        }
+        void* p = nullptr;
+        size_t want = bytes + bytes / 8;
+        if (cudaMallocHost(&p, want) == cudaSuccess) {
+            *pinned = true;
+            std::lock_guard<std::mutex> lk(mu);
+            sizes[p] = want;
+            return p;
+        }
+        cudaGetLastError();
+        *pinned = false;
+        return std::malloc(bytes);
+    }
+    void release(void* p, bool pinned) {
+        if (!p) return;
+        if (!pinned) {
+            std::free(p);
+            return;
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        free_.emplace(sizes[p], p);
+    }
+    std::unordered_map<void*, size_t> sizes;
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* pp = new PinnedPool();  // never destroyed: blocks live for the process
+    return *pp;
+}
+
+// uninitialised page-locked host array (filled in parallel; no zero-fill pass)
+template <typename T>
+struct HostArr {
+    T* p = nullptr;
+    size_t n = 0, cap = 0;
+    bool pinned = false;
+    HostArr() = default;
+    HostArr(const HostArr&) = delete;
+    HostArr& operator=(const HostArr&) = delete;
+    HostArr(HostArr&& o) noexcept : p(o.p), n(o.n), cap(o.cap), pinned(o.pinned) { o.p = nullptr; o.n = o.cap = 0; }
+    HostArr& operator=(HostArr&& o) noexcept {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+        std::swap(cap, o.cap);
+        std::swap(pinned, o.pinned);
+        return *this;
+    }
+    ~HostArr() { pinned_pool().release(p, pinned); }
+    void alloc(size_t m) {
+        if (m > cap || !p) {
+            pinned_pool().release(p, pinned);
+            cap = std::max<size_t>(m, 1);
+            p = (T*)pinned_pool().acquire(cap * sizeof(T), &pinned);
+        }
+        n = m;
+    }
+    size_t size() const { return n; }
+    T* data() { return p; }
+    const T* data() const { return p; }
+    T& operator[](size_t i) { return p[i]; }
+    const T& operator[](size_t i) const { return p[i]; }
 };
 
 // 64-bit FNV-1a over the structure words: the structure-class key
@@ -574,14 +656,16 @@ struct DevicePool {
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
     DevBuf classes, class_next, class_init, warp_class;
     DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
-    DevBuf resume, resume_init, slot64, slot128, timeline;
+    DevBuf resume, resume_init, slot64, slot128, timeline, classes_interp;
+    std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
+    std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evr = nullptr;
     int sms = 148;
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
-                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &timeline})
+                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &timeline, &classes_interp})
             b->release();
     }
 };
@@ -686,10 +770,18 @@ struct DevJob {
     std::vector<uint8_t> is_shadow;  // per scheduled entry
     std::vector<uint32_t> resume_init;  // per scheduled entry (format.h resume words)
     std::vector<uint32_t> slot[2];      // wide jobs: per entry, index of its shadow in job[0] / job[1]
+    // run-time compiled classes (int64 SOLVE jobs, jit.cpp): one kernel each
+    std::vector<uint32_t> jit_cls;      // class ids
+    std::vector<const void*> jit_fn;
+    std::vector<uint32_t> jit_blocks;
+    std::vector<LaunchArgs> jit_args;
+    std::vector<ClassDesc> cls_interp;  // the class table of the interpreting kernel (JIT classes emptied)
+    double jit_ms = 0;
+    uint64_t jit_queries = 0;
     std::vector<uint64_t> mo;    // device-local model offset (vars) per scheduled query
     std::vector<uint32_t> code;  // class code blocks
-    std::vector<int64_t> data;   // per query domains + literal slots
-    std::vector<QDesc> qd;
+    HostArr<int64_t> data;       // per query domains + literal slots
+    HostArr<QDesc> qd;
     std::vector<ClassDesc> cls;
     std::vector<uint32_t> warp_class;
     uint32_t maxv = 1, maxcode = 1, maxlit = 1, maxcsize = 1, maxdepth = 1;
@@ -710,23 +802,34 @@ struct DevJob {
 void pack(const RunCtx& rc, DevJob& j) {
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
-    // group the job's entries (own queries, then shadows) by structure class,
-    // keeping their order within a class (the lockstep kernel runs each warp
-    // on one class)
+    // group the job's entries (own queries, then shadows) by structure class
+    // (batch-wide ids from prepare), keeping their order within a class (the
+    // lockstep kernel runs each warp on one class)
     std::vector<int64_t> entries(j.qs);  // query id, or ~id for a shadow
     for (int64_t q : j.shadows) entries.push_back(~q);
     auto qid = [](int64_t e) { return e < 0 ? ~e : e; };
-    std::vector<uint32_t> cls;
+    std::unordered_map<uint32_t, uint32_t> local;
+    std::vector<uint32_t> cls(entries.size());
     std::vector<size_t> rep;
-    group_classes(entries.size(), [&](size_t i) -> const Compiled& { return comp[qid(entries[i])]; }, cls, rep);
+    for (size_t i = 0; i < entries.size(); i++) {
+        auto it = local.emplace(comp[qid(entries[i])].cls, (uint32_t)rep.size());
+        if (it.second) rep.push_back(i);
+        cls[i] = it.first->second;
+    }
     const size_t nc = rep.size();
     std::vector<uint32_t> count(nc + 1, 0);
     for (uint32_t c : cls) count[c + 1]++;
     for (size_t c = 0; c < nc; c++) count[c + 1] += count[c];
-    std::vector<int64_t> order(entries.size());
+    const size_t n = entries.size();
+    std::vector<int64_t> order(n);
+    std::vector<uint32_t> ocls(n);
     {
         std::vector<uint32_t> at(count.begin(), count.end() - 1);
-        for (size_t i = 0; i < entries.size(); i++) order[at[cls[i]]++] = entries[i];
+        for (size_t i = 0; i < n; i++) {
+            uint32_t k = at[cls[i]]++;
+            order[k] = entries[i];
+            ocls[k] = cls[i];
+        }
     }
     j.code.clear();
     j.cls.assign(nc, ClassDesc{});
@@ -739,52 +842,53 @@ void pack(const RunCtx& rc, DevJob& j) {
         cd.ncode_nlit = c.ncode | (c.nlit << 16);
         cd.q_begin = count[id];
         cd.q_end = count[id + 1];
-    }
-    j.n_classes = (uint32_t)nc;
-    const size_t n = order.size();
-    j.qs.resize(n);
-    j.is_shadow.resize(n);
-    j.resume_init.resize(n);
-    j.qd.assign(n, QDesc{});
-    j.mo.assign(n, 0);
-    // data layout: per entry (2 nv + nlit) values of the job's width, padded
-    // to 16 (int64/int128) or 32 bytes (256-bit)
-    const size_t vw = j.wide == 2 ? 4 : (size_t)j.wide + 1;  // int64 words per value
-    const size_t align = j.wide == 2 ? 4 : 2;
-    std::vector<uint64_t> doff(n + 1, 0);
-    j.model_words = 0;
-    size_t ci = 0;
-    for (size_t i = 0; i < n; i++) {
-        while (i >= j.cls[ci].q_end) ci++;
-        const int64_t e = order[i];
-        const Compiled& c = comp[qid(e)];
-        j.qs[i] = qid(e);
-        j.is_shadow[i] = e < 0;
-        j.resume_init[i] = e < 0 ? RES_SKIP : 0u;
-        QDesc& d = j.qd[i];
-        d.code_off = j.cls[ci].code_off;
-        d.nv_ncon = c.nv | (c.ncon << 16);
-        d.ncode_nlit = c.ncode | (c.nlit << 16);
-        d.out_q = (uint32_t)i;
-        d.data_off = doff[i];
-        d.out_v = j.model_words;
-        j.mo[i] = j.model_words;
-        j.model_words += c.nv;
-        size_t words = (2 * (size_t)c.nv + c.nlit) * vw;
-        doff[i + 1] = doff[i] + ((words + align - 1) / align) * align;
         j.maxv = std::max(j.maxv, c.nv);
         j.maxcode = std::max(j.maxcode, c.ncode);
         j.maxlit = std::max(j.maxlit, c.nlit);
         j.maxcsize = std::max(j.maxcsize, c.maxcsize);
         j.maxdepth = std::max(j.maxdepth, c.maxdepth);
     }
-    j.data.assign(std::max<uint64_t>(doff[n], 4), 0);
+    j.n_classes = (uint32_t)nc;
+    j.qs.resize(n);
+    j.is_shadow.resize(n);
+    j.resume_init.resize(n);
+    j.mo.resize(n);
+    j.qd.alloc(n);
+    // data layout: per entry (2 nv + nlit) values of the job's width, padded
+    // to 16 (int64/int128) or 32 bytes (256-bit)
+    const size_t vw = j.wide == 2 ? 4 : (size_t)j.wide + 1;  // int64 words per value
+    const size_t align = j.wide == 2 ? 4 : 2;
+    std::vector<uint64_t> doff(n + 1, 0), moff(n + 1, 0);
+    for (size_t i = 0; i < n; i++) {
+        const Compiled& c = comp[qid(order[i])];
+        const size_t words = (2 * (size_t)c.nv + c.nlit) * vw;
+        doff[i + 1] = doff[i] + ((words + align - 1) / align) * align;
+        moff[i + 1] = moff[i] + c.nv;
+    }
+    j.model_words = moff[n];
+    j.data.alloc(std::max<uint64_t>(doff[n], 4));
     parallel_for(n, 4096, [&](size_t lo, size_t hi) {
         for (size_t i = lo; i < hi; i++) {
-            if (j.is_shadow[i]) continue;  // written on the device by the root kernel
-            const int64_t q = j.qs[i];
+            const int64_t e = order[i];
+            const int64_t q = qid(e);
             const Compiled& c = comp[q];
+            j.qs[i] = q;
+            j.is_shadow[i] = e < 0;
+            j.resume_init[i] = e < 0 ? RES_SKIP : 0u;
+            QDesc& d = j.qd[i];
+            d.code_off = j.cls[ocls[i]].code_off;
+            d.nv_ncon = c.nv | (c.ncon << 16);
+            d.ncode_nlit = c.ncode | (c.nlit << 16);
+            d.out_q = (uint32_t)i;
+            d.data_off = doff[i];
+            d.out_v = moff[i];
+            j.mo[i] = moff[i];
             int64_t* out = j.data.data() + doff[i];
+            int64_t* end = j.data.data() + doff[i + 1];
+            if (e < 0) {  // a shadow: written on the device by the root kernel
+                std::fill(out, end, 0);
+                continue;
+            }
             auto put = [&](i128 x) {
                 *out++ = (int64_t)(uint64_t)x;
                 if (vw >= 2) *out++ = (int64_t)(x >> 64);
@@ -806,26 +910,49 @@ void pack(const RunCtx& rc, DevJob& j) {
                 }
             }
             for (i128 l : c.lits) put(l);
+            std::fill(out, end, 0);
         }
     });
+    if (n == 0) std::fill(j.data.data(), j.data.data() + j.data.size(), 0);
     if (j.code.empty()) j.code.push_back(0);
     if (j.cls.empty()) j.cls.push_back(ClassDesc{});
 }
 
 // starting class of every warp, in proportion to the class sizes
-void assign_warps(DevJob& j, uint32_t n_warps) {
-    j.warp_class.assign(n_warps, 0);
-    uint64_t total = j.qs.size();
+void assign_warps(DevJob& j, const std::vector<ClassDesc>& cls, uint32_t n_warps) {
+    j.warp_class.assign(n_warps, NO_CLASS);  // no class left for this kernel: its warps exit at once
+    uint64_t total = 0;
+    std::vector<uint32_t> live;
+    for (uint32_t c = 0; c < cls.size(); c++)
+        if (cls[c].q_end > cls[c].q_begin) {
+            total += cls[c].q_end - cls[c].q_begin;
+            live.push_back(c);
+        }
     if (total == 0) return;
     uint32_t w = 0;
-    for (uint32_t c = 0; c < j.n_classes && w < n_warps; c++) {
-        uint64_t size = j.cls[c].q_end - j.cls[c].q_begin;
+    for (uint32_t c : live) {
+        if (w >= n_warps) break;
+        uint64_t size = cls[c].q_end - cls[c].q_begin;
         uint64_t share = std::max<uint64_t>(1, (size * n_warps + total - 1) / total);
         share = std::min<uint64_t>(share, (size + 31) / 32);
         for (uint64_t k = 0; k < share && w < n_warps; k++) j.warp_class[w++] = c;
     }
-    for (uint32_t c = 0; w < n_warps; w++, c = (c + 1) % std::max(1u, j.n_classes)) j.warp_class[w] = c;
+    for (size_t i = 0; w < n_warps; w++, i = (i + 1) % live.size()) j.warp_class[w] = live[i];
 }
+
+// JIT policy: classes with at least jit_min queries in an int64 SOLVE job run
+// as run-time compiled kernels (oob_options.jit_min, else SCUBA_OOB_JIT_MIN;
+// off by default: the interpreting kernel overlaps the long search chains of
+// all classes in one persistent grid, which the per-class kernels do not yet
+// match -- see DESIGN.md; OOB_F_NO_JIT disables)
+uint64_t jit_min() {
+    static const uint64_t m = [] {
+        const char* e = std::getenv("SCUBA_OOB_JIT_MIN");
+        return (e && *e) ? (uint64_t)std::strtoull(e, nullptr, 10) : UINT64_MAX;
+    }();
+    return m;
+}
+constexpr uint32_t JIT_MAX_NV = 48, JIT_MAX_LIT = 48, JIT_MAX_CODE = 1024;
 
 // allocate + upload the packed records of `j` into pool P (caller holds P->mu)
 constexpr uint32_t FR_ECAP = 2048, FR_UCAP = 4096, FR_LOGCAP = 32768;
@@ -851,18 +978,64 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     const uint32_t n = (uint32_t)j.qs.size();
     const size_t tbytes = j.wide == 2 ? 32 : (j.wide ? 16 : 8);
     j.g = make_geom(j.maxv, j.maxcode, j.maxlit, depth_cap, trail_cap, j.maxcsize, j.maxdepth, tbytes);
+    // run-time compiled classes (int64 solve jobs)
+    j.jit_cls.clear();
+    j.jit_fn.clear();
+    j.jit_blocks.clear();
+    j.jit_args.clear();
+    j.jit_queries = 0;
+    j.cls_interp = j.cls;
+    if (j.wide == 0 && rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_JIT)) {
+        const std::vector<Compiled>& comp = *rc.comp;
+        std::vector<JitClass> want;
+        for (uint32_t c = 0; c < j.n_classes; c++) {
+            const ClassDesc& cd = j.cls[c];
+            const uint64_t size = cd.q_end - cd.q_begin;
+            const Compiled& rep = comp[j.qs[cd.q_begin]];
+            const uint64_t min_q = rc.opt.jit_min > 0 ? (uint64_t)rc.opt.jit_min : jit_min();
+            if (size < min_q || rep.ncon > 128 || rep.nv > JIT_MAX_NV || rep.nlit > JIT_MAX_LIT ||
+                rep.ncode > JIT_MAX_CODE)
+                continue;
+            j.jit_cls.push_back(c);
+            want.push_back(JitClass{j.code.data() + cd.code_off, rep.nv, rep.ncon, rep.ncode, rep.nlit});
+        }
+        if (!want.empty()) {
+            std::vector<int> regs;
+            std::string e = jit_prepare(want, j.jit_fn, regs, &j.jit_ms);
+            if (!e.empty()) return "run-time compile: " + e;
+            for (size_t i = 0; i < j.jit_cls.size(); i++) {
+                ClassDesc& cd = j.cls_interp[j.jit_cls[i]];
+                j.jit_queries += cd.q_end - cd.q_begin;
+                cd.q_end = cd.q_begin;  // the interpreting kernel sees the class drained
+            }
+        }
+    }
     int per_sm = BLOCKS_PER_SM;
     CK(kernel_occupancy(j.wide, rc.mode, (size_t)j.g.smem_per_warp * WARPS_PER_BLOCK, &per_sm));
     per_sm = std::max(1, per_sm);
-    const uint32_t warps_needed = (n + 31) / 32;
+    const uint32_t warps_needed = (uint32_t)((n - j.jit_queries + 31) / 32);
     j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
                                                 (uint32_t)(P->sms * per_sm)));
-    const uint32_t n_warps = j.blocks * WARPS_PER_BLOCK;
-    assign_warps(j, n_warps);
+    uint32_t n_warps = j.blocks * WARPS_PER_BLOCK;
+    assign_warps(j, j.cls_interp, n_warps);
+    for (size_t i = 0; i < j.jit_cls.size(); i++) {
+        const ClassDesc& cd = j.cls[j.jit_cls[i]];
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, j.jit_fn[i], WARPS_PER_BLOCK * 32, 0) != cudaSuccess) {
+            cudaGetLastError();
+            occ = 4;
+        }
+        occ = std::max(1, occ);
+        const uint32_t need = (cd.q_end - cd.q_begin + 31) / 32;
+        const uint32_t b = std::max(1u, std::min<uint32_t>((need + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                                           (uint32_t)(P->sms * occ)));
+        j.jit_blocks.push_back(b);
+        n_warps += b * WARPS_PER_BLOCK;
+    }
     // heavy-query hand-off (solve mode): threshold from the options
     int64_t hn = rc.opt.heavy_nodes;
     uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
-    j.fblocks = heavy_nodes ? j.blocks : 0;  // one frontier scratch region per warp of the grid
+    j.fblocks = heavy_nodes ? n_warps / WARPS_PER_BLOCK : 0;  // one frontier scratch region per warp
     const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
@@ -881,8 +1054,8 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->class_next.ensure(j.cls.size() * 4));
     CK(P->class_init.ensure(j.cls.size() * 4));
     CK(P->warp_class.ensure((size_t)n_warps * 4));
-    CK(P->heavy_count.ensure(16));
-    CK(P->heavy_list.ensure((size_t)n * 4));
+    CK(P->heavy_count.ensure(8 * (1 + j.jit_cls.size())));
+    CK(P->heavy_list.ensure((size_t)n * 8));  // [0, n): per compiled class at its q range; [n, 2n): interpreter
     CK(P->heavy_t0.ensure((size_t)n * 8));
     if (j.fblocks) CK(P->fr_region.ensure((size_t)j.fblocks * WARPS_PER_BLOCK * fr_bytes));
     CK(P->resume.ensure((size_t)n * 4));
@@ -895,12 +1068,15 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         if (!j.slot[t].empty())
             CK(cudaMemcpyAsync((t ? P->slot128 : P->slot64).p, j.slot[t].data(), j.slot[t].size() * 4,
                                cudaMemcpyHostToDevice, s));
+    CK(P->classes_interp.ensure(j.cls.size() * sizeof(ClassDesc)));
     {
         std::vector<uint32_t> init(j.cls.size());
         for (size_t c = 0; c < j.cls.size(); c++) init[c] = j.cls[c].q_begin;
         CK(cudaMemcpyAsync(P->classes.p, j.cls.data(), j.cls.size() * sizeof(ClassDesc), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(P->classes_interp.p, j.cls_interp.data(), j.cls.size() * sizeof(ClassDesc),
+                           cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(P->class_init.p, init.data(), init.size() * 4, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(P->warp_class.p, j.warp_class.data(), (size_t)n_warps * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(P->warp_class.p, j.warp_class.data(), j.warp_class.size() * 4, cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));  // host vectors above are temporaries
     }
     CK(cudaMemcpyAsync(P->qdesc.p, j.qd.data(), j.qd.size() * sizeof(QDesc), cudaMemcpyHostToDevice, s));
@@ -913,14 +1089,14 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.data = (const int64_t*)P->data.p;
     a.n = n;
     a.next = (uint32_t*)P->next.p;
-    a.classes = (const ClassDesc*)P->classes.p;
+    a.classes = (const ClassDesc*)P->classes_interp.p;
     a.n_classes = j.n_classes;
     a.class_next = (uint32_t*)P->class_next.p;
     a.warp_class = (const uint32_t*)P->warp_class.p;
     a.heavy_nodes = heavy_nodes;
     a.heavy_count = (uint32_t*)P->heavy_count.p;
     a.heavy_next = (uint32_t*)P->heavy_count.p + 1;
-    a.heavy_list = (uint32_t*)P->heavy_list.p;
+    a.heavy_list = (uint32_t*)P->heavy_list.p + n;
     a.heavy_t0 = (uint64_t*)P->heavy_t0.p;
     a.fr_region = j.fblocks ? P->fr_region.p : nullptr;
     a.fr_region_bytes = fr_bytes;
@@ -945,6 +1121,24 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     if (timeline_path() && rc.mode == MODE_SOLVE) {
         CK(P->timeline.ensure((size_t)n * 32));
         a.timeline = (uint64_t*)P->timeline.p;
+    }
+    // one launch per compiled class: its own class queue and heavy list, and
+    // its own range of per-warp scratch
+    uint64_t warp_base = (uint64_t)j.blocks * WARPS_PER_BLOCK;
+    for (size_t i = 0; i < j.jit_cls.size(); i++) {
+        const uint32_t c = j.jit_cls[i];
+        LaunchArgs b = a;
+        b.classes = (const ClassDesc*)P->classes.p + c;
+        b.n_classes = 1;
+        b.class_next = (uint32_t*)P->class_next.p + c;
+        b.warp_class = nullptr;
+        b.heavy_count = (uint32_t*)P->heavy_count.p + 2 * (1 + i);
+        b.heavy_list = (uint32_t*)P->heavy_list.p + j.cls[c].q_begin;
+        b.slab_T = (unsigned char*)P->slabT.p + warp_base * j.g.slab_T_words * tbytes;
+        b.slab_u32 = (uint32_t*)P->slabU.p + warp_base * j.g.slab_u32_words;
+        if (b.fr_region) b.fr_region = (unsigned char*)P->fr_region.p + warp_base * fr_bytes;
+        j.jit_args.push_back(b);
+        warp_base += (uint64_t)j.jit_blocks[i] * WARPS_PER_BLOCK;
     }
     j.staged = true;
     return "";
@@ -1044,8 +1238,8 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         const size_t n = j.qs.size();
         CK(cudaMemsetAsync(P->next.p, 0, 4, s0));
         CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s0));
-        CK(cudaMemsetAsync(P->heavy_count.p, 0, 16, s0));
-        if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 4, s0));
+        CK(cudaMemsetAsync(P->heavy_count.p, 0, 8 * (1 + j.jit_cls.size()), s0));
+        if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 8, s0));
         if (j.a.timeline) CK(cudaMemsetAsync(j.a.timeline, 0, n * 32, s0));
         CK(cudaMemsetAsync(P->verdict.p, 0xFF, n, s0));
         CK(cudaMemcpyAsync(P->resume.p, P->resume_init.p, n * 4, cudaMemcpyDeviceToDevice, s0));
@@ -1072,9 +1266,36 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
     for (int w = 2; w >= 0; w--) {
         if (!present(G.job[w])) continue;
         DevJob& j = G.job[w];
-        cudaStream_t s = G.pool[w]->stream;
+        DevicePool* P = G.pool[w];
+        cudaStream_t s = P->stream;
+        // compiled classes first (the big ones), each on its own stream after
+        // everything queued so far on the job's stream (resets, root kernels)
+        if (!j.jit_cls.empty()) {
+            static const size_t kmax = [] {
+                const char* e = std::getenv("SCUBA_OOB_JIT_STREAMS");
+                return (size_t)((e && *e) ? std::max(1, std::atoi(e)) : 64);
+            }();
+            const size_t nxs = std::min(kmax, j.jit_cls.size());
+            while (P->xs.size() < nxs) {
+                cudaStream_t xs;
+                cudaEvent_t xe;
+                CK(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+                CK(cudaEventCreateWithFlags(&xe, cudaEventDisableTiming));
+                P->xs.push_back(xs);
+                P->xev.push_back(xe);
+            }
+            CK(cudaEventRecord(P->evr, s));
+            for (size_t x = 0; x < nxs; x++) CK(cudaStreamWaitEvent(P->xs[x], P->evr, 0));
+            for (size_t i = 0; i < j.jit_cls.size(); i++) {
+                void* args[] = {&j.jit_args[i]};
+                CK(cudaLaunchKernel(j.jit_fn[i], dim3(j.jit_blocks[i]), dim3(WARPS_PER_BLOCK * 32), args, 0,
+                                    P->xs[i % nxs]));
+            }
+            for (size_t x = 0; x < nxs; x++) CK(cudaEventRecord(P->xev[x], P->xs[x]));
+        }
         CK(launch_solve(j.a, w, (int)j.blocks, (int)j.fblocks, s));
-        CK(cudaEventRecord(G.pool[w]->ev1, s));
+        for (size_t x = 0; x < std::min(P->xs.size(), j.jit_cls.size()); x++) CK(cudaStreamWaitEvent(s, P->xev[x], 0));
+        CK(cudaEventRecord(P->ev1, s));
     }
     return "";
 }
@@ -1103,9 +1324,15 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
     CK(cudaSetDevice(j.dev));
     const uint32_t n = (uint32_t)j.qs.size();
     cudaStream_t s = P->stream;
-    std::vector<int8_t> verdict(n), err(n);
-    std::vector<int64_t> nodes(n), passes(n), mw(std::max<size_t>(j.out_model_words, 2));
-    std::vector<float> el(n);
+    HostArr<int8_t> verdict, err;
+    HostArr<int64_t> nodes, passes, mw;
+    HostArr<float> el;
+    verdict.alloc(n);
+    err.alloc(n);
+    nodes.alloc(n);
+    passes.alloc(n);
+    el.alloc(n);
+    mw.alloc(std::max<size_t>(j.out_model_words, 2));
     CK(cudaMemcpyAsync(verdict.data(), P->verdict.p, n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(err.data(), P->err.p, n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(nodes.data(), P->nodes.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
@@ -1131,35 +1358,40 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
     }
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
-    for (uint32_t i = 0; i < n; i++) {
-        if (verdict[i] == VERDICT_NONE) continue;
-        int64_t q = j.qs[i];
-        if (err[i] == ERR_DEPTH || err[i] == ERR_TRAIL) {
-            retry[comp[q].regime - R_W64].push_back(q);
-            continue;
-        }
-        (*rc.errs)[q] = err[i];
-        rc.verdict[q] = verdict[i];
-        if (rc.nodes) rc.nodes[q] = nodes[i];
-        if (rc.passes) rc.passes[q] = passes[i];
-        if (rc.elapsed) rc.elapsed[q] = el[i];
-        int64_t vb = b->var_begin[q];
-        uint32_t nv = comp[q].nv;
-        uint64_t m0 = j.mo[i];
-        if (rc.mode == MODE_SOLVE && verdict[i] == VERDICT_SAT && rc.model) {
-            for (uint32_t v = 0; v < nv; v++) {
-                rc.model[vb + v].lo = (uint64_t)mw[2 * (m0 + v)];
-                rc.model[vb + v].hi = mw[2 * (m0 + v) + 1];
+    std::vector<uint8_t> is_retry(n, 0);
+    parallel_for(n, 8192, [&](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; i++) {
+            if (verdict[i] == VERDICT_NONE) continue;
+            int64_t q = j.qs[i];
+            if (err[i] == ERR_DEPTH || err[i] == ERR_TRAIL) {
+                is_retry[i] = 1;
+                continue;
             }
-        } else if (rc.mode == MODE_PROPAGATE && rc.model) {
-            for (uint32_t v = 0; v < nv; v++) {
-                rc.model[2 * (vb + v)].lo = (uint64_t)mw[4 * (m0 + v)];
-                rc.model[2 * (vb + v)].hi = mw[4 * (m0 + v) + 1];
-                rc.model[2 * (vb + v) + 1].lo = (uint64_t)mw[4 * (m0 + v) + 2];
-                rc.model[2 * (vb + v) + 1].hi = mw[4 * (m0 + v) + 3];
+            (*rc.errs)[q] = err[i];
+            rc.verdict[q] = verdict[i];
+            if (rc.nodes) rc.nodes[q] = nodes[i];
+            if (rc.passes) rc.passes[q] = passes[i];
+            if (rc.elapsed) rc.elapsed[q] = el[i];
+            int64_t vb = b->var_begin[q];
+            uint32_t nv = comp[q].nv;
+            uint64_t m0 = j.mo[i];
+            if (rc.mode == MODE_SOLVE && verdict[i] == VERDICT_SAT && rc.model) {
+                for (uint32_t v = 0; v < nv; v++) {
+                    rc.model[vb + v].lo = (uint64_t)mw[2 * (m0 + v)];
+                    rc.model[vb + v].hi = mw[2 * (m0 + v) + 1];
+                }
+            } else if (rc.mode == MODE_PROPAGATE && rc.model) {
+                for (uint32_t v = 0; v < nv; v++) {
+                    rc.model[2 * (vb + v)].lo = (uint64_t)mw[4 * (m0 + v)];
+                    rc.model[2 * (vb + v)].hi = mw[4 * (m0 + v) + 1];
+                    rc.model[2 * (vb + v) + 1].lo = (uint64_t)mw[4 * (m0 + v) + 2];
+                    rc.model[2 * (vb + v) + 1].hi = mw[4 * (m0 + v) + 3];
+                }
             }
         }
-    }
+    });
+    for (uint32_t i = 0; i < n; i++)
+        if (is_retry[i]) retry[comp[j.qs[i]].regime - R_W64].push_back(j.qs[i]);
     return "";
 }
 
@@ -1212,6 +1444,9 @@ std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
             }
             if (!e.empty()) return e;
         }
+        if (trace_on())
+            std::fprintf(stderr, "[oob] round %d dev %d: retry %zu/%zu/%zu (jit classes %zu)\n", round, dev,
+                         retry[0].size(), retry[1].size(), retry[2].size(), G.job[0].jit_cls.size());
         for (int w = 0; w < 3; w++) cur[w].swap(retry[w]);
         depth_cap *= 4;
         trail_cap *= 8;
@@ -1249,6 +1484,33 @@ int visible_devices() {
     return n;
 }
 
+// Batch-wide structure-class ids of the device-bound queries: by hash, then
+// verified word for word in parallel (on a hash collision the exact grouping
+// is used instead).
+void assign_classes(std::vector<Compiled>& comp, const std::vector<int64_t> reg[3]) {
+    std::vector<int64_t> all;
+    for (int w = 0; w < 3; w++) all.insert(all.end(), reg[w].begin(), reg[w].end());
+    std::unordered_map<uint64_t, uint32_t> ids;
+    std::vector<int64_t> rep;
+    for (int64_t q : all) {
+        auto it = ids.emplace(comp[q].key, (uint32_t)rep.size());
+        if (it.second) rep.push_back(q);
+        comp[q].cls = it.first->second;
+    }
+    std::atomic<bool> clash{false};
+    parallel_for(all.size(), 4096, [&](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi && !clash; i++) {
+            const Compiled& c = comp[all[i]];
+            if (!c.same_class(comp[rep[c.cls]])) clash = true;
+        }
+    });
+    if (!clash) return;
+    std::vector<uint32_t> cls;
+    std::vector<size_t> r2;
+    group_classes(all.size(), [&](size_t i) -> const Compiled& { return comp[all[i]]; }, cls, r2);
+    for (size_t i = 0; i < all.size(); i++) comp[all[i]].cls = cls[i];
+}
+
 // Compile + schedule: fills immediate verdicts and returns the device jobs.
 struct Prepared {
     std::vector<Compiled> comp;
@@ -1260,7 +1522,7 @@ struct Prepared {
 };
 
 int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i128* model_in, int8_t* verdict,
-            int64_t* nodes, int64_t* passes, double* elapsed, Prepared& pr) {
+            int64_t* nodes, int64_t* passes, double* elapsed, Prepared& pr, int virtual_devices = 0) {
     g_last_error.clear();
     if (!b || b->n_queries < 0) return fail(OOB_E_INVALID, "null or negative batch");
     pr.opt.timeout_s = 30.0;
@@ -1270,9 +1532,19 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     auto t0 = std::chrono::steady_clock::now();
     {
         Phase ph("validate");
-        for (int64_t q = 0; q < n; q++) {
-            std::string why = validate(b, q);
-            if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
+        std::atomic<int64_t> bad{INT64_MAX};
+        parallel_for((size_t)n, 8192, [&](size_t lo, size_t hi) {
+            for (size_t q = lo; q < hi; q++)
+                if (!validate(b, (int64_t)q).empty()) {
+                    int64_t cur = bad.load();
+                    while ((int64_t)q < cur && !bad.compare_exchange_weak(cur, (int64_t)q)) {
+                    }
+                    break;
+                }
+        });
+        if (bad.load() != INT64_MAX) {
+            int64_t q = bad.load();
+            return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + validate(b, q));
         }
     }
     std::vector<Compiled>& comp = pr.comp;
@@ -1311,7 +1583,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
             reg[c.regime - R_W64].push_back(q);
         }
     }
-    int ndev = visible_devices();
+    int ndev = virtual_devices > 0 ? virtual_devices : visible_devices();
     const size_t n_dev_q = reg[0].size() + reg[1].size() + reg[2].size();
     if (n_dev_q > 0 && ndev == 0)
         return fail(OOB_E_CUDA, "no CUDA device visible: the OOB engine has no CPU fallback");
@@ -1321,6 +1593,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     int want = opt.n_gpus > 0 ? opt.n_gpus : ndev - first;
     want = std::max(1, std::min(want, ndev - first));
     Phase ph_sched("schedule");
+    assign_classes(comp, reg);
     if (n_dev_q > 0) {
         pr.work.resize(want);
         for (int d = 0; d < want; d++) pr.work[d].dev = first + d;
@@ -1330,13 +1603,8 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         if (qs.empty()) continue;
         if (!(opt.flags & OOB_F_NO_SORT)) {
             // class-major, cost-minor: a 32-query tile is (nearly) one class
-            std::vector<uint32_t> cls;
-            std::vector<size_t> rep;
-            group_classes(qs.size(), [&](size_t i) -> const Compiled& { return comp[qs[i]]; }, cls, rep);
-            std::vector<uint32_t> key(n, 0);
-            for (size_t i = 0; i < qs.size(); i++) key[qs[i]] = cls[i];
             std::stable_sort(qs.begin(), qs.end(), [&](int64_t x, int64_t y) {
-                if (key[x] != key[y]) return key[x] < key[y];
+                if (comp[x].cls != comp[y].cls) return comp[x].cls < comp[y].cls;
                 return comp[x].cost > comp[y].cost;
             });
         }
@@ -1433,6 +1701,58 @@ int oob_side_constraint_count(const oob_batch* b, int64_t* counts) {
         for (int d : divs) c += v.op[d] != OOB_NODE_LIT;
         counts[q] = c;
     }
+    return OOB_OK;
+}
+
+int oob_jit_compile(const oob_batch* b, int64_t q, char* src, int64_t src_cap, double* compile_ms) {
+    g_last_error.clear();
+    if (!b || q < 0 || q >= b->n_queries) return fail(OOB_E_INVALID, "bad query index");
+    std::string why = validate(b, q);
+    if (!why.empty()) return fail(OOB_E_INVALID, why);
+    Compiled c = compile_query(b, q, MODE_SOLVE, 30.0, nullptr);
+    if (c.regime == R_IMMEDIATE || c.regime == R_RANGE) return fail(OOB_E_INVALID, "query has no search");
+    JitClass jc{c.words.data(), c.nv, c.ncon, c.ncode, c.nlit};
+    std::string text = jit_source(jc);
+    if (src && src_cap > 0) {
+        size_t n = std::min<size_t>(text.size(), (size_t)src_cap - 1);
+        std::memcpy(src, text.data(), n);
+        src[n] = 0;
+    }
+    std::vector<const void*> k;
+    std::vector<int> regs;
+    std::string e = jit_prepare({jc}, k, regs, compile_ms, false);
+    if (!e.empty()) return fail(OOB_E_INVALID, e);
+    return OOB_OK;
+}
+
+int oob_host_bench(const oob_batch* b, const oob_options* opt, double* ms) {
+    // host pipeline only (no device): compile + schedule (prepare), then pack
+    if (!b || !ms) return fail(OOB_E_INVALID, "null argument");
+    const int64_t n = b->n_queries;
+    std::vector<int8_t> verdict(n);
+    std::vector<int64_t> nodes(n), passes(n);
+    std::vector<double> el(n);
+    auto t0 = std::chrono::steady_clock::now();
+    Prepared pr;
+    int rc0 = prepare(b, opt, MODE_SOLVE, nullptr, verdict.data(), nodes.data(), passes.data(), el.data(), pr, 1);
+    if (rc0 != OOB_OK) return rc0;
+    auto t1 = std::chrono::steady_clock::now();
+    RunCtx rc;
+    rc.b = b;
+    rc.opt = pr.opt;
+    rc.comp = &pr.comp;
+    rc.mode = MODE_SOLVE;
+    rc.errs = &pr.errs;
+    for (auto& wk : pr.work) {
+        DevGroup G;
+        G.dev = wk.dev;
+        for (int w = 0; w < 3; w++) G.job[w].qs = wk.qs[w];
+        pack_group(rc, G);
+    }
+    auto t2 = std::chrono::steady_clock::now();
+    ms[0] = pr.compile_s * 1e3;
+    ms[1] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    ms[2] = std::chrono::duration<double, std::milli>(t2 - t1).count();
     return OOB_OK;
 }
 
@@ -1596,6 +1916,8 @@ void oob_plan_destroy(oob_plan* p) {
             if (P->ev0) cudaEventDestroy(P->ev0);
             if (P->ev1) cudaEventDestroy(P->ev1);
             if (P->evr) cudaEventDestroy(P->evr);
+            for (auto x : P->xs) cudaStreamDestroy(x);
+            for (auto x : P->xev) cudaEventDestroy(x);
             if (P->stream) cudaStreamDestroy(P->stream);
         }
     delete p;

@@ -19,6 +19,7 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
     const unsigned lt_mask = (1u << lane) - 1u;
 
     uint32_t c = a.warp_class ? a.warp_class[warp] : 0u;  // the warp's current class queue (warp-uniform)
+    if (c == NO_CLASS) return;
     ClassDesc cd = a.classes[c];
     L.set_class(a, cd);
     bool drained = false;             // every class queue is empty

@@ -7,7 +7,7 @@
 // templates on this type.  The host proves every intermediate magnitude is
 // below 2^253, so the truncating operations below are exact.
 #pragma once
-#include <cstdint>
+#include "types.h"
 
 #if defined(__CUDACC__)
 #define W_HD __host__ __device__ __forceinline__

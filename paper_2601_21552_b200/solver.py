@@ -120,12 +120,13 @@ def _verdicts_from(out, fb: FlatBatch, types, raise_errors=True):
 
 
 def solve_flat(fb: FlatBatch, timeout_s: float = 30.0, *, node_budget: int = 0,
-               n_gpus: int = 0, device: int = 0, flags: int = 0, heavy_nodes: int = 0) -> dict:
+               n_gpus: int = 0, device: int = 0, flags: int = 0, heavy_nodes: int = 0,
+               jit_min: int = 0) -> dict:
     """Decide a FlatBatch; returns raw numpy results (verdict codes, model
     words, nodes, passes, elapsed).  Raises on engine errors.  heavy_nodes:
     DFS nodes after which a query moves to the warp-cooperative frontier
     kernel (0 = default, < 0 = never)."""
-    out = _lib.solve_flat(fb, timeout_s, node_budget, n_gpus, device, flags, heavy_nodes)
+    out = _lib.solve_flat(fb, timeout_s, node_budget, n_gpus, device, flags, heavy_nodes, jit_min)
     rc = out["status"]
     if rc == _lib.OOB_E_INVALID:
         raise ValueError(out["error"])

@@ -25,7 +25,7 @@ def ref(monkeypatch):
     from oracle import oracle
     from paper_2601_21552_b200 import _lib
 
-    def oracle_engine(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0):
+    def oracle_engine(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0, jit_min=0):
         out = oracle.solve_flat(fb, timeout_s, node_budget)
         out["status"], out["error"] = 0, ""
         return out
