@@ -130,6 +130,8 @@ struct LaunchArgs {
     // heavy-query hand-off: the lockstep kernel gives up a query after
     // heavy_nodes DFS nodes and queues it for the frontier kernel
     uint32_t heavy_nodes;     // 0 = never hand off
+    uint32_t heavy_passes;    // also hand off after this many propagation passes (0 = no)
+    uint32_t frontier_only;   // a tail launch: skip the lockstep phase, serve the heavy list
     uint32_t* heavy_count;    // [0] listed [1] claimed
     uint32_t* heavy_list;     // query index + 1 (0 = not yet published)
     uint64_t* heavy_t0;       // start time of each scheduled query (ns)
@@ -151,6 +153,7 @@ struct LaunchArgs {
     int mode;                 // MODE_SOLVE / MODE_PROPAGATE / MODE_CHECK
     uint32_t* resume;         // per scheduled query (null: all fresh)
     uint64_t* timeline;       // debug (SCUBA_OOB_TIMELINE): per entry start, hand-off, frontier start, end (ns)
+    unsigned long long* stats;  // debug (SCUBA_OOB_TRACE=2): frontier / lockstep lane-efficiency counters
     DemoteTarget dem[2];      // root kernel: [0] int64 job, [1] int128 job (slot null: none)
 };
 

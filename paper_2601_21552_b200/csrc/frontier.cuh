@@ -1,6 +1,7 @@
 // frontier.cuh -- warp-cooperative DFS for heavy queries (K1, second stage).
 //
-// The lockstep kernel hands a query off after `heavy_nodes` DFS nodes.  Here
+// The lockstep kernel hands a query off after `heavy_nodes` DFS nodes (or
+// `heavy_passes` propagation passes: a long chain gets a warp of its own).  Here
 // one warp owns one heavy query and its 32 lanes expand the 32 LEFTMOST
 // pending nodes of the reference's DFS tree (solver.py:385-416) at once:
 //
@@ -86,7 +87,7 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
 
     uint32_t nunits = 1, nfree = 0, ebump = 0, nlog = 0;
     if (lane == 0) R.units[0] = UNIT_ROOT;
-    bool log_ok = true, have_sat = false;
+    bool have_sat = false;
     uint64_t sat_p0 = 0, sat_p1 = 0;
     uint32_t sat_depth = 0;
     int64_t tot_nodes = 0, tot_passes = 0;
@@ -198,21 +199,24 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
             break;
         }
         // ---- log the expanded nodes (pre-order accounting) ----
-        if (__any_sync(FULL, has && depth >= 128)) log_ok = false;  // paths hold 128 levels
+        // paths hold 128 levels and the log `logcap` nodes: beyond that the
+        // query ends with ERR_DEPTH and the host decides it again on the
+        // sequential path with more scratch (counters stay exact)
+        if (__any_sync(FULL, has && depth >= 128) || nlog + k > logcap) {
+            status = VERDICT_ERROR;
+            err = ERR_DEPTH;
+            break;
+        }
         {
             unsigned hm = __ballot_sync(FULL, has);
-            if (log_ok && nlog + k <= logcap) {
-                if (has) {
-                    uint32_t at = nlog + lane;
-                    R.log_path[2 * at] = p0;
-                    R.log_path[2 * at + 1] = p1;
-                    R.log_meta[2 * at] = depth;
-                    R.log_meta[2 * at + 1] = (uint32_t)my_passes;
-                }
-                nlog += k;
-            } else {
-                log_ok = false;
+            if (has) {
+                uint32_t at = nlog + lane;
+                R.log_path[2 * at] = p0;
+                R.log_path[2 * at + 1] = p1;
+                R.log_meta[2 * at] = depth;
+                R.log_meta[2 * at + 1] = (uint32_t)my_passes;
             }
+            nlog += k;
             tot_nodes += __popc(hm);
             tot_passes += __reduce_add_sync(FULL, (unsigned)my_passes);
         }
@@ -271,7 +275,7 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
     int verdict = status;
     if (status == VERDICT_UNSAT && have_sat) verdict = VERDICT_SAT;
     int64_t out_nodes = tot_nodes, out_passes = tot_passes;
-    if (verdict == VERDICT_SAT && log_ok) {
+    if (verdict == VERDICT_SAT) {
         uint32_t cn = 0;
         uint64_t cp = 0;
         for (uint32_t i = lane; i < nlog; i += 32) {

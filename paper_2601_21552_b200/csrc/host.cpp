@@ -55,13 +55,14 @@ static int fail(int code, const std::string& msg) {
 
 // SCUBA_OOB_TRACE=1: per-phase host timings on stderr (compile, pack, stage,
 // kernels, fetch) -- the engine's only tracing hook
-static bool trace_on() {
-    static const bool on = [] {
+static int trace_level() {
+    static const int lv = [] {
         const char* e = std::getenv("SCUBA_OOB_TRACE");
-        return e && *e && *e != '0';
+        return (e && *e) ? std::atoi(e) : 0;
     }();
-    return on;
+    return lv;
 }
+static bool trace_on() { return trace_level() > 0; }
 struct Phase {
     const char* name;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
@@ -656,7 +657,7 @@ struct DevicePool {
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
     DevBuf classes, class_next, class_init, warp_class;
     DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
-    DevBuf resume, resume_init, slot64, slot128, timeline, classes_interp;
+    DevBuf resume, resume_init, slot64, slot128, timeline, classes_interp, stats;
     std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
     std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
@@ -665,7 +666,8 @@ struct DevicePool {
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
-                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &timeline, &classes_interp})
+                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &timeline, &classes_interp,
+                          &stats})
             b->release();
     }
 };
@@ -788,6 +790,8 @@ struct DevJob {
     uint64_t model_words = 0;
     uint32_t n_classes = 0;
     uint32_t blocks = 1, fblocks = 0;
+    uint32_t tail_blocks = 0;    // wide SOLVE jobs: frontier-only launch after the int64 kernel
+    LaunchArgs tail_args{};
     SlabGeom g{};
     LaunchArgs a{};
     size_t out_model_words = 0;
@@ -953,10 +957,28 @@ uint64_t jit_min() {
     return m;
 }
 constexpr uint32_t JIT_MAX_NV = 48, JIT_MAX_LIT = 48, JIT_MAX_CODE = 1024;
+// block geometry of the compiled-class kernels: warps per block and the
+// dynamic shared memory requested per block (an occupancy lever: enough of it
+// keeps one class per SM, so an SM's instruction cache holds one class's code)
+uint32_t jit_warps() {
+    static const uint32_t w = [] {
+        const char* e = std::getenv("SCUBA_OOB_JIT_WARPS");
+        return (uint32_t)std::max(1, std::min(8, (e && *e) ? std::atoi(e) : 2));
+    }();
+    return w;
+}
+uint32_t jit_smem() {
+    static const uint32_t b = [] {
+        const char* e = std::getenv("SCUBA_OOB_JIT_SMEM");
+        return (uint32_t)std::max(0, (e && *e) ? std::atoi(e) : 0);
+    }();
+    return b;
+}
 
 // allocate + upload the packed records of `j` into pool P (caller holds P->mu)
 constexpr uint32_t FR_ECAP = 2048, FR_UCAP = 4096, FR_LOGCAP = 32768;
 constexpr uint32_t HEAVY_NODES_DEFAULT = 16;
+constexpr uint32_t HEAVY_PASSES_DEFAULT = 256;  // long propagation chains leave the shared lockstep warps
 
 size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
     size_t b = (size_t)FR_ECAP * 2 * maxv * tbytes + 2 * (size_t)FR_ECAP * tbytes + (size_t)FR_ECAP * 16 +
@@ -1014,28 +1036,38 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(kernel_occupancy(j.wide, rc.mode, (size_t)j.g.smem_per_warp * WARPS_PER_BLOCK, &per_sm));
     per_sm = std::max(1, per_sm);
     const uint32_t warps_needed = (uint32_t)((n - j.jit_queries + 31) / 32);
-    j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
-                                                (uint32_t)(P->sms * per_sm)));
+    // the wide-regime solve kernels run next to the int64 one and hold their
+    // blocks while their long searches last: one block per SM at most, so
+    // they can never keep the int64 kernel (most of the work) off the SMs
+    const uint32_t cap_blocks = (j.wide && rc.mode == MODE_SOLVE) ? (uint32_t)P->sms : (uint32_t)(P->sms * per_sm);
+    j.blocks = std::max(1u, std::min<uint32_t>((warps_needed + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, cap_blocks));
     uint32_t n_warps = j.blocks * WARPS_PER_BLOCK;
     assign_warps(j, j.cls_interp, n_warps);
     for (size_t i = 0; i < j.jit_cls.size(); i++) {
         const ClassDesc& cd = j.cls[j.jit_cls[i]];
         int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, j.jit_fn[i], WARPS_PER_BLOCK * 32, 0) != cudaSuccess) {
+        const uint32_t jw = jit_warps();
+        if (jit_smem())
+            cudaFuncSetAttribute(j.jit_fn[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jit_smem());
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, j.jit_fn[i], jw * 32, jit_smem()) != cudaSuccess) {
             cudaGetLastError();
             occ = 4;
         }
         occ = std::max(1, occ);
         const uint32_t need = (cd.q_end - cd.q_begin + 31) / 32;
-        const uint32_t b = std::max(1u, std::min<uint32_t>((need + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
-                                                           (uint32_t)(P->sms * occ)));
+        const uint32_t b = std::max(1u, std::min<uint32_t>((need + jw - 1) / jw, (uint32_t)(P->sms * occ)));
         j.jit_blocks.push_back(b);
-        n_warps += b * WARPS_PER_BLOCK;
+        n_warps += b * jw;
     }
     // heavy-query hand-off (solve mode): threshold from the options
     int64_t hn = rc.opt.heavy_nodes;
     uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
-    j.fblocks = heavy_nodes ? n_warps / WARPS_PER_BLOCK : 0;  // one frontier scratch region per warp
+    // wide jobs: a frontier-only tail launch with a full grid serves their
+    // heavy list once the int64 kernel has freed the SMs
+    const uint32_t own_warps = n_warps;
+    j.tail_blocks = (j.wide && heavy_nodes) ? (uint32_t)(P->sms * per_sm) : 0u;
+    n_warps += j.tail_blocks * WARPS_PER_BLOCK;
+    j.fblocks = heavy_nodes ? (n_warps + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK : 0;  // one frontier region per warp
     const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
@@ -1094,6 +1126,13 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.class_next = (uint32_t*)P->class_next.p;
     a.warp_class = (const uint32_t*)P->warp_class.p;
     a.heavy_nodes = heavy_nodes;
+    {
+        static const uint32_t hp = [] {
+            const char* e = std::getenv("SCUBA_OOB_HEAVY_PASSES");
+            return (uint32_t)((e && *e) ? std::atoi(e) : (int)HEAVY_PASSES_DEFAULT);
+        }();
+        a.heavy_passes = hp;
+    }
     a.heavy_count = (uint32_t*)P->heavy_count.p;
     a.heavy_next = (uint32_t*)P->heavy_count.p + 1;
     a.heavy_list = (uint32_t*)P->heavy_list.p + n;
@@ -1117,10 +1156,23 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.node_budget = rc.opt.node_budget;
     a.mode = rc.mode;
     a.resume = (uint32_t*)P->resume.p;
+    a.stats = nullptr;
+    if (trace_level() >= 2 && rc.mode == MODE_SOLVE) {
+        CK(P->stats.ensure(64));
+        CK(cudaMemsetAsync(P->stats.p, 0, 64, s));
+        a.stats = (unsigned long long*)P->stats.p;
+    }
     a.timeline = nullptr;
     if (timeline_path() && rc.mode == MODE_SOLVE) {
         CK(P->timeline.ensure((size_t)n * 32));
         a.timeline = (uint64_t*)P->timeline.p;
+    }
+    if (j.tail_blocks) {
+        j.tail_args = a;
+        j.tail_args.frontier_only = 1;
+        j.tail_args.slab_T = (unsigned char*)P->slabT.p + (uint64_t)own_warps * j.g.slab_T_words * tbytes;
+        j.tail_args.slab_u32 = (uint32_t*)P->slabU.p + (uint64_t)own_warps * j.g.slab_u32_words;
+        j.tail_args.fr_region = (unsigned char*)P->fr_region.p + (uint64_t)own_warps * fr_bytes;
     }
     // one launch per compiled class: its own class queue and heavy list, and
     // its own range of per-warp scratch
@@ -1138,7 +1190,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         b.slab_u32 = (uint32_t*)P->slabU.p + warp_base * j.g.slab_u32_words;
         if (b.fr_region) b.fr_region = (unsigned char*)P->fr_region.p + warp_base * fr_bytes;
         j.jit_args.push_back(b);
-        warp_base += (uint64_t)j.jit_blocks[i] * WARPS_PER_BLOCK;
+        warp_base += (uint64_t)j.jit_blocks[i] * jit_warps();
     }
     j.staged = true;
     return "";
@@ -1288,13 +1340,17 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
             for (size_t x = 0; x < nxs; x++) CK(cudaStreamWaitEvent(P->xs[x], P->evr, 0));
             for (size_t i = 0; i < j.jit_cls.size(); i++) {
                 void* args[] = {&j.jit_args[i]};
-                CK(cudaLaunchKernel(j.jit_fn[i], dim3(j.jit_blocks[i]), dim3(WARPS_PER_BLOCK * 32), args, 0,
+                CK(cudaLaunchKernel(j.jit_fn[i], dim3(j.jit_blocks[i]), dim3(jit_warps() * 32), args, jit_smem(),
                                     P->xs[i % nxs]));
             }
             for (size_t x = 0; x < nxs; x++) CK(cudaEventRecord(P->xev[x], P->xs[x]));
         }
         CK(launch_solve(j.a, w, (int)j.blocks, (int)j.fblocks, s));
         for (size_t x = 0; x < std::min(P->xs.size(), j.jit_cls.size()); x++) CK(cudaStreamWaitEvent(s, P->xev[x], 0));
+        if (w == 0 && rc.mode == MODE_SOLVE)  // the wide jobs' frontier tails, once the int64 work is done
+            for (int t = 1; t < 3; t++)
+                if (present(G.job[t]) && G.job[t].tail_blocks)
+                    CK(launch_solve(G.job[t].tail_args, t, (int)G.job[t].tail_blocks, 0, s));
         CK(cudaEventRecord(P->ev1, s));
     }
     return "";
@@ -1355,6 +1411,15 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
             }
             std::fclose(f);
         }
+    }
+    if (j.a.stats) {
+        unsigned long long st[8];
+        CK(cudaMemcpy(st, j.a.stats, 64, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr,
+                     "[oob] job w%d: frontier rounds %llu units %llu lane-passes %llu / slots %llu (%.1f%%); "
+                     "lockstep lane-passes %llu / slots %llu (%.1f%%)\n",
+                     j.wide, st[2], st[3], st[1], st[0], st[0] ? 100.0 * st[1] / st[0] : 0.0, st[5], st[4],
+                     st[4] ? 100.0 * st[5] / st[4] : 0.0);
     }
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;

@@ -305,7 +305,7 @@ struct Gen {
         o << "  }\n";
         check();
         o << "};\n}  // namespace oob\n";
-        o << "extern \"C\" __global__ void __launch_bounds__(64) " << kname
+        o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname
           << "(oob::LaunchArgs a) { oob::jit_solve<oob::Cls>(a); }\n";
         return o.str();
     }

@@ -39,7 +39,7 @@ __global__ void __maxnreg__(128) oob_solve_kernel(LaunchArgs a) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     Lane<T> L;
     L.bind(a, warp, lane);
-    lockstep_phase(a, L, warp, lane);
+    if (!a.frontier_only) lockstep_phase(a, L, warp, lane);
     frontier_phase(a, L, warp, lane);
 }
 

@@ -85,9 +85,12 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
         if (!active) break;
 
         // ---- node start (_search, solver.py:391-393) ----
-        if (phase == PH_NODE && a.heavy_nodes && nodes >= a.heavy_nodes) {
-            // a heavy search: hand it to the warp-cooperative frontier phase
-            // (which restarts it from the root with 32 lanes); the list entry
+        if ((phase == PH_NODE || phase == PH_PASS) && a.heavy_nodes &&
+            ((phase == PH_NODE && nodes >= a.heavy_nodes) || (a.heavy_passes && passes >= a.heavy_passes))) {
+            // a heavy search (many nodes, or a long propagation chain): hand
+            // it to the warp-cooperative frontier phase, which restarts it
+            // from the root in a warp of its own (so a long chain no longer
+            // shares its warp's steps with 31 other queries); the list entry
             // is published after the start time it carries
             uint32_t slot = atomicAdd(a.heavy_count, 1u);
             a.heavy_t0[qi] = t0;
@@ -129,6 +132,13 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
         const bool run = (phase == PH_PASS) && !post;
         // ---- the pass: constraint loop (solver.py:275-277) ----
         dead = L.pass_sync(run);
+        if (a.stats) {  // [4] warp steps x 32 [5] lanes in a pass
+            unsigned r = __ballot_sync(FULL, run);
+            if (lane == 0) {
+                atomicAdd(a.stats + 4, 32ull);
+                atomicAdd(a.stats + 5, (unsigned long long)__popc(r));
+            }
+        }
         // ---- pass end ----
         if (run || post) {
             if (dead) {

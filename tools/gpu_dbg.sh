@@ -1,1 +1,1 @@
-SCUBA_OOB_TRACE=1 timeout 600 python tools/dbg_plan.py > gpurun_out/dbg.log 2>&1
+for cfg in c3 c4; do timeout 300 python tools/jit_sweep.py $cfg 100000 -1 2>&1 | sed "s/^/interp /"; done > gpurun_out/sweep.log
