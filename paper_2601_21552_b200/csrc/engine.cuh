@@ -41,16 +41,20 @@ __device__ __forceinline__ bool fits64(__int128 v) { return v == (__int128)(long
 // int64: the 32-bit hardware path when both operands lie in [-(2^31-1), 2^31-1]
 // (no INT32_MIN, so no overflow), the 64-bit software routine otherwise
 __device__ __forceinline__ bool fits31(long long v) { return (unsigned long long)v + 0x7FFFFFFFull <= 0xFFFFFFFEull; }
-template <>
-__device__ __forceinline__ long long cdiv<long long>(long long a, long long b) {
+// (one out-of-line copy each: every inlined division site would otherwise
+// carry ~25 instructions of the 32-bit path and blow the instruction cache)
+__device__ __noinline__ long long cdiv_ll(long long a, long long b) {
     if (fits31(a) && fits31(b)) return (long long)((int)a / (int)b);
     return a / b;
 }
-template <>
-__device__ __forceinline__ long long cmod<long long>(long long a, long long b) {
+__device__ __noinline__ long long cmod_ll(long long a, long long b) {
     if (fits31(a) && fits31(b)) return (long long)((int)a % (int)b);
     return a % b;
 }
+template <>
+__device__ __forceinline__ long long cdiv<long long>(long long a, long long b) { return cdiv_ll(a, b); }
+template <>
+__device__ __forceinline__ long long cmod<long long>(long long a, long long b) { return cmod_ll(a, b); }
 template <>
 __device__ __forceinline__ __int128 cdiv<__int128>(__int128 a, __int128 b) {
     if (fits64(a) && fits64(b) && !((long long)a == (-9223372036854775807LL - 1) && (long long)b == -1))
