@@ -35,6 +35,10 @@ from pathlib import Path
 
 import numpy as np
 
+# the engine runs several kernels per device concurrently; more hardware work
+# queues than the default 8 (must be set before any CUDA context exists)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 

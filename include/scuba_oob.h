@@ -123,7 +123,7 @@ typedef struct {
                              <0 = never (one lane per query throughout)      */
     int32_t jit_min;      /* structure classes with at least this many queries
                              in an int64 job run as run-time compiled kernels;
-                             0 = default (SCUBA_OOB_JIT_MIN, else off)        */
+                             0 = default (SCUBA_OOB_JIT_MIN, else 1024)       */
 } oob_options;
 
 enum {

@@ -7,9 +7,14 @@ in-tree by `python -m paper_2601_21552_b200.build` (or __graft_entry__.build()).
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
+
+# several engine kernels run concurrently per device: more hardware work
+# queues than the default 8 (effective only before a CUDA context exists)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "libscuba_oob.so"

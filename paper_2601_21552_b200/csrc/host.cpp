@@ -81,6 +81,15 @@ static const char* timeline_path() {
     return (p && *p) ? p : nullptr;
 }
 
+// The engine runs several kernels per device concurrently (root, int64 and
+// wide solve kernels, one per compiled class): ask for more hardware work
+// queues than the default 8 so that independent streams do not serialise.
+// Only effective before the process creates its CUDA context; never
+// overrides a value the user set.
+__attribute__((constructor)) static void oob_default_connections() {
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+}
+
 static i128 from_w(oob_i128 w) { return (i128)(((unsigned __int128)(uint64_t)w.hi << 64) | w.lo); }
 
 // ============================================================================
@@ -944,15 +953,14 @@ void assign_warps(DevJob& j, const std::vector<ClassDesc>& cls, uint32_t n_warps
     for (size_t i = 0; w < n_warps; w++, i = (i + 1) % live.size()) j.warp_class[w] = live[i];
 }
 
-// JIT policy: classes with at least jit_min queries in an int64 SOLVE job run
-// as run-time compiled kernels (oob_options.jit_min, else SCUBA_OOB_JIT_MIN;
-// off by default: the interpreting kernel overlaps the long search chains of
-// all classes in one persistent grid, which the per-class kernels do not yet
-// match -- see DESIGN.md; OOB_F_NO_JIT disables)
+// JIT policy: classes with at least jit_min queries (default 1024) in an int64
+// SOLVE job run as run-time compiled kernels (oob_options.jit_min, else
+// SCUBA_OOB_JIT_MIN; OOB_F_NO_JIT disables; if NVRTC is unavailable the
+// classes stay on the interpreting kernel)
 uint64_t jit_min() {
     static const uint64_t m = [] {
         const char* e = std::getenv("SCUBA_OOB_JIT_MIN");
-        return (e && *e) ? (uint64_t)std::strtoull(e, nullptr, 10) : UINT64_MAX;
+        return (e && *e) ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)1024;
     }();
     return m;
 }
@@ -963,7 +971,7 @@ constexpr uint32_t JIT_MAX_NV = 48, JIT_MAX_LIT = 48, JIT_MAX_CODE = 1024;
 uint32_t jit_warps() {
     static const uint32_t w = [] {
         const char* e = std::getenv("SCUBA_OOB_JIT_WARPS");
-        return (uint32_t)std::max(1, std::min(8, (e && *e) ? std::atoi(e) : 2));
+        return (uint32_t)std::max(1, std::min(8, (e && *e) ? std::atoi(e) : 8));
     }();
     return w;
 }
@@ -1024,7 +1032,11 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         if (!want.empty()) {
             std::vector<int> regs;
             std::string e = jit_prepare(want, j.jit_fn, regs, &j.jit_ms);
-            if (!e.empty()) return "run-time compile: " + e;
+            if (!e.empty()) {  // no NVRTC / compile failure: the interpreter decides these classes
+                if (trace_on()) std::fprintf(stderr, "[oob] run-time compile unavailable: %s\n", e.c_str());
+                j.jit_cls.clear();
+                j.jit_fn.clear();
+            }
             for (size_t i = 0; i < j.jit_cls.size(); i++) {
                 ClassDesc& cd = j.cls_interp[j.jit_cls[i]];
                 j.jit_queries += cd.q_end - cd.q_begin;
@@ -1325,7 +1337,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         if (!j.jit_cls.empty()) {
             static const size_t kmax = [] {
                 const char* e = std::getenv("SCUBA_OOB_JIT_STREAMS");
-                return (size_t)((e && *e) ? std::max(1, std::atoi(e)) : 64);
+                return (size_t)((e && *e) ? std::max(1, std::atoi(e)) : 16);
             }();
             const size_t nxs = std::min(kmax, j.jit_cls.size());
             while (P->xs.size() < nxs) {
