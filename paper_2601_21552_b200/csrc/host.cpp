@@ -180,7 +180,13 @@ struct Chk {
     bool ovf = false;
     i128 add(i128 a, i128 b) { i128 r; if (__builtin_add_overflow(a, b, &r)) ovf = true; return r; }
     i128 sub(i128 a, i128 b) { i128 r; if (__builtin_sub_overflow(a, b, &r)) ovf = true; return r; }
-    i128 mul(i128 a, i128 b) { i128 r; if (__builtin_mul_overflow(a, b, &r)) ovf = true; return r; }
+    i128 mul(i128 a, i128 b) {
+        // both factors within int64: one 64x64->128 multiply, exact (|a*b| < 2^126)
+        if (a == (int64_t)a && b == (int64_t)b) return (i128)(int64_t)a * (i128)(int64_t)b;
+        i128 r;
+        if (__builtin_mul_overflow(a, b, &r)) ovf = true;
+        return r;
+    }
 };
 inline i128 iabs(i128 a) { return a < 0 ? -a : a; }
 inline i128 imax(i128 a, i128 b) { return a > b ? a : b; }
@@ -194,22 +200,42 @@ const i128 I64MAX = (i128)INT64_MAX;
 const i128 D64MAX = ((i128)1 << 62) - 1;
 const i128 D128MAX = ((i128)1 << 126) - 1;
 
-struct Compiled {
-    int8_t regime = R_IMMEDIATE;
-    int8_t immediate = OOB_UNSAT;
+// The structure of a query (everything but domain and literal VALUES): shared
+// by all queries with identical terms, built once per thread per structure.
+struct Structure {
     uint32_t nv = 0, ncon = 0, ncode = 0, nlit = 0;
     uint32_t maxcsize = 1;        // largest constraint (lhs + rhs nodes)
     uint32_t maxdepth = 1;        // deepest term
-    std::vector<uint32_t> words;  // ncon constraint words + ncode node words
-    std::vector<i128> lits;       // per literal slot
+    std::vector<uint32_t> words;  // ncon constraint words + ncode node words + 4 nv membership words
+    std::vector<std::pair<uint32_t, uint32_t>> roots;  // per constraint: lhs / rhs root node
+    std::vector<uint8_t> rels;
+    std::vector<int32_t> lit_src; // per literal slot: the query's input literal index (-1: the constant 1)
+    uint64_t key = 0;             // structure-class hash (words, nv, ncon)
+    std::string range_why;        // non-empty: the structure alone is beyond the engine (R_RANGE)
+    const uint32_t* code() const { return words.data() + ncon; }
+};
+
+struct Compiled {
+    int8_t regime = R_IMMEDIATE;
+    int8_t immediate = OOB_UNSAT;
+    std::shared_ptr<const Structure> st;
+    uint32_t nv = 0, ncon = 0, ncode = 0, nlit = 0;
+    uint32_t maxcsize = 1, maxdepth = 1;
     double cost = 0;
     uint64_t key = 0;             // structure-class hash (words, nv, ncon)
     uint32_t cls = UINT32_MAX;    // batch-wide structure class id (prepare)
     std::string why;              // reason for R_RANGE
+    const std::vector<uint32_t>& words() const { return st->words; }
     bool same_class(const Compiled& o) const {
-        return key == o.key && nv == o.nv && ncon == o.ncon && words == o.words;
+        return key == o.key && nv == o.nv && ncon == o.ncon && (st == o.st || st->words == o.st->words);
     }
 };
+
+// literal slot i of query q (values are read from the caller's batch)
+inline i128 lit_value(const oob_batch* b, int64_t q, const Structure& st, uint32_t i) {
+    const int32_t src = st.lit_src[i];
+    return src < 0 ? (i128)1 : from_w(b->lits[b->lit_begin[q] + src]);
+}
 
 // Page-locked host blocks, recycled across calls (H2D / D2H at full PCIe /
 // C2C bandwidth without a driver staging copy).  Falls back to pageable
@@ -325,9 +351,20 @@ void group_classes(size_t n, GetComp get, std::vector<uint32_t>& cls, std::vecto
     }
 }
 
+// host worker threads (SCUBA_OOB_HOST_THREADS caps them; default: cores, <= 32)
+unsigned host_threads() {
+    static const unsigned n = [] {
+        const char* e = std::getenv("SCUBA_OOB_HOST_THREADS");
+        unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        unsigned cap = (e && *e) ? (unsigned)std::max(1, std::atoi(e)) : 32u;
+        return std::max(1u, std::min(hw, cap));
+    }();
+    return n;
+}
+
 template <typename F>
 void parallel_for(size_t n, size_t grain, F f) {
-    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    unsigned nt = host_threads();
     if (n < 2 * grain || nt == 1) {
         f(0, n);
         return;
@@ -347,16 +384,21 @@ void parallel_for(size_t n, size_t grain, F f) {
 
 struct Emitter {
     const QView& v;
-    std::vector<uint32_t> code;
-    std::vector<i128>& lits;
+    std::vector<uint32_t>& code;  // per-thread scratch
+    std::vector<int32_t>& lits;   // per literal slot: input literal index (-1: constant 1)
     int max_depth = 0;
-    Emitter(const QView& vv, std::vector<i128>& l) : v(vv), lits(l) {}
+    static std::vector<uint32_t>& scratch() {
+        static thread_local std::vector<uint32_t> c;
+        c.clear();
+        return c;
+    }
+    Emitter(const QView& vv, std::vector<int32_t>& l) : v(vv), code(scratch()), lits(l) {}
     // returns the postfix index of the emitted subtree root
     uint32_t emit(int e, int depth) {
         max_depth = std::max(max_depth, depth);
         int op = v.op[e];
         if (op == OOB_NODE_LIT) {
-            lits.push_back(from_w(v.lits[v.na[e]]));
+            lits.push_back(v.na[e]);
             code.push_back(node_word(NODE_LIT, (uint32_t)(lits.size() - 1)));
         } else if (op == OOB_NODE_VAR) {
             code.push_back(node_word(NODE_VAR, (uint32_t)v.na[e]));
@@ -368,8 +410,8 @@ struct Emitter {
         }
         return (uint32_t)(code.size() - 1);
     }
-    uint32_t emit_lit(i128 value) {
-        lits.push_back(value);
+    uint32_t emit_one() {  // the literal 1 of a divisor side constraint (solver.py:357)
+        lits.push_back(-1);
         code.push_back(node_word(NODE_LIT, (uint32_t)(lits.size() - 1)));
         return (uint32_t)(code.size() - 1);
     }
@@ -380,13 +422,16 @@ inline uint32_t w_arg(uint32_t w) { return w >> 3; }
 
 // Bound proof over the expanded code (see engine.cuh header).  Returns the
 // largest magnitude any intermediate value can reach, or -1 on overflow.
-i128 prove_bound(const std::vector<uint32_t>& code, const std::vector<std::pair<uint32_t, uint32_t>>& cons,
+i128 prove_bound(const uint32_t* code, size_t n, const std::vector<std::pair<uint32_t, uint32_t>>& cons,
                  const std::vector<uint8_t>& rels, const std::vector<i128>& dlo,
                  const std::vector<i128>& dhi, const std::vector<i128>& lits) {
     Chk c;
-    size_t n = code.size();
-    std::vector<i128> flo(n), fhi(n), gm(n);
-    std::vector<char> none(n, 0);
+    static thread_local std::vector<i128> flo, fhi, gm;  // scratch reused across queries
+    static thread_local std::vector<char> none;
+    flo.resize(n);
+    fhi.resize(n);
+    gm.resize(n);
+    none.assign(n, 0);
     i128 B = 0;
     for (size_t i = 0; i < dlo.size(); i++) B = imax(B, imax(iabs(dlo[i]), iabs(dhi[i])));
     for (i128 l : lits) B = imax(B, iabs(l));
@@ -445,7 +490,8 @@ i128 prove_bound(const std::vector<uint32_t>& code, const std::vector<std::pair<
     // per relation (solver.py:240-259): the one-sided ones are +-INF and the
     // other side's forward bound +-1; for "=" arithmetic only happens when the
     // target [max(l0,r0), min(l1,r1)] is non-empty, i.e. inside both sides.
-    std::vector<std::pair<uint32_t, i128>> stack;
+    static thread_local std::vector<std::pair<uint32_t, i128>> stack;
+    stack.clear();
     for (size_t k = 0; k < cons.size(); k++) {
         i128 fl = fmag(cons[k].first), fr = fmag(cons[k].second), tl, tr;
         switch (rels[k]) {
@@ -490,12 +536,15 @@ i128 prove_bound(const std::vector<uint32_t>& code, const std::vector<std::pair<
 // 128-bit proof overflows): |x + y| <= |x| + |y|, |x * y| <= |x||y|,
 // |tdiv(a, d)| <= |a|, |a % d| <= min(|a|, |d|); targets as in prove_bound.
 // Relative rounding error is far below the 2^250 vs 2^255 margin.
-double prove_bound_mag(const std::vector<uint32_t>& code, const std::vector<std::pair<uint32_t, uint32_t>>& cons,
+double prove_bound_mag(const uint32_t* code, size_t n, const std::vector<std::pair<uint32_t, uint32_t>>& cons,
                        const std::vector<uint8_t>& rels, const std::vector<i128>& dlo, const std::vector<i128>& dhi,
                        const std::vector<i128>& lits) {
-    auto mag = [](i128 v) { return (double)(v < 0 ? -(long double)v : (long double)v); };
-    size_t n = code.size();
-    std::vector<double> m(n);
+    auto mag = [](i128 v) -> double {
+        if (v == (int64_t)v) return std::fabs((double)(int64_t)v);  // one conversion in the common case
+        return (double)(v < 0 ? -(long double)v : (long double)v);
+    };
+    static thread_local std::vector<double> m;
+    m.resize(n);
     double B = 0;
     auto size_of = [&](uint32_t i) { return w_op(code[i]) >= NODE_ADD ? w_arg(code[i]) : 1u; };
     for (size_t j = 0; j < n; j++) {
@@ -512,7 +561,8 @@ double prove_bound_mag(const std::vector<uint32_t>& code, const std::vector<std:
         B = std::max(B, m[j]);
     }
     const double INF_D = 1e18;
-    std::vector<std::pair<uint32_t, double>> st;
+    static thread_local std::vector<std::pair<uint32_t, double>> st;
+    st.clear();
     for (size_t k = 0; k < cons.size(); k++) {
         double fl = m[cons[k].first], fr = m[cons[k].second], tl, tr;
         if (rels[k] == OOB_REL_EQ) tl = tr = std::min(fl, fr);
@@ -541,13 +591,155 @@ double prove_bound_mag(const std::vector<uint32_t>& code, const std::vector<std:
     return B;
 }
 
+// The structure of query q (mode: MODE_SOLVE appends the divisor side
+// constraints; they depend on the divisors' literal VALUES, solver.py:353-357).
+std::shared_ptr<Structure> build_structure(const QView& v, int mode) {
+    auto out = std::make_shared<Structure>();
+    Structure& st = *out;
+    st.nv = (uint32_t)v.nv;
+    static thread_local std::vector<int> divs;
+    divs.clear();
+    bool has_div = false;
+    for (int i = 0; i < v.nn && !has_div; i++) has_div = v.op[i] == OOB_NODE_DIV || v.op[i] == OOB_NODE_MOD;
+    if (mode == MODE_SOLVE && has_div)
+        for (int k = 0; k < v.ncon; k++) {  // constraint list + side constraints (solver.py:371)
+            collect_divisors(v, v.lhs[k], divs);
+            collect_divisors(v, v.rhs[k], divs);
+        }
+    Emitter em(v, st.lit_src);
+    for (int k = 0; k < v.ncon; k++) {
+        uint32_t l = em.emit(v.lhs[k], 1);
+        uint32_t r = em.emit(v.rhs[k], 1);
+        st.roots.push_back({l, r});
+        st.rels.push_back(v.rel[k]);
+    }
+    for (int d : divs) {
+        if (v.op[d] == OOB_NODE_LIT) continue;  // solver.py:353-357
+        uint32_t l = em.emit(d, 1);
+        uint32_t r = em.emit_one();
+        st.roots.push_back({l, r});
+        st.rels.push_back(OOB_REL_GE);
+    }
+    st.ncon = (uint32_t)st.roots.size();
+    st.ncode = (uint32_t)em.code.size();
+    st.nlit = (uint32_t)st.lit_src.size();
+    if (st.ncode > MAX_CODE || st.nlit > 65535 || st.ncon > 65535) {
+        st.range_why = "expanded query too large (" + std::to_string(st.ncode) + " term nodes)";
+        return out;
+    }
+    if (em.max_depth > (int)MAX_TREE_DEPTH - 2) {
+        st.range_why = "term nesting deeper than " + std::to_string(MAX_TREE_DEPTH - 2);
+        return out;
+    }
+    st.maxdepth = (uint32_t)std::max(1, em.max_depth);
+    for (auto& rt : st.roots) {
+        uint32_t lsz = w_op(em.code[rt.first]) >= NODE_ADD ? w_arg(em.code[rt.first]) : 1u;
+        st.maxcsize = std::max(st.maxcsize, rt.second + 1 - (rt.first + 1 - lsz));
+    }
+    st.words.reserve(st.ncon + st.ncode + 4 * st.nv);
+    for (size_t k = 0; k < st.roots.size(); k++)
+        st.words.push_back(con_word(st.rels[k], st.roots[k].first, st.roots[k].second));
+    st.words.insert(st.words.end(), em.code.begin(), em.code.end());
+    // membership masks for exact constraint skipping: bit k of variable v is
+    // set iff constraint k mentions v (only used when ncon <= 128)
+    const size_t mbase = st.words.size();
+    st.words.resize(mbase + (size_t)st.nv * 4, 0);
+    if (st.ncon <= 128) {
+        for (uint32_t k = 0; k < st.ncon; k++) {
+            for (uint32_t root : {st.roots[k].first, st.roots[k].second}) {
+                uint32_t sz = w_op(em.code[root]) >= NODE_ADD ? w_arg(em.code[root]) : 1u;
+                for (uint32_t j = root + 1 - sz; j <= root; j++)
+                    if (w_op(em.code[j]) == NODE_VAR)
+                        st.words[mbase + 4 * w_arg(em.code[j]) + k / 32] |= 1u << (k % 32);
+            }
+        }
+    }
+    st.key = class_hash(st.words, st.nv, st.ncon);
+    return out;
+}
+
+// Per-thread cache of structures keyed by the query's input terms: the input
+// arrays are compared exactly, plus -- for side constraints -- whether each
+// literal divisor is >= 1.  Queries with a non-literal divisor are not cached
+// (their side-constraint dedup compares literal values inside the divisors).
+struct StructCache {
+    struct Entry {
+        int mode, nv, ncon, nn, nl;
+        std::vector<uint8_t> op, rel, divok;
+        std::vector<int32_t> na, nb, lhs, rhs;
+        std::shared_ptr<const Structure> st;
+    };
+    std::unordered_multimap<uint64_t, Entry> map;
+
+    static uint64_t fingerprint(const QView& v, int mode, std::vector<uint8_t>& divok, bool& cacheable) {
+        uint64_t h = 1469598103934665603ull ^ ((uint64_t)mode << 56) ^ ((uint64_t)v.nv << 40) ^
+                     ((uint64_t)v.ncon << 20) ^ (uint64_t)v.nn;
+        auto mix = [&](uint64_t x) {
+            h ^= x;
+            h *= 1099511628211ull;
+        };
+        divok.clear();
+        cacheable = true;
+        for (int i = 0; i < v.nn; i++) {
+            mix((uint64_t)v.op[i] | ((uint64_t)(uint32_t)v.na[i] << 8) | ((uint64_t)(uint32_t)v.nb[i] << 36));
+            if (v.op[i] == OOB_NODE_DIV || v.op[i] == OOB_NODE_MOD) {
+                int r = v.nb[i];
+                if (v.op[r] == OOB_NODE_LIT) divok.push_back(from_w(v.lits[v.na[r]]) >= 1);
+                else cacheable = false;
+            }
+        }
+        for (int k = 0; k < v.ncon; k++) mix((uint64_t)v.rel[k] | ((uint64_t)(uint32_t)v.lhs[k] << 8) |
+                                             ((uint64_t)(uint32_t)v.rhs[k] << 36));
+        for (uint8_t d : divok) mix(d);
+        return h;
+    }
+    static bool same(const Entry& e, const QView& v, int mode, const std::vector<uint8_t>& divok) {
+        if (e.mode != mode || e.nv != v.nv || e.ncon != v.ncon || e.nn != v.nn || e.nl != v.nl) return false;
+        return std::memcmp(e.op.data(), v.op, v.nn) == 0 && std::memcmp(e.na.data(), v.na, v.nn * 4) == 0 &&
+               std::memcmp(e.nb.data(), v.nb, v.nn * 4) == 0 && std::memcmp(e.rel.data(), v.rel, v.ncon) == 0 &&
+               std::memcmp(e.lhs.data(), v.lhs, v.ncon * 4) == 0 &&
+               std::memcmp(e.rhs.data(), v.rhs, v.ncon * 4) == 0 && e.divok == divok;
+    }
+    std::shared_ptr<const Structure> get(const QView& v, int mode) {
+        static thread_local std::vector<uint8_t> divok;
+        bool cacheable;
+        uint64_t h = fingerprint(v, mode, divok, cacheable);
+        if (!cacheable) return build_structure(v, mode);
+        auto range = map.equal_range(h);
+        for (auto it = range.first; it != range.second; ++it)
+            if (same(it->second, v, mode, divok)) return it->second.st;
+        std::shared_ptr<const Structure> st = build_structure(v, mode);
+        if (map.size() > 4096) map.clear();  // bounded
+        Entry e;
+        e.mode = mode;
+        e.nv = v.nv;
+        e.ncon = v.ncon;
+        e.nn = v.nn;
+        e.nl = v.nl;
+        e.op.assign(v.op, v.op + v.nn);
+        e.na.assign(v.na, v.na + v.nn);
+        e.nb.assign(v.nb, v.nb + v.nn);
+        e.rel.assign(v.rel, v.rel + v.ncon);
+        e.lhs.assign(v.lhs, v.lhs + v.ncon);
+        e.rhs.assign(v.rhs, v.rhs + v.ncon);
+        e.divok = divok;
+        e.st = st;
+        map.emplace(h, std::move(e));
+        return st;
+    }
+};
+
 // mode: MODE_SOLVE (side constraints), MODE_PROPAGATE / MODE_CHECK (as given)
 Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s,
                        const oob_i128* model_in) {
     Compiled out;
     QView v = view_of(b, q);
     out.nv = (uint32_t)v.nv;
-    std::vector<i128> dlo(v.nv), dhi(v.nv);
+    // per-thread scratch reused across queries (no allocation per query)
+    static thread_local std::vector<i128> dlo, dhi, lits;
+    static thread_local StructCache cache;
+    dlo.resize(v.nv);
+    dhi.resize(v.nv);
     bool empty = false;
     for (int i = 0; i < v.nv; i++) {
         if (mode == MODE_CHECK) {
@@ -557,48 +749,31 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
             dhi[i] = from_w(v.vhi[i]);
         }
         if (dlo[i] > dhi[i]) empty = true;
-        out.cost += (dhi[i] > dlo[i]) ? std::log2((double)(dhi[i] - dlo[i]) + 1.0) : 0.0;
+        if (dhi[i] > dlo[i]) {  // scheduling cost: bits of the domain width
+            unsigned __int128 w = (unsigned __int128)(dhi[i] - dlo[i]);
+            uint64_t hi64 = (uint64_t)(w >> 64), lo64 = (uint64_t)w;
+            out.cost += hi64 ? 128 - __builtin_clzll(hi64) : (lo64 ? 64 - __builtin_clzll(lo64) : 0);
+        }
     }
     if (mode == MODE_SOLVE) {
         if (empty) { out.immediate = OOB_UNSAT; return out; }          // solver.py:374-375
         if (!(timeout_s > 0)) { out.immediate = OOB_TIMEOUT; return out; }  // deadline passed (:391)
     }
-    // constraint list: user constraints + divisor side constraints (solver.py:371)
-    std::vector<std::pair<int, int>> user;
-    for (int k = 0; k < v.ncon; k++) user.push_back({v.lhs[k], v.rhs[k]});
-    std::vector<int> divs;
-    if (mode == MODE_SOLVE)
-        for (auto& c : user) { collect_divisors(v, c.first, divs); collect_divisors(v, c.second, divs); }
-    Emitter em(v, out.lits);
-    std::vector<std::pair<uint32_t, uint32_t>> roots;
-    std::vector<uint8_t> rels;
-    for (int k = 0; k < v.ncon; k++) {
-        uint32_t l = em.emit(user[k].first, 1);
-        uint32_t r = em.emit(user[k].second, 1);
-        roots.push_back({l, r});
-        rels.push_back(v.rel[k]);
-    }
-    for (int d : divs) {
-        if (v.op[d] == OOB_NODE_LIT) continue;  // solver.py:353-357
-        uint32_t l = em.emit(d, 1);
-        uint32_t r = em.emit_lit(1);
-        roots.push_back({l, r});
-        rels.push_back(OOB_REL_GE);
-    }
-    out.ncon = (uint32_t)roots.size();
-    out.ncode = (uint32_t)em.code.size();
-    out.nlit = (uint32_t)out.lits.size();
-    if (out.ncode > MAX_CODE || out.nlit > 65535 || out.ncon > 65535) {
+    out.st = cache.get(v, mode);
+    const Structure& st = *out.st;
+    out.ncon = st.ncon;
+    out.ncode = st.ncode;
+    out.nlit = st.nlit;
+    out.maxcsize = st.maxcsize;
+    out.maxdepth = st.maxdepth;
+    out.key = st.key;
+    if (!st.range_why.empty()) {
         out.regime = R_RANGE;
-        out.why = "expanded query too large (" + std::to_string(out.ncode) + " term nodes)";
+        out.why = st.range_why;
         return out;
     }
-    if (em.max_depth > (int)MAX_TREE_DEPTH - 2) {
-        out.regime = R_RANGE;
-        out.why = "term nesting deeper than " + std::to_string(MAX_TREE_DEPTH - 2);
-        return out;
-    }
-    i128 B = prove_bound(em.code, roots, rels, dlo, dhi, out.lits);
+    lits.resize(st.nlit);
+    for (uint32_t i = 0; i < st.nlit; i++) lits[i] = lit_value(b, q, st, i);
     i128 Dmax = 0;
     for (int i = 0; i < v.nv; i++) Dmax = imax(Dmax, imax(iabs(dlo[i]), iabs(dhi[i])));
     if (Dmax > D128MAX) {
@@ -606,38 +781,26 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
         out.why = "domain bounds exceed the 128-bit wire format";
         return out;
     }
+    // Fast acceptance: the magnitude bound in double precision dominates the
+    // exact one (|x|+|y|, |x||y| instead of interval corners); its rounding
+    // error over < 2^14 operations is below 1e-12 relative, so a value under
+    // 9.2e18 (I64MAX = 9.223e18) proves the int64 regime.  Otherwise the exact
+    // checked 128-bit proof decides.
+    const double mag = prove_bound_mag(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits);
+    if (mag < 9.2e18 && Dmax <= D64MAX) {
+        out.regime = R_W64;
+        return out;
+    }
+    i128 B = prove_bound(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits);
     if (B >= 0) {
         out.regime = (B <= I64MAX && Dmax <= D64MAX) ? R_W64 : R_W128;
-    } else if (prove_bound_mag(em.code, roots, rels, dlo, dhi, out.lits) < 1.8e75) {  // < 2^250
+    } else if (mag < 1.8e75) {  // < 2^250
         out.regime = R_W256;
     } else {
         out.regime = R_RANGE;
         out.why = "intermediate magnitudes exceed the exact 256-bit regime";
         return out;
     }
-    out.maxdepth = (uint32_t)std::max(1, em.max_depth);
-    for (auto& rt : roots) {
-        uint32_t lsz = w_op(em.code[rt.first]) >= NODE_ADD ? w_arg(em.code[rt.first]) : 1u;
-        out.maxcsize = std::max(out.maxcsize, rt.second + 1 - (rt.first + 1 - lsz));
-    }
-    out.words.reserve(out.ncon + out.ncode + 4 * out.nv);
-    for (size_t k = 0; k < roots.size(); k++)
-        out.words.push_back(con_word(rels[k], roots[k].first, roots[k].second));
-    out.words.insert(out.words.end(), em.code.begin(), em.code.end());
-    // membership masks for exact constraint skipping: bit k of variable v is
-    // set iff constraint k mentions v (only used when ncon <= 128)
-    std::vector<uint32_t> member((size_t)out.nv * 4, 0);
-    if (out.ncon <= 128) {
-        for (uint32_t k = 0; k < out.ncon; k++) {
-            for (uint32_t root : {roots[k].first, roots[k].second}) {
-                uint32_t sz = w_op(em.code[root]) >= NODE_ADD ? w_arg(em.code[root]) : 1u;
-                for (uint32_t j = root + 1 - sz; j <= root; j++)
-                    if (w_op(em.code[j]) == NODE_VAR) member[4 * w_arg(em.code[j]) + k / 32] |= 1u << (k % 32);
-            }
-        }
-    }
-    out.words.insert(out.words.end(), member.begin(), member.end());
-    out.key = class_hash(out.words, out.nv, out.ncon);
     return out;
 }
 
@@ -824,10 +987,16 @@ void pack(const RunCtx& rc, DevJob& j) {
     std::unordered_map<uint32_t, uint32_t> local;
     std::vector<uint32_t> cls(entries.size());
     std::vector<size_t> rep;
+    uint32_t last_g = UINT32_MAX, last_l = 0;  // entries arrive in class runs
     for (size_t i = 0; i < entries.size(); i++) {
-        auto it = local.emplace(comp[qid(entries[i])].cls, (uint32_t)rep.size());
-        if (it.second) rep.push_back(i);
-        cls[i] = it.first->second;
+        const uint32_t g = comp[qid(entries[i])].cls;
+        if (g != last_g) {
+            auto it = local.emplace(g, (uint32_t)rep.size());
+            if (it.second) rep.push_back(i);
+            last_g = g;
+            last_l = it.first->second;
+        }
+        cls[i] = last_l;
     }
     const size_t nc = rep.size();
     std::vector<uint32_t> count(nc + 1, 0);
@@ -850,7 +1019,7 @@ void pack(const RunCtx& rc, DevJob& j) {
         const Compiled& c = comp[qid(entries[rep[id]])];
         ClassDesc& cd = j.cls[id];
         cd.code_off = (uint32_t)j.code.size();
-        j.code.insert(j.code.end(), c.words.begin(), c.words.end());
+        j.code.insert(j.code.end(), c.words().begin(), c.words().end());
         cd.nv_ncon = c.nv | (c.ncon << 16);
         cd.ncode_nlit = c.ncode | (c.nlit << 16);
         cd.q_begin = count[id];
@@ -922,7 +1091,7 @@ void pack(const RunCtx& rc, DevJob& j) {
                     put(from_w(b->var_hi[vb + v]));
                 }
             }
-            for (i128 l : c.lits) put(l);
+            for (uint32_t i = 0; i < c.nlit; i++) put(lit_value(b, q, *c.st, i));
             std::fill(out, end, 0);
         }
     });
@@ -1628,7 +1797,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     comp.assign(n, Compiled{});
     {
         Phase ph("compile");
-        unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        unsigned nt = host_threads();
         if (n < 2048) nt = 1;
         std::vector<std::thread> th;
         std::atomic<int64_t> next{0};
@@ -1679,11 +1848,18 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         auto& qs = reg[w];
         if (qs.empty()) continue;
         if (!(opt.flags & OOB_F_NO_SORT)) {
-            // class-major, cost-minor: a 32-query tile is (nearly) one class
-            std::stable_sort(qs.begin(), qs.end(), [&](int64_t x, int64_t y) {
-                if (comp[x].cls != comp[y].cls) return comp[x].cls < comp[y].cls;
-                return comp[x].cost > comp[y].cost;
+            // class-major, cost-minor (expensive first), ties by query index:
+            // one packed 64-bit key per query, sorted in a contiguous array
+            std::vector<std::pair<uint64_t, int64_t>> keyed(qs.size());
+            parallel_for(qs.size(), 16384, [&](size_t lo, size_t hi) {
+                for (size_t i = lo; i < hi; i++) {
+                    const Compiled& c = comp[qs[i]];
+                    const uint64_t cost = (uint64_t)std::min(c.cost, 65535.0);
+                    keyed[i] = {((uint64_t)c.cls << 32) | ((0xFFFFull - cost) << 16), qs[i]};
+                }
             });
+            std::sort(keyed.begin(), keyed.end());
+            for (size_t i = 0; i < qs.size(); i++) qs[i] = keyed[i].second;
         }
         for (size_t i = 0; i < qs.size(); i++) pr.work[(i / 32) % want].qs[w].push_back(qs[i]);
     }
@@ -1719,7 +1895,12 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
     rc.errs = &pr.errs;
     std::string e = run_all(rc, pr.work);
     if (!e.empty()) return fail(OOB_E_CUDA, e);
-    return finish(pr, b->n_queries);
+    int rcode = finish(pr, b->n_queries);
+    {
+        Phase ph("teardown");
+        Prepared gone(std::move(pr));
+    }
+    return rcode;
 }
 
 }  // namespace
@@ -1788,7 +1969,7 @@ int oob_jit_compile(const oob_batch* b, int64_t q, char* src, int64_t src_cap, d
     if (!why.empty()) return fail(OOB_E_INVALID, why);
     Compiled c = compile_query(b, q, MODE_SOLVE, 30.0, nullptr);
     if (c.regime == R_IMMEDIATE || c.regime == R_RANGE) return fail(OOB_E_INVALID, "query has no search");
-    JitClass jc{c.words.data(), c.nv, c.ncon, c.ncode, c.nlit};
+    JitClass jc{c.words().data(), c.nv, c.ncon, c.ncode, c.nlit};
     std::string text = jit_source(jc);
     if (src && src_cap > 0) {
         size_t n = std::min<size_t>(text.size(), (size_t)src_cap - 1);
