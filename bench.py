@@ -207,12 +207,12 @@ def load_peak_hbm():
 
 
 def ncu_traffic(config: str):
-    """DRAM bytes per launch of the decision kernel from the committed ncu
-    capture summary (profiles/), or None."""
+    """DRAM bytes of one step (all launches of one plan run) from the
+    committed ncu launch-list summary (profiles/ncu_summary.json), or None."""
     p = ROOT / "profiles" / "ncu_summary.json"
     try:
         d = json.loads(p.read_text())
-        return d.get(config, {}).get("dram_bytes_per_launch")
+        return d.get(config, {}).get("dram_bytes_per_step")
     except Exception:
         return None
 

@@ -2151,7 +2151,8 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
             cls += j.n_classes;
             if (w) wide += own;
             jobs++;
-            launches += 1 + ((w && (!j.slot[0].empty() || !j.slot[1].empty())) ? 1 : 0);
+            launches += 1 + (int64_t)j.jit_cls.size() + (j.tail_blocks ? 1 : 0) +
+                        ((w && (!j.slot[0].empty() || !j.slot[1].empty())) ? 1 : 0);
         }
     info[0] = nq;
     info[1] = rec;
