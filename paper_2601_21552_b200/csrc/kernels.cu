@@ -58,8 +58,34 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     Lane<T> L;
     L.bind(a, warp, lane);
+    // domains + literal slots of the lane's query into a data block of width w
+    auto store_state = [&](int64_t* dst, int w) {
+        if (w == 0) {
+            for (uint32_t v = 0; v < L.nv; ++v) {
+                dst[2 * v] = low64(L.E(L.env_lo, v));
+                dst[2 * v + 1] = low64(L.E(L.env_hi, v));
+            }
+            for (uint32_t i = 0; i < L.nlit; ++i) dst[2 * L.nv + i] = low64(L.E(L.lit, i));
+        } else {
+            auto put = [&](uint32_t at, __int128 x) {
+                dst[2 * at] = (int64_t)(uint64_t)x;
+                dst[2 * at + 1] = (int64_t)(x >> 64);
+            };
+            for (uint32_t v = 0; v < L.nv; ++v) {
+                put(2 * v, low128(L.E(L.env_lo, v)));
+                put(2 * v + 1, low128(L.E(L.env_hi, v)));
+            }
+            for (uint32_t i = 0; i < L.nlit; ++i) put(2 * L.nv + i, low128(L.E(L.lit, i)));
+        }
+    };
     for (uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x; qi < a.n; qi += gridDim.x * blockDim.x) {
-        if (a.resume[qi] != 0u) continue;  // a shadow of a wider job's query
+        // own fresh entries, and (int128 job) shadows the 256-bit root phase
+        // resumed here: their root propagation continues in this narrower
+        // width until it fits int64 (a 256-bit query typically fits int128
+        // after one pass and int64 only after the asserts have propagated)
+        const uint32_t rs = a.resume[qi];
+        if (rs == RES_SKIP || (rs != 0u && (SELF == 2 || (rs & RES_FIX)))) continue;
+        const bool from_shadow = rs != 0u;
         const QDesc d = a.qdesc[qi];
         ClassDesc cd;
         cd.code_off = d.code_off;
@@ -67,9 +93,9 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
         cd.ncode_nlit = d.ncode_nlit;
         L.set_class(a, cd);
         L.load(a, d);
-        const uint64_t t0 = global_ns();
+        const uint64_t t0 = from_shadow ? a.heavy_t0[qi] : global_ns();
         const uint64_t deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
-        uint32_t passes = 0;
+        uint32_t passes = from_shadow ? (rs & RES_PASSES) : 0u;
         bool dead = false, fix = false, expired = false;
         int target = -1;
         while (passes < ROOT_MAX_PASSES) {
@@ -96,8 +122,11 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
             }
             if (fix) break;
         }
-        if (expired || L.err) continue;  // the lockstep kernel redoes it and reports
-        if (dead) {                      // Unsat after the root node (solver.py:393-394)
+        if (expired || L.err) {  // the lockstep kernel redoes it and reports
+            if (from_shadow) a.resume[qi] = rs;
+            continue;
+        }
+        if (dead) {  // Unsat after the root node (solver.py:393-394)
             a.verdict[qi] = (int8_t)VERDICT_UNSAT;
             a.err[qi] = (int8_t)ERR_NONE;
             a.nodes[qi] = 1;
@@ -110,27 +139,17 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
             a.resume[qi] = RES_SKIP;
             continue;
         }
-        if (target < 0) continue;
+        if (target < 0) {
+            if (from_shadow) {  // continue from here in this job (the shadow block is ours to rewrite)
+                store_state(const_cast<int64_t*>(a.data) + d.data_off, SELF);
+                __threadfence();
+                a.resume[qi] = RES_ROOT | (fix ? RES_FIX : 0u) | passes;
+            }
+            continue;
+        }
         const DemoteTarget& tg = a.dem[target];
         const uint32_t s = tg.slot[qi];
-        int64_t* dst = tg.data + tg.qdesc[s].data_off;
-        if (target == 0) {
-            for (uint32_t v = 0; v < L.nv; ++v) {
-                dst[2 * v] = low64(L.E(L.env_lo, v));
-                dst[2 * v + 1] = low64(L.E(L.env_hi, v));
-            }
-            for (uint32_t i = 0; i < L.nlit; ++i) dst[2 * L.nv + i] = low64(L.E(L.lit, i));
-        } else {
-            auto put = [&](uint32_t at, __int128 x) {
-                dst[2 * at] = (int64_t)(uint64_t)x;
-                dst[2 * at + 1] = (int64_t)(x >> 64);
-            };
-            for (uint32_t v = 0; v < L.nv; ++v) {
-                put(2 * v, low128(L.E(L.env_lo, v)));
-                put(2 * v + 1, low128(L.E(L.env_hi, v)));
-            }
-            for (uint32_t i = 0; i < L.nlit; ++i) put(2 * L.nv + i, low128(L.E(L.lit, i)));
-        }
+        store_state(tg.data + tg.qdesc[s].data_off, target);
         tg.t0[s] = t0;
         __threadfence();
         tg.resume[s] = RES_ROOT | (fix ? RES_FIX : 0u) | passes;

@@ -1,4 +1,3 @@
-export CUDA_DEVICE_MAX_CONNECTIONS=32
-for k in 4 16 64; do SCUBA_OOB_JIT_WARPS=8 SCUBA_OOB_JIT_STREAMS=$k timeout 300 python tools/jit_runs.py c3 1024 2>&1 | tail -3 | sed "s/^/c3 K=$k /"; done > gpurun_out/runs.log
-for k in 4 16 64; do SCUBA_OOB_JIT_WARPS=8 SCUBA_OOB_JIT_STREAMS=$k timeout 300 python tools/jit_runs.py c4 1024 2>&1 | tail -3 | sed "s/^/c4 K=$k /"; done >> gpurun_out/runs.log
-timeout 300 python tools/jit_runs.py c3 -1 2>&1 | tail -2 | sed "s/^/c3 interp /" >> gpurun_out/runs.log
+rm -f gpurun_out/tl_c4.bin
+SCUBA_OOB_TIMELINE=gpurun_out/tl_c4.bin timeout 300 python tools/tl_run.py c4 > gpurun_out/tl.log 2>&1
+python tools/timeline.py gpurun_out/tl_c4.bin 10 > gpurun_out/tl_c4.txt

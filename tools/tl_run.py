@@ -1,0 +1,10 @@
+"""Device timeline of the LAST of a few plan runs (SCUBA_OOB_TIMELINE must be set)."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2601_21552_b200 import _lib, synth
+cfg = sys.argv[1]
+fb = synth.generate(cfg, 100000, names=False)
+p = _lib.Plan(fb, 30.0)
+print([round(p.run(), 2) for _ in range(3)], flush=True)
+p.results()
