@@ -1235,7 +1235,13 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
             occ = 4;
         }
         occ = std::max(1, occ);
-        const uint32_t need = (cd.q_end - cd.q_begin + 31) / 32;
+        // warps: one per 32 queries of the class, times SCUBA_OOB_JIT_GRID_MULT
+        // (extra blocks start as others finish and serve the class's heavy list)
+        static const uint32_t mult = [] {
+            const char* e = std::getenv("SCUBA_OOB_JIT_GRID_MULT");
+            return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : 1);
+        }();
+        const uint32_t need = mult * ((cd.q_end - cd.q_begin + 31) / 32);
         const uint32_t b = std::max(1u, std::min<uint32_t>((need + jw - 1) / jw, (uint32_t)(P->sms * occ)));
         j.jit_blocks.push_back(b);
         n_warps += b * jw;

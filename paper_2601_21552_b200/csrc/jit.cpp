@@ -28,6 +28,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -344,9 +345,14 @@ std::string compile_entry(Entry& e, const JitClass& c) {
                               kSrc_phases_cuh, kSrc_jit_lane_cuh};
     if (nvrtcCreateProgram(&prog, src.c_str(), "oob_jit_class.cu", 7, hdr_src, kHeaderNames) != NVRTC_SUCCESS)
         return "nvrtcCreateProgram failed";
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DOOB_JIT=1",
-                          "--device-int128"};
-    nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DOOB_JIT=1",
+                                     "--device-int128"};
+    static const std::string maxreg = [] {  // SCUBA_OOB_JIT_MAXREG: register cap (occupancy experiments)
+        const char* e = std::getenv("SCUBA_OOB_JIT_MAXREG");
+        return (e && *e) ? std::string("--maxrregcount=") + e : std::string();
+    }();
+    if (!maxreg.empty()) opts.push_back(maxreg.c_str());
+    nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
     size_t logn = 0;
     nvrtcGetProgramLogSize(prog, &logn);
     e.log.resize(logn);
