@@ -1040,12 +1040,16 @@ void pack(const RunCtx& rc, DevJob& j) {
     // to 16 (int64/int128) or 32 bytes (256-bit)
     const size_t vw = j.wide == 2 ? 4 : (size_t)j.wide + 1;  // int64 words per value
     const size_t align = j.wide == 2 ? 4 : 2;
+    // every entry of a class has the same data size: offsets per class run
     std::vector<uint64_t> doff(n + 1, 0), moff(n + 1, 0);
-    for (size_t i = 0; i < n; i++) {
-        const Compiled& c = comp[qid(order[i])];
-        const size_t words = (2 * (size_t)c.nv + c.nlit) * vw;
-        doff[i + 1] = doff[i] + ((words + align - 1) / align) * align;
-        moff[i + 1] = moff[i] + c.nv;
+    for (size_t id = 0; id < nc; id++) {
+        const Compiled& c = comp[qid(entries[rep[id]])];
+        const uint64_t words = (2 * (uint64_t)c.nv + c.nlit) * vw;
+        const uint64_t dsz = ((words + align - 1) / align) * align;
+        for (uint32_t i = j.cls[id].q_begin; i < j.cls[id].q_end; i++) {
+            doff[i + 1] = doff[i] + dsz;
+            moff[i + 1] = moff[i] + c.nv;
+        }
     }
     j.model_words = moff[n];
     j.data.alloc(std::max<uint64_t>(doff[n], 4));
@@ -1740,27 +1744,56 @@ int visible_devices() {
 // verified word for word in parallel (on a hash collision the exact grouping
 // is used instead).
 void assign_classes(std::vector<Compiled>& comp, const std::vector<int64_t> reg[3]) {
-    std::vector<int64_t> all;
-    for (int w = 0; w < 3; w++) all.insert(all.end(), reg[w].begin(), reg[w].end());
-    std::unordered_map<uint64_t, uint32_t> ids;
-    std::vector<int64_t> rep;
-    for (int64_t q : all) {
-        auto it = ids.emplace(comp[q].key, (uint32_t)rep.size());
-        if (it.second) rep.push_back(q);
-        comp[q].cls = it.first->second;
-    }
-    std::atomic<bool> clash{false};
-    parallel_for(all.size(), 4096, [&](size_t lo, size_t hi) {
-        for (size_t i = lo; i < hi && !clash; i++) {
-            const Compiled& c = comp[all[i]];
-            if (!c.same_class(comp[rep[c.cls]])) clash = true;
+    // queries share Structure objects (one per structure and compile thread):
+    // number the distinct pointers with a small open-addressing table, then
+    // merge pointers whose structures are equal word for word
+    const size_t TB = 1u << 14;
+    std::vector<const Structure*> slot_ptr(TB, nullptr);
+    std::vector<uint32_t> slot_id(TB, 0);
+    std::vector<const Structure*> ptrs;
+    std::unordered_map<const Structure*, uint32_t> overflow;  // only if the table fills up
+    auto pid_of = [&](const Structure* p) -> uint32_t {
+        size_t h = (std::hash<const void*>{}(p) * 0x9E3779B97F4A7C15ull) >> 50;
+        for (size_t k = 0; k < 64; k++) {
+            size_t i = (h + k) & (TB - 1);
+            if (slot_ptr[i] == p) return slot_id[i];
+            if (!slot_ptr[i]) {
+                slot_ptr[i] = p;
+                slot_id[i] = (uint32_t)ptrs.size();
+                ptrs.push_back(p);
+                return slot_id[i];
+            }
         }
-    });
-    if (!clash) return;
-    std::vector<uint32_t> cls;
-    std::vector<size_t> r2;
-    group_classes(all.size(), [&](size_t i) -> const Compiled& { return comp[all[i]]; }, cls, r2);
-    for (size_t i = 0; i < all.size(); i++) comp[all[i]].cls = cls[i];
+        auto it = overflow.emplace(p, (uint32_t)ptrs.size());
+        if (it.second) ptrs.push_back(p);
+        return it.first->second;
+    };
+    for (int w = 0; w < 3; w++)
+        for (int64_t q : reg[w]) comp[q].cls = pid_of(comp[q].st.get());
+    // canonical class per pointer
+    std::vector<uint32_t> canon(ptrs.size());
+    std::unordered_multimap<uint64_t, uint32_t> by_key;  // key -> class id (first pointer index)
+    std::vector<uint32_t> first_ptr;
+    for (uint32_t i = 0; i < ptrs.size(); i++) {
+        const Structure& st = *ptrs[i];
+        uint32_t id = UINT32_MAX;
+        auto range = by_key.equal_range(st.key);
+        for (auto it = range.first; it != range.second; ++it) {
+            const Structure& o = *ptrs[first_ptr[it->second]];
+            if (o.nv == st.nv && o.ncon == st.ncon && o.words == st.words) {
+                id = it->second;
+                break;
+            }
+        }
+        if (id == UINT32_MAX) {
+            id = (uint32_t)first_ptr.size();
+            first_ptr.push_back(i);
+            by_key.emplace(st.key, id);
+        }
+        canon[i] = id;
+    }
+    for (int w = 0; w < 3; w++)
+        for (int64_t q : reg[w]) comp[q].cls = canon[comp[q].cls];
 }
 
 // Compile + schedule: fills immediate verdicts and returns the device jobs.
@@ -1854,17 +1887,22 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         auto& qs = reg[w];
         if (qs.empty()) continue;
         if (!(opt.flags & OOB_F_NO_SORT)) {
-            // class-major, cost-minor (expensive first), ties by query index:
-            // one packed 64-bit key per query, sorted in a contiguous array
-            std::vector<std::pair<uint64_t, int64_t>> keyed(qs.size());
-            parallel_for(qs.size(), 16384, [&](size_t lo, size_t hi) {
-                for (size_t i = lo; i < hi; i++) {
-                    const Compiled& c = comp[qs[i]];
-                    const uint64_t cost = (uint64_t)std::min(c.cost, 65535.0);
-                    keyed[i] = {((uint64_t)c.cls << 32) | ((0xFFFFull - cost) << 16), qs[i]};
-                }
+            // class-major (counting sort, stable), cost-minor: expensive first,
+            // ties by query index (per-class sorts run in parallel)
+            uint32_t ncls = 0;
+            for (int64_t q : qs) ncls = std::max(ncls, comp[q].cls + 1);
+            std::vector<uint32_t> start(ncls + 1, 0);
+            for (int64_t q : qs) start[comp[q].cls + 1]++;
+            for (uint32_t c = 0; c < ncls; c++) start[c + 1] += start[c];
+            std::vector<std::pair<uint32_t, int64_t>> keyed(qs.size());  // (inverted cost, query)
+            {
+                std::vector<uint32_t> at(start.begin(), start.end() - 1);
+                for (int64_t q : qs)
+                    keyed[at[comp[q].cls]++] = {0xFFFFu - (uint32_t)std::min(comp[q].cost, 65535.0), q};
+            }
+            parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
+                for (size_t c = lo; c < hi; c++) std::sort(keyed.begin() + start[c], keyed.begin() + start[c + 1]);
             });
-            std::sort(keyed.begin(), keyed.end());
             for (size_t i = 0; i < qs.size(); i++) qs[i] = keyed[i].second;
         }
         for (size_t i = 0; i < qs.size(); i++) pr.work[(i / 32) % want].qs[w].push_back(qs[i]);
