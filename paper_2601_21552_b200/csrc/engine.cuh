@@ -516,6 +516,19 @@ struct Lane {
         E(env_hi, v) = hi;
     }
     __device__ __forceinline__ uint32_t nvars() const { return nv; }
+    // whole domain vectors: (lo, hi) pairs in / out, model = the lower bounds
+    __device__ __forceinline__ void load_env(const T* env) {
+        for (uint32_t v = 0; v < nv; ++v) put_env(v, env[2 * v], env[2 * v + 1]);
+    }
+    __device__ __forceinline__ void store_env(T* env) const {
+        for (uint32_t v = 0; v < nv; ++v) {
+            env[2 * v] = get_lo(v);
+            env[2 * v + 1] = get_hi(v);
+        }
+    }
+    __device__ __forceinline__ void store_model(int64_t* m) const {
+        for (uint32_t v = 0; v < nv; ++v) store_i128(m + 2 * v, get_lo(v));
+    }
     __device__ __forceinline__ bool check_env() { return check_point(env_lo); }
     // One propagation pass of every lane with run set, warp-synchronously: the
     // warp visits, in order, every constraint that is dirty in at least one

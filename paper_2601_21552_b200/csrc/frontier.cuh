@@ -121,7 +121,7 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
             if (u != UNIT_ROOT) {
                 uint32_t e = u >> 1, half = u & 1;
                 const T* env = R.e_env + (size_t)e * 2 * nv;
-                for (uint32_t v = 0; v < nv; ++v) L.put_env(v, env[2 * v], env[2 * v + 1]);
+                L.load_env(env);
                 const uint32_t* c = R.e_clean + (size_t)e * 4;
                 L.clean0 = ((uint64_t)c[1] << 32) | c[0];
                 L.clean1 = ((uint64_t)c[3] << 32) | c[2];
@@ -228,7 +228,7 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
             limit = (uint32_t)j;
             if ((int)lane == j) {
                 int64_t* m = a.model + 2 * d.out_v;
-                for (uint32_t v = 0; v < nv; ++v) store_i128(m + 2 * v, L.get_lo(v));
+                L.store_model(m);
             }
             sat_p0 = __shfl_sync(FULL, p0, j);
             sat_p1 = __shfl_sync(FULL, p1, j);
@@ -246,10 +246,7 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
             uint32_t h = __popc(spm & ~((2u << lane) - 1u));       // splitters to my right
             uint32_t e = r < nfree ? R.freel[nfree - 1 - r] : ebump + (r - nfree);
             T* env = R.e_env + (size_t)e * 2 * nv;
-            for (uint32_t v = 0; v < nv; ++v) {
-                env[2 * v] = L.get_lo(v);
-                env[2 * v + 1] = L.get_hi(v);
-            }
+            L.store_env(env);
             T lo = L.get_lo(pick), hi = L.get_hi(pick);
             R.e_mid[e] = (lo + hi) >> 1;  // floor midpoint (solver.py:409)
             R.e_hi[e] = hi;

@@ -289,7 +289,8 @@ struct Gen {
     std::string source(const std::string& kname) {
         o << "#include \"jit_lane.cuh\"\nnamespace oob {\nstruct Cls {\n";
         o << "  typedef long long T;\n  typedef Arith<T> A;\n";
-        o << "  static constexpr uint32_t NV = " << nv << ", NCON = " << ncon << ", NLIT = " << nlit << ";\n";
+        o << "  static constexpr uint32_t NV = " << nv << ", NCON = " << ncon << ", NCODE = " << ncode
+          << ", NLIT = " << nlit << ";\n";
         for (int half = 0; half < 2; half++) {
             o << "  static __device__ __forceinline__ uint64_t M" << half << "(uint32_t v) {\n    switch (v) {\n";
             for (uint32_t v = 0; v < nv; v++) {

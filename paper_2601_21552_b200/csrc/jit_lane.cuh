@@ -31,10 +31,10 @@ struct JitLane {
 
     T lo[NV], hi[NV];
     T lit[NL];
-    uint32_t stamp[NV];
     // per-warp global slab, lane-minor (element i of this lane is p[i * 32])
     T *fr_mid, *fr_hi, *tr_lo, *tr_hi;
-    uint32_t *fr_pick, *fr_mark, *fr_clean, *tr_var;
+    uint32_t *fr_pick, *fr_mark, *fr_clean, *tr_var, *stamp;
+    const uint32_t* member;  // the class's membership words (dynamic-index touch)
     uint32_t trail_cap, depth_cap;
     uint32_t depth, trail_len, seg;
     uint64_t clean0, clean1;
@@ -54,6 +54,8 @@ struct JitLane {
         fr_mark = sU + g.o_fr_mark;
         fr_clean = sU + g.o_fr_clean;
         tr_var = sU + g.o_tr_var;
+        stamp = sU + g.o_stamp;
+        member = a.code + a.classes[0].code_off + C::NCON + C::NCODE;
         trail_cap = g.trail_cap;
         depth_cap = g.depth_cap;
         seg = 0;
@@ -69,7 +71,7 @@ struct JitLane {
         for (uint32_t v = 0; v < NV; ++v) {
             lo[v] = src[2 * v];
             hi[v] = src[2 * v + 1];
-            stamp[v] = 0xFFFFFFFFu;
+            stamp[(size_t)v * 32] = 0xFFFFFFFFu;
         }
 #pragma unroll
         for (uint32_t i = 0; i < C::NLIT; ++i) lit[i] = src[2 * NV + i];
@@ -101,6 +103,25 @@ struct JitLane {
                 hi[i] = h;
             }
     }
+    // whole domain vectors, constant indices (no select chains)
+    __device__ __forceinline__ void load_env(const T* env) {
+#pragma unroll
+        for (uint32_t v = 0; v < NV; ++v) {
+            lo[v] = env[2 * v];
+            hi[v] = env[2 * v + 1];
+        }
+    }
+    __device__ __forceinline__ void store_env(T* env) const {
+#pragma unroll
+        for (uint32_t v = 0; v < NV; ++v) {
+            env[2 * v] = lo[v];
+            env[2 * v + 1] = hi[v];
+        }
+    }
+    __device__ __forceinline__ void store_model(int64_t* m) const {
+#pragma unroll
+        for (uint32_t v = 0; v < NV; ++v) store_i128(m + 2 * v, lo[v]);
+    }
     __device__ __forceinline__ bool pass_sync(bool run) {
         bool dead = false;
         if (run) C::pass(*this, dead);
@@ -127,31 +148,41 @@ struct JitLane {
         return ok;
     }
 
-    // ----- domain updates (i is a compile-time constant after inlining) --------
-    __device__ __forceinline__ bool set_dom_i(uint32_t i, T l, T h) {
-        if (depth > 0 && stamp[i] != seg) {
+    // ----- domain updates --------------------------------------------------------
+    // trail entry for variable v (its domain before the first change in this
+    // DFS segment); false on capacity overflow
+    __device__ __forceinline__ bool trail(uint32_t v, T ol, T oh) {
+        if (depth > 0 && stamp[(size_t)v * 32] != seg) {
             if (trail_len >= trail_cap) {
                 err = ERR_TRAIL;
                 return false;
             }
-            tr_var[(size_t)trail_len * 32] = i;
-            tr_lo[(size_t)trail_len * 32] = lo[i];
-            tr_hi[(size_t)trail_len * 32] = hi[i];
+            tr_var[(size_t)trail_len * 32] = v;
+            tr_lo[(size_t)trail_len * 32] = ol;
+            tr_hi[(size_t)trail_len * 32] = oh;
             ++trail_len;
-            stamp[i] = seg;
+            stamp[(size_t)v * 32] = seg;
         }
+        return true;
+    }
+    // i is a compile-time constant after inlining (narrowing sites)
+    __device__ __forceinline__ bool set_dom_i(uint32_t i, T l, T h) {
+        if (!trail(i, lo[i], hi[i])) return false;
         lo[i] = l;
         hi[i] = h;
         clean0 &= ~C::M0(i);
         clean1 &= ~C::M1(i);
         return true;
     }
+    // v dynamic (DFS split / backtrack / frontier child): one select chain per
+    // access instead of an unrolled copy of set_dom_i per variable
     __device__ __forceinline__ bool set_dom(uint32_t v, T l, T h) {
-        bool ok = true;
-#pragma unroll
-        for (uint32_t i = 0; i < NV; ++i)
-            if (v == i) ok = set_dom_i(i, l, h);
-        return ok;
+        if (!trail(v, get_lo(v), get_hi(v))) return false;
+        put_env(v, l, h);
+        const uint32_t* m = member + 4 * v;
+        clean0 &= ~(((uint64_t)__ldg(m + 1) << 32) | __ldg(m));
+        clean1 &= ~(((uint64_t)__ldg(m + 3) << 32) | __ldg(m + 2));
+        return true;
     }
     // _Narrower.narrow on a VarRef (solver.py:165-173)
     __device__ __forceinline__ bool narrow_var(uint32_t i, T a, T b) {

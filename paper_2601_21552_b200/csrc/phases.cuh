@@ -1,7 +1,8 @@
 // phases.cuh -- the scheduling phases of the solve kernels, generic over the
 // lane type (the interpreting Lane<T> of engine.cuh or a compiled JitLane of
 // jit_lane.cuh).  A lane type provides: T, set_class, load, get_lo/get_hi,
-// put_env, nvars, pass_sync, check_env, pick_var, split, set_dom, backtrack,
+// put_env, load_env/store_env/store_model (whole domain vectors), nvars,
+// pass_sync, check_env, pick_var, split, set_dom, backtrack,
 // and the fields changed, err, depth, clean0, clean1.
 #pragma once
 #include "engine.cuh"
@@ -190,7 +191,7 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
             if (a.timeline) a.timeline[4 * (size_t)qi + 3] = global_ns();
             if (verdict == VERDICT_SAT) {
                 int64_t* m = a.model + 2 * d.out_v;
-                for (uint32_t v = 0; v < L.nvars(); ++v) store_i128(m + 2 * v, L.get_lo(v));
+                L.store_model(m);
             }
             phase = PH_IDLE;
         }
