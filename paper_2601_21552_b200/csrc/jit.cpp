@@ -39,6 +39,9 @@
 #include <thread>
 #include <vector>
 
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include "format.h"
 #include "jit.h"
 
@@ -322,6 +325,7 @@ struct Entry {
     cudaKernel_t kernel = nullptr;
     int regs = 0;
     double compile_ms = 0;
+    bool from_disk = false;
 };
 
 std::mutex g_mu;
@@ -329,6 +333,69 @@ std::map<std::string, std::shared_ptr<Entry>> g_cache;
 
 const char* kHeaderNames[] = {"types.h", "format.h", "wide.cuh", "engine.cuh", "frontier.cuh", "phases.cuh",
                               "jit_lane.cuh"};
+
+// On-disk cubin cache shared by the processes of a box (one per GPU under
+// torchrun compile the same classes): $SCUBA_OOB_JIT_CACHE, else
+// $HOME/.cache/scuba_oob_jit; "0" disables it.  The file name is a hash of the
+// complete NVRTC input (generated source, every embedded header, options), so
+// a stale entry can never be picked up; files are written to a temporary name
+// and renamed (atomic on one file system).
+std::string cache_dir() {
+    static const std::string d = [] {
+        const char* e = std::getenv("SCUBA_OOB_JIT_CACHE");
+        if (e && std::string(e) == "0") return std::string();
+        if (e && *e) return std::string(e);
+        const char* h = std::getenv("HOME");
+        return h && *h ? std::string(h) + "/.cache/scuba_oob_jit" : std::string();
+    }();
+    return d;
+}
+uint64_t fnv(const std::string& x, uint64_t h = 1469598103934665603ull) {
+    for (unsigned char ch : x) {
+        h ^= ch;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+std::string cache_path(const std::string& src, const std::string& opts) {
+    const std::string d = cache_dir();
+    if (d.empty()) return "";
+    uint64_t h = fnv(src);
+    for (const char* hs : {kSrc_types_h, kSrc_format_h, kSrc_wide_cuh, kSrc_engine_cuh, kSrc_frontier_cuh,
+                           kSrc_phases_cuh, kSrc_jit_lane_cuh})
+        h = fnv(hs, h);
+    h = fnv(opts, h);
+    int maj = 0, min = 0;
+    nvrtcVersion(&maj, &min);
+    h = fnv(std::to_string(maj) + "." + std::to_string(min), h);
+    char name[64];
+    std::snprintf(name, sizeof name, "/%016llx.cubin", (unsigned long long)h);
+    return d + name;
+}
+bool read_file(const std::string& path, std::string& out) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) return false;
+    std::fseek(f, 0, SEEK_END);
+    long n = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    out.resize(n > 0 ? (size_t)n : 0);
+    bool ok = n > 0 && std::fread(&out[0], 1, (size_t)n, f) == (size_t)n;
+    std::fclose(f);
+    return ok;
+}
+void write_file(const std::string& path, const std::string& data) {
+    const std::string dir = path.substr(0, path.rfind('/'));
+    std::string cmd_dir = dir;
+    for (size_t i = 1; i <= cmd_dir.size(); i++)  // mkdir -p
+        if (i == cmd_dir.size() || cmd_dir[i] == '/') ::mkdir(cmd_dir.substr(0, i).c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string((unsigned long long)::getpid());
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    bool ok = std::fwrite(data.data(), 1, data.size(), f) == data.size();
+    ok = (std::fclose(f) == 0) && ok;
+    if (ok) std::rename(tmp.c_str(), path.c_str());
+    else std::remove(tmp.c_str());
+}
 
 std::string compile_entry(Entry& e, const JitClass& c) {
     Gen g;
@@ -341,6 +408,13 @@ std::string compile_entry(Entry& e, const JitClass& c) {
     g.nlit = c.nlit;
     std::string src = g.source("oob_jit_solve");
     auto t0 = std::chrono::steady_clock::now();
+    static const char* maxreg_env = std::getenv("SCUBA_OOB_JIT_MAXREG");
+    const std::string cpath = cache_path(src, maxreg_env ? maxreg_env : "");
+    if (!cpath.empty() && read_file(cpath, e.cubin)) {
+        e.from_disk = true;
+        e.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return "";
+    }
     nvrtcProgram prog;
     const char* hdr_src[7] = {kSrc_types_h, kSrc_format_h, kSrc_wide_cuh, kSrc_engine_cuh, kSrc_frontier_cuh,
                               kSrc_phases_cuh, kSrc_jit_lane_cuh};
@@ -367,6 +441,7 @@ std::string compile_entry(Entry& e, const JitClass& c) {
     e.cubin.resize(n);
     nvrtcGetCUBIN(prog, &e.cubin[0]);
     nvrtcDestroyProgram(&prog);
+    if (!cpath.empty()) write_file(cpath, e.cubin);
     e.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return "";
 }
