@@ -206,6 +206,16 @@ def load_peak_hbm():
         return HBM_FALLBACK, "fallback"
 
 
+def ncu_alu(config: str):
+    """Issue / ALU-pipe utilisation of the dominant kernel from the committed
+    ncu --set full summary (profiles/ncu_summary.json), or None."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
+        return d.get(config, {}).get("alu_evidence")
+    except Exception:
+        return None
+
+
 def ncu_traffic(config: str):
     """DRAM bytes of one step (all launches of one plan run) from the
     committed ncu launch-list summary (profiles/ncu_summary.json), or None."""
@@ -346,7 +356,8 @@ def run_ours(args, rank, world, local):
                      "traffic": ncu_traffic(args.config),
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "note": "interval-propagation DFS is integer-ALU/latency bound; "
-                             "bytes = compiled records + results (DESIGN.md)"},
+                             "bytes = compiled records + results per step, all launches (DESIGN.md)",
+                     "alu": ncu_alu(args.config)},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
                 "h2d_bytes_per_step": info["record_bytes"],
