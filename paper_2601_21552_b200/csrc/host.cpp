@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -850,9 +851,32 @@ std::vector<std::unique_ptr<DevicePool>> g_pools;
 // one pool (buffers + stream) per (device, regime): the int64, int128 and
 // 256-bit jobs of a batch run concurrently on their own streams, so their
 // tails overlap on the device
+// Pipelined calls (oob_solve_batch on a large batch) run chunks concurrently
+// on separate pool slots; the host-heavy part of a chunk (compile, pack,
+// upload, launch) is serialised by a gate so that chunk k+1's host work
+// overlaps chunk k's kernels.
+struct HostGate {
+    std::mutex mu;
+    std::condition_variable cv;
+    int turn = 0;  // the chunk whose host phase may run
+};
+thread_local int tl_pool_slot = 0;
+thread_local HostGate* tl_gate = nullptr;
+thread_local int tl_chunk = 0;
+thread_local bool tl_gate_held = false;
+void gate_release() {
+    if (!tl_gate || !tl_gate_held) return;
+    {
+        std::lock_guard<std::mutex> lk(tl_gate->mu);
+        tl_gate->turn = tl_chunk + 1;
+    }
+    tl_gate->cv.notify_all();
+    tl_gate_held = false;
+}
+
 DevicePool* pool_for(int dev, int wide) {
     std::lock_guard<std::mutex> lk(g_pools_mu);
-    size_t slot = (size_t)dev * 3 + (size_t)wide;
+    size_t slot = ((size_t)tl_pool_slot * 64 + (size_t)dev) * 3 + (size_t)wide;
     if (g_pools.size() <= slot) g_pools.resize(slot + 1);
     if (!g_pools[slot]) g_pools[slot].reset(new DevicePool());
     return g_pools[slot].get();
@@ -1691,6 +1715,7 @@ std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
             if (e.empty()) {
                 Phase ph("kernels");
                 e = launch_group(rc, G);
+                gate_release();  // the next chunk's host work overlaps these kernels
                 float ms = 0;
                 if (e.empty()) e = group_ms(G, &ms);
             }
@@ -1722,10 +1747,18 @@ struct DevWork {
 
 std::string run_all(RunCtx& rc, std::vector<DevWork>& work) {
     std::vector<std::string> errs(work.size());
-    std::vector<std::thread> th;
-    for (size_t k = 0; k < work.size(); k++)
-        th.emplace_back([&, k]() { errs[k] = run_group(rc, work[k].dev, work[k].qs); });
-    for (auto& t : th) t.join();
+    if (work.size() == 1) {  // one device: stay on the caller's thread (pipeline slot / gate)
+        errs[0] = run_group(rc, work[0].dev, work[0].qs);
+    } else {
+        const int slot = tl_pool_slot;
+        std::vector<std::thread> th;
+        for (size_t k = 0; k < work.size(); k++)
+            th.emplace_back([&, k, slot]() {
+                tl_pool_slot = slot;
+                errs[k] = run_group(rc, work[k].dev, work[k].qs);
+            });
+        for (auto& t : th) t.join();
+    }
     for (auto& e : errs)
         if (!e.empty()) return e;
     return "";
@@ -1956,8 +1989,56 @@ extern "C" {
 
 int oob_solve_batch(const oob_batch* batch, const oob_options* opt, oob_result* out) {
     if (!out || !out->verdict) return fail(OOB_E_INVALID, "result arrays missing");
-    return drive(batch, opt, MODE_SOLVE, nullptr, out->model, out->verdict, out->nodes, out->passes,
-                 out->elapsed_s);
+    if (!batch) return fail(OOB_E_INVALID, "null batch");
+    // SCUBA_OOB_CHUNK=<queries>: large single-device calls are pipelined: the batch is cut into chunks
+    // (each an oob_batch view; all offsets are per query) decided
+    // concurrently on separate device buffers, with the host-heavy phases
+    // taken in chunk order.  Results are identical (queries are independent).
+    const int64_t n = batch->n_queries;
+    static const int64_t chunk_q = [] {
+        const char* e = std::getenv("SCUBA_OOB_CHUNK");
+        return (int64_t)((e && *e) ? std::atoll(e) : 0);  // off by default: measured slower
+    }();
+    const bool one_dev = (opt && opt->n_gpus == 1) || visible_devices() <= 1;
+    if (chunk_q <= 0 || n < 2 * chunk_q || !one_dev || tl_gate)
+        return drive(batch, opt, MODE_SOLVE, nullptr, out->model, out->verdict, out->nodes, out->passes,
+                     out->elapsed_s);
+    const int k = (int)std::min<int64_t>(4, (n + chunk_q - 1) / chunk_q);
+    HostGate gate;
+    std::vector<int> rcs(k, OOB_OK);
+    std::vector<std::string> msgs(k);
+    std::vector<std::thread> th;
+    for (int c = 0; c < k; c++) {
+        th.emplace_back([&, c]() {
+            const int64_t q0 = n * c / k, q1 = n * (c + 1) / k;
+            oob_batch sub = *batch;
+            sub.n_queries = q1 - q0;
+            sub.var_begin += q0;
+            sub.con_begin += q0;
+            sub.node_begin += q0;
+            sub.lit_begin += q0;
+            tl_pool_slot = c;
+            tl_gate = &gate;
+            tl_chunk = c;
+            {
+                std::unique_lock<std::mutex> lk(gate.mu);
+                gate.cv.wait(lk, [&] { return gate.turn >= c; });
+            }
+            tl_gate_held = true;
+            rcs[c] = drive(&sub, opt, MODE_SOLVE, nullptr, out->model, out->verdict + q0,
+                           out->nodes ? out->nodes + q0 : nullptr, out->passes ? out->passes + q0 : nullptr,
+                           out->elapsed_s ? out->elapsed_s + q0 : nullptr);
+            if (rcs[c] != OOB_OK) msgs[c] = g_last_error;
+            gate_release();  // also on early exits (no launch happened)
+            tl_gate = nullptr;
+            tl_pool_slot = 0;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int c = 0; c < k; c++)
+        if (rcs[c] != OOB_OK) return fail(rcs[c], "chunk " + std::to_string(c) + ": " + msgs[c]);
+    g_last_error.clear();
+    return OOB_OK;
 }
 
 int oob_propagate_batch(const oob_batch* batch, const oob_options* opt, oob_i128* out_lo, oob_i128* out_hi,

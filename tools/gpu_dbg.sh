@@ -1,1 +1,2 @@
-for m in 1 2 4; do SCUBA_OOB_JIT_GRID_MULT=$m timeout 600 python tools/sweep_heavy.py c3 16 | sed "s/^/mult=$m /"; SCUBA_OOB_JIT_GRID_MULT=$m timeout 600 python tools/sweep_heavy.py c4 16 | sed "s/^/mult=$m /"; done > gpurun_out/sweep.log 2>&1
+for ch in 0 16384 25000 34000 50000; do SCUBA_OOB_CHUNK=$ch timeout 300 python tools/e2e_sweep.py c3; done > gpurun_out/e2e.log 2>&1
+for ch in 0 34000; do SCUBA_OOB_CHUNK=$ch timeout 300 python tools/e2e_sweep.py c4; done >> gpurun_out/e2e.log 2>&1
