@@ -55,3 +55,29 @@ def test_jit_plan_runs_match(gpu):
     ref = solve_flat(fb, 30.0, flags=_lib.F_NO_JIT)
     for k in ("verdict", "nodes", "passes"):
         assert np.array_equal(r[k], ref[k]), k
+
+
+def test_chunked_pipeline_matches_single_call(gpu, monkeypatch):
+    """SCUBA_OOB_CHUNK cuts a large call into concurrently decided chunks;
+    results must be identical (queries are independent).  The knob is read
+    once per process, so the chunked run happens in a subprocess."""
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys, json; sys.path.insert(0, %r)\n"
+        "from paper_2601_21552_b200 import synth\n"
+        "from paper_2601_21552_b200.solver import solve_flat\n"
+        "fb = synth.generate('c3', 30000, names=False)\n"
+        "o = solve_flat(fb, 30.0)\n"
+        "print(json.dumps([o['verdict'].tolist(), o['nodes'].tolist(), o['passes'].tolist()]))\n" % str(ROOT))
+    env = dict(__import__("os").environ, SCUBA_OOB_CHUNK="8000")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+    v, nodes, passes = json.loads(out.stdout.strip().splitlines()[-1])
+    from paper_2601_21552_b200 import synth
+    fb = synth.generate("c3", 30000, names=False)
+    ref = solve_flat(fb, 30.0)
+    assert v == ref["verdict"].tolist()
+    assert nodes == ref["nodes"].tolist()
+    assert passes == ref["passes"].tolist()
