@@ -288,6 +288,11 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
         out_nodes = cn;
         out_passes = (int64_t)cp;
     }
+    if (a.stats && lane == 0) {  // [6,7] Sat: expanded / reference passes, [8,9] Unsat
+        const int o = verdict == VERDICT_SAT ? 6 : 8;
+        atomicAdd(a.stats + o, (unsigned long long)tot_passes);
+        atomicAdd(a.stats + o + 1, (unsigned long long)out_passes);
+    }
     if (lane == 0) {
         a.verdict[qi] = (int8_t)verdict;
         a.err[qi] = (int8_t)err;

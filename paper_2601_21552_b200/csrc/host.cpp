@@ -1373,8 +1373,8 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.resume = (uint32_t*)P->resume.p;
     a.stats = nullptr;
     if (trace_level() >= 2 && rc.mode == MODE_SOLVE) {
-        CK(P->stats.ensure(64));
-        CK(cudaMemsetAsync(P->stats.p, 0, 64, s));
+        CK(P->stats.ensure(128));
+        CK(cudaMemsetAsync(P->stats.p, 0, 128, s));
         a.stats = (unsigned long long*)P->stats.p;
     }
     a.timeline = nullptr;
@@ -1628,13 +1628,15 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
         }
     }
     if (j.a.stats) {
-        unsigned long long st[8];
-        CK(cudaMemcpy(st, j.a.stats, 64, cudaMemcpyDeviceToHost));
+        unsigned long long st[16];
+        CK(cudaMemcpy(st, j.a.stats, 128, cudaMemcpyDeviceToHost));
         std::fprintf(stderr,
                      "[oob] job w%d: frontier rounds %llu units %llu lane-passes %llu / slots %llu (%.1f%%); "
                      "lockstep lane-passes %llu / slots %llu (%.1f%%)\n",
                      j.wide, st[2], st[3], st[1], st[0], st[0] ? 100.0 * st[1] / st[0] : 0.0, st[5], st[4],
                      st[4] ? 100.0 * st[5] / st[4] : 0.0);
+        std::fprintf(stderr, "[oob] job w%d: frontier Sat passes expanded %llu / reference %llu; Unsat %llu / %llu\n",
+                     j.wide, st[6], st[7], st[8], st[9]);
     }
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;

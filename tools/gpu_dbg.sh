@@ -1,2 +1,1 @@
-for ch in 0 16384 25000 34000 50000; do SCUBA_OOB_CHUNK=$ch timeout 300 python tools/e2e_sweep.py c3; done > gpurun_out/e2e.log 2>&1
-for ch in 0 34000; do SCUBA_OOB_CHUNK=$ch timeout 300 python tools/e2e_sweep.py c4; done >> gpurun_out/e2e.log 2>&1
+SCUBA_OOB_TRACE=2 SCUBA_OOB_JIT_MIN=100000000 timeout 600 python tools/stats_run.py c3 c4 > gpurun_out/stats.log 2>&1
