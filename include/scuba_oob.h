@@ -130,8 +130,10 @@ enum {
     OOB_F_NO_SORT = 1,   /* keep input order on device (testing the scheduler) */
     OOB_F_NO_DEMOTE = 2, /* decide wide-regime queries entirely in their proven
                             regime (no root-phase demotion; testing) */
-    OOB_F_NO_JIT = 4     /* interpret every structure class (no run-time
+    OOB_F_NO_JIT = 4,    /* interpret every structure class (no run-time
                             compiled class kernels; testing) */
+    OOB_F_NO_X32 = 8     /* keep int64-regime queries in int64 (no x32
+                            demotion after the root phase; testing) */
 };
 
 /* Results (caller-allocated; optional arrays may be NULL). */

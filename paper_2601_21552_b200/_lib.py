@@ -25,6 +25,7 @@ UNSAT, SAT, TIMEOUT, ERROR = 0, 1, 2, 3
 F_NO_SORT = 1
 F_NO_DEMOTE = 2
 F_NO_JIT = 4
+F_NO_X32 = 8
 
 class EngineError(RuntimeError):
     """The GPU engine could not decide a batch (no device, capacity, range)."""

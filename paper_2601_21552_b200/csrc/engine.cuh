@@ -68,9 +68,34 @@ __device__ __forceinline__ __int128 cmod<__int128>(__int128 a, __int128 b) {
     return a % b;
 }
 
+// The x32 regime (int32 values): narrowing targets derived from
+// the reference's +-10**18 clamp are carried as +-2^30 ("beyond range") while
+// every real value is below 2^28 (device proof Lane::fit_x32).  A target
+// computed from an out-of-range one is renormalised to +-2^30, and a division
+// or multiplication of one stays out of range -- exactly how the reference's
+// huge finite values behave against values below 2^28.
+template <typename T>
+struct Ext {
+    static constexpr bool X32 = false;
+    __device__ static inline T sat(T x) { return x; }
+    __device__ static inline bool big_hi(T) { return false; }
+    __device__ static inline bool big_lo(T) { return false; }
+};
+template <>
+struct Ext<int> {
+    static constexpr bool X32 = true;
+    static constexpr int INF = 1 << 30, HALF = 1 << 29;
+    __device__ static inline int sat(int x) { return x >= HALF ? INF : (x <= -HALF ? -INF : x); }
+    __device__ static inline bool big_hi(int x) { return x >= HALF; }
+    __device__ static inline bool big_lo(int x) { return x <= -HALF; }
+};
+
 template <typename T>
 struct Arith {
-    __device__ static inline T inf() { return T(1000000000000000000LL); }  // _INF = 10**18 (solver.py:23)
+    __device__ static inline T inf() {  // _INF = 10**18 (solver.py:23); x32: 2^30 (out of range)
+        if constexpr (Ext<T>::X32) return T(1 << 30);
+        else return T(1000000000000000000LL);
+    }
     __device__ static inline T mn(T a, T b) { return a < b ? a : b; }
     __device__ static inline T mx(T a, T b) { return a > b ? a : b; }
     // Python floor division a // b (C division truncates: that is tdiv, solver.py:94)
@@ -85,6 +110,10 @@ struct Arith {
 
 // model / domain output in the caller's int128 wire format (values are
 // within the declared domains, which the wire format bounds to 128 bits)
+__device__ __forceinline__ void store_i128(int64_t* out, int v) {
+    out[0] = v;
+    out[1] = v < 0 ? -1 : 0;
+}
 __device__ __forceinline__ void store_i128(int64_t* out, long long v) {
     out[0] = v;
     out[1] = v < 0 ? -1 : 0;
@@ -103,9 +132,11 @@ template <typename T>
 __device__ __forceinline__ T from_i128(__int128 v) { return (T)v; }
 template <>
 __device__ __forceinline__ i256 from_i128<i256>(__int128 v) { return i256::from128(v); }
+__device__ __forceinline__ long long low64(int v) { return v; }
 __device__ __forceinline__ long long low64(long long v) { return v; }
 __device__ __forceinline__ long long low64(__int128 v) { return (long long)v; }
 __device__ __forceinline__ long long low64(const i256& v) { return (long long)v.w[0]; }
+__device__ __forceinline__ __int128 low128(int v) { return v; }
 __device__ __forceinline__ __int128 low128(long long v) { return v; }
 __device__ __forceinline__ __int128 low128(__int128 v) { return v; }
 __device__ __forceinline__ __int128 low128(const i256& v) { return v.low128(); }
@@ -306,12 +337,13 @@ struct Lane {
                 err = ERR_STACK;
                 return false;
             }
+            using X = Ext<T>;
             if (op == NODE_ADD) {                                      // :181-185
-                U(st_n, sp) = R; E(st_0, sp) = a - l1; E(st_1, sp) = b - l0; ++sp;
-                U(st_n, sp) = L; E(st_0, sp) = a - r1; E(st_1, sp) = b - r0; ++sp;
+                U(st_n, sp) = R; E(st_0, sp) = X::sat(a - l1); E(st_1, sp) = X::sat(b - l0); ++sp;
+                U(st_n, sp) = L; E(st_0, sp) = X::sat(a - r1); E(st_1, sp) = X::sat(b - r0); ++sp;
             } else if (op == NODE_SUB) {                               // :186-190
-                U(st_n, sp) = R; E(st_0, sp) = l0 - b; E(st_1, sp) = l1 - a; ++sp;
-                U(st_n, sp) = L; E(st_0, sp) = a + r0; E(st_1, sp) = b + r1; ++sp;
+                U(st_n, sp) = R; E(st_0, sp) = X::sat(l0 - b); E(st_1, sp) = X::sat(l1 - a); ++sp;
+                U(st_n, sp) = L; E(st_0, sp) = X::sat(a + r0); E(st_1, sp) = X::sat(b + r1); ++sp;
             } else if (op == NODE_MUL) {                               // :191-216
                 if (l0 < T(0) || r0 < T(0)) continue;
                 if (b < T(0)) return false;
@@ -322,8 +354,8 @@ struct Lane {
                     lo_l = A::ceil_div(t0n, r1);
                     lo_r = A::ceil_div(t0n, l1);
                 }
-                if (r0 > T(0)) hi_l = A::fdiv(b, r0);
-                if (l0 > T(0)) hi_r = A::fdiv(b, l0);
+                if (r0 > T(0)) hi_l = X::big_hi(b) ? A::inf() : A::fdiv(b, r0);
+                if (l0 > T(0)) hi_r = X::big_hi(b) ? A::inf() : A::fdiv(b, l0);
                 U(st_n, sp) = R; E(st_0, sp) = lo_r; E(st_1, sp) = hi_r; ++sp;
                 U(st_n, sp) = L; E(st_0, sp) = lo_l; E(st_1, sp) = hi_l; ++sp;
             } else if (op == NODE_DIV) {                               // :217-223
@@ -331,8 +363,8 @@ struct Lane {
                 if (op_of(rw) == NODE_LIT) {
                     T c = E(lit, arg_of(rw));
                     if (c >= T(1)) {
-                        T lo_req = a > T(0) ? a * c : a * c - (c - T(1));
-                        T hi_req = b >= T(0) ? b * c + (c - T(1)) : b * c;
+                        T lo_req = X::big_lo(a) ? -A::inf() : (a > T(0) ? a * c : a * c - (c - T(1)));
+                        T hi_req = X::big_hi(b) ? A::inf() : (b >= T(0) ? b * c + (c - T(1)) : b * c);
                         U(st_n, sp) = L; E(st_0, sp) = lo_req; E(st_1, sp) = hi_req; ++sp;
                     }
                 }
@@ -737,6 +769,165 @@ struct Lane {
         if (B <= from_i128<T>((__int128)(~((unsigned __int128)0) >> 1)) && D <= from_i128<T>((one << 126) - 1))
             return 1;
         return 2;
+    }
+
+    // ----- x32 eligibility (int64 root kernel) -----------------------------------
+    // At the current domains (they only shrink below), every REAL value the
+    // reference can produce -- domains, literals, forward intervals, exact
+    // values, narrowing targets not derived from the 10**18 clamp -- must stay
+    // below 2^28, and every clamp-derived target must stay beyond them all (its
+    // magnitude, tracked as a lower bound through +, -, * narrowing and literal
+    // division, must exceed 2 B + 2).  Then int32 with out-of-range targets
+    // carried as +-2^30 (Ext<int>) reproduces every comparison, narrowing and
+    // contradiction of the reference.  Double precision: the real bound is
+    // rounded up, the clamp-derived bound down (margins far beyond rounding).
+    __device__ bool fit_x32() {
+        double B = 0.0, minf = 1e300;
+        auto ad = [](T x) { return x < T(0) ? -(double)x : (double)x; };
+        for (uint32_t v = 0; v < nv; ++v) B = fmax(B, fmax(ad(E(env_lo, v)), ad(E(env_hi, v))));
+        for (uint32_t i = 0; i < nlit; ++i) B = fmax(B, ad(E(lit, i)));
+        const double INFD = 1e18;
+        constexpr int SMAX = 40;
+        uint32_t sn[SMAX];
+        double slo[SMAX], shi[SMAX];  // real: signed value; clamp-derived: magnitude (>= 0)
+        bool ilo[SMAX], ihi[SMAX];
+        for (uint32_t k = 0; k < ncon; ++k) {
+            uint32_t w = __ldg(cons + k);
+            uint32_t rel = w & 7u, lr = (w >> 3) & 0x3FFFu, rr = w >> 17;
+            uint32_t start = lr + 1 - size_of(lr);
+            vbase = start;
+            // forward intervals (exact in T) and exact-value magnitudes
+            for (uint32_t j = start; j <= rr; ++j) {
+                uint32_t cw = __ldg(code + j), op = op_of(cw);
+                T lo, hi;
+                if (op == NODE_LIT) {
+                    lo = hi = E(lit, arg_of(cw));
+                } else if (op == NODE_VAR) {
+                    lo = E(env_lo, arg_of(cw));
+                    hi = E(env_hi, arg_of(cw));
+                } else {
+                    uint32_t R = j - 1, L = R - size_of(R);
+                    T l0 = VL(L), l1 = VH(L), r0 = VL(R), r1 = VH(R);
+                    lo = T(1);
+                    hi = T(0);
+                    if (l0 <= l1 && r0 <= r1) {
+                        if (op == NODE_ADD) { lo = l0 + r0; hi = l1 + r1; }
+                        else if (op == NODE_SUB) { lo = l0 - r1; hi = l1 - r0; }
+                        else if (op == NODE_MUL) {
+                            T k0 = l0 * r0, k1 = l0 * r1, k2 = l1 * r0, k3 = l1 * r1;
+                            lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
+                            hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
+                        } else {
+                            T d0 = A::mx(r0, T(1)), d1 = r1;
+                            if (d0 <= d1) {
+                                if (op == NODE_DIV) {
+                                    T k0 = cdiv(l0, d0), k1 = cdiv(l0, d1), k2 = cdiv(l1, d0), k3 = cdiv(l1, d1);
+                                    lo = A::mn(A::mn(k0, k1), A::mn(k2, k3));
+                                    hi = A::mx(A::mx(k0, k1), A::mx(k2, k3));
+                                } else {
+                                    T m = d1 - T(1);
+                                    lo = l0 >= T(0) ? T(0) : A::mx(l0, -m);
+                                    hi = l1 <= T(0) ? T(0) : A::mn(l1, m);
+                                }
+                            }
+                        }
+                    }
+                }
+                VL(j) = lo;
+                VH(j) = hi;
+                if (lo <= hi) B = fmax(B, fmax(ad(lo), ad(hi)));
+            }
+            auto F = [&](uint32_t j) -> double {
+                T lo = VL(j), hi = VH(j);
+                return lo <= hi ? fmax(ad(lo), ad(hi)) : 0.0;
+            };
+            auto defined = [&](uint32_t j) { return VL(j) <= VH(j); };
+            // exact values are bounded by the magnitude recurrence (G)
+            {
+                double g[64];
+                uint32_t n = rr + 1 - start;
+                if (n > 64) return false;
+                for (uint32_t j = start; j <= rr; ++j) {
+                    uint32_t cw = __ldg(code + j), op = op_of(cw);
+                    double x;
+                    if (op == NODE_LIT) x = ad(E(lit, arg_of(cw)));
+                    else if (op == NODE_VAR) x = fmax(ad(E(env_lo, arg_of(cw))), ad(E(env_hi, arg_of(cw))));
+                    else {
+                        uint32_t R = j - 1, L = R - size_of(R);
+                        double gl = g[L - start], gr = g[R - start];
+                        x = op == NODE_ADD || op == NODE_SUB ? gl + gr : op == NODE_MUL ? gl * gr
+                            : op == NODE_DIV ? gl : fmin(gl, gr);
+                    }
+                    g[j - start] = x;
+                    B = fmax(B, x);
+                }
+            }
+            if (!defined(lr) || !defined(rr)) continue;  // this constraint fails before any narrowing
+            const double l0 = (double)VL(lr), l1 = (double)VH(lr), r0 = (double)VL(rr), r1 = (double)VH(rr);
+            int sp = 0;
+            auto push = [&](uint32_t node, double lo, bool il, double hi, bool ih) {
+                sn[sp] = node;
+                slo[sp] = lo;
+                ilo[sp] = il;
+                shi[sp] = hi;
+                ihi[sp] = ih;
+                ++sp;
+            };
+            switch (rel) {  // root targets (solver.py:240-259)
+            case REL_LT: push(lr, INFD, true, r1 - 1, false); push(rr, l0 + 1, false, INFD, true); break;
+            case REL_LE: push(lr, INFD, true, r1, false); push(rr, l0, false, INFD, true); break;
+            case REL_EQ: push(lr, fmax(l0, r0), false, fmin(l1, r1), false);
+                         push(rr, fmax(l0, r0), false, fmin(l1, r1), false); break;
+            case REL_GE: push(lr, r0, false, INFD, true); push(rr, INFD, true, l1, false); break;
+            default:     push(lr, r0 + 1, false, INFD, true); push(rr, INFD, true, l1 - 1, false); break;
+            }
+            while (sp > 0) {
+                --sp;
+                const uint32_t i = sn[sp];
+                const double a = slo[sp], b = shi[sp];
+                const bool ia = ilo[sp], ib = ihi[sp];
+                if (ia) minf = fmin(minf, a); else B = fmax(B, fabs(a));
+                if (ib) minf = fmin(minf, b); else B = fmax(B, fabs(b));
+                uint32_t cw = __ldg(code + i), op = op_of(cw);
+                if (op < NODE_ADD) continue;
+                uint32_t R = i - 1, L = R - size_of(R);
+                if (!defined(L) || !defined(R)) continue;
+                if (sp + 2 > SMAX) return false;
+                const double cl0 = (double)VL(L), cl1 = (double)VH(L), cr0 = (double)VL(R), cr1 = (double)VH(R);
+                const double fL = F(L), fR = F(R);
+                if (op == NODE_ADD) {
+                    push(R, ia ? a - fL : a - cl1, ia, ib ? b - fL : b - cl0, ib);
+                    push(L, ia ? a - fR : a - cr1, ia, ib ? b - fR : b - cr0, ib);
+                } else if (op == NODE_SUB) {
+                    // R: [l0 - b, l1 - a]: a clamp-derived upper b makes the lower one clamp-derived
+                    push(R, ib ? b - fL : cl0 - b, ib, ia ? a - fL : cl1 - a, ia);
+                    push(L, ia ? a - fR : a + cr0, ia, ib ? b - fR : b + cr1, ib);
+                } else if (op == NODE_MUL) {
+                    if (cl0 < 0 || cr0 < 0) continue;
+                    const double t0n = ia ? 0.0 : fmax(a, 0.0);
+                    // lower targets: real ceil divisions, or the clamp (-INF) when t0n <= 0
+                    const bool lo_inf = !(t0n > 0);
+                    const double lol = lo_inf ? INFD : ceil(t0n / fmax(cr1, 1.0)), lor = lo_inf ? INFD : ceil(t0n / fmax(cl1, 1.0));
+                    const bool hil_inf = !(cr0 > 0) || ib, hir_inf = !(cl0 > 0) || ib;
+                    const double hil = !(cr0 > 0) ? INFD : (ib ? b / cr0 - 1.0 : floor(b / cr0));
+                    const double hir = !(cl0 > 0) ? INFD : (ib ? b / cl0 - 1.0 : floor(b / cl0));
+                    push(R, lor, lo_inf, hir, hir_inf);
+                    push(L, lol, lo_inf, hil, hil_inf);
+                } else if (op == NODE_DIV) {
+                    uint32_t rw = __ldg(code + R);
+                    if (op_of(rw) == NODE_LIT) {
+                        const T cc = E(lit, arg_of(rw));
+                        if (cc >= T(1)) {
+                            const double c = (double)cc;
+                            push(L, ia ? a * c : (a > 0 ? a * c : a * c - (c - 1.0)), ia,
+                                 ib ? b * c : (b >= 0 ? b * c + (c - 1.0) : b * c), ib);
+                        }
+                    }
+                }
+            }
+        }
+        const double LIM = 268435456.0;  // 2^28
+        return B < LIM && minf > 2.0 * B + 2.0;
     }
 
     __device__ void undo_to(uint32_t mark) {

@@ -154,7 +154,7 @@ struct LaunchArgs {
     uint32_t* resume;         // per scheduled query (null: all fresh)
     uint64_t* timeline;       // debug (SCUBA_OOB_TIMELINE): per entry start, hand-off, frontier start, end (ns)
     unsigned long long* stats;  // debug (SCUBA_OOB_TRACE=2): frontier / lockstep lane-efficiency counters
-    DemoteTarget dem[2];      // root kernel: [0] int64 job, [1] int128 job (slot null: none)
+    DemoteTarget dem[3];      // root kernel: [0] int64 job, [1] int128 job, [2] x32 job (slot null: none)
 };
 
 enum { MODE_SOLVE = 0, MODE_PROPAGATE = 1, MODE_CHECK = 2 };

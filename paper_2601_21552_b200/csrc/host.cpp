@@ -830,7 +830,7 @@ struct DevicePool {
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
     DevBuf classes, class_next, class_init, warp_class;
     DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
-    DevBuf resume, resume_init, slot64, slot128, timeline, classes_interp, stats;
+    DevBuf resume, resume_init, slot64, slot128, slotx32, timeline, classes_interp, stats;
     std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
     std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
@@ -839,8 +839,8 @@ struct DevicePool {
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
-                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &timeline, &classes_interp,
-                          &stats})
+                          &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &slotx32, &timeline,
+                          &classes_interp, &stats})
             b->release();
     }
 };
@@ -874,9 +874,15 @@ void gate_release() {
     tl_gate_held = false;
 }
 
+// device jobs: 0 int64, 1 int128, 2 256-bit (proven at the declared domains),
+// 3 x32 (only shadows: queries the int64 root phase proves small enough)
+constexpr int NJOBS = 4;
+constexpr int W_X32 = 3;
+inline size_t tbytes_of(int w) { return w == 3 ? 4 : (w == 2 ? 32 : (w == 1 ? 16 : 8)); }
+
 DevicePool* pool_for(int dev, int wide) {
     std::lock_guard<std::mutex> lk(g_pools_mu);
-    size_t slot = ((size_t)tl_pool_slot * 64 + (size_t)dev) * 3 + (size_t)wide;
+    size_t slot = ((size_t)tl_pool_slot * 64 + (size_t)dev) * NJOBS + (size_t)wide;
     if (g_pools.size() <= slot) g_pools.resize(slot + 1);
     if (!g_pools[slot]) g_pools[slot].reset(new DevicePool());
     return g_pools[slot].get();
@@ -967,7 +973,7 @@ struct DevJob {
     std::vector<int64_t> shadows;  // wider-regime queries this job may resume (SOLVE mode)
     std::vector<uint8_t> is_shadow;  // per scheduled entry
     std::vector<uint32_t> resume_init;  // per scheduled entry (format.h resume words)
-    std::vector<uint32_t> slot[2];      // wide jobs: per entry, index of its shadow in job[0] / job[1]
+    std::vector<uint32_t> slot[3];      // per entry, index of its shadow in job[0] / job[1] / job[3] (x32)
     // run-time compiled classes (int64 SOLVE jobs, jit.cpp): one kernel each
     std::vector<uint32_t> jit_cls;      // class ids
     std::vector<const void*> jit_fn;
@@ -1061,14 +1067,15 @@ void pack(const RunCtx& rc, DevJob& j) {
     j.mo.resize(n);
     j.qd.alloc(n);
     // data layout: per entry (2 nv + nlit) values of the job's width, padded
-    // to 16 (int64/int128) or 32 bytes (256-bit)
-    const size_t vw = j.wide == 2 ? 4 : (size_t)j.wide + 1;  // int64 words per value
+    // to 16 bytes (x32/int64/int128) or 32 bytes (256-bit)
+    const size_t tb = tbytes_of(j.wide);
+    const size_t vw = tb >= 8 ? tb / 8 : 1;  // int64 words per value (x32 entries are shadows only)
     const size_t align = j.wide == 2 ? 4 : 2;
     // every entry of a class has the same data size: offsets per class run
     std::vector<uint64_t> doff(n + 1, 0), moff(n + 1, 0);
     for (size_t id = 0; id < nc; id++) {
         const Compiled& c = comp[qid(entries[rep[id]])];
-        const uint64_t words = (2 * (uint64_t)c.nv + c.nlit) * vw;
+        const uint64_t words = ((2 * (uint64_t)c.nv + c.nlit) * tb + 7) / 8;
         const uint64_t dsz = ((words + align - 1) / align) * align;
         for (uint32_t i = j.cls[id].q_begin; i < j.cls[id].q_end; i++) {
             doff[i + 1] = doff[i] + dsz;
@@ -1150,6 +1157,9 @@ void assign_warps(DevJob& j, const std::vector<ClassDesc>& cls, uint32_t n_warps
     for (size_t i = 0; w < n_warps; w++, i = (i + 1) % live.size()) j.warp_class[w] = live[i];
 }
 
+inline bool demote_on(const RunCtx& rc) { return rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_DEMOTE); }
+inline bool x32_on(const RunCtx& rc) { return demote_on(rc) && !(rc.opt.flags & OOB_F_NO_X32); }
+
 // JIT policy: classes with at least jit_min queries (default 1024) in an int64
 // SOLVE job run as run-time compiled kernels (oob_options.jit_min, else
 // SCUBA_OOB_JIT_MIN; OOB_F_NO_JIT disables; if NVRTC is unavailable the
@@ -1203,7 +1213,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, j.dev));
     }
     const uint32_t n = (uint32_t)j.qs.size();
-    const size_t tbytes = j.wide == 2 ? 32 : (j.wide ? 16 : 8);
+    const size_t tbytes = tbytes_of(j.wide);
     j.g = make_geom(j.maxv, j.maxcode, j.maxlit, depth_cap, trail_cap, j.maxcsize, j.maxdepth, tbytes);
     // run-time compiled classes (int64 solve jobs)
     j.jit_cls.clear();
@@ -1212,7 +1222,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     j.jit_args.clear();
     j.jit_queries = 0;
     j.cls_interp = j.cls;
-    if (j.wide == 0 && rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_JIT)) {
+    if (j.wide == (x32_on(rc) ? W_X32 : 0) && rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_JIT)) {
         const std::vector<Compiled>& comp = *rc.comp;
         std::vector<JitClass> want;
         for (uint32_t c = 0; c < j.n_classes; c++) {
@@ -1224,7 +1234,8 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
                 rep.ncode > JIT_MAX_CODE)
                 continue;
             j.jit_cls.push_back(c);
-            want.push_back(JitClass{j.code.data() + cd.code_off, rep.nv, rep.ncon, rep.ncode, rep.nlit});
+            want.push_back(JitClass{j.code.data() + cd.code_off, rep.nv, rep.ncon, rep.ncode, rep.nlit,
+                                    j.wide == W_X32 ? 32 : 64});
         }
         if (!want.empty()) {
             std::vector<int> regs;
@@ -1307,13 +1318,14 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     if (j.fblocks) CK(P->fr_region.ensure((size_t)j.fblocks * WARPS_PER_BLOCK * fr_bytes));
     CK(P->resume.ensure((size_t)n * 4));
     CK(P->resume_init.ensure((size_t)n * 4));
-    for (int t = 0; t < 2; t++)
-        if (!j.slot[t].empty()) CK((t ? P->slot128 : P->slot64).ensure(j.slot[t].size() * 4));
+    auto slot_buf = [&](int t) -> DevBuf& { return t == 0 ? P->slot64 : (t == 1 ? P->slot128 : P->slotx32); };
+    for (int t = 0; t < 3; t++)
+        if (!j.slot[t].empty()) CK(slot_buf(t).ensure(j.slot[t].size() * 4));
     cudaStream_t s = P->stream;
     CK(cudaMemcpyAsync(P->resume_init.p, j.resume_init.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
-    for (int t = 0; t < 2; t++)
+    for (int t = 0; t < 3; t++)
         if (!j.slot[t].empty())
-            CK(cudaMemcpyAsync((t ? P->slot128 : P->slot64).p, j.slot[t].data(), j.slot[t].size() * 4,
+            CK(cudaMemcpyAsync(slot_buf(t).p, j.slot[t].data(), j.slot[t].size() * 4,
                                cudaMemcpyHostToDevice, s));
     CK(P->classes_interp.ensure(j.cls.size() * sizeof(ClassDesc)));
     {
@@ -1420,39 +1432,44 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
 // streams.
 struct DevGroup {
     int dev = 0;
-    DevJob job[3];
-    DevicePool* pool[3] = {nullptr, nullptr, nullptr};
+    DevJob job[NJOBS];
+    DevicePool* pool[NJOBS] = {nullptr, nullptr, nullptr, nullptr};
     bool has(int w) const { return !job[w].qs.empty(); }
 };
 
 // shadows + pack + demotion slots of a group (before staging)
 void pack_group(const RunCtx& rc, DevGroup& G) {
-    for (int w = 0; w < 3; w++) {
+    for (int w = 0; w < NJOBS; w++) {
         G.job[w].dev = G.dev;
         G.job[w].wide = w;
         G.job[w].shadows.clear();
-        G.job[w].slot[0].clear();
-        G.job[w].slot[1].clear();
+        for (auto& sl : G.job[w].slot) sl.clear();
     }
+    G.job[W_X32].qs.clear();  // x32 entries are always shadows
     // the original (own-regime) query lists, before pack() reorders them
     std::vector<int64_t> own[3];
     for (int w = 0; w < 3; w++) own[w] = G.job[w].qs;
-    if (rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_DEMOTE)) {
+    if (demote_on(rc)) {
         for (int w = 1; w < 3; w++)
             for (int t = 0; t < w; t++)
                 G.job[t].shadows.insert(G.job[t].shadows.end(), own[w].begin(), own[w].end());
     }
-    for (int w = 0; w < 3; w++)
+    if (x32_on(rc))
+        for (int w = 0; w < 3; w++)
+            G.job[W_X32].shadows.insert(G.job[W_X32].shadows.end(), own[w].begin(), own[w].end());
+    for (int w = 0; w < NJOBS; w++)
         if (!G.job[w].qs.empty() || !G.job[w].shadows.empty()) pack(rc, G.job[w]);
-    if (rc.mode != MODE_SOLVE || (rc.opt.flags & OOB_F_NO_DEMOTE)) return;
-    for (int t = 0; t < 2; t++) {
-        const DevJob& T = G.job[t];
+    if (!demote_on(rc)) return;
+    // demotion slots: target t (0 int64, 1 int128, 2 x32 = job 3) of the jobs that hand down to it
+    for (int t = 0; t < 3; t++) {
+        const DevJob& T = G.job[t == 2 ? W_X32 : t];
         if (T.shadows.empty()) continue;
         std::unordered_map<int64_t, uint32_t> at;
         at.reserve(T.shadows.size() * 2);
         for (size_t i = 0; i < T.qs.size(); i++)
             if (T.is_shadow[i]) at.emplace(T.qs[i], (uint32_t)i);
-        for (int w = t + 1; w < 3; w++) {
+        for (int w = 0; w < 3; w++) {
+            if (t == 2 ? w != 0 : w <= t) continue;  // x32: from the int64 job; else from the wider jobs
             DevJob& W = G.job[w];
             if (W.qs.empty()) continue;
             W.slot[t].resize(W.qs.size());
@@ -1465,24 +1482,25 @@ void pack_group(const RunCtx& rc, DevGroup& G) {
 inline bool present(const DevJob& j) { return !j.qs.empty(); }
 
 std::string stage_group(const RunCtx& rc, DevGroup& G, uint32_t depth_cap, uint32_t trail_cap, bool heavy) {
-    for (int w = 0; w < 3; w++) {
+    for (int w = 0; w < NJOBS; w++) {
         if (!present(G.job[w])) continue;
         std::string e = stage(rc, G.job[w], G.pool[w], depth_cap, trail_cap, heavy);
         if (!e.empty()) return e;
     }
-    // demotion targets of the wide jobs
-    for (int w = 1; w < 3; w++) {
+    // demotion targets: t = 0 int64 job, 1 int128 job, 2 x32 job (index 3)
+    for (int w = 0; w < 3; w++) {
         if (!present(G.job[w])) continue;
         LaunchArgs& a = G.job[w].a;
-        for (int t = 0; t < 2; t++) {
+        for (int t = 0; t < 3; t++) {
             a.dem[t] = DemoteTarget{};
-            if (t >= w || G.job[w].slot[t].empty()) continue;
-            DevicePool* T = G.pool[t];
+            if (G.job[w].slot[t].empty()) continue;
+            DevicePool* T = G.pool[t == 2 ? W_X32 : t];
+            DevicePool* S = G.pool[w];
             a.dem[t].qdesc = (const QDesc*)T->qdesc.p;
             a.dem[t].data = (int64_t*)T->data.p;
             a.dem[t].resume = (uint32_t*)T->resume.p;
             a.dem[t].t0 = (uint64_t*)T->heavy_t0.p;
-            a.dem[t].slot = (const uint32_t*)(t ? G.pool[w]->slot128.p : G.pool[w]->slot64.p);
+            a.dem[t].slot = (const uint32_t*)(t == 0 ? S->slot64.p : (t == 1 ? S->slot128.p : S->slotx32.p));
         }
     }
     return "";
@@ -1492,13 +1510,13 @@ std::string stage_group(const RunCtx& rc, DevGroup& G, uint32_t depth_cap, uint3
 std::string launch_group(const RunCtx& rc, DevGroup& G) {
     CK(cudaSetDevice(G.dev));
     int first = -1;
-    for (int w = 0; w < 3; w++)
+    for (int w = 0; w < NJOBS; w++)
         if (present(G.job[w])) { first = w; break; }
     if (first < 0) return "";
     cudaStream_t s0 = G.pool[first]->stream;
     // every per-run reset on the first stream, so that the root kernels may
     // write into the other jobs' buffers once it is done
-    for (int w = first; w < 3; w++) {
+    for (int w = first; w < NJOBS; w++) {
         if (!present(G.job[w])) continue;
         DevicePool* P = G.pool[w];
         const DevJob& j = G.job[w];
@@ -1512,25 +1530,27 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         CK(cudaMemcpyAsync(P->resume.p, P->resume_init.p, n * 4, cudaMemcpyDeviceToDevice, s0));
     }
     CK(cudaEventRecord(G.pool[first]->ev0, s0));
-    for (int w = first + 1; w < 3; w++)
+    for (int w = first + 1; w < NJOBS; w++)
         if (present(G.job[w])) {
             CK(cudaStreamWaitEvent(G.pool[w]->stream, G.pool[first]->ev0, 0));
             CK(cudaEventRecord(G.pool[w]->ev0, G.pool[w]->stream));
         }
     if (rc.mode == MODE_SOLVE) {
-        for (int w = 2; w >= 1; w--) {
+        // root phases, widest first: 256-bit -> int128 -> int64 -> x32
+        for (int w = 2; w >= 0; w--) {
             if (!present(G.job[w])) continue;
             DevJob& j = G.job[w];
-            if (!j.slot[0].empty() || !j.slot[1].empty()) {
-                CK(launch_root(j.a, w, (int)j.blocks, G.pool[w]->stream));
-                CK(cudaEventRecord(G.pool[w]->evr, G.pool[w]->stream));
-                for (int t = 0; t < w; t++)
-                    if (present(G.job[t]) && !j.slot[t].empty())
-                        CK(cudaStreamWaitEvent(G.pool[t]->stream, G.pool[w]->evr, 0));
+            if (j.slot[0].empty() && j.slot[1].empty() && j.slot[2].empty()) continue;
+            CK(launch_root(j.a, w, (int)j.blocks, G.pool[w]->stream));
+            CK(cudaEventRecord(G.pool[w]->evr, G.pool[w]->stream));
+            for (int t = 0; t < 3; t++) {
+                const int tj = t == 2 ? W_X32 : t;
+                if (present(G.job[tj]) && !j.slot[t].empty())
+                    CK(cudaStreamWaitEvent(G.pool[tj]->stream, G.pool[w]->evr, 0));
             }
         }
     }
-    for (int w = 2; w >= 0; w--) {
+    for (int w = NJOBS - 1; w >= 0; w--) {
         if (!present(G.job[w])) continue;
         DevJob& j = G.job[w];
         DevicePool* P = G.pool[w];
@@ -1562,10 +1582,12 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         }
         CK(launch_solve(j.a, w, (int)j.blocks, (int)j.fblocks, s));
         for (size_t x = 0; x < std::min(P->xs.size(), j.jit_cls.size()); x++) CK(cudaStreamWaitEvent(s, P->xev[x], 0));
-        if (w == 0 && rc.mode == MODE_SOLVE)  // the wide jobs' frontier tails, once the int64 work is done
+        if (w == 0 && rc.mode == MODE_SOLVE) {  // the wide jobs' frontier tails, once the int64 / x32 work is done
+            if (present(G.job[W_X32])) CK(cudaStreamWaitEvent(s, G.pool[W_X32]->ev1, 0));
             for (int t = 1; t < 3; t++)
                 if (present(G.job[t]) && G.job[t].tail_blocks)
                     CK(launch_solve(G.job[t].tail_args, t, (int)G.job[t].tail_blocks, 0, s));
+        }
         CK(cudaEventRecord(P->ev1, s));
     }
     return "";
@@ -1576,7 +1598,7 @@ std::string group_ms(DevGroup& G, float* ms) {
     CK(cudaSetDevice(G.dev));
     *ms = 0;
     int first = -1;
-    for (int w = 0; w < 3; w++)
+    for (int w = 0; w < NJOBS; w++)
         if (present(G.job[w])) {
             if (first < 0) first = w;
             CK(cudaEventSynchronize(G.pool[w]->ev1));
@@ -1678,7 +1700,7 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
 }
 
 std::string fetch_group(RunCtx& rc, DevGroup& G, std::vector<int64_t> retry[3]) {
-    for (int w = 0; w < 3; w++) {
+    for (int w = 0; w < NJOBS; w++) {
         if (!present(G.job[w])) continue;
         std::string e = fetch(rc, G.job[w], G.pool[w], retry);
         if (!e.empty()) return e;
@@ -1689,14 +1711,14 @@ std::string fetch_group(RunCtx& rc, DevGroup& G, std::vector<int64_t> retry[3]) 
 // full run of one device's queries on the shared pools, with capacity retries
 std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
     uint32_t depth_cap = DEPTH_CAP0, trail_cap = TRAIL_CAP0;
-    DevicePool* pools[3] = {pool_for(dev, 0), pool_for(dev, 1), pool_for(dev, 2)};
+    DevicePool* pools[NJOBS] = {pool_for(dev, 0), pool_for(dev, 1), pool_for(dev, 2), pool_for(dev, 3)};
     std::vector<int64_t> cur[3] = {qs[0], qs[1], qs[2]};
     for (int round = 0; round < 5; round++) {
         if (cur[0].empty() && cur[1].empty() && cur[2].empty()) return "";
         DevGroup G;
         G.dev = dev;
-        for (int w = 0; w < 3; w++) {
-            G.job[w].qs = cur[w];
+        for (int w = 0; w < NJOBS; w++) {
+            G.job[w].qs = w < 3 ? cur[w] : std::vector<int64_t>();
             G.pool[w] = pools[w];
         }
         {
@@ -1705,12 +1727,12 @@ std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
         }
         std::vector<int64_t> retry[3];
         {
-            std::lock_guard<std::mutex> l0(pools[0]->mu), l1(pools[1]->mu), l2(pools[2]->mu);
+            std::lock_guard<std::mutex> l0(pools[0]->mu), l1(pools[1]->mu), l2(pools[2]->mu), l3(pools[3]->mu);
             std::string e;
             {
                 Phase ph("stage");
                 e = stage_group(rc, G, depth_cap, trail_cap, round == 0);
-                for (int w = 0; w < 3 && e.empty(); w++)
+                for (int w = 0; w < NJOBS && e.empty(); w++)
                     if (present(G.job[w]) && cudaStreamSynchronize(G.pool[w]->stream) != cudaSuccess)
                         e = "stage sync failed";
             }
@@ -2196,8 +2218,8 @@ int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** o
     for (size_t k = 0; k < p->pr.work.size(); k++) {
         DevGroup& G = p->groups[k];
         G.dev = p->pr.work[k].dev;
-        for (int w = 0; w < 3; w++) {
-            G.job[w].qs = p->pr.work[k].qs[w];
+        for (int w = 0; w < NJOBS; w++) {
+            if (w < 3) G.job[w].qs = p->pr.work[k].qs[w];
             p->pools.emplace_back(new DevicePool());
             G.pool[w] = p->pools.back().get();
         }
@@ -2206,7 +2228,7 @@ int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** o
         if (!e.empty()) return fail(OOB_E_CUDA, e);
     }
     for (auto& G : p->groups)
-        for (int w = 0; w < 3; w++)
+        for (int w = 0; w < NJOBS; w++)
             if (present(G.job[w])) {
                 cudaSetDevice(G.dev);
                 if (cudaStreamSynchronize(G.pool[w]->stream) != cudaSuccess)
@@ -2267,7 +2289,7 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
     if (!p || !info) return fail(OOB_E_INVALID, "null argument");
     int64_t nq = 0, rec = 0, res = 0, cls = 0, wide = 0, jobs = 0, launches = 0;
     for (auto& G : p->groups)
-        for (int w = 0; w < 3; w++) {
+        for (int w = 0; w < NJOBS; w++) {
             const DevJob& j = G.job[w];
             if (!present(j)) continue;
             int64_t own = 0;
@@ -2276,10 +2298,10 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
             rec += (int64_t)j.record_bytes();
             res += (int64_t)j.qs.size() * (1 + 1 + 8 + 8 + 4) + (int64_t)j.out_model_words * 8;
             cls += j.n_classes;
-            if (w) wide += own;
+            if (w == 1 || w == 2) wide += own;
             jobs++;
             launches += 1 + (int64_t)j.jit_cls.size() + (j.tail_blocks ? 1 : 0) +
-                        ((w && (!j.slot[0].empty() || !j.slot[1].empty())) ? 1 : 0);
+                        ((!j.slot[0].empty() || !j.slot[1].empty() || !j.slot[2].empty()) ? 1 : 0);
         }
     info[0] = nq;
     info[1] = rec;
@@ -2295,7 +2317,7 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
 void oob_plan_destroy(oob_plan* p) {
     if (!p) return;
     for (auto& G : p->groups)
-        for (int w = 0; w < 3; w++) {
+        for (int w = 0; w < NJOBS; w++) {
             cudaSetDevice(G.dev);
             DevicePool* P = G.pool[w];
             P->release_all();

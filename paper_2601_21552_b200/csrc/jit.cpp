@@ -60,6 +60,7 @@ struct Gen {
     const uint32_t* code;
     const uint32_t* member;
     uint32_t nv, ncon, ncode, nlit;
+    int bits = 64;
     std::ostringstream o;
 
     uint32_t size_of(uint32_t i) const { return w_op(code[i]) >= NODE_ADD ? w_arg(code[i]) : 1u; }
@@ -149,15 +150,17 @@ struct Gen {
         std::string l0 = V(L, "lo"), l1 = V(L, "hi"), r0 = V(R, "lo"), r1 = V(R, "hi");
         switch (op) {
         case NODE_ADD:
-            o << ind << "{ const T " << p << "la = " << ta << " - " << r1 << ", " << p << "lb = " << tb << " - " << r0
-              << ", " << p << "ra = " << ta << " - " << l1 << ", " << p << "rb = " << tb << " - " << l0 << ";\n";
+            o << ind << "{ const T " << p << "la = X::sat(" << ta << " - " << r1 << "), " << p << "lb = X::sat(" << tb
+              << " - " << r0 << "), " << p << "ra = X::sat(" << ta << " - " << l1 << "), " << p << "rb = X::sat(" << tb
+              << " - " << l0 << ");\n";
             narrow(L, p + "la", p + "lb", seen, ind + "  ");
             narrow(R, p + "ra", p + "rb", seen, ind + "  ");
             o << ind << "}\n";
             break;
         case NODE_SUB:
-            o << ind << "{ const T " << p << "la = " << ta << " + " << r0 << ", " << p << "lb = " << tb << " + " << r1
-              << ", " << p << "ra = " << l0 << " - " << tb << ", " << p << "rb = " << l1 << " - " << ta << ";\n";
+            o << ind << "{ const T " << p << "la = X::sat(" << ta << " + " << r0 << "), " << p << "lb = X::sat(" << tb
+              << " + " << r1 << "), " << p << "ra = X::sat(" << l0 << " - " << tb << "), " << p << "rb = X::sat(" << l1
+              << " - " << ta << ");\n";
             narrow(L, p + "la", p + "lb", seen, ind + "  ");
             narrow(R, p + "ra", p + "rb", seen, ind + "  ");
             o << ind << "}\n";
@@ -171,8 +174,10 @@ struct Gen {
             o << ind << "  if (" << p << "t0 > T(0)) { if (" << r1 << " == T(0) || " << l1
               << " == T(0)) return false; " << p << "la = A::ceil_div(" << p << "t0, " << r1 << "); " << p
               << "ra = A::ceil_div(" << p << "t0, " << l1 << "); }\n";
-            o << ind << "  if (" << r0 << " > T(0)) " << p << "lb = A::fdiv(" << tb << ", " << r0 << ");\n";
-            o << ind << "  if (" << l0 << " > T(0)) " << p << "rb = A::fdiv(" << tb << ", " << l0 << ");\n";
+            o << ind << "  if (" << r0 << " > T(0)) " << p << "lb = X::big_hi(" << tb << ") ? A::inf() : A::fdiv(" << tb
+              << ", " << r0 << ");\n";
+            o << ind << "  if (" << l0 << " > T(0)) " << p << "rb = X::big_hi(" << tb << ") ? A::inf() : A::fdiv(" << tb
+              << ", " << l0 << ");\n";
             narrow(L, p + "la", p + "lb", seen, ind + "  ");
             narrow(R, p + "ra", p + "rb", seen, ind + "  ");
             o << ind << "}\n";
@@ -182,10 +187,10 @@ struct Gen {
                 std::string c = "s.lit[" + std::to_string(w_arg(code[R])) + "]";
                 o << ind << "if (" << c << " >= T(1)) {\n";
                 o << ind << "  const T " << p << "c = " << c << ";\n";
-                o << ind << "  const T " << p << "la = " << ta << " > T(0) ? " << ta << " * " << p << "c : " << ta
-                  << " * " << p << "c - (" << p << "c - T(1));\n";
-                o << ind << "  const T " << p << "lb = " << tb << " >= T(0) ? " << tb << " * " << p << "c + (" << p
-                  << "c - T(1)) : " << tb << " * " << p << "c;\n";
+                o << ind << "  const T " << p << "la = X::big_lo(" << ta << ") ? -A::inf() : (" << ta << " > T(0) ? " << ta
+                  << " * " << p << "c : " << ta << " * " << p << "c - (" << p << "c - T(1)));\n";
+                o << ind << "  const T " << p << "lb = X::big_hi(" << tb << ") ? A::inf() : (" << tb << " >= T(0) ? " << tb
+                  << " * " << p << "c + (" << p << "c - T(1)) : " << tb << " * " << p << "c);\n";
                 narrow(L, p + "la", p + "lb", seen, ind + "  ");
                 o << ind << "}\n";
             }
@@ -291,7 +296,7 @@ struct Gen {
 
     std::string source(const std::string& kname) {
         o << "#include \"jit_lane.cuh\"\nnamespace oob {\nstruct Cls {\n";
-        o << "  typedef long long T;\n  typedef Arith<T> A;\n";
+        o << "  typedef " << (bits == 32 ? "int" : "long long") << " T;\n  typedef Arith<T> A;\n  typedef Ext<T> X;\n";
         o << "  static constexpr uint32_t NV = " << nv << ", NCON = " << ncon << ", NCODE = " << ncode
           << ", NLIT = " << nlit << ";\n";
         for (int half = 0; half < 2; half++) {
@@ -406,6 +411,7 @@ std::string compile_entry(Entry& e, const JitClass& c) {
     g.ncon = c.ncon;
     g.ncode = c.ncode;
     g.nlit = c.nlit;
+    g.bits = c.bits;
     std::string src = g.source("oob_jit_solve");
     auto t0 = std::chrono::steady_clock::now();
     static const char* maxreg_env = std::getenv("SCUBA_OOB_JIT_MAXREG");
@@ -450,7 +456,7 @@ std::string compile_entry(Entry& e, const JitClass& c) {
 
 std::string jit_key(const JitClass& c) {
     std::string k((const char*)c.words, (size_t)(c.ncon + c.ncode + 4 * c.nv) * 4);
-    uint32_t dims[4] = {c.nv, c.ncon, c.ncode, c.nlit};
+    uint32_t dims[5] = {c.nv, c.ncon, c.ncode, c.nlit, (uint32_t)c.bits};
     k.append((const char*)dims, sizeof dims);
     return k;
 }
@@ -532,6 +538,7 @@ std::string jit_source(const JitClass& c) {
     g.ncon = c.ncon;
     g.ncode = c.ncode;
     g.nlit = c.nlit;
+    g.bits = c.bits;
     return g.source("oob_jit_solve");
 }
 

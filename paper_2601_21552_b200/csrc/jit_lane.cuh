@@ -24,7 +24,7 @@ namespace oob {
 
 template <class C>
 struct JitLane {
-    using T = long long;
+    using T = typename C::T;  // long long (int64 regime) or int (x32 regime)
     using A = Arith<T>;
     static constexpr uint32_t NV = C::NV;
     static constexpr uint32_t NL = C::NLIT > 0 ? C::NLIT : 1;

@@ -60,7 +60,14 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
     L.bind(a, warp, lane);
     // domains + literal slots of the lane's query into a data block of width w
     auto store_state = [&](int64_t* dst, int w) {
-        if (w == 0) {
+        if (w == 2) {  // x32: packed int32 values
+            int32_t* d32 = reinterpret_cast<int32_t*>(dst);
+            for (uint32_t v = 0; v < L.nv; ++v) {
+                d32[2 * v] = (int32_t)low64(L.E(L.env_lo, v));
+                d32[2 * v + 1] = (int32_t)low64(L.E(L.env_hi, v));
+            }
+            for (uint32_t i = 0; i < L.nlit; ++i) d32[2 * L.nv + i] = (int32_t)low64(L.E(L.lit, i));
+        } else if (w == 0) {
             for (uint32_t v = 0; v < L.nv; ++v) {
                 dst[2 * v] = low64(L.E(L.env_lo, v));
                 dst[2 * v + 1] = low64(L.E(L.env_hi, v));
@@ -84,7 +91,10 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
         // width until it fits int64 (a 256-bit query typically fits int128
         // after one pass and int64 only after the asserts have propagated)
         const uint32_t rs = a.resume[qi];
-        if (rs == RES_SKIP || (rs != 0u && (SELF == 2 || (rs & RES_FIX)))) continue;
+        if (rs == RES_SKIP || (rs != 0u && SELF == 2)) continue;
+        // a shadow at its fixpoint: the wider phase already proved it cannot
+        // narrow further except int64 -> x32, which only this job checks
+        if (rs != 0u && (rs & RES_FIX) && SELF != 0) continue;
         const bool from_shadow = rs != 0u;
         const QDesc d = a.qdesc[qi];
         ClassDesc cd;
@@ -96,9 +106,12 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
         const uint64_t t0 = from_shadow ? a.heavy_t0[qi] : global_ns();
         const uint64_t deadline = a.timeout_ns ? t0 + a.timeout_ns : 0;
         uint32_t passes = from_shadow ? (rs & RES_PASSES) : 0u;
-        bool dead = false, fix = false, expired = false;
+        bool dead = false, fix = from_shadow && (rs & RES_FIX), expired = false;
         int target = -1;
-        while (passes < ROOT_MAX_PASSES) {
+        if constexpr (SELF == 0) {
+            if (fix && a.dem[2].slot && L.fit_x32()) target = 2;
+        }
+        while (!fix && passes < ROOT_MAX_PASSES) {
             if (deadline && global_ns() > deadline) {
                 expired = true;
                 break;
@@ -114,10 +127,17 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
             if (dead) break;
             fix = !L.changed;
             if (fix || (passes & (passes - 1)) == 0) {
-                int r = L.fit_regime();
-                if (r < SELF && a.dem[r].slot) {
-                    target = r;
-                    break;
+                if constexpr (SELF == 0) {  // int64 -> x32
+                    if (a.dem[2].slot && L.fit_x32()) {
+                        target = 2;
+                        break;
+                    }
+                } else {
+                    int r = L.fit_regime();
+                    if (r < SELF && a.dem[r].slot) {
+                        target = r;
+                        break;
+                    }
                 }
             }
             if (fix) break;
@@ -141,7 +161,7 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
         }
         if (target < 0) {
             if (from_shadow) {  // continue from here in this job (the shadow block is ours to rewrite)
-                store_state(const_cast<int64_t*>(a.data) + d.data_off, SELF);
+                store_state(const_cast<int64_t*>(a.data) + d.data_off, SELF == 0 ? 0 : 1);
                 __threadfence();
                 a.resume[qi] = RES_ROOT | (fix ? RES_FIX : 0u) | passes;
             }
@@ -221,10 +241,14 @@ static cudaError_t occupancy_impl(int mode, size_t smem, int* blocks_per_sm) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, THREADS, smem);
 }
 
-// root phase of a wide job (wide = 1 or 2)
+// root phase of job `wide` (0 int64 -> x32, 1 int128, 2 256-bit)
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s) {
     size_t smem = (size_t)a.g.smem_per_warp * (THREADS / 32);
-    if (wide == 2) {
+    if (wide == 0) {
+        cudaFuncSetAttribute((const void*)oob_root_kernel<long long, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        oob_root_kernel<long long, 0><<<blocks, THREADS, smem, s>>>(a);
+    } else if (wide == 2) {
         cudaFuncSetAttribute((const void*)oob_root_kernel<i256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         oob_root_kernel<i256, 2><<<blocks, THREADS, smem, s>>>(a);
@@ -236,14 +260,16 @@ cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t 
     return cudaGetLastError();
 }
 
-// wide: 0 = int64, 1 = __int128, 2 = 256-bit regime
+// wide: 0 = int64, 1 = __int128, 2 = 256-bit, 3 = x32 regime
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s) {
+    if (wide == 3) return launch_impl<int>(a, blocks, fblocks, s);
     if (wide == 2) return launch_impl<i256>(a, blocks, fblocks, s);
     return wide ? launch_impl<__int128>(a, blocks, fblocks, s) : launch_impl<long long>(a, blocks, fblocks, s);
 }
 
 // resident blocks per SM of the kernel for `mode` with `smem` dynamic bytes per block
 cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm) {
+    if (wide == 3) return occupancy_impl<int>(mode, smem, blocks_per_sm);
     if (wide == 2) return occupancy_impl<i256>(mode, smem, blocks_per_sm);
     return wide ? occupancy_impl<__int128>(mode, smem, blocks_per_sm)
                 : occupancy_impl<long long>(mode, smem, blocks_per_sm);

@@ -30,7 +30,7 @@ def _by_timeout(recs):
 # 1 = every query goes through the warp-cooperative frontier kernel;
 # flags: 0 = wide-regime queries demote after their root phase, F_NO_DEMOTE =
 # they stay in their proven regime throughout
-@pytest.mark.parametrize("flags", [0, _lib.F_NO_DEMOTE])
+@pytest.mark.parametrize("flags", [0, _lib.F_NO_DEMOTE, _lib.F_NO_X32])
 @pytest.mark.parametrize("heavy", [0, -1, 1])
 @pytest.mark.parametrize("name", GOLDEN_SETS)
 def test_golden_exact(gpu, name, heavy, flags):
@@ -93,6 +93,7 @@ def test_frontier_matches_sequential_on_synthetic_streams(gpu, cfg):
     b = solve_flat(fb, 30.0, heavy_nodes=1)
     c = solve_flat(fb, 30.0)
     d = solve_flat(fb, 30.0, flags=_lib.F_NO_DEMOTE)
-    for o in (b, c, d):
+    e = solve_flat(fb, 30.0, flags=_lib.F_NO_X32)
+    for o in (b, c, d, e):
         for k in ("verdict", "nodes", "passes", "model"):
             assert np.array_equal(a[k], o[k]), k
