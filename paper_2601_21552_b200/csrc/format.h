@@ -104,7 +104,8 @@ constexpr uint32_t RES_SKIP = 0xFFFFFFFFu;
 constexpr uint32_t RES_ROOT = 0x80000000u;
 constexpr uint32_t RES_FIX = 0x40000000u;
 constexpr uint32_t RES_PASSES = 0x3FFFFFFFu;
-constexpr uint32_t ROOT_MAX_PASSES = 64;  // root-kernel pass budget before giving up on demotion
+constexpr uint32_t ROOT_MAX_PASSES = 64;      // wide root phases: pass budget before giving up on demotion
+constexpr uint32_t ROOT_MAX_PASSES_X32 = 16;  // int64 root phase (x32 probe)
 
 struct DemoteTarget {
     const QDesc* qdesc;     // target job's descriptors (data_off of the shadow)

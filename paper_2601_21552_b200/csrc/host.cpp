@@ -1102,10 +1102,7 @@ void pack(const RunCtx& rc, DevJob& j) {
             j.mo[i] = moff[i];
             int64_t* out = j.data.data() + doff[i];
             int64_t* end = j.data.data() + doff[i + 1];
-            if (e < 0) {  // a shadow: written on the device by the root kernel
-                std::fill(out, end, 0);
-                continue;
-            }
+            if (e < 0) continue;  // a shadow: written on the device before it is ever read
             auto put = [&](i128 x) {
                 *out++ = (int64_t)(uint64_t)x;
                 if (vw >= 2) *out++ = (int64_t)(x >> 64);
@@ -1222,7 +1219,9 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     j.jit_args.clear();
     j.jit_queries = 0;
     j.cls_interp = j.cls;
-    if (j.wide == (x32_on(rc) ? W_X32 : 0) && rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_JIT)) {
+    // compiled classes: the x32 job and the int64 job (queries the root phase
+    // could not move to x32 -- long root propagations -- stay there)
+    if ((j.wide == 0 || j.wide == W_X32) && rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_JIT)) {
         const std::vector<Compiled>& comp = *rc.comp;
         std::vector<JitClass> want;
         for (uint32_t c = 0; c < j.n_classes; c++) {
@@ -1464,16 +1463,16 @@ void pack_group(const RunCtx& rc, DevGroup& G) {
     for (int t = 0; t < 3; t++) {
         const DevJob& T = G.job[t == 2 ? W_X32 : t];
         if (T.shadows.empty()) continue;
-        std::unordered_map<int64_t, uint32_t> at;
-        at.reserve(T.shadows.size() * 2);
+        static thread_local std::vector<uint32_t> at;  // query id -> shadow index in T
+        if (at.size() < (size_t)rc.b->n_queries) at.resize((size_t)rc.b->n_queries);
         for (size_t i = 0; i < T.qs.size(); i++)
-            if (T.is_shadow[i]) at.emplace(T.qs[i], (uint32_t)i);
+            if (T.is_shadow[i]) at[T.qs[i]] = (uint32_t)i;
         for (int w = 0; w < 3; w++) {
             if (t == 2 ? w != 0 : w <= t) continue;  // x32: from the int64 job; else from the wider jobs
             DevJob& W = G.job[w];
             if (W.qs.empty()) continue;
             W.slot[t].resize(W.qs.size());
-            for (size_t i = 0; i < W.qs.size(); i++) W.slot[t][i] = at.at(W.qs[i]);
+            for (size_t i = 0; i < W.qs.size(); i++) W.slot[t][i] = at[W.qs[i]];
         }
     }
 }

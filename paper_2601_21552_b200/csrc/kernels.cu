@@ -111,7 +111,10 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
         if constexpr (SELF == 0) {
             if (fix && a.dem[2].slot && L.fit_x32()) target = 2;
         }
-        while (!fix && passes < ROOT_MAX_PASSES) {
+        // the int64 root phase only probes for x32 (long root propagations
+        // continue in the int64 job); the wide ones run until they fit int64
+        const uint32_t max_passes = SELF == 0 ? ROOT_MAX_PASSES_X32 : ROOT_MAX_PASSES;
+        while (!fix && passes < max_passes) {
             if (deadline && global_ns() > deadline) {
                 expired = true;
                 break;

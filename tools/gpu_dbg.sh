@@ -1,1 +1,3 @@
-SCUBA_OOB_TRACE=2 SCUBA_OOB_JIT_MIN=100000000 timeout 600 python tools/stats_run.py c3 c4 > gpurun_out/stats.log 2>&1
+timeout 300 python tools/sweep_heavy.py c3 16 > gpurun_out/sweep.log 2>&1
+timeout 300 python tools/jit_runs.py c4 0 | tail -2 >> gpurun_out/sweep.log 2>&1
+timeout 300 python tools/e2e_sweep.py c3 >> gpurun_out/sweep.log 2>&1
