@@ -107,3 +107,49 @@ def analyze_batched(analyzer_module, analyze, *args, stats=None, **kwargs):
     if stats is not None:
         stats["queries"] = len(rec.calls)
     return result
+
+
+def analyze_many(analyzer_module, analyze, jobs, stats=None):
+    """a whole set of analyses (e.g. the 20-program
+    corpus) with ALL their solver queries decided in ONE device batch.
+
+    `jobs` is a list of (args, kwargs) for `analyze`.  Pass 1 runs every
+    analysis with a recording stub, one batch decides the union of the
+    recorded queries, pass 2 re-runs each analysis replaying its own slice of
+    verdicts in call order.  Returns the list of results, in job order."""
+    types = _types(analyzer_module)
+    saved = analyzer_module.solve
+    recs = []
+    try:
+        for args, kwargs in jobs:
+            rec = _Recorder(types[1])
+            analyzer_module.solve = rec
+            analyze(*args, **kwargs)
+            recs.append(rec)
+    finally:
+        analyzer_module.solve = saved
+    calls = [c for rec in recs for c in rec.calls]
+    verdicts = decide_calls(calls, types)
+    results = []
+    base = 0
+    for (args, kwargs), rec in zip(jobs, recs):
+        mine = verdicts[base:base + len(rec.calls)]
+        it = iter(range(len(mine)))
+
+        def replay(variables, constraints, timeout_s=30.0, rec=rec, mine=mine, it=it):
+            i = next(it)
+            want = rec.calls[i]
+            if query_to_json(variables, constraints) != query_to_json(want[0], want[1]):
+                raise RuntimeError("analysis is not deterministic between passes")
+            return mine[i]
+
+        analyzer_module.solve = replay
+        try:
+            results.append(analyze(*args, **kwargs))
+        finally:
+            analyzer_module.solve = saved
+        base += len(rec.calls)
+    if stats is not None:
+        stats["queries"] = len(calls)
+        stats["batches"] = len({c[2] for c in calls})
+    return results

@@ -68,3 +68,24 @@ def test_installed_solve_replaces_reference_binding(ref):
     with installed(ref):
         res = analyze_source(src, "sosfilt_intra.mcu")
     assert render_json_lines(res.diagnostics) == want["figs/sosfilt_intra.mcu"]["m1048576"]["json"]
+
+
+def test_whole_corpus_in_one_batch(ref):
+    """analyze_many: every corpus program's queries in one device batch, the
+    diagnostics of each program still the reference's byte for byte."""
+    from pathlib import Path
+
+    from scuba_mini.analyzer import AnalyzerConfig, analyze_source
+    from scuba_mini.report import render_json_lines
+
+    from paper_2601_21552_b200.analyzer import analyze_many
+
+    want = json.loads((GOLDEN / "corpus_diags.json").read_text())
+    progs = sorted(Path("/root/reference/pkg/corpus").glob("*/*.mcu"))
+    jobs = [((p.read_text(), p.name, AnalyzerConfig()), {}) for p in progs]
+    stats = {}
+    results = analyze_many(ref, analyze_source, jobs, stats=stats)
+    assert stats["queries"] == 110 and stats["batches"] == 1
+    for p, res in zip(progs, results):
+        rel = f"{p.parent.name}/{p.name}"
+        assert render_json_lines(res.diagnostics) == want[rel]["m1048576"]["json"], rel
