@@ -18,6 +18,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -363,24 +364,86 @@ unsigned host_threads() {
     return n;
 }
 
+// Persistent host worker pool (thread creation per parallel loop cost ~0.5 ms
+// a call, and a solve runs about ten such loops).  One loop at a time; a
+// caller that finds the pool busy -- or a loop nested inside a worker -- runs
+// its loop inline.
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool* p = new HostPool(host_threads() - 1);  // never destroyed (detached workers)
+        return *p;
+    }
+    // runs body(lo, hi) over [0, n) in chunks of `grain`; false if busy
+    bool run(size_t n, size_t grain, const std::function<void(size_t, size_t)>& body) {
+        if (workers_.empty() || tl_in_pool) return false;
+        std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
+        if (!busy.owns_lock()) return false;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            body_ = &body;
+            n_ = n;
+            grain_ = grain;
+            next_.store(0);
+            active_ = (int)workers_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();  // the caller takes chunks too
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return active_ == 0; });
+        body_ = nullptr;
+        return true;
+    }
+
+  private:
+    explicit HostPool(unsigned n) {
+        for (unsigned i = 0; i < n; i++) {
+            workers_.emplace_back([this] { loop(); });
+            workers_.back().detach();
+        }
+    }
+    void work() {
+        for (;;) {
+            size_t a = next_.fetch_add(grain_);
+            if (a >= n_) break;
+            (*body_)(a, std::min(n_, a + grain_));
+        }
+    }
+    void loop() {
+        tl_in_pool = true;
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            work();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--active_ == 0) done_cv_.notify_all();
+        }
+    }
+    static thread_local bool tl_in_pool;
+    std::vector<std::thread> workers_;
+    std::mutex mu_, run_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(size_t, size_t)>* body_ = nullptr;
+    size_t n_ = 0, grain_ = 1;
+    std::atomic<size_t> next_{0};
+    int active_ = 0;
+    uint64_t gen_ = 0;
+};
+thread_local bool HostPool::tl_in_pool = false;
+
 template <typename F>
 void parallel_for(size_t n, size_t grain, F f) {
-    unsigned nt = host_threads();
-    if (n < 2 * grain || nt == 1) {
+    if (n < 2 * grain || host_threads() == 1) {
         f(0, n);
         return;
     }
-    std::atomic<size_t> next{0};
-    std::vector<std::thread> th;
-    for (unsigned t = 0; t < nt; t++)
-        th.emplace_back([&]() {
-            for (;;) {
-                size_t a = next.fetch_add(grain);
-                if (a >= n) break;
-                f(a, std::min(n, a + grain));
-            }
-        });
-    for (auto& t : th) t.join();
+    const std::function<void(size_t, size_t)> body = f;
+    if (!HostPool::get().run(n, grain, body)) f(0, n);
 }
 
 struct Emitter {
@@ -892,6 +955,7 @@ struct RunCtx {
     const oob_batch* b;
     oob_options opt;
     std::vector<Compiled>* comp;
+    const std::vector<uint32_t>* qcls;  // structure class per query (compact copy of comp[q].cls)
     int mode;
     // outputs (caller arrays, or internal for propagate/check)
     int8_t* verdict;
@@ -1018,8 +1082,9 @@ void pack(const RunCtx& rc, DevJob& j) {
     std::vector<uint32_t> cls(entries.size());
     std::vector<size_t> rep;
     uint32_t last_g = UINT32_MAX, last_l = 0;  // entries arrive in class runs
+    const std::vector<uint32_t>& qcls = *rc.qcls;  // 4 bytes per query: cache-resident, unlike comp[]
     for (size_t i = 0; i < entries.size(); i++) {
-        const uint32_t g = comp[qid(entries[i])].cls;
+        const uint32_t g = qcls[qid(entries[i])];
         if (g != last_g) {
             auto it = local.emplace(g, (uint32_t)rep.size());
             if (it.second) rep.push_back(i);
@@ -1456,8 +1521,13 @@ void pack_group(const RunCtx& rc, DevGroup& G) {
     if (x32_on(rc))
         for (int w = 0; w < 3; w++)
             G.job[W_X32].shadows.insert(G.job[W_X32].shadows.end(), own[w].begin(), own[w].end());
+    static const char* pk_names[NJOBS] = {"pack.int64", "pack.int128", "pack.i256", "pack.x32"};
     for (int w = 0; w < NJOBS; w++)
-        if (!G.job[w].qs.empty() || !G.job[w].shadows.empty()) pack(rc, G.job[w]);
+        if (!G.job[w].qs.empty() || !G.job[w].shadows.empty()) {
+            Phase ph(pk_names[w]);
+            pack(rc, G.job[w]);
+        }
+    Phase ph_slots("pack.slots");
     if (!demote_on(rc)) return;
     // demotion slots: target t (0 int64, 1 int128, 2 x32 = job 3) of the jobs that hand down to it
     for (int t = 0; t < 3; t++) {
@@ -1855,6 +1925,7 @@ void assign_classes(std::vector<Compiled>& comp, const std::vector<int64_t> reg[
 // Compile + schedule: fills immediate verdicts and returns the device jobs.
 struct Prepared {
     std::vector<Compiled> comp;
+    std::vector<uint32_t> qcls;  // comp[q].cls, compact
     std::vector<int8_t> errs;
     std::vector<DevWork> work;  // per device: queries by proven regime
     std::string range_msg;
@@ -1892,20 +1963,9 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     comp.assign(n, Compiled{});
     {
         Phase ph("compile");
-        unsigned nt = host_threads();
-        if (n < 2048) nt = 1;
-        std::vector<std::thread> th;
-        std::atomic<int64_t> next{0};
-        for (unsigned t = 0; t < nt; t++)
-            th.emplace_back([&]() {
-                for (;;) {
-                    int64_t q0 = next.fetch_add(256);
-                    if (q0 >= n) break;
-                    for (int64_t q = q0; q < std::min(n, q0 + 256); q++)
-                        comp[q] = compile_query(b, q, mode, opt.timeout_s, model_in);
-                }
-            });
-        for (auto& t : th) t.join();
+        parallel_for((size_t)n, 256, [&](size_t lo, size_t hi) {
+            for (size_t q = lo; q < hi; q++) comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in);
+        });
     }
     pr.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     pr.errs.assign(n, 0);
@@ -1935,6 +1995,9 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     want = std::max(1, std::min(want, ndev - first));
     Phase ph_sched("schedule");
     assign_classes(comp, reg);
+    pr.qcls.assign(n, 0);
+    for (int w = 0; w < 3; w++)
+        for (int64_t q : reg[w]) pr.qcls[q] = comp[q].cls;
     if (n_dev_q > 0) {
         pr.work.resize(want);
         for (int d = 0; d < want; d++) pr.work[d].dev = first + d;
@@ -1986,6 +2049,7 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
     rc.b = b;
     rc.opt = pr.opt;
     rc.comp = &pr.comp;
+    rc.qcls = &pr.qcls;
     rc.mode = mode;
     rc.verdict = verdict;
     rc.model = mode == MODE_CHECK ? const_cast<oob_i128*>(model_in) : model_out;
@@ -2147,6 +2211,7 @@ int oob_host_bench(const oob_batch* b, const oob_options* opt, double* ms) {
     rc.b = b;
     rc.opt = pr.opt;
     rc.comp = &pr.comp;
+    rc.qcls = &pr.qcls;
     rc.mode = MODE_SOLVE;
     rc.errs = &pr.errs;
     for (auto& wk : pr.work) {
@@ -2206,6 +2271,7 @@ int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** o
     rc.b = batch;
     rc.opt = p->pr.opt;
     rc.comp = &p->pr.comp;
+    rc.qcls = &p->pr.qcls;
     rc.mode = MODE_SOLVE;
     rc.verdict = p->verdict.data();
     rc.model = p->model.data();
