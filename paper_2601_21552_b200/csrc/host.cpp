@@ -1376,7 +1376,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->class_next.ensure(j.cls.size() * 4));
     CK(P->class_init.ensure(j.cls.size() * 4));
     CK(P->warp_class.ensure((size_t)n_warps * 4));
-    CK(P->heavy_count.ensure(8 * (1 + j.jit_cls.size())));
+    CK(P->heavy_count.ensure(16 * (1 + j.jit_cls.size())));
     CK(P->heavy_list.ensure((size_t)n * 8));  // [0, n): per compiled class at its q range; [n, 2n): interpreter
     CK(P->heavy_t0.ensure((size_t)n * 8));
     if (j.fblocks) CK(P->fr_region.ensure((size_t)j.fblocks * WARPS_PER_BLOCK * fr_bytes));
@@ -1475,7 +1475,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         b.n_classes = 1;
         b.class_next = (uint32_t*)P->class_next.p + c;
         b.warp_class = nullptr;
-        b.heavy_count = (uint32_t*)P->heavy_count.p + 2 * (1 + i);
+        b.heavy_count = (uint32_t*)P->heavy_count.p + 4 * (1 + i);
         b.heavy_list = (uint32_t*)P->heavy_list.p + j.cls[c].q_begin;
         b.slab_T = (unsigned char*)P->slabT.p + warp_base * j.g.slab_T_words * tbytes;
         b.slab_u32 = (uint32_t*)P->slabU.p + warp_base * j.g.slab_u32_words;
@@ -1592,7 +1592,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         const size_t n = j.qs.size();
         CK(cudaMemsetAsync(P->next.p, 0, 4, s0));
         CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s0));
-        CK(cudaMemsetAsync(P->heavy_count.p, 0, 8 * (1 + j.jit_cls.size()), s0));
+        CK(cudaMemsetAsync(P->heavy_count.p, 0, 16 * (1 + j.jit_cls.size()), s0));
         if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 8, s0));
         if (j.a.timeline) CK(cudaMemsetAsync(j.a.timeline, 0, n * 32, s0));
         CK(cudaMemsetAsync(P->verdict.p, 0xFF, n, s0));
@@ -1619,7 +1619,12 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
             }
         }
     }
-    for (int w = NJOBS - 1; w >= 0; w--) {
+    // launch order = block dispatch priority: the int64 job first (its few
+    // remaining queries are the long root propagations), then x32 (the bulk),
+    // then the wide jobs
+    static const int order[NJOBS] = {0, W_X32, 1, 2};
+    for (int oi = 0; oi < NJOBS; oi++) {
+        const int w = order[oi];
         if (!present(G.job[w])) continue;
         DevJob& j = G.job[w];
         DevicePool* P = G.pool[w];
@@ -1651,13 +1656,17 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         }
         CK(launch_solve(j.a, w, (int)j.blocks, (int)j.fblocks, s));
         for (size_t x = 0; x < std::min(P->xs.size(), j.jit_cls.size()); x++) CK(cudaStreamWaitEvent(s, P->xev[x], 0));
-        if (w == 0 && rc.mode == MODE_SOLVE) {  // the wide jobs' frontier tails, once the int64 / x32 work is done
+        if (w != 0) CK(cudaEventRecord(P->ev1, s));
+    }
+    if (present(G.job[0])) {  // the wide jobs' frontier tails once the int64 and x32 work is done
+        cudaStream_t s = G.pool[0]->stream;
+        if (rc.mode == MODE_SOLVE) {
             if (present(G.job[W_X32])) CK(cudaStreamWaitEvent(s, G.pool[W_X32]->ev1, 0));
             for (int t = 1; t < 3; t++)
                 if (present(G.job[t]) && G.job[t].tail_blocks)
                     CK(launch_solve(G.job[t].tail_args, t, (int)G.job[t].tail_blocks, 0, s));
         }
-        CK(cudaEventRecord(P->ev1, s));
+        CK(cudaEventRecord(G.pool[0]->ev1, s));
     }
     return "";
 }

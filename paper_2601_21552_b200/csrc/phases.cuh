@@ -19,6 +19,7 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << lane) - 1u;
 
+    if (lane == 0) atomicAdd(a.heavy_count + 2, 1u);  // a producer of this launch's heavy list
     uint32_t c = a.warp_class ? a.warp_class[warp] : 0u;  // the warp's current class queue (warp-uniform)
     if (c == NO_CLASS) return;
     ClassDesc cd = a.classes[c];
@@ -200,16 +201,25 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
 
 // Phase 2 of the solve kernel: heavy queries, one warp per query, lanes
 // expand the leftmost pending nodes (frontier.cuh).  A warp whose lockstep
-// phase is over serves the heavy list until it finds nothing left to claim,
-// then exits (it never spins: an idle resident warp would keep the SMs from
-// the other regimes' kernels).  An entry appended later comes from a warp
-// still in its lockstep phase, which serves the list itself afterwards, so
-// every entry is taken.
+// phase is over serves the heavy list; when the list is empty it waits while
+// warps of the same launch are still in their lockstep phase (they may hand
+// off more: a warp of creeping chains hands off 32 at once, and a lone
+// producer would then serve them one after another) -- only warps that have
+// STARTED count, so no warp ever waits on a block that is not resident -- and
+// exits once every started producer is done (or after WAIT_NS).  An entry
+// appended after that comes from a warp still in its lockstep phase, which
+// serves the list itself afterwards, so every entry is taken.
 template <typename LaneT>
 __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, uint32_t warp, uint32_t lane) {
     const unsigned FULL = 0xffffffffu;
-    volatile uint32_t* ctl = a.heavy_count;  // [0] listed [1] claimed
+    volatile uint32_t* ctl = a.heavy_count;  // [0] listed [1] claimed [2] lockstep started [3] lockstep done
+    if (!a.frontier_only && lane == 0) {
+        __threadfence();
+        atomicAdd(a.heavy_count + 3, 1u);
+    }
     if (!a.heavy_nodes) return;
+    constexpr uint64_t WAIT_NS = 20000000ull;  // bound on waiting for producers (20 ms)
+    uint64_t idle_since = 0;
     FrontierRegion<typename LaneT::T> R;  // one scratch region per warp of the grid
     R.bind((unsigned char*)a.fr_region + (size_t)warp * a.fr_region_bytes, a.g.maxv, a.fr_ecap, a.fr_ucap,
            a.fr_logcap);
@@ -217,12 +227,22 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
         int idx = -1;
         if (lane == 0) {
             for (;;) {
+                const uint32_t done = ctl[3], started = ctl[2];
+                __threadfence();
                 const uint32_t listed = ctl[0], claimed = ctl[1];
-                if (claimed >= listed) break;
-                if (atomicCAS(a.heavy_count + 1, claimed, claimed + 1) == claimed) {
-                    idx = (int)claimed;
-                    break;
+                if (claimed < listed) {
+                    if (atomicCAS(a.heavy_count + 1, claimed, claimed + 1) == claimed) {
+                        idx = (int)claimed;
+                        idle_since = 0;
+                        break;
+                    }
+                    continue;
                 }
+                if (done >= started) break;  // no producer of this launch left
+                const uint64_t now = global_ns();
+                if (!idle_since) idle_since = now;
+                else if (now - idle_since > WAIT_NS) break;
+                __nanosleep(4000);
             }
         }
         idx = __shfl_sync(FULL, idx, 0);
