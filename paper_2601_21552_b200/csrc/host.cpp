@@ -1056,6 +1056,7 @@ struct DevJob {
     uint64_t model_words = 0;
     uint32_t n_classes = 0;
     uint32_t blocks = 1, fblocks = 0;
+    uint32_t root_blocks = 1;  // root kernel: one thread per query (grid-stride)
     uint32_t tail_blocks = 0;    // wide SOLVE jobs: frontier-only launch after the int64 kernel
     LaunchArgs tail_args{};
     SlabGeom g{};
@@ -1358,6 +1359,11 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     j.tail_blocks = (j.wide && heavy_nodes) ? (uint32_t)(P->sms * per_sm) : 0u;
     n_warps += j.tail_blocks * WARPS_PER_BLOCK;
     j.fblocks = heavy_nodes ? (n_warps + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK : 0;  // one frontier region per warp
+    // the root kernel walks every query of the job (JIT classes included), one
+    // thread each: its grid follows n, not the interpreting kernel's share,
+    // bounded by the per-warp slabs allocated below
+    j.root_blocks = std::max<uint32_t>(
+        1u, std::min<uint64_t>((n + 32 * WARPS_PER_BLOCK - 1) / (32 * WARPS_PER_BLOCK), n_warps / WARPS_PER_BLOCK));
     const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
@@ -1417,6 +1423,13 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.class_next = (uint32_t*)P->class_next.p;
     a.warp_class = (const uint32_t*)P->warp_class.p;
     a.heavy_nodes = heavy_nodes;
+    {
+        static const uint32_t wus = [] {
+            const char* e = std::getenv("SCUBA_OOB_FRONTIER_WAIT_US");
+            return (uint32_t)((e && *e) ? std::atoi(e) : 20000);
+        }();
+        a.frontier_wait_us = wus;
+    }
     {
         static const uint32_t hp = [] {
             const char* e = std::getenv("SCUBA_OOB_HEAVY_PASSES");
@@ -1610,7 +1623,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
             if (!present(G.job[w])) continue;
             DevJob& j = G.job[w];
             if (j.slot[0].empty() && j.slot[1].empty() && j.slot[2].empty()) continue;
-            CK(launch_root(j.a, w, (int)j.blocks, G.pool[w]->stream));
+            CK(launch_root(j.a, w, (int)j.root_blocks, G.pool[w]->stream));
             CK(cudaEventRecord(G.pool[w]->evr, G.pool[w]->stream));
             for (int t = 0; t < 3; t++) {
                 const int tj = t == 2 ? W_X32 : t;
@@ -1622,7 +1635,12 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
     // launch order = block dispatch priority: the int64 job first (its few
     // remaining queries are the long root propagations), then x32 (the bulk),
     // then the wide jobs
-    static const int order[NJOBS] = {0, W_X32, 1, 2};
+    static const bool x32_first = [] {
+        const char* e = std::getenv("SCUBA_OOB_X32_FIRST");
+        return e && *e == '1';
+    }();
+    static const int order_a[NJOBS] = {0, W_X32, 1, 2}, order_b[NJOBS] = {W_X32, 0, 1, 2};
+    const int* order = x32_first ? order_b : order_a;
     for (int oi = 0; oi < NJOBS; oi++) {
         const int w = order[oi];
         if (!present(G.job[w])) continue;

@@ -206,7 +206,7 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
 // off more: a warp of creeping chains hands off 32 at once, and a lone
 // producer would then serve them one after another) -- only warps that have
 // STARTED count, so no warp ever waits on a block that is not resident -- and
-// exits once every started producer is done (or after WAIT_NS).  An entry
+// exits once every started producer is done (or after frontier_wait_us).  An entry
 // appended after that comes from a warp still in its lockstep phase, which
 // serves the list itself afterwards, so every entry is taken.
 template <typename LaneT>
@@ -218,7 +218,7 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
         atomicAdd(a.heavy_count + 3, 1u);
     }
     if (!a.heavy_nodes) return;
-    constexpr uint64_t WAIT_NS = 20000000ull;  // bound on waiting for producers (20 ms)
+    const uint64_t WAIT_NS = 1000ull * a.frontier_wait_us;  // bound on waiting for producers
     uint64_t idle_since = 0;
     FrontierRegion<typename LaneT::T> R;  // one scratch region per warp of the grid
     R.bind((unsigned char*)a.fr_region + (size_t)warp * a.fr_region_bytes, a.g.maxv, a.fr_ecap, a.fr_ucap,
@@ -238,7 +238,7 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
                     }
                     continue;
                 }
-                if (done >= started) break;  // no producer of this launch left
+                if (done >= started || !WAIT_NS) break;  // no producer of this launch left
                 const uint64_t now = global_ns();
                 if (!idle_since) idle_since = now;
                 else if (now - idle_since > WAIT_NS) break;
