@@ -330,7 +330,24 @@ def run_ours(args, rank, world, local):
         cpu, cres, n = cpu_baseline(fb, args.cpu_seconds, threads)
         mism = int((cres["verdict"][:n] != res["verdict"][:n]).sum())
         mism += int((cres["nodes"][:n] != res["nodes"][:n]).sum())
-        cpu["parity_sample"] = {"queries": n, "verdict_or_node_mismatches": mism}
+        mism += int((cres["passes"][:n] != res["passes"][:n]).sum())
+        vend = int(fb.var_begin[n])
+        model_mism = int((cres["model"][:vend] != out["model"][:vend]).any(axis=1).sum())
+        cpu["parity_sample"] = {"queries": n, "verdict_node_or_pass_mismatches": mism,
+                                "model_word_mismatches": model_mism}
+
+    # ---- witness replay: every Sat model of the step through the reference's
+    # evaluator (check_model over constraints + divisor side constraints,
+    # solver.py:319/:345, restated in oracle/) -------------------------------------
+    replay = None
+    if rank == 0:
+        from oracle import oracle
+        ok = oracle.check_model_flat(fb, out["model"])
+        sat = out["verdict"] == 1
+        replay = {"sat_witnesses": int(sat.sum()),
+                  "replayed_true": int((ok[sat] == 1).sum()),
+                  "evaluator": "check_model(constraints + divisor_side_constraints) restated "
+                               "in oracle/oob_oracle.cpp"}
 
     dist.close()
     if rank != 0:
@@ -365,6 +382,7 @@ def run_ours(args, rank, world, local):
         "clocks": clocks.summary(),
         "gpu_launches": info["launches_per_run"] * args.steps,
         "corpus": corpus,
+        "witness_replay": replay,
         "kernel_ms_per_step": [round(x, 3) for x in kernel_ms],
     }
     print(json.dumps(line), flush=True)
