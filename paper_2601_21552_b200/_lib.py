@@ -99,6 +99,10 @@ def lib():
     L.oob_host_bench.restype = ctypes.c_int
     L.oob_query_regime.argtypes = [vp, vp, vp]
     L.oob_query_regime.restype = ctypes.c_int
+    L.oob_sweep_run.argtypes = [vp, ctypes.c_int64, ctypes.c_int32, vp, vp]
+    L.oob_sweep_run.restype = ctypes.c_int
+    L.oob_sweep_replay.argtypes = [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp, vp, vp]
+    L.oob_sweep_replay.restype = ctypes.c_int
     L.oob_last_error.restype = ctypes.c_char_p
     L.oob_device_count.restype = ctypes.c_int
     L.oob_version.restype = ctypes.c_char_p

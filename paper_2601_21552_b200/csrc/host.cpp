@@ -55,6 +55,9 @@ static int fail(int code, const std::string& msg) {
     return code;
 }
 
+// error reporting for the other translation units of the library (sweep.cu)
+int oob_internal_fail(int code, const std::string& msg) { return fail(code, msg); }
+
 // SCUBA_OOB_TRACE=1: per-phase host timings on stderr (compile, pack, stage,
 // kernels, fetch) -- the engine's only tracing hook
 static int trace_level() {
