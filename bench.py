@@ -325,7 +325,7 @@ def run_ours(args, rank, world, local):
 
     # ---- CPU baseline + parity on its sample ---------------------------------------
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = host_threads()
         cpu, cres, n = cpu_baseline(fb, args.cpu_seconds, threads)
         mism = int((cres["verdict"][:n] != res["verdict"][:n]).sum())
@@ -391,6 +391,11 @@ def run_ours(args, rank, world, local):
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if world > 1 and "SCUBA_OOB_HOST_THREADS" not in os.environ:
+        # one process per GPU on one node: split the host cores between the
+        # ranks' host pipelines instead of oversubscribing them
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        os.environ["SCUBA_OOB_HOST_THREADS"] = str(max(1, host_threads() // max(local_world, 1)))
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:
