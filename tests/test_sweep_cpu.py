@@ -87,7 +87,7 @@ def test_replay_matches_reference_replay_witness(host, name):
             assert (hit, tr.halted, tr.halt_reason) == (want["hit"], want["halted"], want["halt_reason"]), (i, want)
 
 
-@pytest.mark.parametrize("name", sorted(k for k in PROGS if k.startswith("corpus/")))
+@pytest.mark.parametrize("name", sorted(k for k in PROGS if k.startswith(("corpus/", "synth/"))))
 def test_criterion_8_on_the_sweep_interpreter(host, name):
     """acceptance criterion 8 (test_acceptance.py:243-278): the analyzer's
     per-access flags at max_domain 64 equal the exhaustive sweep at bound 64,
@@ -98,9 +98,11 @@ def test_criterion_8_on_the_sweep_interpreter(host, name):
     for acc in EXPECT[name]["analyzer"]["64"]:
         site = (acc["line"], acc["col"])
         assert acc["flagged"] == bool(sweep.violations.get(site, set()) & oob), site
-        for w in acc["witnesses"]:
+        for w, ref_hit in zip(acc["witnesses"], acc["witness_replays"]):
             hit, _ = S.replay_witness(sp, {int(s): v for s, v in w.items()}, 64, *site, backend=host)
-            assert hit, (site, w)
+            assert hit == ref_hit, (site, w)
+            if name.startswith("corpus/"):
+                assert hit, (site, w)  # criterion 8: every corpus witness replays
 
 
 def test_stop_when_violated_and_verdict(host):

@@ -17,9 +17,9 @@ records, for each program:
     sweep cannot reach).
 
 Programs: the 20 corpus files, the reference's own test_oracle.py sources
-(imported from the reference test module), and seeded variants of the corpus
-with their assert caps changed (sources generated here, regenerated on every
-run).
+(imported from the reference test module), seeded variants of the corpus with
+their assert caps changed, and 70 seeded synthetic programs
+(tools/synth_programs.py) -- sources generated here, regenerated on every run.
 
 Usage:  python tools/golden_sweep.py      -> tests/golden/sweep_programs.json,
                                              tests/golden/sweep_expect.json
@@ -62,6 +62,10 @@ def _sources() -> dict:
                 k = int(m.group(2))
                 return f"{m.group(1)}{max(1, k + rng.choice((-3, -1, 1, 2, 5)))})"
             out[f"variant/{name[7:]}#{v}"] = re.sub(r"(assert\([^)]*<=?\s*)(\d+)\)", cap, src)
+    # seeded synthetic programs (tools/synth_programs.py, corpus-shaped templates)
+    sys.path.insert(0, str(REPO / "tools"))
+    from synth_programs import generate
+    out.update(generate(70, 2601215526))
     return out
 
 
@@ -111,7 +115,7 @@ def main():
             rec["replays"].append({"inputs": {str(s): v for s, v in vals.items()}, "default": default,
                                    "line": line, "col": col, "hit": bool(hit),
                                    "halted": bool(tr.halted), "halt_reason": tr.halt_reason})
-        if name.startswith("corpus/"):
+        if name.startswith(("corpus/", "synth/")):
             rec["analyzer"] = {}
             for m in (64, 1024):
                 res = analyze_source(src, name.split("/")[-1], AnalyzerConfig(max_domain=m))
@@ -121,8 +125,13 @@ def main():
                     wits = [{str(s): v for s, v in o.witness_inputs.items()}
                             for o in acr.outcomes
                             if isinstance(o.verdict, Sat) and o.witness_inputs is not None]
+                    # the reference's own replay of each witness (default = the bound,
+                    # as criterion 8 does): a witness that leaves a data-dependent
+                    # input site unpinned may halt on the default
+                    reps = [bool(replay_witness(prog, {int(s): v for s, v in w.items()}, m,
+                                                loc.line, loc.column)[0]) for w in wits]
                     acc.append({"line": loc.line, "col": loc.column, "flagged": bool(acr.flagged),
-                                "witnesses": wits})
+                                "witnesses": wits, "witness_replays": reps})
                 rec["analyzer"][str(m)] = acc
         expect[name] = rec
         print(name, k, [(s["bound"], s["executions"], s["ref_s"]) for s in rec["sweeps"]], flush=True)
