@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -113,12 +115,37 @@ __global__ void __launch_bounds__(BLOCK) oob_sweep_kernel(sweep::Prog P, Dev D, 
             return oob_internal_fail(OOB_E_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
     } while (0)
 
-struct DevBuf {
+// device buffers pooled per device across calls (a sweep is often tiny: the
+// allocation of a fresh arena would dominate it); grown on demand
+struct PoolBuf {
     void* p = nullptr;
-    ~DevBuf() {
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        if (bytes <= cap) return cudaSuccess;
         if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
     }
 };
+
+struct SweepPool {
+    std::mutex mu;
+    PoolBuf code, lits, kern, kpar, counters, slab, sfirst, tup, tst, taux, tlab, arena;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+SweepPool& pool_of(int dev) {
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<SweepPool>> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)pools.size() <= dev) pools.resize(dev + 1);
+    if (!pools[dev]) pools[dev].reset(new SweepPool());
+    return *pools[dev];
+}
 
 int validate(const oob_sweep_program* pr, int32_t arity) {
     if (!pr || !pr->code || pr->n_code <= 0) return oob_internal_fail(OOB_E_INVALID, "sweep: empty program");
@@ -143,6 +170,57 @@ int validate(const oob_sweep_program* pr, int32_t arity) {
             (c[0] == sweep::LAUNCH && (c[1] < 0 || c[1] >= pr->n_kernels)))
             return oob_internal_fail(OOB_E_INVALID, "sweep: bad operand at " + std::to_string(i));
     }
+    // stack discipline: every reachable pc has one value-stack depth, never
+    // negative nor above the device stack (the interpreter does not re-check)
+    std::vector<int> depth(pr->n_code, -1);
+    std::vector<int> work;
+    auto reach = [&](int pc, int d) -> bool {
+        if (pc < 0 || pc >= pr->n_code || d < 0 || d > sweep::MAX_STACK) return false;
+        if (depth[pc] == -1) {
+            depth[pc] = d;
+            work.push_back(pc);
+            return true;
+        }
+        return depth[pc] == d;
+    };
+    bool ok = reach(0, 0);
+    for (int k = 0; k < pr->n_kernels && ok; k++) ok = reach(pr->kernels[4 * k], 0);
+    while (ok && !work.empty()) {
+        const int pc = work.back();
+        work.pop_back();
+        const int32_t* c = pr->code + 4 * pc;
+        const int d = depth[pc];
+        int nd = d, need = 0;
+        switch (c[0]) {
+        case sweep::LIT: case sweep::LD: case sweep::INP: case sweep::BLT: case sweep::PARG: nd = d + 1; break;
+        case sweep::BIN: case sweep::CMP: need = 2; nd = d - 1; break;
+        case sweep::RD: need = c[3]; nd = d - c[3] + 1; break;
+        case sweep::ST: case sweep::JZ: case sweep::ASRT: case sweep::MALLOC: case sweep::PART: need = 1; nd = d - 1; break;
+        case sweep::WR: need = c[3] + 1; nd = d - need; break;
+        case sweep::ATOM: need = 2; nd = d - 2; break;
+        case sweep::ADECL: need = c[3] & 3; nd = d - need; break;
+        case sweep::NNEG: need = c[1]; break;
+        case sweep::LAUNCH:
+            need = 7 + c[2];
+            nd = d - need;
+            if (c[2] < 0 || c[2] > pr->kernels[4 * c[1] + 1]) ok = false;
+            break;
+        default: break;
+        }
+        if (d < need || (c[0] == sweep::RD && c[3] != 1 && c[3] != 2) ||
+            (c[0] == sweep::WR && c[3] != 1 && c[3] != 2)) {
+            ok = false;
+            break;
+        }
+        if (c[0] == sweep::RET || c[0] == sweep::KEND || c[0] == sweep::END) continue;
+        if (c[0] == sweep::JMP) {
+            ok = reach(c[1], nd);
+            continue;
+        }
+        if (c[0] == sweep::JZ) ok = reach(c[1], nd);
+        if (ok) ok = reach(pc + 1, nd);
+    }
+    if (!ok) return oob_internal_fail(OOB_E_INVALID, "sweep: malformed program (value stack discipline)");
     return OOB_OK;
 }
 
@@ -156,28 +234,32 @@ int drive(const oob_sweep_program* pr, Dev D, int64_t n_out_tuples, const int64_
     SCK(cudaGetDeviceProperties(&prop, dev));
     const int ns = std::max(pr->n_sites, 1);
 
-    DevBuf code, lits, kern, kpar, counters, slab, sfirst, tup, tst, taux, tlab;
-    SCK(cudaMalloc(&code.p, sizeof(int32_t) * 4 * pr->n_code));
+    SweepPool& pool = pool_of(dev);
+    std::lock_guard<std::mutex> lk(pool.mu);
+    PoolBuf &code = pool.code, &lits = pool.lits, &kern = pool.kern, &kpar = pool.kpar, &counters = pool.counters,
+            &slab = pool.slab, &sfirst = pool.sfirst, &tup = pool.tup, &tst = pool.tst, &taux = pool.taux,
+            &tlab = pool.tlab;
+    SCK(code.ensure(sizeof(int32_t) * 4 * pr->n_code));
     SCK(cudaMemcpy(code.p, pr->code, sizeof(int32_t) * 4 * pr->n_code, cudaMemcpyHostToDevice));
-    SCK(cudaMalloc(&lits.p, sizeof(int64_t) * std::max(pr->n_lits, 1)));
+    SCK(lits.ensure(sizeof(int64_t) * std::max(pr->n_lits, 1)));
     if (pr->n_lits)
         SCK(cudaMemcpy(lits.p, pr->lits, sizeof(int64_t) * pr->n_lits, cudaMemcpyHostToDevice));
-    SCK(cudaMalloc(&kern.p, sizeof(int32_t) * 4 * std::max(pr->n_kernels, 1)));
+    SCK(kern.ensure(sizeof(int32_t) * 4 * std::max(pr->n_kernels, 1)));
     if (pr->n_kernels)
         SCK(cudaMemcpy(kern.p, pr->kernels, sizeof(int32_t) * 4 * pr->n_kernels, cudaMemcpyHostToDevice));
-    SCK(cudaMalloc(&kpar.p, sizeof(int32_t) * 2 * std::max(pr->n_kparams, 1)));
+    SCK(kpar.ensure(sizeof(int32_t) * 2 * std::max(pr->n_kparams, 1)));
     if (pr->n_kparams)
         SCK(cudaMemcpy(kpar.p, pr->kparams, sizeof(int32_t) * 2 * pr->n_kparams, cudaMemcpyHostToDevice));
-    SCK(cudaMalloc(&counters.p, sizeof(unsigned long long) * 8));
-    SCK(cudaMalloc(&slab.p, sizeof(uint32_t) * ns));
-    SCK(cudaMalloc(&sfirst.p, sizeof(unsigned long long) * 4 * ns));
+    SCK(counters.ensure(sizeof(unsigned long long) * 8));
+    SCK(slab.ensure(sizeof(uint32_t) * ns));
+    SCK(sfirst.ensure(sizeof(unsigned long long) * 4 * ns));
     if (D.mode == 1) {
-        SCK(cudaMalloc(&tup.p, sizeof(int64_t) * std::max<int64_t>(n_out_tuples * D.arity, 1)));
+        SCK(tup.ensure(sizeof(int64_t) * std::max<int64_t>(n_out_tuples * D.arity, 1)));
         if (n_out_tuples * D.arity)
             SCK(cudaMemcpy(tup.p, tuples, sizeof(int64_t) * n_out_tuples * D.arity, cudaMemcpyHostToDevice));
-        SCK(cudaMalloc(&tst.p, sizeof(int32_t) * std::max<int64_t>(n_out_tuples, 1)));
-        SCK(cudaMalloc(&taux.p, sizeof(int32_t) * std::max<int64_t>(n_out_tuples, 1)));
-        SCK(cudaMalloc(&tlab.p, std::max<int64_t>(n_out_tuples * ns, 1)));
+        SCK(tst.ensure(sizeof(int32_t) * std::max<int64_t>(n_out_tuples, 1)));
+        SCK(taux.ensure(sizeof(int32_t) * std::max<int64_t>(n_out_tuples, 1)));
+        SCK(tlab.ensure(std::max<int64_t>(n_out_tuples * ns, 1)));
     }
     sweep::Prog P{(const int32_t*)code.p, (const int64_t*)lits.p, (const int32_t*)kern.p,
                   (const int32_t*)kpar.p, pr->n_code, pr->n_sites, pr->n_slots, pr->n_kernels,
@@ -200,15 +282,17 @@ int drive(const oob_sweep_program* pr, Dev D, int64_t n_out_tuples, const int64_
     int64_t words = (opt && opt->arena_words > 0) ? opt->arena_words : 512;
     const int64_t budget = (int64_t)8 << 30;  // arena bytes
     const int64_t max_words = (int64_t)1 << 26;
-    cudaEvent_t e0, e1;
-    SCK(cudaEventCreate(&e0));
-    SCK(cudaEventCreate(&e1));
+    if (!pool.e0) {
+        SCK(cudaEventCreate(&pool.e0));
+        SCK(cudaEventCreate(&pool.e1));
+    }
+    cudaEvent_t e0 = pool.e0, e1 = pool.e1;
     float ms = 0.f;
     unsigned long long host_c[8];
     for (;;) {
         while (blocks > 1 && blocks * BLOCK * words * 8 > budget) blocks = (blocks + 1) / 2;
-        DevBuf arena;
-        SCK(cudaMalloc(&arena.p, (size_t)blocks * BLOCK * words * 8));
+        PoolBuf& arena = pool.arena;
+        SCK(arena.ensure((size_t)blocks * BLOCK * words * 8));
         unsigned long long init_c[8] = {0, 0, ~0ull, ~0ull, 0, 0, 0, 0};
         SCK(cudaMemcpy(counters.p, init_c, sizeof(init_c), cudaMemcpyHostToDevice));
         SCK(cudaMemset(slab.p, 0, sizeof(uint32_t) * ns));
@@ -274,8 +358,6 @@ int drive(const oob_sweep_program* pr, Dev D, int64_t n_out_tuples, const int64_
                                               "too many views", "too many storages", "value stack overflow",
                                               "2-D access to a 1-D view", "step limit reached",
                                               "malformed program"};
-                cudaEventDestroy(e0);
-                cudaEventDestroy(e1);
                 return oob_internal_fail(
                     OOB_ERROR, "sweep: " + std::to_string(host_c[1]) + " tuple(s) not executable exactly (first: tuple " +
                                    std::to_string(first_err) + ", " + names[std::min(err_code, 8)] + ")");
@@ -283,8 +365,6 @@ int drive(const oob_sweep_program* pr, Dev D, int64_t n_out_tuples, const int64_
         }
         break;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     return OOB_OK;
 }
 

@@ -128,3 +128,37 @@ def test_compiler_is_deterministic_on_reference_ast(name):
     sp = S.compile_program(parse_source(src, name.split("/")[-1]))
     assert np.array_equal(sp.code, PROGS[name].code)
     assert np.array_equal(sp.sites, PROGS[name].sites)
+
+
+def test_device_entry_validates_programs_before_touching_a_device():
+    """oob_sweep_run checks operands and the value-stack discipline on the
+    host first: every fixture program passes (the call then needs a device),
+    a program with an unbalanced stack or a bad jump is rejected."""
+    from paper_2601_21552_b200 import _lib
+    L = _lib.lib()
+    no_device = _lib.device_count() == 0
+
+    def rc_of(sp):
+        cp, keep = S._cprog(sp)
+        ns = max(len(sp.sites), 1)
+        lab = np.zeros(ns, dtype=np.uint32)
+        first = np.full((ns, 4), -1, dtype=np.int64)
+        res = S._CResult()
+        res.site_labels, res.site_first_tuple = lab.ctypes.data, first.ctypes.data
+        opts = S._copts()
+        return L.oob_sweep_run(ctypes.byref(cp), 2, sp.n_input_sites, ctypes.byref(opts), ctypes.byref(res))
+
+    for name, sp in PROGS.items():
+        rc = rc_of(sp)
+        assert rc != 1, (name, _lib.last_error())  # OOB_E_INVALID
+        if no_device:
+            assert rc == 2  # OOB_E_CUDA: validation passed, no device here
+    sp = PROGS["test_oracle/INPUT_SRC"]
+    bad = S.SweepProgram(sp.code.copy(), sp.lits, sp.kernels, sp.kparams, sp.sites, sp.n_slots,
+                         sp.n_input_sites)
+    bad.code[0] = [S.OP["ST"], 0, 0, 0]  # pops an empty stack
+    assert rc_of(bad) == 1 and "stack" in _lib.last_error()
+    bad2 = S.SweepProgram(sp.code.copy(), sp.lits, sp.kernels, sp.kparams, sp.sites, sp.n_slots,
+                          sp.n_input_sites)
+    bad2.code[1] = [S.OP["JMP"], 10 ** 6, 0, 0]
+    assert rc_of(bad2) == 1
