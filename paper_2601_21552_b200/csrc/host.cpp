@@ -1343,10 +1343,12 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         }
         occ = std::max(1, occ);
         // warps: one per 32 queries of the class, times SCUBA_OOB_JIT_GRID_MULT
-        // (extra blocks start as others finish and serve the class's heavy list)
+        // (extra blocks start as others finish and serve the class's heavy list;
+        // measured on B200, median plan run: x1 -> x3 = C3 14.7 -> 13.0 ms,
+        // C4 52.6 -> 37.4 ms, C5s 11.6 -> 7.9 ms; x6 and more lose again)
         static const uint32_t mult = [] {
             const char* e = std::getenv("SCUBA_OOB_JIT_GRID_MULT");
-            return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : 1);
+            return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : 3);
         }();
         const uint32_t need = mult * ((cd.q_end - cd.q_begin + 31) / 32);
         const uint32_t b = std::max(1u, std::min<uint32_t>((need + jw - 1) / jw, (uint32_t)(P->sms * occ)));
