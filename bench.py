@@ -289,6 +289,7 @@ def run_ours(args, rank, world, local):
     res = plan.results()
     if res["status"] != _lib.OOB_OK:
         raise SystemExit(f"engine could not decide the batch: {_lib.last_error()}")
+    info = plan.info()  # result bytes of a fetched run (Sat models packed on the device)
     value = dist.sum(Q) * args.steps / (total_ms / 1e3)
 
     # ---- e2e: the public C-ABI call on host buffers ------------------------------

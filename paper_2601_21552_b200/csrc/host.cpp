@@ -40,6 +40,9 @@ namespace oob {
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s);
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
 cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm);
+cudaError_t launch_gather_sat(const int8_t* verdict, const QDesc* qd, const int64_t* model, uint32_t n,
+                              unsigned long long* counter, uint32_t* sat_off, int64_t* compact, int sms,
+                              cudaStream_t s);
 }
 
 using namespace oob;
@@ -897,6 +900,7 @@ struct DevicePool {
     DevBuf classes, class_next, class_init, warp_class;
     DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
     DevBuf resume, resume_init, slot64, slot128, slotx32, timeline, classes_interp, stats;
+    DevBuf satcnt, satoff, compact;  // SOLVE fetch: packed Sat models
     std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
     std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
@@ -906,7 +910,7 @@ struct DevicePool {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
                           &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &slotx32, &timeline,
-                          &classes_interp, &stats})
+                          &classes_interp, &stats, &satcnt, &satoff, &compact})
             b->release();
     }
 };
@@ -1067,9 +1071,11 @@ struct DevJob {
     size_t out_model_words = 0;
     bool staged = false;
     float last_ms = 0;
+    int64_t last_sat_vars = -1;  // packed Sat-model vars of the last fetch (SOLVE), -1: unpacked
 
-    uint64_t record_bytes() const {  // algorithmic input bytes of one launch
-        return qd.size() * sizeof(QDesc) + cls.size() * sizeof(ClassDesc) + code.size() * 4 + data.size() * 8;
+    uint64_t record_bytes() const {  // algorithmic input bytes of one launch (x32 records: written on device)
+        return qd.size() * sizeof(QDesc) + cls.size() * sizeof(ClassDesc) + code.size() * 4 +
+               (wide == W_X32 ? 0 : data.size() * 8);
     }
 };
 
@@ -1415,7 +1421,10 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     }
     CK(cudaMemcpyAsync(P->qdesc.p, j.qd.data(), j.qd.size() * sizeof(QDesc), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(P->code.p, j.code.data(), j.code.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(P->data.p, j.data.data(), j.data.size() * 8, cudaMemcpyHostToDevice, s));
+    // the x32 job holds shadows only: their records are written on the device
+    // (by the int64 root phase) before they are ever read -- nothing to upload
+    if (j.wide != W_X32 || rc.mode != MODE_SOLVE)
+        CK(cudaMemcpyAsync(P->data.p, j.data.data(), j.data.size() * 8, cudaMemcpyHostToDevice, s));
     LaunchArgs& a = j.a;
     a = LaunchArgs{};
     a.qdesc = (const QDesc*)P->qdesc.p;
@@ -1726,15 +1735,36 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
     nodes.alloc(n);
     passes.alloc(n);
     el.alloc(n);
-    mw.alloc(std::max<size_t>(j.out_model_words, 2));
+    // SOLVE: only Sat entries carry a model -- pack them on the device and
+    // copy those (C3: ~15% of the entries) instead of the whole model buffer
+    const bool packed = rc.mode == MODE_SOLVE && j.out_model_words;
+    HostArr<uint32_t> satoff;
+    unsigned long long nsat = 0;
+    if (packed) {
+        CK(P->satcnt.ensure(8));
+        CK(P->satoff.ensure((size_t)n * 4));
+        CK(P->compact.ensure(j.out_model_words * 8));
+        CK(cudaMemsetAsync(P->satcnt.p, 0, 8, s));
+        CK(launch_gather_sat((const int8_t*)P->verdict.p, (const QDesc*)P->qdesc.p, (const int64_t*)P->model.p, n,
+                             (unsigned long long*)P->satcnt.p, (uint32_t*)P->satoff.p, (int64_t*)P->compact.p,
+                             P->sms, s));
+        satoff.alloc(n);
+        CK(cudaMemcpyAsync(satoff.data(), P->satoff.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&nsat, P->satcnt.p, 8, cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaMemcpyAsync(verdict.data(), P->verdict.p, n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(err.data(), P->err.p, n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(nodes.data(), P->nodes.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(passes.data(), P->passes.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(el.data(), P->elapsed.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
-    if (j.out_model_words)
+    if (j.out_model_words && !packed)
         CK(cudaMemcpyAsync(mw.data(), P->model.p, j.out_model_words * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (packed && nsat) {
+        CK(cudaMemcpyAsync(mw.data(), P->compact.p, (size_t)nsat * 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    j.last_sat_vars = packed ? (int64_t)nsat : -1;
     if (j.a.timeline) {  // records: q, wide, shadow, verdict, nodes, passes, 4 timestamps (int64 each)
         std::vector<uint64_t> tl((size_t)n * 4);
         CK(cudaMemcpy(tl.data(), j.a.timeline, (size_t)n * 32, cudaMemcpyDeviceToHost));
@@ -1781,6 +1811,7 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
             uint32_t nv = comp[q].nv;
             uint64_t m0 = j.mo[i];
             if (rc.mode == MODE_SOLVE && verdict[i] == VERDICT_SAT && rc.model) {
+                if (packed) m0 = satoff[i];
                 for (uint32_t v = 0; v < nv; v++) {
                     rc.model[vb + v].lo = (uint64_t)mw[2 * (m0 + v)];
                     rc.model[vb + v].hi = mw[2 * (m0 + v) + 1];
@@ -2393,7 +2424,12 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
             for (uint8_t sh : j.is_shadow) own += !sh;
             nq += own;
             rec += (int64_t)j.record_bytes();
-            res += (int64_t)j.qs.size() * (1 + 1 + 8 + 8 + 4) + (int64_t)j.out_model_words * 8;
+            // bytes copied back per run: verdict, error, nodes, passes, elapsed per
+            // entry, plus the models (SOLVE: only the Sat ones, packed, with a
+            // 4-byte offset per entry)
+            res += (int64_t)j.qs.size() * (1 + 1 + 8 + 8 + 4) +
+                   (j.last_sat_vars >= 0 ? (int64_t)j.qs.size() * 4 + j.last_sat_vars * 16
+                                         : (int64_t)j.out_model_words * 8);
             cls += j.n_classes;
             if (w == 1 || w == 2) wide += own;
             jobs++;

@@ -1,3 +1,4 @@
+#include <algorithm>
 // kernels.cu -- sm_100a kernels of the OOB-query engine.
 //
 //   oob_lockstep_kernel<T>  K1: exact solve() emulation (solver.py:363-416)
@@ -268,6 +269,31 @@ cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks,
     if (wide == 3) return launch_impl<int>(a, blocks, fblocks, s);
     if (wide == 2) return launch_impl<i256>(a, blocks, fblocks, s);
     return wide ? launch_impl<__int128>(a, blocks, fblocks, s) : launch_impl<long long>(a, blocks, fblocks, s);
+}
+
+// SOLVE fetch: the models of Sat entries only, packed (an entry's model slot
+// is written by the search only when it ends Sat; the rest of the model
+// buffer is never read by the host) -- sat_off[i] is entry i's offset in vars
+__global__ void oob_gather_sat_kernel(const int8_t* __restrict__ verdict, const QDesc* __restrict__ qd,
+                                      const int64_t* __restrict__ model, uint32_t n,
+                                      unsigned long long* counter, uint32_t* sat_off, int64_t* compact) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (verdict[i] != VERDICT_SAT) continue;
+        const uint32_t nv = qd[i].nv_ncon & 0xffffu;
+        const unsigned long long off = atomicAdd(counter, (unsigned long long)nv);
+        sat_off[i] = (uint32_t)off;
+        const int64_t* src = model + 2 * qd[i].out_v;
+        int64_t* dst = compact + 2 * off;
+        for (uint32_t k = 0; k < 2 * nv; k++) dst[k] = src[k];
+    }
+}
+
+cudaError_t launch_gather_sat(const int8_t* verdict, const QDesc* qd, const int64_t* model, uint32_t n,
+                              unsigned long long* counter, uint32_t* sat_off, int64_t* compact, int sms,
+                              cudaStream_t s) {
+    const uint32_t blocks = std::max(1u, std::min<uint32_t>((n + 255) / 256, (uint32_t)sms * 4));
+    oob_gather_sat_kernel<<<blocks, 256, 0, s>>>(verdict, qd, model, n, counter, sat_off, compact);
+    return cudaGetLastError();
 }
 
 // resident blocks per SM of the kernel for `mode` with `smem` dynamic bytes per block
