@@ -1735,6 +1735,7 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
     nodes.alloc(n);
     passes.alloc(n);
     el.alloc(n);
+    mw.alloc(std::max<size_t>(j.out_model_words, 2));
     // SOLVE: only Sat entries carry a model -- pack them on the device and
     // copy those (C3: ~15% of the entries) instead of the whole model buffer
     const bool packed = rc.mode == MODE_SOLVE && j.out_model_words;
@@ -1760,6 +1761,10 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
     if (j.out_model_words && !packed)
         CK(cudaMemcpyAsync(mw.data(), P->model.p, j.out_model_words * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (packed && nsat * 2 > j.out_model_words)
+        return "packed Sat models exceed the model buffer (" + std::to_string(nsat) + " vars, " +
+               std::to_string(j.out_model_words) + " words, job " + std::to_string(j.wide) + ", " +
+               std::to_string(n) + " entries)";
     if (packed && nsat) {
         CK(cudaMemcpyAsync(mw.data(), P->compact.p, (size_t)nsat * 16, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
