@@ -1072,6 +1072,8 @@ struct DevJob {
     bool staged = false;
     float last_ms = 0;
     int64_t last_sat_vars = -1;  // packed Sat-model vars of the last fetch (SOLVE), -1: unpacked
+    bool data_uploaded = false;  // records already on their way (uploaded right after pack)
+    std::string upload_err;
 
     uint64_t record_bytes() const {  // algorithmic input bytes of one launch (x32 records: written on device)
         return qd.size() * sizeof(QDesc) + cls.size() * sizeof(ClassDesc) + code.size() * 4 +
@@ -1274,15 +1276,24 @@ size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
     return (b + 255) & ~(size_t)255;
 }
 
-std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap, uint32_t trail_cap,
-                  bool heavy = true) {
-    CK(cudaSetDevice(j.dev));
+std::string ensure_stream(DevicePool* P, int dev) {
+    CK(cudaSetDevice(dev));
     if (!P->stream) {
         CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
         CK(cudaEventCreate(&P->ev0));
         CK(cudaEventCreate(&P->ev1));
         CK(cudaEventCreateWithFlags(&P->evr, cudaEventDisableTiming));
-        CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, j.dev));
+        CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return "";
+}
+
+std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap, uint32_t trail_cap,
+                  bool heavy = true) {
+    if (!j.upload_err.empty()) return j.upload_err;
+    {
+        std::string e = ensure_stream(P, j.dev);
+        if (!e.empty()) return e;
     }
     const uint32_t n = (uint32_t)j.qs.size();
     const size_t tbytes = tbytes_of(j.wide);
@@ -1423,7 +1434,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(cudaMemcpyAsync(P->code.p, j.code.data(), j.code.size() * 4, cudaMemcpyHostToDevice, s));
     // the x32 job holds shadows only: their records are written on the device
     // (by the int64 root phase) before they are ever read -- nothing to upload
-    if (j.wide != W_X32 || rc.mode != MODE_SOLVE)
+    if ((j.wide != W_X32 || rc.mode != MODE_SOLVE) && !j.data_uploaded)
         CK(cudaMemcpyAsync(P->data.p, j.data.data(), j.data.size() * 8, cudaMemcpyHostToDevice, s));
     LaunchArgs& a = j.a;
     a = LaunchArgs{};
@@ -1528,8 +1539,19 @@ struct DevGroup {
     bool has(int w) const { return !job[w].qs.empty(); }
 };
 
+// start the upload of a packed job's records at once (caller holds P->mu):
+// the copy overlaps the packing of the next jobs instead of following it
+std::string upload_data(DevJob& j, DevicePool* P) {
+    std::string e = ensure_stream(P, j.dev);
+    if (!e.empty()) return e;
+    CK(P->data.ensure(j.data.size() * 8));
+    CK(cudaMemcpyAsync(P->data.p, j.data.data(), j.data.size() * 8, cudaMemcpyHostToDevice, P->stream));
+    j.data_uploaded = true;
+    return "";
+}
+
 // shadows + pack + demotion slots of a group (before staging)
-void pack_group(const RunCtx& rc, DevGroup& G) {
+void pack_group(const RunCtx& rc, DevGroup& G, bool upload = false) {
     for (int w = 0; w < NJOBS; w++) {
         G.job[w].dev = G.dev;
         G.job[w].wide = w;
@@ -1549,11 +1571,17 @@ void pack_group(const RunCtx& rc, DevGroup& G) {
         for (int w = 0; w < 3; w++)
             G.job[W_X32].shadows.insert(G.job[W_X32].shadows.end(), own[w].begin(), own[w].end());
     static const char* pk_names[NJOBS] = {"pack.int64", "pack.int128", "pack.i256", "pack.x32"};
-    for (int w = 0; w < NJOBS; w++)
+    for (int w = 0; w < NJOBS; w++) {
+        G.job[w].data_uploaded = false;
+        G.job[w].upload_err.clear();
         if (!G.job[w].qs.empty() || !G.job[w].shadows.empty()) {
             Phase ph(pk_names[w]);
             pack(rc, G.job[w]);
+            // (the x32 job's records are written on the device: no upload)
+            if (upload && G.pool[w] && !(w == W_X32 && rc.mode == MODE_SOLVE))
+                G.job[w].upload_err = upload_data(G.job[w], G.pool[w]);
         }
+    }
     Phase ph_slots("pack.slots");
     if (!demote_on(rc)) return;
     // demotion slots: target t (0 int64, 1 int128, 2 x32 = job 3) of the jobs that hand down to it
@@ -1858,13 +1886,13 @@ std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
             G.job[w].qs = w < 3 ? cur[w] : std::vector<int64_t>();
             G.pool[w] = pools[w];
         }
-        {
-            Phase ph("pack");
-            pack_group(rc, G);
-        }
         std::vector<int64_t> retry[3];
         {
             std::lock_guard<std::mutex> l0(pools[0]->mu), l1(pools[1]->mu), l2(pools[2]->mu), l3(pools[3]->mu);
+            {
+                Phase ph("pack");
+                pack_group(rc, G, true);  // each job's upload overlaps the next job's packing
+            }
             std::string e;
             {
                 Phase ph("stage");
