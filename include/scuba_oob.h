@@ -139,7 +139,9 @@ enum {
 /* Results (caller-allocated; optional arrays may be NULL). */
 typedef struct {
     int8_t* verdict;     /* n: OOB_UNSAT / OOB_SAT / OOB_TIMEOUT / OOB_ERROR        */
-    oob_i128* model;     /* var_begin[n] entries: SAT model at the query's var range */
+    oob_i128* model;     /* var_begin[n] entries: SAT model at the query's var range;
+                            every entry is written (zero for queries not SAT), so the
+                            caller need not clear it */
     int64_t* nodes;      /* n, optional: DFS nodes visited (reference _search calls) */
     int64_t* passes;     /* n, optional: propagation passes (one _Narrower each)     */
     double* elapsed_s;   /* n, optional: device time spent on the query            */

@@ -155,7 +155,8 @@ def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, h
     n = fb.n
     out = {
         "verdict": np.full(n, -1, dtype=np.int8),
-        "model": np.zeros((max(fb.n_vars_total, 1), 2), dtype=np.int64),
+        # every row is written by the library (zero unless Sat): no clearing here
+        "model": np.empty((max(fb.n_vars_total, 1), 2), dtype=np.int64),
         "nodes": np.zeros(n, dtype=np.int64),
         "passes": np.zeros(n, dtype=np.int64),
         "elapsed": np.zeros(n, dtype=np.float64),

@@ -2138,6 +2138,17 @@ int finish(Prepared& pr, int64_t n) {
 // Common driver of the three batched entry points.
 int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i128* model_in, oob_i128* model_out,
           int8_t* verdict, int64_t* nodes, int64_t* passes, double* elapsed) {
+    if (mode == MODE_SOLVE && model_out && b && b->n_queries > 0) {
+        // every model row is written (zero unless SAT): cleared here in
+        // parallel, so the caller's fresh buffer is faulted in by all host
+        // threads instead of one
+        Phase ph("clear");
+        const int64_t v0 = b->var_begin[0], v1 = b->var_begin[b->n_queries];
+        if (v1 > v0)
+            parallel_for((size_t)(v1 - v0), 1 << 14, [&](size_t lo, size_t hi) {
+                std::memset((void*)(model_out + v0 + lo), 0, (hi - lo) * sizeof(oob_i128));
+            });
+    }
     Prepared pr;
     int rc0 = prepare(b, opt_in, mode, model_in, verdict, nodes, passes, elapsed, pr);
     if (rc0 != OOB_OK) return rc0;
