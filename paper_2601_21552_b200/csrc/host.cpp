@@ -220,6 +220,8 @@ struct Structure {
     std::vector<int32_t> lit_src; // per literal slot: the query's input literal index (-1: the constant 1)
     uint64_t key = 0;             // structure-class hash (words, nv, ncon)
     std::string range_why;        // non-empty: the structure alone is beyond the engine (R_RANGE)
+    int w64_log2 = -1;            // every query of this structure whose domain bounds and literals
+                                  // are <= 2^w64_log2 in magnitude is in the int64 regime (-1: none)
     const uint32_t* code() const { return words.data() + ncon; }
 };
 
@@ -725,6 +727,31 @@ std::shared_ptr<Structure> build_structure(const QView& v, int mode) {
         }
     }
     st.key = class_hash(st.words, st.nv, st.ncon);
+    // int64 acceptance threshold of the structure.  prove_bound_mag is
+    // nondecreasing in every domain-bound and literal magnitude (|x|+|y|,
+    // |x||y|, min, max, T+m, T*c+c), so the bound computed with every domain
+    // [-D, D] and every literal D dominates that of any query whose
+    // magnitudes are <= D: the largest D = 2^k passing the int64 test admits
+    // such queries without a per-query proof (bisection over k, once per
+    // structure and thread).
+    {
+        std::vector<i128> dlo(st.nv), dhi(st.nv), lits(st.nlit);
+        auto ok = [&](int k) {
+            const i128 D = (i128)1 << k;
+            for (uint32_t i = 0; i < st.nv; i++) { dlo[i] = -D; dhi[i] = D; }
+            for (uint32_t i = 0; i < st.nlit; i++) lits[i] = D;
+            return prove_bound_mag(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits) < 9.2e18;
+        };
+        int lo = -1, hi = 62;  // invariant: ok(lo) (or lo = -1), !ok(hi + 1)
+        if (ok(hi)) lo = hi;
+        else
+            while (hi - lo > 1) {
+                int mid = lo + (hi - lo) / 2;
+                if (mid >= 0 && ok(mid)) lo = mid;
+                else hi = mid;
+            }
+        st.w64_log2 = lo;
+    }
     return out;
 }
 
@@ -843,12 +870,21 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
         return out;
     }
     lits.resize(st.nlit);
-    for (uint32_t i = 0; i < st.nlit; i++) lits[i] = lit_value(b, q, st, i);
+    i128 Lmax = 0;
+    for (uint32_t i = 0; i < st.nlit; i++) {
+        lits[i] = lit_value(b, q, st, i);
+        Lmax = imax(Lmax, iabs(lits[i]));
+    }
     i128 Dmax = 0;
     for (int i = 0; i < v.nv; i++) Dmax = imax(Dmax, imax(iabs(dlo[i]), iabs(dhi[i])));
     if (Dmax > D128MAX) {
         out.regime = R_RANGE;
         out.why = "domain bounds exceed the 128-bit wire format";
+        return out;
+    }
+    // structure-level acceptance (build_structure): no per-query proof needed
+    if (st.w64_log2 >= 0 && imax(Dmax, Lmax) <= ((i128)1 << st.w64_log2) && Dmax <= D64MAX) {
+        out.regime = R_W64;
         return out;
     }
     // Fast acceptance: the magnitude bound in double precision dominates the
