@@ -2156,7 +2156,12 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
             });
             for (size_t i = 0; i < qs.size(); i++) qs[i] = keyed[i].second;
         }
-        for (size_t i = 0; i < qs.size(); i++) pr.work[(i / 32) % want].qs[w].push_back(qs[i]);
+        if (want == 1) {
+            pr.work[0].qs[w] = qs;
+        } else {
+            for (int d = 0; d < want; d++) pr.work[d].qs[w].reserve(qs.size() / want + 32);
+            for (size_t i = 0; i < qs.size(); i++) pr.work[(i / 32) % want].qs[w].push_back(qs[i]);
+        }
     }
     return OOB_OK;
 }
