@@ -216,6 +216,37 @@ def ncu_alu(config: str):
         return None
 
 
+def alu_roofline(config: str, launch_ms: float, sms: int = 148):
+    """Integer-pipe roofline of the decision kernels: warp instructions of one
+    step (ncu smsp__inst_executed.sum over all launches, committed in
+    profiles/ncu_summary.json) / the live device time of a step, against the
+    SM issue peak (4 schedulers x 1 warp-instruction/clock x sm_max_mhz x
+    SMs), next to the measured LOP3 peak (tools/alu_peak.cu,
+    profiles/alu_peak.jsonl)."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text()).get(config, {})
+        inst = float(d["warp_inst_per_step"])
+    except Exception:
+        return None
+    try:
+        mhz = float(json.loads(PEAKS.read_text())["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    peak = sms * 4 * mhz * 1e6
+    lop3 = None
+    try:
+        for line in (ROOT / "profiles" / "alu_peak.jsonl").read_text().splitlines():
+            r = json.loads(line)
+            if r["kind"] == "lop3":
+                lop3 = r["warp_inst_per_s"]
+    except Exception:
+        pass
+    achieved = inst / (launch_ms / 1e3)
+    return {"bound": "issue (integer ALU / latency)", "unit": "warp-inst/s",
+            "warp_inst_per_step": inst, "achieved": round(achieved, 1), "issue_peak": peak,
+            "frac": round(achieved / peak, 4), "lop3_peak_measured": lop3}
+
+
 def ncu_traffic(config: str):
     """DRAM bytes of one step (all launches of one plan run) from the
     committed ncu launch-list summary (profiles/ncu_summary.json), or None."""
@@ -375,7 +406,8 @@ def run_ours(args, rank, world, local):
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "note": "interval-propagation DFS is integer-ALU/latency bound; "
                              "bytes = compiled records + results per step, all launches (DESIGN.md)",
-                     "alu": ncu_alu(args.config)},
+                     "alu": ncu_alu(args.config),
+                     "issue": alu_roofline(args.config, launch_ms)},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
                 "h2d_bytes_per_step": info["record_bytes"],

@@ -1403,7 +1403,13 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
             const char* e = std::getenv("SCUBA_OOB_JIT_GRID_MULT");
             return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : 3);
         }();
-        const uint32_t need = mult * ((cd.q_end - cd.q_begin + 31) / 32);
+        // the int64 job's classes hold the queries the x32 probe could not take
+        // (long root propagations, wide values): fewer queries, heavier each
+        static const uint32_t mult64 = [] {
+            const char* e = std::getenv("SCUBA_OOB_JIT_GRID_MULT64");
+            return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : (int)mult);
+        }();
+        const uint32_t need = (j.wide == 0 ? mult64 : mult) * ((cd.q_end - cd.q_begin + 31) / 32);
         const uint32_t b = std::max(1u, std::min<uint32_t>((need + jw - 1) / jw, (uint32_t)(P->sms * occ)));
         j.jit_blocks.push_back(b);
         n_warps += b * jw;
