@@ -295,8 +295,14 @@ def run_ours(args, rank, world, local):
     from paper_2601_21552_b200.solver import solve_flat
     from paper_2601_21552_b200.wire import flatten
 
-    dist = Dist(world, local)
-    device = local if world > 1 else 0
+    ndev = _lib.device_count()
+    if ndev < 1:
+        raise SystemExit("bench.py needs a CUDA device (the engine has no CPU path)")
+    # one rank per GPU over NCCL; with fewer GPUs than ranks (a test of the
+    # multi-rank path on a small box) ranks share devices and the barrier /
+    # max-over-ranks reductions run over gloo
+    dist = Dist(world, local % ndev, backend="nccl" if ndev >= world else "gloo")
+    device = local % ndev
     Q = args.queries
     fb = synth.generate(args.config, Q, first=rank * Q, names=False)
 
@@ -321,6 +327,7 @@ def run_ours(args, rank, world, local):
     if res["status"] != _lib.OOB_OK:
         raise SystemExit(f"engine could not decide the batch: {_lib.last_error()}")
     info = plan.info()  # result bytes of a fetched run (Sat models packed on the device)
+    plan.close()  # its device pools are freed before the e2e leg allocates its own
     value = dist.sum(Q) * args.steps / (total_ms / 1e3)
 
     # ---- e2e: the public C-ABI call on host buffers ------------------------------

@@ -138,10 +138,14 @@ struct LaunchArgs {
     uint32_t* heavy_list;     // query index + 1 (0 = not yet published)
     uint64_t* heavy_t0;       // start time of each scheduled query (ns)
     uint32_t* heavy_next;     // frontier kernel work cursor
-    // frontier scratch (one region per frontier warp, see frontier.cuh)
+    // frontier scratch (frontier.cuh): fr_nregions regions shared by every
+    // launch of the job; a warp holds one (bit set in fr_bitmap) only while it
+    // expands a heavy query
     void* fr_region;
     uint64_t fr_region_bytes;
     uint32_t fr_ecap, fr_ucap, fr_logcap;
+    uint32_t* fr_bitmap;
+    uint32_t fr_nregions;
     // outputs (indexed by QDesc::out_q / out_v)
     int8_t* verdict;
     int64_t* model;           // int128 words, 2 per var

@@ -937,6 +937,7 @@ struct DevicePool {
     DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
     DevBuf resume, resume_init, slot64, slot128, slotx32, timeline, classes_interp, stats;
     DevBuf satcnt, satoff, compact;  // SOLVE fetch: packed Sat models
+    DevBuf fr_map;                   // frontier region pool: held bits
     std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
     std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
@@ -946,7 +947,7 @@ struct DevicePool {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
                           &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &slotx32, &timeline,
-                          &classes_interp, &stats, &satcnt, &satoff, &compact})
+                          &classes_interp, &stats, &satcnt, &satoff, &compact, &fr_map})
             b->release();
     }
 };
@@ -1099,6 +1100,7 @@ struct DevJob {
     uint64_t model_words = 0;
     uint32_t n_classes = 0;
     uint32_t blocks = 1, fblocks = 0;
+    uint32_t fr_regions = 0;     // frontier scratch regions of the job (shared by its launches)
     uint32_t root_blocks = 1;  // root kernel: one thread per query (grid-stride)
     uint32_t tail_blocks = 0;    // wide SOLVE jobs: frontier-only launch after the int64 kernel
     LaunchArgs tail_args{};
@@ -1422,7 +1424,13 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     const uint32_t own_warps = n_warps;
     j.tail_blocks = (j.wide && heavy_nodes) ? (uint32_t)(P->sms * per_sm) : 0u;
     n_warps += j.tail_blocks * WARPS_PER_BLOCK;
-    j.fblocks = heavy_nodes ? (n_warps + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK : 0;  // one frontier region per warp
+    j.fblocks = heavy_nodes ? (n_warps + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK : 0;
+    // frontier scratch: a pool of regions shared by every launch of the job,
+    // held per heavy query (phases.cuh claim_region) -- sized for the warps
+    // that can be resident at once, not for every warp of every launch
+    // (C3: 74 -> ~20 GB per plan)
+    const uint32_t regions_cap = (uint32_t)P->sms * (j.wide == 1 || j.wide == 2 ? 8u : 32u);
+    j.fr_regions = heavy_nodes ? std::max(1u, std::min(n_warps, regions_cap)) : 0u;
     // the root kernel walks every query of the job (JIT classes included), one
     // thread each: its grid follows n, not the interpreting kernel's share,
     // bounded by the per-warp slabs allocated below
@@ -1449,7 +1457,10 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->heavy_count.ensure(16 * (1 + j.jit_cls.size())));
     CK(P->heavy_list.ensure((size_t)n * 8));  // [0, n): per compiled class at its q range; [n, 2n): interpreter
     CK(P->heavy_t0.ensure((size_t)n * 8));
-    if (j.fblocks) CK(P->fr_region.ensure((size_t)j.fblocks * WARPS_PER_BLOCK * fr_bytes));
+    if (j.fr_regions) {
+        CK(P->fr_region.ensure((size_t)j.fr_regions * fr_bytes));
+        CK(P->fr_map.ensure(((size_t)j.fr_regions + 31) / 32 * 4));
+    }
     CK(P->resume.ensure((size_t)n * 4));
     CK(P->resume_init.ensure((size_t)n * 4));
     auto slot_buf = [&](int t) -> DevBuf& { return t == 0 ? P->slot64 : (t == 1 ? P->slot128 : P->slotx32); };
@@ -1508,8 +1519,10 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.heavy_next = (uint32_t*)P->heavy_count.p + 1;
     a.heavy_list = (uint32_t*)P->heavy_list.p + n;
     a.heavy_t0 = (uint64_t*)P->heavy_t0.p;
-    a.fr_region = j.fblocks ? P->fr_region.p : nullptr;
+    a.fr_region = j.fr_regions ? P->fr_region.p : nullptr;
     a.fr_region_bytes = fr_bytes;
+    a.fr_bitmap = j.fr_regions ? (uint32_t*)P->fr_map.p : nullptr;
+    a.fr_nregions = j.fr_regions;
     a.fr_ecap = FR_ECAP;
     a.fr_ucap = FR_UCAP;
     a.fr_logcap = FR_LOGCAP;
@@ -1543,7 +1556,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         j.tail_args.frontier_only = 1;
         j.tail_args.slab_T = (unsigned char*)P->slabT.p + (uint64_t)own_warps * j.g.slab_T_words * tbytes;
         j.tail_args.slab_u32 = (uint32_t*)P->slabU.p + (uint64_t)own_warps * j.g.slab_u32_words;
-        j.tail_args.fr_region = (unsigned char*)P->fr_region.p + (uint64_t)own_warps * fr_bytes;
+
     }
     // one launch per compiled class: its own class queue and heavy list, and
     // its own range of per-warp scratch
@@ -1559,7 +1572,6 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         b.heavy_list = (uint32_t*)P->heavy_list.p + j.cls[c].q_begin;
         b.slab_T = (unsigned char*)P->slabT.p + warp_base * j.g.slab_T_words * tbytes;
         b.slab_u32 = (uint32_t*)P->slabU.p + warp_base * j.g.slab_u32_words;
-        if (b.fr_region) b.fr_region = (unsigned char*)P->fr_region.p + warp_base * fr_bytes;
         j.jit_args.push_back(b);
         warp_base += (uint64_t)j.jit_blocks[i] * jit_warps();
     }
@@ -1691,6 +1703,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s0));
         CK(cudaMemsetAsync(P->heavy_count.p, 0, 16 * (1 + j.jit_cls.size()), s0));
         if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 8, s0));
+        if (j.fr_regions) CK(cudaMemsetAsync(P->fr_map.p, 0, ((size_t)j.fr_regions + 31) / 32 * 4, s0));
         if (j.a.timeline) CK(cudaMemsetAsync(j.a.timeline, 0, n * 32, s0));
         CK(cudaMemsetAsync(P->verdict.p, 0xFF, n, s0));
         CK(cudaMemcpyAsync(P->resume.p, P->resume_init.p, n * 4, cudaMemcpyDeviceToDevice, s0));

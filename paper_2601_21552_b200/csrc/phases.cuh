@@ -209,6 +209,28 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
 // exits once every started producer is done (or after frontier_wait_us).  An entry
 // appended after that comes from a warp still in its lockstep phase, which
 // serves the list itself afterwards, so every entry is taken.
+// first free region of the job's pool (bitmap, starting at a warp-dependent
+// word to spread contention); spins while all are held
+__device__ __forceinline__ uint32_t claim_region(uint32_t* bitmap, uint32_t n, uint32_t warp) {
+    const uint32_t words = (n + 31) >> 5;
+    uint32_t w = (warp * 2654435761u) % words;
+    for (uint32_t tries = 0;; tries++) {
+        const uint32_t valid = (w == words - 1 && (n & 31)) ? ((1u << (n & 31)) - 1u) : 0xffffffffu;
+        uint32_t freeb = ~*(volatile uint32_t*)(bitmap + w) & valid;
+        while (freeb) {
+            const uint32_t b = __ffs(freeb) - 1;
+            const uint32_t old = atomicOr(bitmap + w, 1u << b);
+            if (!(old & (1u << b))) {
+                __threadfence();
+                return w * 32 + b;
+            }
+            freeb = ~old & valid;
+        }
+        w = (w + 1) % words;
+        if (tries % words == words - 1) __nanosleep(2000);
+    }
+}
+
 template <typename LaneT>
 __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, uint32_t warp, uint32_t lane) {
     const unsigned FULL = 0xffffffffu;
@@ -220,9 +242,7 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
     if (!a.heavy_nodes) return;
     const uint64_t WAIT_NS = 1000ull * a.frontier_wait_us;  // bound on waiting for producers
     uint64_t idle_since = 0;
-    FrontierRegion<typename LaneT::T> R;  // one scratch region per warp of the grid
-    R.bind((unsigned char*)a.fr_region + (size_t)warp * a.fr_region_bytes, a.g.maxv, a.fr_ecap, a.fr_ucap,
-           a.fr_logcap);
+    FrontierRegion<typename LaneT::T> R;  // scratch region, claimed per heavy query
     for (;;) {
         int idx = -1;
         if (lane == 0) {
@@ -261,7 +281,20 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
         cd.ncode_nlit = d.ncode_nlit;
         L.set_class(a, cd);
         L.load(a, d);
+        // a scratch region of the job's pool, held for this query only (every
+        // query re-initialises what it uses); a waiter always gets one in the
+        // end because holders release theirs without waiting on anything
+        uint32_t region = 0;
+        if (lane == 0) region = claim_region(a.fr_bitmap, a.fr_nregions, warp);
+        region = __shfl_sync(FULL, region, 0);
+        R.bind((unsigned char*)a.fr_region + (size_t)region * a.fr_region_bytes, a.g.maxv, a.fr_ecap, a.fr_ucap,
+               a.fr_logcap);
         frontier_query(L, a, R, qi, lane);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAnd(a.fr_bitmap + (region >> 5), ~(1u << (region & 31)));
+        }
     }
 }
 
