@@ -146,6 +146,10 @@ struct LaunchArgs {
     uint32_t fr_ecap, fr_ucap, fr_logcap;
     uint32_t* fr_bitmap;
     uint32_t fr_nregions;
+    // per-warp slabs of the SOLVE kernels: a pool of slab_nslots shared by the
+    // job's launches, one held per running warp (null: slab index = warp id)
+    uint32_t* slab_bitmap;
+    uint32_t slab_nslots;
     // outputs (indexed by QDesc::out_q / out_v)
     int8_t* verdict;
     int64_t* model;           // int128 words, 2 per var

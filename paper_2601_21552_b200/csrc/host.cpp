@@ -938,6 +938,7 @@ struct DevicePool {
     DevBuf resume, resume_init, slot64, slot128, slotx32, timeline, classes_interp, stats;
     DevBuf satcnt, satoff, compact;  // SOLVE fetch: packed Sat models
     DevBuf fr_map;                   // frontier region pool: held bits
+    DevBuf slab_map;                 // slab pool (SOLVE kernels): held bits
     std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
     std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
@@ -947,7 +948,7 @@ struct DevicePool {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
                           &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &slotx32, &timeline,
-                          &classes_interp, &stats, &satcnt, &satoff, &compact, &fr_map})
+                          &classes_interp, &stats, &satcnt, &satoff, &compact, &fr_map, &slab_map})
             b->release();
     }
 };
@@ -1101,6 +1102,7 @@ struct DevJob {
     uint32_t n_classes = 0;
     uint32_t blocks = 1, fblocks = 0;
     uint32_t fr_regions = 0;     // frontier scratch regions of the job (shared by its launches)
+    uint32_t slab_slots = 0;     // per-warp slabs of the job (SOLVE: a pool shared by its launches)
     uint32_t root_blocks = 1;  // root kernel: one thread per query (grid-stride)
     uint32_t tail_blocks = 0;    // wide SOLVE jobs: frontier-only launch after the int64 kernel
     LaunchArgs tail_args{};
@@ -1421,7 +1423,6 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
     // wide jobs: a frontier-only tail launch with a full grid serves their
     // heavy list once the int64 kernel has freed the SMs
-    const uint32_t own_warps = n_warps;
     j.tail_blocks = (j.wide && heavy_nodes) ? (uint32_t)(P->sms * per_sm) : 0u;
     n_warps += j.tail_blocks * WARPS_PER_BLOCK;
     j.fblocks = heavy_nodes ? (n_warps + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK : 0;
@@ -1434,15 +1435,20 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     // the root kernel walks every query of the job (JIT classes included), one
     // thread each: its grid follows n, not the interpreting kernel's share,
     // bounded by the per-warp slabs allocated below
+    // per-warp slabs: in SOLVE mode a pool shared by the job's launches, one
+    // slab held per running warp (phases.cuh claim_slab) -- at most 64 warps
+    // per SM are resident, so no warp ever waits for one
+    j.slab_slots = rc.mode == MODE_SOLVE ? std::max(1u, std::min(n_warps, (uint32_t)P->sms * 64u)) : n_warps;
     j.root_blocks = std::max<uint32_t>(
-        1u, std::min<uint64_t>((n + 32 * WARPS_PER_BLOCK - 1) / (32 * WARPS_PER_BLOCK), n_warps / WARPS_PER_BLOCK));
+        1u, std::min<uint64_t>((n + 32 * WARPS_PER_BLOCK - 1) / (32 * WARPS_PER_BLOCK), j.slab_slots / WARPS_PER_BLOCK));
     const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
     CK(P->code.ensure(j.code.size() * 4));
     CK(P->data.ensure(j.data.size() * 8));
-    CK(P->slabT.ensure((size_t)n_warps * j.g.slab_T_words * tbytes));
-    CK(P->slabU.ensure((size_t)n_warps * j.g.slab_u32_words * 4));
+    CK(P->slabT.ensure((size_t)j.slab_slots * j.g.slab_T_words * tbytes));
+    CK(P->slabU.ensure((size_t)j.slab_slots * j.g.slab_u32_words * 4));
+    if (rc.mode == MODE_SOLVE) CK(P->slab_map.ensure(((size_t)j.slab_slots + 31) / 32 * 4));
     CK(P->next.ensure(16));
     CK(P->verdict.ensure(n));
     CK(P->err.ensure(n));
@@ -1523,6 +1529,8 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.fr_region_bytes = fr_bytes;
     a.fr_bitmap = j.fr_regions ? (uint32_t*)P->fr_map.p : nullptr;
     a.fr_nregions = j.fr_regions;
+    a.slab_bitmap = rc.mode == MODE_SOLVE ? (uint32_t*)P->slab_map.p : nullptr;
+    a.slab_nslots = j.slab_slots;
     a.fr_ecap = FR_ECAP;
     a.fr_ucap = FR_UCAP;
     a.fr_logcap = FR_LOGCAP;
@@ -1554,13 +1562,10 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     if (j.tail_blocks) {
         j.tail_args = a;
         j.tail_args.frontier_only = 1;
-        j.tail_args.slab_T = (unsigned char*)P->slabT.p + (uint64_t)own_warps * j.g.slab_T_words * tbytes;
-        j.tail_args.slab_u32 = (uint32_t*)P->slabU.p + (uint64_t)own_warps * j.g.slab_u32_words;
 
     }
-    // one launch per compiled class: its own class queue and heavy list, and
-    // its own range of per-warp scratch
-    uint64_t warp_base = (uint64_t)j.blocks * WARPS_PER_BLOCK;
+    // one launch per compiled class: its own class queue and heavy list (slabs
+    // and frontier regions come from the job's pools)
     for (size_t i = 0; i < j.jit_cls.size(); i++) {
         const uint32_t c = j.jit_cls[i];
         LaunchArgs b = a;
@@ -1570,10 +1575,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         b.warp_class = nullptr;
         b.heavy_count = (uint32_t*)P->heavy_count.p + 4 * (1 + i);
         b.heavy_list = (uint32_t*)P->heavy_list.p + j.cls[c].q_begin;
-        b.slab_T = (unsigned char*)P->slabT.p + warp_base * j.g.slab_T_words * tbytes;
-        b.slab_u32 = (uint32_t*)P->slabU.p + warp_base * j.g.slab_u32_words;
         j.jit_args.push_back(b);
-        warp_base += (uint64_t)j.jit_blocks[i] * jit_warps();
     }
     j.staged = true;
     return "";
@@ -1704,6 +1706,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         CK(cudaMemsetAsync(P->heavy_count.p, 0, 16 * (1 + j.jit_cls.size()), s0));
         if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 8, s0));
         if (j.fr_regions) CK(cudaMemsetAsync(P->fr_map.p, 0, ((size_t)j.fr_regions + 31) / 32 * 4, s0));
+        if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->slab_map.p, 0, ((size_t)j.slab_slots + 31) / 32 * 4, s0));
         if (j.a.timeline) CK(cudaMemsetAsync(j.a.timeline, 0, n * 32, s0));
         CK(cudaMemsetAsync(P->verdict.p, 0xFF, n, s0));
         CK(cudaMemcpyAsync(P->resume.p, P->resume_init.p, n * 4, cudaMemcpyDeviceToDevice, s0));

@@ -278,9 +278,11 @@ __device__ __forceinline__ void jit_solve(const LaunchArgs& a) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     JitLane<C> L;
-    L.bind(a, warp, lane);
+    const uint32_t slot = claim_slab(a, warp, lane);
+    L.bind(a, slot, lane);
     lockstep_phase(a, L, warp, lane);
     frontier_phase(a, L, warp, lane);
+    release_slab(a, slot, lane);
 }
 
 }  // namespace oob

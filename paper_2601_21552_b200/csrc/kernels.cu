@@ -39,9 +39,11 @@ __global__ void __maxnreg__(128) oob_solve_kernel(LaunchArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     Lane<T> L;
-    L.bind(a, warp, lane);
+    const uint32_t slot = claim_slab(a, warp, lane);
+    L.bind(a, slot, lane);
     if (!a.frontier_only) lockstep_phase(a, L, warp, lane);
     frontier_phase(a, L, warp, lane);
+    release_slab(a, slot, lane);
 }
 
 // Root phase of the wide regimes (format.h, "regime demotion"): one lane per

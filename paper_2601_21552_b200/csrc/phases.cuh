@@ -231,6 +231,21 @@ __device__ __forceinline__ uint32_t claim_region(uint32_t* bitmap, uint32_t n, u
     }
 }
 
+// slab of a SOLVE-kernel warp: from the job's pool, held for the warp's life
+__device__ __forceinline__ uint32_t claim_slab(const LaunchArgs& a, uint32_t warp, uint32_t lane) {
+    if (!a.slab_bitmap) return warp;
+    uint32_t slot = 0;
+    if (lane == 0) slot = claim_region(a.slab_bitmap, a.slab_nslots, warp);
+    return __shfl_sync(0xffffffffu, slot, 0);
+}
+__device__ __forceinline__ void release_slab(const LaunchArgs& a, uint32_t slot, uint32_t lane) {
+    __syncwarp();
+    if (a.slab_bitmap && lane == 0) {
+        __threadfence();
+        atomicAnd(a.slab_bitmap + (slot >> 5), ~(1u << (slot & 31)));
+    }
+}
+
 template <typename LaneT>
 __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, uint32_t warp, uint32_t lane) {
     const unsigned FULL = 0xffffffffu;
