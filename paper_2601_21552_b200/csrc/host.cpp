@@ -1435,10 +1435,18 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     // the root kernel walks every query of the job (JIT classes included), one
     // thread each: its grid follows n, not the interpreting kernel's share,
     // bounded by the per-warp slabs allocated below
-    // per-warp slabs: in SOLVE mode a pool shared by the job's launches, one
-    // slab held per running warp (phases.cuh claim_slab) -- at most 64 warps
-    // per SM are resident, so no warp ever waits for one
-    j.slab_slots = rc.mode == MODE_SOLVE ? std::max(1u, std::min(n_warps, (uint32_t)P->sms * 64u)) : n_warps;
+    // per-warp slabs: one per warp of every launch, or (SCUBA_OOB_SLAB_POOL=1,
+    // SOLVE) a pool shared by the job's launches, one slab held per running
+    // warp (phases.cuh claim_slab; at most 64 warps per SM are resident, so no
+    // warp ever waits for one)
+    // SCUBA_OOB_SLAB_POOL=1: slabs from the job pool (saves ~2 GB per plan on
+    // C3, but measured 5-15% slower on C4/C5s than one slab per warp -- off)
+    static const bool slab_pool = [] {
+        const char* e = std::getenv("SCUBA_OOB_SLAB_POOL");
+        return e && *e == '1';
+    }();
+    const bool pooled = rc.mode == MODE_SOLVE && slab_pool;
+    j.slab_slots = pooled ? std::max(1u, std::min(n_warps, (uint32_t)P->sms * 64u)) : n_warps;
     j.root_blocks = std::max<uint32_t>(
         1u, std::min<uint64_t>((n + 32 * WARPS_PER_BLOCK - 1) / (32 * WARPS_PER_BLOCK), j.slab_slots / WARPS_PER_BLOCK));
     const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
@@ -1448,7 +1456,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->data.ensure(j.data.size() * 8));
     CK(P->slabT.ensure((size_t)j.slab_slots * j.g.slab_T_words * tbytes));
     CK(P->slabU.ensure((size_t)j.slab_slots * j.g.slab_u32_words * 4));
-    if (rc.mode == MODE_SOLVE) CK(P->slab_map.ensure(((size_t)j.slab_slots + 31) / 32 * 4));
+    if (pooled) CK(P->slab_map.ensure(((size_t)j.slab_slots + 31) / 32 * 4));
     CK(P->next.ensure(16));
     CK(P->verdict.ensure(n));
     CK(P->err.ensure(n));
@@ -1529,7 +1537,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.fr_region_bytes = fr_bytes;
     a.fr_bitmap = j.fr_regions ? (uint32_t*)P->fr_map.p : nullptr;
     a.fr_nregions = j.fr_regions;
-    a.slab_bitmap = rc.mode == MODE_SOLVE ? (uint32_t*)P->slab_map.p : nullptr;
+    a.slab_bitmap = pooled ? (uint32_t*)P->slab_map.p : nullptr;
     a.slab_nslots = j.slab_slots;
     a.fr_ecap = FR_ECAP;
     a.fr_ucap = FR_UCAP;
@@ -1576,6 +1584,14 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         b.heavy_count = (uint32_t*)P->heavy_count.p + 4 * (1 + i);
         b.heavy_list = (uint32_t*)P->heavy_list.p + j.cls[c].q_begin;
         j.jit_args.push_back(b);
+    }
+    if (trace_on()) {
+        auto mb = [](const DevBuf& b) { return (double)b.cap / (1 << 20); };
+        std::fprintf(stderr,
+                     "[oob] pool w%d: slabT %.0f slabU %.0f fr %.0f data %.0f model %.0f heavy %.0f MiB "
+                     "(warps %u slots %u regions %u fr_bytes %zu)\n",
+                     j.wide, mb(P->slabT), mb(P->slabU), mb(P->fr_region), mb(P->data), mb(P->model),
+                     mb(P->heavy_list) + mb(P->heavy_t0), n_warps, j.slab_slots, j.fr_regions, fr_bytes);
     }
     j.staged = true;
     return "";
@@ -1706,7 +1722,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         CK(cudaMemsetAsync(P->heavy_count.p, 0, 16 * (1 + j.jit_cls.size()), s0));
         if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 8, s0));
         if (j.fr_regions) CK(cudaMemsetAsync(P->fr_map.p, 0, ((size_t)j.fr_regions + 31) / 32 * 4, s0));
-        if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->slab_map.p, 0, ((size_t)j.slab_slots + 31) / 32 * 4, s0));
+        if (j.a.slab_bitmap) CK(cudaMemsetAsync(P->slab_map.p, 0, ((size_t)j.slab_slots + 31) / 32 * 4, s0));
         if (j.a.timeline) CK(cudaMemsetAsync(j.a.timeline, 0, n * 32, s0));
         CK(cudaMemsetAsync(P->verdict.p, 0xFF, n, s0));
         CK(cudaMemcpyAsync(P->resume.p, P->resume_init.p, n * 4, cudaMemcpyDeviceToDevice, s0));
