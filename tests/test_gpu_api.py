@@ -105,3 +105,20 @@ def test_determinism_across_calls(gpu, golden):
     for k in ("verdict", "model", "nodes", "passes"):
         assert np.array_equal(a[k], b[k])
     assert all(int(a["verdict"][q]) == VCODE[r["verdict"]] for q, r in enumerate(recs))
+
+
+def test_every_model_row_is_written(gpu, golden):
+    """oob_solve_batch writes every row of the caller's model array: the Sat
+    models (packed on the device, include/scuba_oob.h) and zeros elsewhere --
+    the shim hands it an uninitialised buffer."""
+    for name in ("synth_c4", "crafted", "corpus_m1048576"):
+        recs = golden[name]
+        fb = flatten(recs)
+        out = _lib.solve_flat(fb, 30.0)
+        ref = oracle.solve_flat(fb, 30.0)
+        assert np.array_equal(out["verdict"], ref["verdict"]), name
+        assert np.array_equal(out["model"], ref["model"]), name  # oracle: zeros unless Sat
+        sat = out["verdict"] == 1
+        for q in np.flatnonzero(~sat)[:50]:
+            vb, ve = int(fb.var_begin[q]), int(fb.var_begin[q + 1])
+            assert not out["model"][vb:ve].any(), (name, q)
