@@ -1425,6 +1425,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
     // wide jobs: a frontier-only tail launch with a full grid serves their
     // heavy list once the int64 kernel has freed the SMs
+    const uint32_t own_warps = n_warps;  // slabs [0, own_warps): the interpreting kernel + class kernels
     j.tail_blocks = (j.wide && heavy_nodes) ? (uint32_t)(P->sms * per_sm) : 0u;
     n_warps += j.tail_blocks * WARPS_PER_BLOCK;
     j.fblocks = heavy_nodes ? (n_warps + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK : 0;
@@ -1572,13 +1573,23 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     if (j.tail_blocks) {
         j.tail_args = a;
         j.tail_args.frontier_only = 1;
+        if (!a.slab_bitmap) {  // one slab per warp: the tail's warps follow the job's own
+            j.tail_args.slab_T = (unsigned char*)P->slabT.p + (uint64_t)own_warps * j.g.slab_T_words * tbytes;
+            j.tail_args.slab_u32 = (uint32_t*)P->slabU.p + (uint64_t)own_warps * j.g.slab_u32_words;
+        }
 
     }
     // one launch per compiled class: its own class queue and heavy list (slabs
     // and frontier regions come from the job's pools)
+    uint64_t warp_base = (uint64_t)j.blocks * WARPS_PER_BLOCK;  // one slab per warp: per-launch ranges
     for (size_t i = 0; i < j.jit_cls.size(); i++) {
         const uint32_t c = j.jit_cls[i];
         LaunchArgs b = a;
+        if (!a.slab_bitmap) {
+            b.slab_T = (unsigned char*)P->slabT.p + warp_base * j.g.slab_T_words * tbytes;
+            b.slab_u32 = (uint32_t*)P->slabU.p + warp_base * j.g.slab_u32_words;
+            warp_base += (uint64_t)j.jit_blocks[i] * jit_warps();
+        }
         b.classes = (const ClassDesc*)P->classes.p + c;
         b.n_classes = 1;
         b.class_next = (uint32_t*)P->class_next.p + c;

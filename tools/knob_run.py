@@ -13,4 +13,8 @@ p = _lib.Plan(fb, 30.0, heavy_nodes=hn)
 for _ in range(3):
     p.run()
 ms = [p.run() for _ in range(8)]
-print(f"{cfg} {label:28s} median {statistics.median(ms):7.2f} ms  min {min(ms):7.2f}  {[round(x, 1) for x in ms]}", flush=True)
+r = p.results()
+import hashlib  # noqa: E402
+h = hashlib.sha1(r["verdict"].tobytes() + r["nodes"].tobytes() + r["passes"].tobytes()).hexdigest()[:10]
+print(f"{cfg} {label:28s} median {statistics.median(ms):7.2f} ms  min {min(ms):7.2f}  results {h}  "
+      f"{[round(x, 1) for x in ms]}", flush=True)
