@@ -1308,7 +1308,8 @@ uint32_t jit_smem() {
 constexpr uint32_t FR_ECAP = 2048, FR_UCAP = 4096, FR_LOGCAP = 32768;
 constexpr uint32_t HEAVY_NODES_DEFAULT = 16;
 // long propagation chains leave the shared lockstep warps (B200 A/B, two
-// repeats, median plan run: 256 -> 192 passes C3 -3%, C4 -2.5%, C5s -11%)
+// repeats, identical results, median plan run: 256 -> 192 passes C3 -2%,
+// C4 -2%, C5s -4%)
 constexpr uint32_t HEAVY_PASSES_DEFAULT = 192;
 
 size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
@@ -1443,7 +1444,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     // warp (phases.cuh claim_slab; at most 64 warps per SM are resident, so no
     // warp ever waits for one)
     // SCUBA_OOB_SLAB_POOL=1: slabs from the job pool (saves ~2 GB per plan on
-    // C3, but measured 5-15% slower on C4/C5s than one slab per warp -- off)
+    // C3, measured equal to 5% slower than one slab per warp -- off)
     static const bool slab_pool = [] {
         const char* e = std::getenv("SCUBA_OOB_SLAB_POOL");
         return e && *e == '1';
