@@ -1122,16 +1122,31 @@ struct DevJob {
 };
 
 void pack(const RunCtx& rc, DevJob& j) {
+    const auto pack_t0 = std::chrono::steady_clock::now();
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
     // group the job's entries (own queries, then shadows) by structure class
     // (batch-wide ids from prepare), keeping their order within a class (the
     // lockstep kernel runs each warp on one class)
-    std::vector<int64_t> entries(j.qs);  // query id, or ~id for a shadow
+    // scratch reused across calls (per thread): fresh vectors of this size
+    // would be page-faulted in on every call
+    // (local references: thread_local names inside the parallel lambdas below
+    // would resolve to the worker threads' own instances)
+    static thread_local std::vector<int64_t> tl_entries, tl_order;
+    static thread_local std::vector<uint32_t> tl_cls, tl_ocls;
+    static thread_local std::vector<uint64_t> tl_doff, tl_moff;
+    std::vector<int64_t>& entries = tl_entries;
+    std::vector<int64_t>& order = tl_order;
+    std::vector<uint32_t>& cls = tl_cls;
+    std::vector<uint32_t>& ocls = tl_ocls;
+    std::vector<uint64_t>& doff = tl_doff;
+    std::vector<uint64_t>& moff = tl_moff;
+    entries.assign(j.qs.begin(), j.qs.end());  // query id, or ~id for a shadow
+    entries.reserve(j.qs.size() + j.shadows.size());
     for (int64_t q : j.shadows) entries.push_back(~q);
     auto qid = [](int64_t e) { return e < 0 ? ~e : e; };
     std::unordered_map<uint32_t, uint32_t> local;
-    std::vector<uint32_t> cls(entries.size());
+    cls.resize(entries.size());
     std::vector<size_t> rep;
     uint32_t last_g = UINT32_MAX, last_l = 0;  // entries arrive in class runs
     const std::vector<uint32_t>& qcls = *rc.qcls;  // 4 bytes per query: cache-resident, unlike comp[]
@@ -1150,8 +1165,8 @@ void pack(const RunCtx& rc, DevJob& j) {
     for (uint32_t c : cls) count[c + 1]++;
     for (size_t c = 0; c < nc; c++) count[c + 1] += count[c];
     const size_t n = entries.size();
-    std::vector<int64_t> order(n);
-    std::vector<uint32_t> ocls(n);
+    order.resize(n);
+    ocls.resize(n);
     {
         std::vector<uint32_t> at(count.begin(), count.end() - 1);
         for (size_t i = 0; i < n; i++) {
@@ -1189,7 +1204,8 @@ void pack(const RunCtx& rc, DevJob& j) {
     const size_t vw = tb >= 8 ? tb / 8 : 1;  // int64 words per value (x32 entries are shadows only)
     const size_t align = j.wide == 2 ? 4 : 2;
     // every entry of a class has the same data size: offsets per class run
-    std::vector<uint64_t> doff(n + 1, 0), moff(n + 1, 0);
+    doff.assign(n + 1, 0);
+    moff.assign(n + 1, 0);
     for (size_t id = 0; id < nc; id++) {
         const Compiled& c = comp[qid(entries[rep[id]])];
         const uint64_t words = ((2 * (uint64_t)c.nv + c.nlit) * tb + 7) / 8;
@@ -1200,6 +1216,9 @@ void pack(const RunCtx& rc, DevJob& j) {
         }
     }
     j.model_words = moff[n];
+    if (trace_level() >= 2)
+        std::fprintf(stderr, "[oob]   pack w%d: %zu entries, %zu classes, serial part %.3f ms\n", j.wide, n, nc,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pack_t0).count());
     j.data.alloc(std::max<uint64_t>(doff[n], 4));
     parallel_for(n, 4096, [&](size_t lo, size_t hi) {
         for (size_t i = lo; i < hi; i++) {
@@ -1970,10 +1989,36 @@ std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
         if (cur[0].empty() && cur[1].empty() && cur[2].empty()) return "";
         DevGroup G;
         G.dev = dev;
+        // per-entry host vectors recycled per thread (see drive)
+        struct JobScratch {
+            std::vector<int64_t> qs, shadows;
+            std::vector<uint8_t> is_shadow;
+            std::vector<uint32_t> resume_init, slot[3];
+            std::vector<uint64_t> mo;
+        };
+        static thread_local JobScratch tl_js[NJOBS];
+        auto swap_scratch = [&]() {
+            for (int w = 0; w < NJOBS; w++) {
+                DevJob& j = G.job[w];
+                JobScratch& x = tl_js[w];
+                j.qs.swap(x.qs);
+                j.shadows.swap(x.shadows);
+                j.is_shadow.swap(x.is_shadow);
+                j.resume_init.swap(x.resume_init);
+                j.mo.swap(x.mo);
+                for (int t = 0; t < 3; t++) j.slot[t].swap(x.slot[t]);
+            }
+        };
+        swap_scratch();
         for (int w = 0; w < NJOBS; w++) {
-            G.job[w].qs = w < 3 ? cur[w] : std::vector<int64_t>();
+            if (w < 3) G.job[w].qs.assign(cur[w].begin(), cur[w].end());
+            else G.job[w].qs.clear();
             G.pool[w] = pools[w];
         }
+        struct SwapBack {
+            std::function<void()> f;
+            ~SwapBack() { f(); }
+        } swap_back{swap_scratch};
         std::vector<int64_t> retry[3];
         {
             std::lock_guard<std::mutex> l0(pools[0]->mu), l1(pools[1]->mu), l2(pools[2]->mu), l3(pools[3]->mu);
@@ -2242,9 +2287,26 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
                 std::memset((void*)(model_out + v0 + lo), 0, (hi - lo) * sizeof(oob_i128));
             });
     }
+    // the per-query vectors of a call are recycled per thread (fresh 10+ MB
+    // vectors would be page-faulted in on every call)
+    static thread_local std::vector<Compiled> tl_comp;
+    static thread_local std::vector<uint32_t> tl_qcls;
+    static thread_local std::vector<int8_t> tl_errs;
     Prepared pr;
+    pr.comp.swap(tl_comp);
+    pr.qcls.swap(tl_qcls);
+    pr.errs.swap(tl_errs);
+    auto recycle = [&]() {
+        pr.comp.clear();
+        pr.comp.swap(tl_comp);
+        pr.qcls.swap(tl_qcls);
+        pr.errs.swap(tl_errs);
+    };
     int rc0 = prepare(b, opt_in, mode, model_in, verdict, nodes, passes, elapsed, pr);
-    if (rc0 != OOB_OK) return rc0;
+    if (rc0 != OOB_OK) {
+        recycle();
+        return rc0;
+    }
     RunCtx rc;
     rc.b = b;
     rc.opt = pr.opt;
@@ -2258,10 +2320,14 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
     rc.elapsed = elapsed;
     rc.errs = &pr.errs;
     std::string e = run_all(rc, pr.work);
-    if (!e.empty()) return fail(OOB_E_CUDA, e);
+    if (!e.empty()) {
+        recycle();
+        return fail(OOB_E_CUDA, e);
+    }
     int rcode = finish(pr, b->n_queries);
     {
         Phase ph("teardown");
+        recycle();
         Prepared gone(std::move(pr));
     }
     return rcode;
