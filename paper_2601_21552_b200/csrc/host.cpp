@@ -1121,7 +1121,7 @@ struct DevJob {
     }
 };
 
-void pack(const RunCtx& rc, DevJob& j) {
+void pack(const RunCtx& rc, DevJob& j, bool inline_fill = false) {
     const auto pack_t0 = std::chrono::steady_clock::now();
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
@@ -1220,7 +1220,7 @@ void pack(const RunCtx& rc, DevJob& j) {
         std::fprintf(stderr, "[oob]   pack w%d: %zu entries, %zu classes, serial part %.3f ms\n", j.wide, n, nc,
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pack_t0).count());
     j.data.alloc(std::max<uint64_t>(doff[n], 4));
-    parallel_for(n, 4096, [&](size_t lo, size_t hi) {
+    auto fill = [&](size_t lo, size_t hi) {
         for (size_t i = lo; i < hi; i++) {
             const int64_t e = order[i];
             const int64_t q = qid(e);
@@ -1262,7 +1262,9 @@ void pack(const RunCtx& rc, DevJob& j) {
             for (uint32_t i = 0; i < c.nlit; i++) put(lit_value(b, q, *c.st, i));
             std::fill(out, end, 0);
         }
-    });
+    };
+    if (inline_fill) fill(0, n);
+    else parallel_for(n, 4096, fill);
     if (n == 0) std::fill(j.data.data(), j.data.data() + j.data.size(), 0);
     if (j.code.empty()) j.code.push_back(0);
     if (j.cls.empty()) j.cls.push_back(ClassDesc{});
@@ -1679,14 +1681,30 @@ void pack_group(const RunCtx& rc, DevGroup& G, bool upload = false) {
     for (int w = 0; w < NJOBS; w++) {
         G.job[w].data_uploaded = false;
         G.job[w].upload_err.clear();
-        if (!G.job[w].qs.empty() || !G.job[w].shadows.empty()) {
-            Phase ph(pk_names[w]);
-            pack(rc, G.job[w]);
-            // (the x32 job's records are written on the device: no upload)
-            if (upload && G.pool[w] && !(w == W_X32 && rc.mode == MODE_SOLVE))
-                G.job[w].upload_err = upload_data(G.job[w], G.pool[w]);
-        }
     }
+    auto has = [&](int w) { return !G.job[w].qs.empty() || !G.job[w].shadows.empty(); };
+    // the x32 job (shadows only: descriptors, no record data) is packed on a
+    // thread of its own, its per-entry loop inline, while this thread packs
+    // the other jobs with the host pool
+    std::thread x32_thread;
+    if (has(W_X32) && host_threads() > 2)
+        x32_thread = std::thread([&]() { pack(rc, G.job[W_X32], true); });
+    else if (has(W_X32)) {
+        Phase ph(pk_names[W_X32]);
+        pack(rc, G.job[W_X32]);
+    }
+    for (int w = 0; w < 3; w++) {
+        if (!has(w)) continue;
+        Phase ph(pk_names[w]);
+        pack(rc, G.job[w]);
+        if (upload && G.pool[w]) G.job[w].upload_err = upload_data(G.job[w], G.pool[w]);
+    }
+    if (x32_thread.joinable()) {
+        Phase ph("pack.x32.join");
+        x32_thread.join();
+    }
+    if (upload && G.pool[W_X32] && has(W_X32) && rc.mode != MODE_SOLVE)
+        G.job[W_X32].upload_err = upload_data(G.job[W_X32], G.pool[W_X32]);
     Phase ph_slots("pack.slots");
     if (!demote_on(rc)) return;
     // demotion slots: target t (0 int64, 1 int128, 2 x32 = job 3) of the jobs that hand down to it
