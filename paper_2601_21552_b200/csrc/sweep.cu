@@ -230,8 +230,8 @@ int drive(const oob_sweep_program* pr, Dev D, int64_t n_out_tuples, const int64_
           uint8_t* labels) {
     const int dev = opt ? opt->device : 0;
     SCK(cudaSetDevice(dev));
-    cudaDeviceProp prop;
-    SCK(cudaGetDeviceProperties(&prop, dev));
+    int sms = 0;  // (cudaGetDeviceProperties costs milliseconds per call)
+    SCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int ns = std::max(pr->n_sites, 1);
 
     SweepPool& pool = pool_of(dev);
@@ -272,11 +272,11 @@ int drive(const oob_sweep_program* pr, Dev D, int64_t n_out_tuples, const int64_
     D.t_aux = (int32_t*)taux.p;
     D.t_labels = (uint8_t*)tlab.p;
 
-    int occ = 0;
-    SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oob_sweep_kernel, BLOCK, 0));
+    static int occ = 0;  // the same kernel and block on every device of the box
+    if (!occ) SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oob_sweep_kernel, BLOCK, 0));
     occ = std::max(occ, 1);
     int64_t want_blocks = (D.total + BLOCK - 1) / BLOCK;
-    int64_t blocks = std::min<int64_t>(want_blocks, (int64_t)prop.multiProcessorCount * occ);
+    int64_t blocks = std::min<int64_t>(want_blocks, (int64_t)sms * occ);
     if (opt && opt->max_threads > 0) blocks = std::min<int64_t>(blocks, std::max<int64_t>(opt->max_threads / BLOCK, 1));
     blocks = std::max<int64_t>(blocks, 1);
     int64_t words = (opt && opt->arena_words > 0) ? opt->arena_words : 512;
