@@ -1414,15 +1414,28 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     assign_warps(j, j.cls_interp, n_warps);
     for (size_t i = 0; i < j.jit_cls.size(); i++) {
         const ClassDesc& cd = j.cls[j.jit_cls[i]];
-        int occ = 0;
         const uint32_t jw = jit_warps();
-        if (jit_smem())
-            cudaFuncSetAttribute(j.jit_fn[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jit_smem());
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, j.jit_fn[i], jw * 32, jit_smem()) != cudaSuccess) {
-            cudaGetLastError();
-            occ = 4;
+        // resident blocks of a compiled class kernel: computed once per loaded
+        // function (the block shape and shared memory never change)
+        static std::mutex occ_mu;
+        static std::unordered_map<const void*, int> occ_of;
+        int occ = 0;
+        {
+            std::lock_guard<std::mutex> lk(occ_mu);
+            auto it = occ_of.find(j.jit_fn[i]);
+            if (it != occ_of.end()) occ = it->second;
         }
-        occ = std::max(1, occ);
+        if (!occ) {
+            if (jit_smem())
+                cudaFuncSetAttribute(j.jit_fn[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jit_smem());
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, j.jit_fn[i], jw * 32, jit_smem()) != cudaSuccess) {
+                cudaGetLastError();
+                occ = 4;
+            }
+            occ = std::max(1, occ);
+            std::lock_guard<std::mutex> lk(occ_mu);
+            occ_of[j.jit_fn[i]] = occ;
+        }
         // warps: one per 32 queries of the class, times SCUBA_OOB_JIT_GRID_MULT
         // (extra blocks start as others finish and serve the class's heavy list;
         // measured on B200, median plan run: x1 -> x3 = C3 14.7 -> 13.0 ms,
