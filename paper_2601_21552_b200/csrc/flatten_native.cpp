@@ -135,6 +135,16 @@ class Query {
     ~Query() {
         Py_XDECREF(index_);
         Py_XDECREF(names_);
+        release_bad();
+    }
+    void release_bad() {
+        for (PyObject* b : bad_lo_) Py_XDECREF(b);
+        for (PyObject* b : bad_hi_) Py_XDECREF(b);
+        bad_lo_.clear();
+        bad_hi_.clear();
+        Py_XDECREF(e_blo);
+        Py_XDECREF(e_bhi);
+        e_blo = e_bhi = nullptr;
     }
 
     bool add(PyObject* variables, PyObject* constraints) {
@@ -144,6 +154,7 @@ class Query {
         index_ = PyDict_New();
         names_ = PyList_New(0);
         if (!index_ || !names_) return false;
+        release_bad();
         lo_.clear();
         hi_.clear();
         nodes_.clear();
@@ -160,10 +171,12 @@ class Query {
         for (Py_ssize_t k = 0; k < nc && ok; k++) ok = add_con(PySequence_Fast_GET_ITEM(seq, k));
         Py_DECREF(seq);
         if (!ok) return false;
-        // append
+        // append (finish() range-checks the stored values: var_lo, var_hi, lits)
         for (size_t i = 0; i < lo_.size(); i++) {
             o_.var_lo.push_back(lo_[i]);
             o_.var_hi.push_back(hi_[i]);
+            if (bad_lo_[i]) note_bad(0, bad_lo_[i]);
+            if (bad_hi_[i]) note_bad(1, bad_hi_[i]);
         }
         o_.var_begin.push_back(o_.var_begin.back() + (int64_t)lo_.size());
         o_.con_begin.push_back((int64_t)o_.con_rel.size());
@@ -189,6 +202,13 @@ class Query {
     PyObject* index_ = nullptr;  // name -> position
     PyObject* names_ = nullptr;
     std::vector<i128> lo_, hi_;
+    std::vector<PyObject*> bad_lo_, bad_hi_;  // stored out-of-range values (or null)
+    PyObject *e_blo = nullptr, *e_bhi = nullptr;
+    static int sign_of(PyObject* big) {  // sign of an int beyond the long long range
+        int ovf = 0;
+        PyLong_AsLongLongAndOverflow(big, &ovf);
+        return ovf;
+    }
     std::unordered_map<uint64_t, int32_t, KeyHash> nodes_;
     std::unordered_map<i128, int32_t, LitHash> lit_index_;
     std::vector<uint8_t> n_op_;
@@ -202,14 +222,25 @@ class Query {
         }
     }
 
-    bool int_field(PyObject* raw, int arr, i128* out) {  // int(x), range-checked later
+    // int(x); an out-of-range value is kept (*bad, new reference) for the
+    // range check of the stored values, which happens after the whole batch
+    bool int_field(PyObject* raw, i128* out, PyObject** bad) {
+        *bad = nullptr;
         PyObject* v = PyNumber_Long(raw);
         if (!v) return false;
         bool oor;
         bool ok = to_i128(v, out, &oor);
-        if (ok && oor) note_bad(arr, v);
+        if (ok && oor) {
+            *bad = v;
+            return true;
+        }
         Py_DECREF(v);
         return ok;
+    }
+    static void set_ref(PyObject*& slot, PyObject* v) {
+        Py_XINCREF(v);
+        Py_XDECREF(slot);
+        slot = v;
     }
 
     bool add_vars(PyObject* variables) {
@@ -238,22 +269,35 @@ class Query {
             }
             PyObject* name = (rn && rlo && rhi) ? PyObject_Str(rn) : nullptr;
             i128 lo = 0, hi = 0;
-            ok = name && int_field(rlo, 0, &lo) && int_field(rhi, 1, &hi);
+            PyObject *blo = nullptr, *bhi = nullptr;
+            ok = name && int_field(rlo, &lo, &blo) && int_field(rhi, &hi, &bhi);
             Py_XDECREF(rn);
             Py_XDECREF(rlo);
             Py_XDECREF(rhi);
             if (ok) {
-                if (lo > hi && !have_empty) {
+                // lo > hi with Python ints: a value beyond int128 is past every
+                // in-range value on its side
+                int empty;
+                if (blo && bhi) empty = PyObject_RichCompareBool(blo, bhi, Py_GT);
+                else if (blo) empty = sign_of(blo) > 0;
+                else if (bhi) empty = sign_of(bhi) < 0;
+                else empty = lo > hi;
+                if (empty < 0) ok = false;
+                if (ok && empty && !have_empty) {
                     have_empty = true;
                     e_lo = lo;
                     e_hi = hi;
+                    set_ref(e_blo, blo);
+                    set_ref(e_bhi, bhi);
                 }
-                PyObject* at = PyDict_GetItemWithError(index_, name);
+                PyObject* at = ok ? PyDict_GetItemWithError(index_, name) : nullptr;
                 if (at) {  // last declaration wins, first position kept
                     const Py_ssize_t k = PyLong_AsSsize_t(at);
                     lo_[k] = lo;
                     hi_[k] = hi;
-                } else if (PyErr_Occurred()) {
+                    set_ref(bad_lo_[k], blo);
+                    set_ref(bad_hi_[k], bhi);
+                } else if (!ok || PyErr_Occurred()) {
                     ok = false;
                 } else {
                     PyObject* pos = PyLong_FromSsize_t((Py_ssize_t)lo_.size());
@@ -261,14 +305,22 @@ class Query {
                     Py_XDECREF(pos);
                     lo_.push_back(lo);
                     hi_.push_back(hi);
+                    bad_lo_.push_back(nullptr);
+                    bad_hi_.push_back(nullptr);
+                    set_ref(bad_lo_.back(), blo);
+                    set_ref(bad_hi_.back(), bhi);
                 }
             }
+            Py_XDECREF(blo);
+            Py_XDECREF(bhi);
             Py_XDECREF(name);
         }
         Py_DECREF(seq);
         if (ok && have_empty) {  // Unsat before search (solver.py:374)
             lo_[0] = e_lo;
             hi_[0] = e_hi;
+            set_ref(bad_lo_[0], e_blo);
+            set_ref(bad_hi_[0], e_bhi);
         }
         return ok;
     }

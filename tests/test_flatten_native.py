@@ -79,3 +79,20 @@ def test_native_errors_match(bad, exc):
             fn([bad])
         if exc is KeyError:
             assert e.value.args == ("y",)
+
+
+@pytest.mark.parametrize("case", [
+    # an out-of-range bound overwritten by a later declaration is not stored
+    [q([("x", 0, 1 << 130), ("y", 0, 1), ("x", 0, 9)], [Constraint("<", x, y)])],
+    # an out-of-range empty declaration is stored into slot 0 (then overflows)
+    [q([("x", 0, 9), ("y", 1 << 130, 0)], [Constraint("<", x, y)])],
+    [q([("x", 0, 9), ("y", 5, -(1 << 130))], [Constraint("<", x, y)])],
+])
+def test_native_range_check_follows_stored_values(case):
+    def outcome(fn):
+        try:
+            fb = fn(case)
+            return ("ok", fb.var_lo.tolist(), fb.var_hi.tolist())
+        except OverflowError as e:
+            return ("overflow", str(e))
+    assert outcome(wire.flatten) == outcome(wire.flatten_py)
