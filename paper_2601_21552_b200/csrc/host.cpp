@@ -1371,7 +1371,12 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     j.cls_interp = j.cls;
     // compiled classes: the x32 job and the int64 job (queries the root phase
     // could not move to x32 -- long root propagations -- stay there)
-    if ((j.wide == 0 || j.wide == W_X32) && rc.mode == MODE_SOLVE && !(rc.opt.flags & OOB_F_NO_JIT)) {
+    static const bool jit128 = [] {  // SCUBA_OOB_JIT128=0: int128 classes stay on the interpreter
+        const char* e = std::getenv("SCUBA_OOB_JIT128");
+        return !(e && *e == '0');
+    }();
+    if ((j.wide == 0 || j.wide == W_X32 || (j.wide == 1 && jit128)) && rc.mode == MODE_SOLVE &&
+        !(rc.opt.flags & OOB_F_NO_JIT)) {
         const std::vector<Compiled>& comp = *rc.comp;
         std::vector<JitClass> want;
         for (uint32_t c = 0; c < j.n_classes; c++) {
@@ -1384,7 +1389,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
                 continue;
             j.jit_cls.push_back(c);
             want.push_back(JitClass{j.code.data() + cd.code_off, rep.nv, rep.ncon, rep.ncode, rep.nlit,
-                                    j.wide == W_X32 ? 32 : 64});
+                                    j.wide == W_X32 ? 32 : (j.wide == 1 ? 128 : 64)});
         }
         if (!want.empty()) {
             std::vector<int> regs;
@@ -2478,7 +2483,7 @@ int oob_jit_compile(const oob_batch* b, int64_t q, char* src, int64_t src_cap, d
     if (!why.empty()) return fail(OOB_E_INVALID, why);
     Compiled c = compile_query(b, q, MODE_SOLVE, 30.0, nullptr);
     if (c.regime == R_IMMEDIATE || c.regime == R_RANGE) return fail(OOB_E_INVALID, "query has no search");
-    JitClass jc{c.words().data(), c.nv, c.ncon, c.ncode, c.nlit};
+    JitClass jc{c.words().data(), c.nv, c.ncon, c.ncode, c.nlit, c.regime == R_W128 ? 128 : 64};
     std::string text = jit_source(jc);
     if (src && src_cap > 0) {
         size_t n = std::min<size_t>(text.size(), (size_t)src_cap - 1);

@@ -296,7 +296,8 @@ struct Gen {
 
     std::string source(const std::string& kname) {
         o << "#include \"jit_lane.cuh\"\nnamespace oob {\nstruct Cls {\n";
-        o << "  typedef " << (bits == 32 ? "int" : "long long") << " T;\n  typedef Arith<T> A;\n  typedef Ext<T> X;\n";
+        o << "  typedef " << (bits == 32 ? "int" : (bits == 128 ? "__int128" : "long long"))
+          << " T;\n  typedef Arith<T> A;\n  typedef Ext<T> X;\n";
         o << "  static constexpr uint32_t NV = " << nv << ", NCON = " << ncon << ", NCODE = " << ncode
           << ", NLIT = " << nlit << ";\n";
         for (int half = 0; half < 2; half++) {

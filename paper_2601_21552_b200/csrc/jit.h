@@ -12,7 +12,7 @@ namespace oob {
 struct JitClass {
     const uint32_t* words;
     uint32_t nv, ncon, ncode, nlit;
-    int bits = 64;  // value type: 64 = int64 regime, 32 = x32 regime (engine.cuh Ext<int>)
+    int bits = 64;  // value type: 64 = int64 regime, 32 = x32 regime (engine.cuh Ext<int>), 128 = int128
 };
 
 // Compiles (or finds in the process-wide cache) every class and returns the

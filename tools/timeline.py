@@ -36,3 +36,8 @@ order = np.argsort(-d)[:12]
 print("longest (ms from own start): q wide heavy nodes passes dur start")
 for i in order:
     print(f"  {q[i]:7d} {wide[i]} {int(heavy[i])} {nodes[i]:6d} {passes[i]:6d} {d[i]:7.2f} {ms(np.where(heavy, tf, t0)[i]):7.2f}")
+order = np.argsort(-te)[:12]
+print("last to finish: q wide shadow heavy nodes passes end_ms frontier_start_ms")
+for i in order:
+    print(f"  {q[i]:7d} {wide[i]} {shadow[i]} {int(heavy[i])} {nodes[i]:6d} {passes[i]:6d} {ms(te[i]):7.2f} "
+          f"{ms(tf[i]) if tf[i] > 0 else -1:7.2f}")
