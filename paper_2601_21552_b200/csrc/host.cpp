@@ -1371,9 +1371,12 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     j.cls_interp = j.cls;
     // compiled classes: the x32 job and the int64 job (queries the root phase
     // could not move to x32 -- long root propagations -- stay there)
-    static const bool jit128 = [] {  // SCUBA_OOB_JIT128=0: int128 classes stay on the interpreter
+    // SCUBA_OOB_JIT128=1: int128-job classes compiled too (parity-exact; A/B on
+    // B200 neutral on C3/C4/C5s while adding ~10 s of NVRTC per class on a
+    // cold cache -- off)
+    static const bool jit128 = [] {
         const char* e = std::getenv("SCUBA_OOB_JIT128");
-        return !(e && *e == '0');
+        return e && *e == '1';
     }();
     if ((j.wide == 0 || j.wide == W_X32 || (j.wide == 1 && jit128)) && rc.mode == MODE_SOLVE &&
         !(rc.opt.flags & OOB_F_NO_JIT)) {
