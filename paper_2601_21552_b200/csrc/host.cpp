@@ -1382,7 +1382,23 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         !(rc.opt.flags & OOB_F_NO_JIT)) {
         const std::vector<Compiled>& comp = *rc.comp;
         std::vector<JitClass> want;
-        for (uint32_t c = 0; c < j.n_classes; c++) {
+        // launch order = start order on the shared streams: class id, or
+        // (SCUBA_OOB_JIT_ORDER=1) the classes with the most estimated work
+        // (queries x domain bits) first -- A/B on B200: C3/C4 equal, C5s 10%
+        // slower, so off
+        static const bool by_work = [] {
+            const char* e = std::getenv("SCUBA_OOB_JIT_ORDER");
+            return e && *e == '1';
+        }();
+        std::vector<uint32_t> corder(j.n_classes);
+        for (uint32_t c = 0; c < j.n_classes; c++) corder[c] = c;
+        if (by_work) {
+            std::vector<double> work(j.n_classes, 0.0);
+            for (uint32_t c = 0; c < j.n_classes; c++)
+                for (uint32_t i = j.cls[c].q_begin; i < j.cls[c].q_end; i++) work[c] += 1.0 + comp[j.qs[i]].cost;
+            std::stable_sort(corder.begin(), corder.end(), [&](uint32_t a, uint32_t b) { return work[a] > work[b]; });
+        }
+        for (uint32_t c : corder) {
             const ClassDesc& cd = j.cls[c];
             const uint64_t size = cd.q_end - cd.q_begin;
             const Compiled& rep = comp[j.qs[cd.q_begin]];
