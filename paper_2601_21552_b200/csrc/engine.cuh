@@ -631,8 +631,18 @@ struct Lane {
     }
 
     // stage a query's domains and literal slots into lane-minor scratch
-    __device__ __forceinline__ void load(const LaunchArgs& a, const QDesc& d) {
-        const T* src = reinterpret_cast<const T*>(a.data + d.data_off);
+    __device__ __forceinline__ void load(const LaunchArgs& a, const QDesc& d) { load_from(a.data, d); }
+    // current domains + literals in the job's data layout (hand-off at the root)
+    __device__ __forceinline__ void save_state(int64_t* base, const QDesc& d) const {
+        T* dst = reinterpret_cast<T*>(base + d.data_off);
+        for (uint32_t v = 0; v < nv; ++v) {
+            dst[2 * v] = E(env_lo, v);
+            dst[2 * v + 1] = E(env_hi, v);
+        }
+        for (uint32_t i = 0; i < nlit; ++i) dst[2 * nv + i] = E(lit, i);
+    }
+    __device__ __forceinline__ void load_from(const int64_t* base, const QDesc& d) {
+        const T* src = reinterpret_cast<const T*>(base + d.data_off);
         for (uint32_t v = 0; v < nv; ++v) {
             E(env_lo, v) = src[2 * v];
             E(env_hi, v) = src[2 * v + 1];

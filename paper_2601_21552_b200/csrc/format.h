@@ -103,7 +103,10 @@ static_assert(sizeof(ClassDesc) == 32, "ClassDesc is two int4 words");
 constexpr uint32_t RES_SKIP = 0xFFFFFFFFu;
 constexpr uint32_t RES_ROOT = 0x80000000u;
 constexpr uint32_t RES_FIX = 0x40000000u;
-constexpr uint32_t RES_PASSES = 0x3FFFFFFFu;
+// the root state comes from the hand-off buffer (LaunchArgs::handoff): a query
+// handed to the frontier while still at its root node resumes there
+constexpr uint32_t RES_HANDOFF = 0x20000000u;
+constexpr uint32_t RES_PASSES = 0x1FFFFFFFu;
 constexpr uint32_t ROOT_MAX_PASSES = 64;      // wide root phases: pass budget before giving up on demotion
 constexpr uint32_t ROOT_MAX_PASSES_X32 = 16;  // int64 root phase (x32 probe)
 
@@ -150,6 +153,9 @@ struct LaunchArgs {
     // job's launches, one held per running warp (null: slab index = warp id)
     uint32_t* slab_bitmap;
     uint32_t slab_nslots;
+    // root state of queries handed off at their root node (data layout, at
+    // QDesc::data_off; null: hand-offs restart from the declared domains)
+    int64_t* handoff;
     // outputs (indexed by QDesc::out_q / out_v)
     int8_t* verdict;
     int64_t* model;           // int128 words, 2 per var

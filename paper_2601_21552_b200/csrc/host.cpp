@@ -939,6 +939,7 @@ struct DevicePool {
     DevBuf satcnt, satoff, compact;  // SOLVE fetch: packed Sat models
     DevBuf fr_map;                   // frontier region pool: held bits
     DevBuf slab_map;                 // slab pool (SOLVE kernels): held bits
+    DevBuf handoff;                  // root states of queries handed off at their root
     std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
     std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
@@ -948,7 +949,7 @@ struct DevicePool {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
                           &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &slotx32, &timeline,
-                          &classes_interp, &stats, &satcnt, &satoff, &compact, &fr_map, &slab_map})
+                          &classes_interp, &stats, &satcnt, &satoff, &compact, &fr_map, &slab_map, &handoff})
             b->release();
     }
 };
@@ -1601,6 +1602,17 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.fr_nregions = j.fr_regions;
     a.slab_bitmap = pooled ? (uint32_t*)P->slab_map.p : nullptr;
     a.slab_nslots = j.slab_slots;
+    // hand-offs at the root resume in the frontier (SCUBA_OOB_HANDOFF_RESUME=0:
+    // they restart from the declared domains, as before)
+    static const bool handoff_resume = [] {
+        const char* e = std::getenv("SCUBA_OOB_HANDOFF_RESUME");
+        return !(e && *e == '0');
+    }();
+    a.handoff = nullptr;
+    if (rc.mode == MODE_SOLVE && heavy_nodes && handoff_resume) {
+        CK(P->handoff.ensure(j.data.size() * 8));
+        a.handoff = (int64_t*)P->handoff.p;
+    }
     a.fr_ecap = FR_ECAP;
     a.fr_ucap = FR_UCAP;
     a.fr_logcap = FR_LOGCAP;

@@ -65,8 +65,19 @@ struct JitLane {
         changed = dirty = false;
     }
     __device__ __forceinline__ void set_class(const LaunchArgs&, const ClassDesc&) {}
-    __device__ __forceinline__ void load(const LaunchArgs& a, const QDesc& d) {
-        const T* src = reinterpret_cast<const T*>(a.data + d.data_off);
+    __device__ __forceinline__ void load(const LaunchArgs& a, const QDesc& d) { load_from(a.data, d); }
+    __device__ __forceinline__ void save_state(int64_t* base, const QDesc& d) const {
+        T* dst = reinterpret_cast<T*>(base + d.data_off);
+#pragma unroll
+        for (uint32_t v = 0; v < NV; ++v) {
+            dst[2 * v] = lo[v];
+            dst[2 * v + 1] = hi[v];
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < C::NLIT; ++i) dst[2 * NV + i] = lit[i];
+    }
+    __device__ __forceinline__ void load_from(const int64_t* base, const QDesc& d) {
+        const T* src = reinterpret_cast<const T*>(base + d.data_off);
 #pragma unroll
         for (uint32_t v = 0; v < NV; ++v) {
             lo[v] = src[2 * v];

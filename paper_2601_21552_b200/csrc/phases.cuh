@@ -94,6 +94,13 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
             // from the root in a warp of its own (so a long chain no longer
             // shares its warp's steps with 31 other queries); the list entry
             // is published after the start time it carries
+            if (phase == PH_PASS && nodes == 1 && a.handoff) {
+                // still at the root node, between two passes (the last one
+                // changed something): the frontier resumes here instead of
+                // redoing these passes (the same resume as regime demotion)
+                L.save_state(a.handoff, a.qdesc[qi]);
+                a.resume[qi] = RES_ROOT | RES_HANDOFF | passes;
+            }
             uint32_t slot = atomicAdd(a.heavy_count, 1u);
             a.heavy_t0[qi] = t0;
             if (a.timeline) a.timeline[4 * (size_t)qi + 1] = global_ns();
@@ -295,7 +302,9 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
         cd.nv_ncon = d.nv_ncon;
         cd.ncode_nlit = d.ncode_nlit;
         L.set_class(a, cd);
-        L.load(a, d);
+        const uint32_t rs0 = a.resume ? a.resume[qi] : 0u;
+        if ((rs0 & RES_HANDOFF) && a.handoff) L.load_from(a.handoff, d);
+        else L.load(a, d);
         // a scratch region of the job's pool, held for this query only (every
         // query re-initialises what it uses); a waiter always gets one in the
         // end because holders release theirs without waiting on anything
