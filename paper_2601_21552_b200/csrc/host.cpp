@@ -1328,7 +1328,9 @@ uint32_t jit_smem() {
 
 // allocate + upload the packed records of `j` into pool P (caller holds P->mu)
 constexpr uint32_t FR_ECAP = 2048, FR_UCAP = 4096, FR_LOGCAP = 32768;
-constexpr uint32_t HEAVY_NODES_DEFAULT = 16;
+// (B200 A/B with the root hand-off resume, identical results: 16 -> 24 nodes
+// C3 -9%, C4 -3%, C5s neutral)
+constexpr uint32_t HEAVY_NODES_DEFAULT = 24;
 // long propagation chains leave the shared lockstep warps (B200 A/B, two
 // repeats, identical results, median plan run: 256 -> 192 passes C3 -2%,
 // C4 -2%, C5s -4%)
