@@ -1333,8 +1333,9 @@ constexpr uint32_t FR_ECAP = 2048, FR_UCAP = 4096, FR_LOGCAP = 32768;
 constexpr uint32_t HEAVY_NODES_DEFAULT = 24;
 // long propagation chains leave the shared lockstep warps (B200 A/B, two
 // repeats, identical results, median plan run: 256 -> 192 passes C3 -2%,
-// C4 -2%, C5s -4%)
-constexpr uint32_t HEAVY_PASSES_DEFAULT = 192;
+// C4 -2%, C5s -4%; with the root hand-off resume and 24-node hand-off,
+// 192 -> 128: C3 -7%, C4 +0.5%, C5s neutral)
+constexpr uint32_t HEAVY_PASSES_DEFAULT = 128;
 
 size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
     size_t b = (size_t)FR_ECAP * 2 * maxv * tbytes + 2 * (size_t)FR_ECAP * tbytes + (size_t)FR_ECAP * 16 +
