@@ -19,7 +19,16 @@ independent).
           in one batch (wall time, verdicts vs the golden capture).
   cpu_baseline / --impl reference
           the C restatement of the reference solver (oracle/, kind "port") on
-          the host cores, on a bounded sample of the same stream.
+          the host cores, on a bounded sample of the same stream (N=1 only),
+          with verdict / node / pass / model-word parity on that sample.
+  witness_replay
+          every Sat model of the e2e step checked by the restated reference
+          evaluator (check_model over constraints + divisor side constraints).
+  roofline / roofline.issue
+          HBM (contract form: algorithmic bytes / kernel time vs the measured
+          copy bandwidth, ncu DRAM bytes as `traffic`) and the integer-issue
+          roofline (ncu warp instructions per step / live step time vs the SM
+          issue peak), from the committed profiles/ncu_summary.json.
 """
 from __future__ import annotations
 
