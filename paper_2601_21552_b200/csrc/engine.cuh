@@ -782,31 +782,59 @@ struct Lane {
     }
 
     // ----- x32 eligibility (int64 root kernel) -----------------------------------
-    // At the current domains (they only shrink below), every REAL value the
-    // reference can produce -- domains, literals, forward intervals, exact
-    // values, narrowing targets not derived from the 10**18 clamp -- must stay
-    // below 2^28, and every clamp-derived target must stay beyond them all (its
-    // magnitude, tracked as a lower bound through +, -, * narrowing and literal
-    // division, must exceed 2 B + 2).  Then int32 with out-of-range targets
-    // carried as +-2^30 (Ext<int>) reproduces every comparison, narrowing and
-    // contradiction of the reference.  Double precision: the real bound is
-    // rounded up, the clamp-derived bound down (margins far beyond rounding).
+    // Proof, at the current domains D0, that int32 reproduces the reference on
+    // EVERY node of the subtree below (domains only shrink there, so every
+    // forward interval at a descendant lies inside its interval at D0).  Each
+    // narrowing target is tracked as the SET of values it can take at any
+    // descendant: a real part (an interval, every value exact in int32) and a
+    // far part (values derived from the 10**18 clamp; a lower bound on their
+    // magnitude; lower targets are only ever far-negative, upper targets
+    // far-positive).  The rules follow _Narrower.narrow (solver.py:159-226)
+    // with the children's intervals ranging over their D0 intervals -- in
+    // particular `*` is assumed to narrow whenever some descendant could make
+    // both sides non-negative, `other_lo` may be 0 (clamp) or any value up to
+    // its D0 maximum (real quotient), and far magnitudes shrink by the largest
+    // divisor.  Eligible when every real value (domains, literals, forward
+    // intervals, exact values, real targets) is below 2^28 and every far
+    // value exceeds 2 B + 2, so Ext<int>'s +-2^30 stands in for it in every
+    // comparison.  Doubles: real bounds are widened and far bounds shrunk by
+    // a relative 1e-9 plus 1 (the margins are many orders larger).
+    struct X32Tg {
+        double rlo, rhi;  // real part (valid when rl)
+        double fm;        // far part: magnitude lower bound (valid when fr)
+        bool rl, fr;
+    };
+    struct X32Pair {
+        X32Tg a, b;
+    };
     __device__ bool fit_x32() {
         double B = 0.0, minf = 1e300;
         auto ad = [](T x) { return x < T(0) ? -(double)x : (double)x; };
         for (uint32_t v = 0; v < nv; ++v) B = fmax(B, fmax(ad(E(env_lo, v)), ad(E(env_hi, v))));
         for (uint32_t i = 0; i < nlit; ++i) B = fmax(B, ad(E(lit, i)));
         const double INFD = 1e18;
-        constexpr int SMAX = 40;
+        auto up = [](double x) { return x + fabs(x) * 1e-9 + 1.0; };    // round a bound outward (up)
+        auto dn = [](double x) { return x - fabs(x) * 1e-9 - 1.0; };    // ... (down)
+        auto real = [&](double lo, double hi) { X32Tg t; t.rlo = dn(lo); t.rhi = up(hi); t.rl = true; t.fr = false; t.fm = 0; return t; };
+        auto far = [](double m) { X32Tg t; t.rlo = t.rhi = 0; t.rl = false; t.fr = true; t.fm = m; return t; };
+        auto none = []() { X32Tg t; t.rlo = t.rhi = t.fm = 0; t.rl = t.fr = false; return t; };
+        auto join = [](X32Tg a, const X32Tg& b) {
+            if (b.rl) {
+                if (a.rl) { a.rlo = fmin(a.rlo, b.rlo); a.rhi = fmax(a.rhi, b.rhi); }
+                else { a.rlo = b.rlo; a.rhi = b.rhi; a.rl = true; }
+            }
+            if (b.fr) { a.fm = a.fr ? fmin(a.fm, b.fm) : b.fm; a.fr = true; }
+            return a;
+        };
+        constexpr int SMAX = 24;
         uint32_t sn[SMAX];
-        double slo[SMAX], shi[SMAX];  // real: signed value; clamp-derived: magnitude (>= 0)
-        bool ilo[SMAX], ihi[SMAX];
+        X32Tg slo[SMAX], shi[SMAX];
         for (uint32_t k = 0; k < ncon; ++k) {
             uint32_t w = __ldg(cons + k);
             uint32_t rel = w & 7u, lr = (w >> 3) & 0x3FFFu, rr = w >> 17;
             uint32_t start = lr + 1 - size_of(lr);
             vbase = start;
-            // forward intervals (exact in T) and exact-value magnitudes
+            // forward intervals at D0 (exact in T)
             for (uint32_t j = start; j <= rr; ++j) {
                 uint32_t cw = __ldg(code + j), op = op_of(cw);
                 T lo, hi;
@@ -847,12 +875,9 @@ struct Lane {
                 VH(j) = hi;
                 if (lo <= hi) B = fmax(B, fmax(ad(lo), ad(hi)));
             }
-            auto F = [&](uint32_t j) -> double {
-                T lo = VL(j), hi = VH(j);
-                return lo <= hi ? fmax(ad(lo), ad(hi)) : 0.0;
-            };
             auto defined = [&](uint32_t j) { return VL(j) <= VH(j); };
-            // exact values are bounded by the magnitude recurrence (G)
+            auto F = [&](uint32_t j) -> double { return fmax(ad(VL(j)), ad(VH(j))); };
+            // exact values are bounded by the magnitude recurrence
             {
                 double g[64];
                 uint32_t n = rr + 1 - start;
@@ -872,65 +897,98 @@ struct Lane {
                     B = fmax(B, x);
                 }
             }
-            if (!defined(lr) || !defined(rr)) continue;  // this constraint fails before any narrowing
-            const double l0 = (double)VL(lr), l1 = (double)VH(lr), r0 = (double)VL(rr), r1 = (double)VH(rr);
+            // a constraint with an empty side fails before any narrowing, at D0
+            // and (inclusion) at every descendant
+            if (!defined(lr) || !defined(rr)) continue;
+            const double L0 = (double)VL(lr), L1 = (double)VH(lr), R0 = (double)VL(rr), R1 = (double)VH(rr);
             int sp = 0;
-            auto push = [&](uint32_t node, double lo, bool il, double hi, bool ih) {
+            auto push = [&](uint32_t node, const X32Tg& lo, const X32Tg& hi) {
                 sn[sp] = node;
                 slo[sp] = lo;
-                ilo[sp] = il;
                 shi[sp] = hi;
-                ihi[sp] = ih;
                 ++sp;
             };
-            switch (rel) {  // root targets (solver.py:240-259)
-            case REL_LT: push(lr, INFD, true, r1 - 1, false); push(rr, l0 + 1, false, INFD, true); break;
-            case REL_LE: push(lr, INFD, true, r1, false); push(rr, l0, false, INFD, true); break;
-            case REL_EQ: push(lr, fmax(l0, r0), false, fmin(l1, r1), false);
-                         push(rr, fmax(l0, r0), false, fmin(l1, r1), false); break;
-            case REL_GE: push(lr, r0, false, INFD, true); push(rr, INFD, true, l1, false); break;
-            default:     push(lr, r0 + 1, false, INFD, true); push(rr, INFD, true, l1 - 1, false); break;
+            // root targets (solver.py:240-259); l0, l1 range over [L0, L1] etc.
+            switch (rel) {
+            case REL_LT: push(lr, far(INFD), real(R0 - 1, R1 - 1)); push(rr, real(L0 + 1, L1 + 1), far(INFD)); break;
+            case REL_LE: push(lr, far(INFD), real(R0, R1)); push(rr, real(L0, L1), far(INFD)); break;
+            case REL_EQ: {
+                X32Tg lo = real(fmax(L0, R0), fmax(L1, R1)), hi = real(fmin(L0, R0), fmin(L1, R1));
+                push(lr, lo, hi);
+                push(rr, lo, hi);
+                break;
+            }
+            case REL_GE: push(lr, real(R0, R1), far(INFD)); push(rr, far(INFD), real(L0, L1)); break;
+            default:     push(lr, real(R0 + 1, R1 + 1), far(INFD)); push(rr, far(INFD), real(L0 - 1, L1 - 1)); break;
             }
             while (sp > 0) {
                 --sp;
                 const uint32_t i = sn[sp];
-                const double a = slo[sp], b = shi[sp];
-                const bool ia = ilo[sp], ib = ihi[sp];
-                if (ia) minf = fmin(minf, a); else B = fmax(B, fabs(a));
-                if (ib) minf = fmin(minf, b); else B = fmax(B, fabs(b));
+                const X32Tg lo = slo[sp], hi = shi[sp];
+                if (lo.rl) B = fmax(B, fmax(fabs(lo.rlo), fabs(lo.rhi)));
+                if (hi.rl) B = fmax(B, fmax(fabs(hi.rlo), fabs(hi.rhi)));
+                if (lo.fr) minf = fmin(minf, lo.fm);
+                if (hi.fr) minf = fmin(minf, hi.fm);
                 uint32_t cw = __ldg(code + i), op = op_of(cw);
                 if (op < NODE_ADD) continue;
                 uint32_t R = i - 1, L = R - size_of(R);
-                if (!defined(L) || !defined(R)) continue;
+                if (!defined(L) || !defined(R)) continue;  // _eval_iv None: contradiction, no narrowing
                 if (sp + 2 > SMAX) return false;
                 const double cl0 = (double)VL(L), cl1 = (double)VH(L), cr0 = (double)VL(R), cr1 = (double)VH(R);
                 const double fL = F(L), fR = F(R);
-                if (op == NODE_ADD) {
-                    push(R, ia ? a - fL : a - cl1, ia, ib ? b - fL : b - cl0, ib);
-                    push(L, ia ? a - fR : a - cr1, ia, ib ? b - fR : b - cr0, ib);
+                // target - [x0, x1] (sibling interval), far magnitudes shrink by its magnitude
+                auto shift = [&](X32Tg t, double x0, double x1, double fx) {
+                    if (t.rl) { t.rlo = dn(t.rlo - x1); t.rhi = up(t.rhi - x0); }
+                    if (t.fr) t.fm = dn(t.fm - fx);
+                    return t;
+                };
+                if (op == NODE_ADD) {  // (t0 - r1, t1 - r0) / (t0 - l1, t1 - l0)
+                    push(R, shift(lo, cl0, cl1, fL), shift(hi, cl0, cl1, fL));
+                    push(L, shift(lo, cr0, cr1, fR), shift(hi, cr0, cr1, fR));
                 } else if (op == NODE_SUB) {
-                    // R: [l0 - b, l1 - a]: a clamp-derived upper b makes the lower one clamp-derived
-                    push(R, ib ? b - fL : cl0 - b, ib, ia ? a - fL : cl1 - a, ia);
-                    push(L, ia ? a - fR : a + cr0, ia, ib ? b - fR : b + cr1, ib);
+                    // right: (l0 - t1, l1 - t0); a far upper becomes a far lower and vice versa
+                    auto neg = [&](X32Tg t) {  // [l0, l1] - t
+                        X32Tg o = t;
+                        if (t.rl) { o.rlo = dn(cl0 - t.rhi); o.rhi = up(cl1 - t.rlo); }
+                        if (t.fr) o.fm = dn(t.fm - fL);
+                        return o;
+                    };
+                    push(R, neg(hi), neg(lo));
+                    // left: (t0 + r0, t1 + r1)
+                    push(L, shift(lo, -cr1, -cr0, fR), shift(hi, -cr1, -cr0, fR));
                 } else if (op == NODE_MUL) {
-                    if (cl0 < 0 || cr0 < 0) continue;
-                    const double t0n = ia ? 0.0 : fmax(a, 0.0);
-                    // lower targets: real ceil divisions, or the clamp (-INF) when t0n <= 0
-                    const bool lo_inf = !(t0n > 0);
-                    const double lol = lo_inf ? INFD : ceil(t0n / fmax(cr1, 1.0)), lor = lo_inf ? INFD : ceil(t0n / fmax(cl1, 1.0));
-                    const bool hil_inf = !(cr0 > 0) || ib, hir_inf = !(cl0 > 0) || ib;
-                    const double hil = !(cr0 > 0) ? INFD : (ib ? b / cr0 - 1.0 : floor(b / cr0));
-                    const double hir = !(cl0 > 0) ? INFD : (ib ? b / cl0 - 1.0 : floor(b / cl0));
-                    push(R, lor, lo_inf, hir, hir_inf);
-                    push(L, lol, lo_inf, hil, hil_inf);
+                    // narrows only when l0 >= 0 and r0 >= 0 at the node: possible
+                    // at some descendant iff both D0 maxima are >= 0
+                    if (cl1 < 0 || cr1 < 0) continue;
+                    auto side = [&](double o0, double o1) {  // other side's interval (clipped to >= 0)
+                        o0 = fmax(o0, 0.0);
+                        X32Tg nlo = none(), nhi = none();
+                        // lo_req: -INF when t0n = max(t0, 0) <= 0, else ceil(t0n / other_hi), other_hi in [1, o1]
+                        if (lo.fr || (lo.rl && lo.rlo <= 0)) nlo = join(nlo, far(INFD));
+                        if (lo.rl && lo.rhi > 0 && o1 >= 1) nlo = join(nlo, real(fmax(lo.rlo, 1.0) / o1, lo.rhi));
+                        // hi_req: INF when other_lo = 0, else t1 // other_lo, other_lo in [max(o0, 1), o1]
+                        if (o0 <= 0) nhi = join(nhi, far(INFD));
+                        if (o1 >= 1) {
+                            if (hi.rl && hi.rhi >= 0) nhi = join(nhi, real(fmax(hi.rlo, 0.0) / o1, hi.rhi));
+                            if (hi.fr) nhi = join(nhi, far(dn(hi.fm / o1)));
+                        }
+                        return X32Pair{nlo, nhi};
+                    };
+                    auto pl = side(cr0, cr1), pr = side(cl0, cl1);
+                    push(R, pr.a, pr.b);
+                    push(L, pl.a, pl.b);
                 } else if (op == NODE_DIV) {
                     uint32_t rw = __ldg(code + R);
                     if (op_of(rw) == NODE_LIT) {
                         const T cc = E(lit, arg_of(rw));
                         if (cc >= T(1)) {
                             const double c = (double)cc;
-                            push(L, ia ? a * c : (a > 0 ? a * c : a * c - (c - 1.0)), ia,
-                                 ib ? b * c : (b >= 0 ? b * c + (c - 1.0) : b * c), ib);
+                            auto sc = [&](X32Tg t) {  // t * c (+- (c - 1))
+                                if (t.rl) { t.rlo = dn(t.rlo * c - (c - 1.0)); t.rhi = up(t.rhi * c + (c - 1.0)); }
+                                if (t.fr) t.fm = dn(t.fm);  // |t * c +- (c - 1)| >= |t|
+                                return t;
+                            };
+                            push(L, sc(lo), sc(hi));
                         }
                     }
                 }

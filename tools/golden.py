@@ -279,6 +279,21 @@ def crafted_cases():
          C("=", B("%", V("r"), L(3)), L(2)), C(">", V("q"), V("p"))])
     add("big_split", [SV("x", 0, 10**6), SV("y", 0, 10**6)],
         [C("=", B("*", x, y), L(999_983 * 7)), C("<", x, y)])
+    # x32-regime proof regressions: narrowing targets that only
+    # become real below the root (a `*` side whose lower bound is 0 or
+    # negative at the root) must be bounded by the x32 eligibility proof
+    add("x32_mul_late", [SV("x", 0, 5), SV("z", 0, 2**24)],
+        [C("<=", B("*", x, B("/", z, L(1000))), L(7_000_000)),
+         C("=", B("%", x, L(8)), L(3))])
+    add("x32_mul_negroot", [SV("b", 0, 5), SV("z", 0, 2**24)],
+        [C("<=", B("*", B("-", V("b"), L(1)), B("/", z, L(1000))), L(7_000_000)),
+         C("=", B("%", V("b"), L(8)), L(3))])
+    add("x32_mul_late_unsat", [SV("x", 0, 5), SV("z", 0, 2**24)],
+        [C("<=", B("*", x, B("/", z, L(1000))), L(7_000_000)),
+         C("=", B("%", x, L(8)), L(3)), C(">", z, L(2_333_334_000 // 1000))])
+    add("x32_add_chain", [SV("x", 0, 6), SV("y", 0, 2**20), SV("z", 0, 2**24)],
+        [C("<=", B("+", B("*", x, B("/", z, L(100))), y), L(2**27)),
+         C(">", x, L(2)), C(">=", z, B("*", y, L(8)))])
     return cases
 
 
