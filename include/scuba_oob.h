@@ -119,7 +119,8 @@ typedef struct {
     int32_t device;       /* first device ordinal                                 */
     int32_t flags;        /* OOB_F_* below                                        */
     int32_t heavy_nodes;  /* DFS nodes after which a query moves to the warp-
-                             cooperative frontier kernel; 0 = default (64),
+                             cooperative frontier kernel; 0 = default (24;
+                             fast mode: SCUBA_OOB_FAST_HEAVY_NODES, 8),
                              <0 = never (one lane per query throughout)      */
     int32_t jit_min;      /* structure classes with at least this many queries
                              in an int64 job run as run-time compiled kernels;
@@ -132,8 +133,16 @@ enum {
                             regime (no root-phase demotion; testing) */
     OOB_F_NO_JIT = 4,    /* interpret every structure class (no run-time
                             compiled class kernels; testing) */
-    OOB_F_NO_X32 = 8     /* keep int64-regime queries in int64 (no x32
+    OOB_F_NO_X32 = 8,    /* keep int64-regime queries in int64 (no x32
                             demotion after the root phase; testing) */
+    OOB_F_FAST = 16      /* fast mode: heavy queries first meet a symbolic
+                            Unsat prover (sound: a refuted query has no
+                            integer solution in its root box, so the reference
+                            can never return Sat on it); what it does not
+                            refute is decided by the exact emulation.  Verdicts
+                            and Sat models are the reference's; nodes/passes
+                            of refuted queries are 0 (not the reference's
+                            counters).  DESIGN.md section 4.9. */
 };
 
 /* Results (caller-allocated; optional arrays may be NULL). */
@@ -170,6 +179,14 @@ int oob_side_constraint_count(const oob_batch* batch, int64_t* counts);
  * decided in (0 immediate verdict, 1 int64, 2 int128, 3 256-bit, 4 out of
  * range -> OOB_ERROR).  No device is touched. */
 int oob_query_regime(const oob_batch* batch, const oob_options* opt, int8_t* regime);
+/* Fast-mode compiler audit (no device is touched): the Unsat certificates the
+ * engine compiles for the batch's structure classes (csrc/cert.cuh layout:
+ * per class [n] then n x [length][words]), each query's class entry in
+ * words[] (cert_off[q], -1: none), and each query's literal slot values
+ * (slots[slot_begin[q] .. slot_begin[q+1]), the order the certificates'
+ * parameters index).  The device checks these certificates numerically. */
+int oob_cert_compile(const oob_batch* batch, const oob_options* opt, uint64_t* words, int64_t words_cap,
+                     int64_t* n_words, int64_t* cert_off, oob_i128* slots, int64_t slots_cap, int64_t* slot_begin);
 /* Run-time specialisation audit: the CUDA source generated for query q's
  * structure class (written to src, NUL-terminated, truncated to src_cap) and
  * its NVRTC compile for sm_100a (*compile_ms); no device is touched. */

@@ -26,6 +26,7 @@ F_NO_SORT = 1
 F_NO_DEMOTE = 2
 F_NO_JIT = 4
 F_NO_X32 = 8
+F_FAST = 16  # fast mode: symbolic Unsat prover in front of the exact emulation
 
 class EngineError(RuntimeError):
     """The GPU engine could not decide a batch (no device, capacity, range)."""

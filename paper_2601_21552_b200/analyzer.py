@@ -27,15 +27,20 @@ def _types(analyzer_module):
     return (analyzer_module.Sat, analyzer_module.Unsat, analyzer_module.Timeout)
 
 
-@contextlib.contextmanager
-def installed(analyzer_module):
-    """Context manager: analyzer_module.solve -> the GPU engine."""
-    types = _types(analyzer_module)
-    saved = analyzer_module.solve
-
+def _gpu_solve(types, mode):
+    # one query per call: one device (the in-call multi-device dealing is for
+    # batches)
     def gpu_solve(variables, constraints, timeout_s=30.0):
-        return solve_batch([(variables, constraints)], timeout_s, verdict_types=types)[0]
+        return solve_batch([(variables, constraints)], timeout_s, n_gpus=1, verdict_types=types, mode=mode)[0]
 
+    return gpu_solve
+
+
+@contextlib.contextmanager
+def installed(analyzer_module, mode="canonical"):
+    """Context manager: analyzer_module.solve -> the GPU engine."""
+    saved = analyzer_module.solve
+    gpu_solve = _gpu_solve(_types(analyzer_module), mode)
     analyzer_module.solve = gpu_solve
     try:
         yield gpu_solve
@@ -43,13 +48,9 @@ def installed(analyzer_module):
         analyzer_module.solve = saved
 
 
-def install(analyzer_module):
+def install(analyzer_module, mode="canonical"):
     """Permanently bind the GPU engine into the analyzer module."""
-    types = _types(analyzer_module)
-
-    def gpu_solve(variables, constraints, timeout_s=30.0):
-        return solve_batch([(variables, constraints)], timeout_s, verdict_types=types)[0]
-
+    gpu_solve = _gpu_solve(_types(analyzer_module), mode)
     analyzer_module.solve = gpu_solve
     return gpu_solve
 
@@ -78,7 +79,33 @@ def decide_calls(calls, types, **engine_kw):
     return verdicts
 
 
-def analyze_batched(analyzer_module, analyze, *args, stats=None, **kwargs):
+class _Replay:
+    """Pass 2: hands back the recorded verdicts in call order and checks that
+    the analysis makes exactly the recorded calls."""
+
+    def __init__(self, calls, verdicts):
+        self.calls = calls
+        self.verdicts = verdicts
+        self.i = 0
+
+    def __call__(self, variables, constraints, timeout_s=30.0):
+        if self.i >= len(self.calls):
+            raise RuntimeError("analysis is not deterministic between passes "
+                               f"(pass 2 made more than the {len(self.calls)} recorded solver calls)")
+        want = self.calls[self.i]
+        if query_to_json(variables, constraints) != query_to_json(want[0], want[1]):
+            raise RuntimeError(f"analysis is not deterministic between passes (solver call {self.i} differs)")
+        v = self.verdicts[self.i]
+        self.i += 1
+        return v
+
+    def finish(self):
+        if self.i != len(self.calls):
+            raise RuntimeError("analysis is not deterministic between passes "
+                               f"(pass 2 made {self.i} of the {len(self.calls)} recorded solver calls)")
+
+
+def analyze_batched(analyzer_module, analyze, *args, stats=None, mode="canonical", **kwargs):
     """Run `analyze(*args, **kwargs)` (e.g. analyzer_module.analyze_source)
     with all of its solver queries decided in one GPU batch."""
     types = _types(analyzer_module)
@@ -89,27 +116,19 @@ def analyze_batched(analyzer_module, analyze, *args, stats=None, **kwargs):
         analyze(*args, **kwargs)
     finally:
         analyzer_module.solve = saved
-    verdicts = decide_calls(rec.calls, types)
-    it = iter(range(len(verdicts)))
-
-    def replay(variables, constraints, timeout_s=30.0):
-        i = next(it)
-        want = rec.calls[i]
-        if query_to_json(variables, constraints) != query_to_json(want[0], want[1]):
-            raise RuntimeError("analysis is not deterministic between passes")
-        return verdicts[i]
-
+    replay = _Replay(rec.calls, decide_calls(rec.calls, types, mode=mode))
     analyzer_module.solve = replay
     try:
         result = analyze(*args, **kwargs)
     finally:
         analyzer_module.solve = saved
+    replay.finish()
     if stats is not None:
         stats["queries"] = len(rec.calls)
     return result
 
 
-def analyze_many(analyzer_module, analyze, jobs, stats=None):
+def analyze_many(analyzer_module, analyze, jobs, stats=None, mode="canonical"):
     """a whole set of analyses (e.g. the 20-program
     corpus) with ALL their solver queries decided in ONE device batch.
 
@@ -129,25 +148,17 @@ def analyze_many(analyzer_module, analyze, jobs, stats=None):
     finally:
         analyzer_module.solve = saved
     calls = [c for rec in recs for c in rec.calls]
-    verdicts = decide_calls(calls, types)
+    verdicts = decide_calls(calls, types, mode=mode)
     results = []
     base = 0
     for (args, kwargs), rec in zip(jobs, recs):
-        mine = verdicts[base:base + len(rec.calls)]
-        it = iter(range(len(mine)))
-
-        def replay(variables, constraints, timeout_s=30.0, rec=rec, mine=mine, it=it):
-            i = next(it)
-            want = rec.calls[i]
-            if query_to_json(variables, constraints) != query_to_json(want[0], want[1]):
-                raise RuntimeError("analysis is not deterministic between passes")
-            return mine[i]
-
+        replay = _Replay(rec.calls, verdicts[base:base + len(rec.calls)])
         analyzer_module.solve = replay
         try:
             results.append(analyze(*args, **kwargs))
         finally:
             analyzer_module.solve = saved
+        replay.finish()
         base += len(rec.calls)
     if stats is not None:
         stats["queries"] = len(calls)

@@ -86,8 +86,10 @@ struct ClassDesc {
     uint32_t ncode_nlit;
     uint32_t q_begin;
     uint32_t q_end;
-    uint32_t pad[3];
+    uint32_t cert;     // fast mode: word offset of the class's Unsat certificates (cert.cuh), NO_CERT: none
+    uint32_t pad[2];
 };
+constexpr uint32_t NO_CERT = 0xFFFFFFFFu;
 static_assert(sizeof(ClassDesc) == 32, "ClassDesc is two int4 words");
 
 // Regime demotion (SOLVE mode).  A query whose declared domains need the
@@ -171,6 +173,15 @@ struct LaunchArgs {
     uint64_t* timeline;       // debug (SCUBA_OOB_TIMELINE): per entry start, hand-off, frontier start, end (ns)
     unsigned long long* stats;  // debug (SCUBA_OOB_TRACE=2): frontier / lockstep lane-efficiency counters
     DemoteTarget dem[3];      // root kernel: [0] int64 job, [1] int128 job, [2] x32 job (slot null: none)
+    // fast mode (OOB_F_FAST): a heavy query first meets the symbolic Unsat
+    // prover (symbolic.cuh) in the frontier phase; refuted = final Unsat
+    uint32_t fast;
+    unsigned long long* fast_stats;  // [0] heavy queries tried [1] refuted [2,3] cycles [4] certified (null: off)
+    // fast mode certificate check (oob_cert_kernel): the job's full class
+    // table (ClassDesc::cert) and the certificate words
+    const ClassDesc* cert_classes;
+    uint32_t cert_nclasses;
+    const uint64_t* certs;
 };
 
 enum { MODE_SOLVE = 0, MODE_PROPAGATE = 1, MODE_CHECK = 2 };

@@ -34,11 +34,14 @@
 #include "../../include/scuba_oob.h"
 #include "format.h"
 #include "jit.h"
+#include "cert.cuh"
+#include "symbolic.cuh"
 #include "wide.cuh"
 
 namespace oob {
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s);
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
+cudaError_t launch_cert(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
 cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm);
 cudaError_t launch_gather_sat(const int8_t* verdict, const QDesc* qd, const int64_t* model, uint32_t n,
                               unsigned long long* counter, uint32_t* sat_off, int64_t* compact, int sms,
@@ -935,7 +938,7 @@ struct DevicePool {
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
     DevBuf classes, class_next, class_init, warp_class;
     DevBuf heavy_count, heavy_list, heavy_t0, fr_region;
-    DevBuf resume, resume_init, slot64, slot128, slotx32, timeline, classes_interp, stats;
+    DevBuf resume, resume_init, slot64, slot128, slotx32, timeline, classes_interp, stats, certs;
     DevBuf satcnt, satoff, compact;  // SOLVE fetch: packed Sat models
     DevBuf fr_map;                   // frontier region pool: held bits
     DevBuf slab_map;                 // slab pool (SOLVE kernels): held bits
@@ -949,7 +952,7 @@ struct DevicePool {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
                           &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &slotx32, &timeline,
-                          &classes_interp, &stats, &satcnt, &satoff, &compact, &fr_map, &slab_map, &handoff})
+                          &classes_interp, &stats, &certs, &satcnt, &satoff, &compact, &fr_map, &slab_map, &handoff})
             b->release();
     }
 };
@@ -1010,6 +1013,9 @@ struct RunCtx {
     int64_t* passes;
     double* elapsed;
     std::vector<int8_t>* errs;
+    // fast mode: Unsat certificates per batch-wide structure class (cert.cuh)
+    const std::vector<uint64_t>* certs = nullptr;
+    const std::vector<uint32_t>* cert_off = nullptr;  // per class, NO_CERT: none
 };
 
 constexpr size_t SMEM_WARP_MAX = 48 * 1024;  // hot state per warp kept on chip up to this
@@ -1187,6 +1193,7 @@ void pack(const RunCtx& rc, DevJob& j, bool inline_fill = false) {
         cd.ncode_nlit = c.ncode | (c.nlit << 16);
         cd.q_begin = count[id];
         cd.q_end = count[id + 1];
+        cd.cert = (rc.cert_off && c.cls < rc.cert_off->size()) ? (*rc.cert_off)[c.cls] : NO_CERT;
         j.maxv = std::max(j.maxv, c.nv);
         j.maxcode = std::max(j.maxcode, c.ncode);
         j.maxlit = std::max(j.maxlit, c.nlit);
@@ -1337,6 +1344,35 @@ constexpr uint32_t HEAVY_NODES_DEFAULT = 24;
 // 192 -> 128: C3 -7%, C4 +0.5%, C5s neutral)
 constexpr uint32_t HEAVY_PASSES_DEFAULT = 128;
 
+// fast mode (OOB_F_FAST): every entry's class certificate is checked first
+// (oob_cert_kernel); SCUBA_OOB_FAST_FRONTIER=1 additionally runs the symbolic
+// prover itself on heavy queries in the (interpreting) frontier, which then
+// receives them earlier than in canonical mode
+bool fast_frontier() {
+    static const bool v = [] {
+        const char* e = std::getenv("SCUBA_OOB_FAST_FRONTIER");
+        return e && *e == '1';
+    }();
+    return v;
+}
+uint32_t fast_heavy_nodes() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("SCUBA_OOB_FAST_HEAVY_NODES");
+        return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : 8);
+    }();
+    return v;
+}
+uint32_t fast_heavy_passes() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("SCUBA_OOB_FAST_HEAVY_PASSES");
+        return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : 32);
+    }();
+    return v;
+}
+// the symbolic prover's scratch at the start of a frontier region: the
+// query's store plus one working set per lane
+size_t sym_scratch_bytes() { return sizeof(sym::Store) + 32 * sizeof(sym::LaneWork); }
+
 size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
     size_t b = (size_t)FR_ECAP * 2 * maxv * tbytes + 2 * (size_t)FR_ECAP * tbytes + (size_t)FR_ECAP * 16 +
                (size_t)FR_LOGCAP * 16 + (size_t)FR_ECAP * 4 * 2 + (size_t)FR_ECAP * 16 + (size_t)FR_UCAP * 4 +
@@ -1483,9 +1519,13 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         j.jit_blocks.push_back(b);
         n_warps += b * jw;
     }
-    // heavy-query hand-off (solve mode): threshold from the options
+    // heavy-query hand-off (solve mode): threshold from the options; in fast
+    // mode the frontier is where the symbolic prover meets heavy queries, so
+    // it is always on, with its own (earlier) thresholds
     int64_t hn = rc.opt.heavy_nodes;
+    const bool fast = rc.mode == MODE_SOLVE && (rc.opt.flags & OOB_F_FAST);
     uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
+    if (fast && fast_frontier()) heavy_nodes = hn > 0 ? (uint32_t)hn : fast_heavy_nodes();
     // wide jobs: a frontier-only tail launch with a full grid serves their
     // heavy list once the int64 kernel has freed the SMs
     const uint32_t own_warps = n_warps;  // slabs [0, own_warps): the interpreting kernel + class kernels
@@ -1515,7 +1555,8 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     j.slab_slots = pooled ? std::max(1u, std::min(n_warps, (uint32_t)P->sms * 64u)) : n_warps;
     j.root_blocks = std::max<uint32_t>(
         1u, std::min<uint64_t>((n + 32 * WARPS_PER_BLOCK - 1) / (32 * WARPS_PER_BLOCK), j.slab_slots / WARPS_PER_BLOCK));
-    const size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
+    size_t fr_bytes = frontier_region_bytes(j.maxv, tbytes);
+    if (fast && fast_frontier()) fr_bytes = std::max(fr_bytes, (sym_scratch_bytes() + 255) & ~(size_t)255);
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
     CK(P->code.ensure(j.code.size() * 4));
@@ -1593,7 +1634,18 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
             const char* e = std::getenv("SCUBA_OOB_HEAVY_PASSES");
             return (uint32_t)((e && *e) ? std::atoi(e) : (int)HEAVY_PASSES_DEFAULT);
         }();
-        a.heavy_passes = hp;
+        a.heavy_passes = (fast && fast_frontier()) ? fast_heavy_passes() : hp;
+    }
+    a.fast = (fast && fast_frontier()) ? 1u : 0u;
+    a.fast_stats = nullptr;
+    a.cert_classes = nullptr;
+    a.certs = nullptr;
+    a.cert_nclasses = (uint32_t)j.cls.size();
+    if (fast && rc.certs && !rc.certs->empty() && j.wide != W_X32) {
+        CK(P->certs.ensure(rc.certs->size() * 8));
+        CK(cudaMemcpyAsync(P->certs.p, rc.certs->data(), rc.certs->size() * 8, cudaMemcpyHostToDevice, s));
+        a.certs = (const uint64_t*)P->certs.p;
+        a.cert_classes = (const ClassDesc*)P->classes.p;
     }
     a.heavy_count = (uint32_t*)P->heavy_count.p;
     a.heavy_next = (uint32_t*)P->heavy_count.p + 1;
@@ -1638,6 +1690,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         CK(P->stats.ensure(128));
         CK(cudaMemsetAsync(P->stats.p, 0, 128, s));
         a.stats = (unsigned long long*)P->stats.p;
+        if (fast) a.fast_stats = a.stats + 10;  // [10..14]
     }
     a.timeline = nullptr;
     if (timeline_path() && rc.mode == MODE_SOLVE) {
@@ -1837,6 +1890,15 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
             CK(cudaEventRecord(G.pool[w]->ev0, G.pool[w]->stream));
         }
     if (rc.mode == MODE_SOLVE) {
+        // fast mode: class certificates first (refuted entries are never
+        // searched: RES_SKIP)
+        for (int w = 0; w < 3; w++) {
+            if (!present(G.job[w]) || !G.job[w].a.certs) continue;
+            const DevJob& j = G.job[w];
+            const uint32_t n = (uint32_t)j.qs.size();
+            const int blocks = (int)std::max<uint32_t>(1, std::min<uint32_t>((n + 127) / 128, (uint32_t)G.pool[w]->sms * 8));
+            CK(launch_cert(j.a, w, blocks, G.pool[w]->stream));
+        }
         // root phases, widest first: 256-bit -> int128 -> int64 -> x32
         for (int w = 2; w >= 0; w--) {
             if (!present(G.job[w])) continue;
@@ -2000,6 +2062,12 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
                      st[4] ? 100.0 * st[5] / st[4] : 0.0);
         std::fprintf(stderr, "[oob] job w%d: frontier Sat passes expanded %llu / reference %llu; Unsat %llu / %llu\n",
                      j.wide, st[6], st[7], st[8], st[9]);
+        if (j.a.fast)
+            std::fprintf(stderr,
+                         "[oob] job w%d: fast mode: %llu entries refuted by their class certificate; %llu heavy "
+                         "queries met the frontier prover, %llu refuted; cycles per query: prepare %.0f search %.0f\n",
+                         j.wide, st[14], st[10], st[11], st[10] ? (double)st[12] / st[10] : 0.0,
+                         st[10] ? (double)st[13] / st[10] : 0.0);
     }
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
@@ -2221,10 +2289,108 @@ void assign_classes(std::vector<Compiled>& comp, const std::vector<int64_t> reg[
         for (int64_t q : reg[w]) comp[q].cls = canon[comp[q].cls];
 }
 
+// Fast mode: compile the Unsat certificates of every structure class
+// (cert.cuh) from up to CERT_REPS representatives spread over the class; the
+// literal slots whose value varies inside the class are parameters.  Layout
+// per class: [n certificates] then per certificate [length] [words].  The
+// host only COMPILES (symbolic algebra on a few representatives); every
+// query is decided by the device's numeric check of its class certificate.
+constexpr int CERT_REPS = 8;
+void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const std::vector<int64_t> reg[3],
+                 std::vector<uint64_t>& certs, std::vector<uint32_t>& cert_off) {
+    uint32_t ncls = 0;
+    for (int w = 0; w < 3; w++)
+        for (int64_t q : reg[w]) ncls = std::max(ncls, comp[q].cls + 1);
+    std::vector<uint32_t> start(ncls + 1, 0);
+    for (int w = 0; w < 3; w++)
+        for (int64_t q : reg[w]) start[comp[q].cls + 1]++;
+    for (uint32_t c = 0; c < ncls; c++) start[c + 1] += start[c];
+    std::vector<int64_t> mem(start[ncls]);
+    {
+        std::vector<uint32_t> at(start.begin(), start.end() - 1);
+        for (int w = 0; w < 3; w++)  // ascending query order within a class
+            for (int64_t q : reg[w]) mem[at[comp[q].cls]++] = q;
+        parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
+            for (size_t c = lo; c < hi; c++) std::sort(mem.begin() + start[c], mem.begin() + start[c + 1]);
+        });
+    }
+    std::vector<std::vector<uint64_t>> per(ncls);
+    parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
+        static thread_local std::unique_ptr<sym::Store> S;
+        static thread_local std::unique_ptr<sym::LaneWork> W;
+        static thread_local std::unique_ptr<sym::Moves> M;
+        static thread_local std::vector<uint64_t> buf;
+        if (!S) {
+            S.reset(new sym::Store());
+            W.reset(new sym::LaneWork());
+            M.reset(new sym::Moves());
+            buf.resize(1 << 15);
+        }
+        for (size_t c = lo; c < hi; c++) {
+            const int64_t* m = mem.data() + start[c];
+            const size_t nm = start[c + 1] - start[c];
+            if (!nm) continue;
+            const Structure& st = *comp[m[0]].st;
+            if (!st.range_why.empty()) continue;
+            // literal slots whose value varies inside the class: parameters
+            std::vector<int16_t> pmap(st.nlit, -1), pslot;
+            std::vector<i128> v0(st.nlit);
+            for (uint32_t i = 0; i < st.nlit; i++) v0[i] = lit_value(b, m[0], st, i);
+            std::vector<uint8_t> vary(st.nlit, 0);
+            // (each query through its own Structure: equal code words do not
+            // imply equal literal-slot sources)
+            for (size_t k = 1; k < nm; k++) {
+                const Structure& sk = *comp[m[k]].st;
+                for (uint32_t i = 0; i < st.nlit; i++)
+                    if (!vary[i] && lit_value(b, m[k], sk, i) != v0[i]) vary[i] = 1;
+            }
+            for (uint32_t i = 0; i < st.nlit; i++)
+                if (vary[i]) {
+                    pmap[i] = (int16_t)pslot.size();
+                    pslot.push_back((int16_t)i);
+                }
+            std::vector<std::vector<uint64_t>> got;
+            const size_t nr = std::min<size_t>(CERT_REPS, nm);
+            for (size_t r = 0; r < nr; r++) {
+                const int64_t q = m[r * nm / nr];
+                const int64_t vb = b->var_begin[q];
+                auto dom = [&](uint32_t i) -> i128 { return from_w(i % 2 ? b->var_hi[vb + i / 2] : b->var_lo[vb + i / 2]); };
+                const Structure& sq = *comp[q].st;
+                auto lit = [&](uint32_t i) -> i128 { return lit_value(b, q, sq, i); };
+                const size_t n = cert::cert_build(*S, *W, *M, st.words.data(), st.code(), st.nv, st.ncon, st.nlit,
+                                                  dom, lit,
+                                                  pmap.data(), (int)pslot.size(), pslot.data(), buf.data(),
+                                                  buf.size());
+                if (!n) continue;
+                std::vector<uint64_t> blob(buf.begin(), buf.begin() + n);
+                bool dup = false;
+                for (const auto& o : got) dup = dup || o == blob;
+                if (!dup) got.push_back(std::move(blob));
+            }
+            if (got.empty()) continue;
+            std::vector<uint64_t>& out = per[c];
+            out.push_back(got.size());
+            for (const auto& g : got) {
+                out.push_back(g.size());
+                out.insert(out.end(), g.begin(), g.end());
+            }
+        }
+    });
+    certs.clear();
+    cert_off.assign(ncls, NO_CERT);
+    for (uint32_t c = 0; c < ncls; c++) {
+        if (per[c].empty()) continue;
+        cert_off[c] = (uint32_t)certs.size();
+        certs.insert(certs.end(), per[c].begin(), per[c].end());
+    }
+}
+
 // Compile + schedule: fills immediate verdicts and returns the device jobs.
 struct Prepared {
     std::vector<Compiled> comp;
     std::vector<uint32_t> qcls;  // comp[q].cls, compact
+    std::vector<uint64_t> certs;     // fast mode: Unsat certificates (cert.cuh)
+    std::vector<uint32_t> cert_off;  // per structure class: offset in certs, NO_CERT: none
     std::vector<int8_t> errs;
     std::vector<DevWork> work;  // per device: queries by proven regime
     std::string range_msg;
@@ -2294,6 +2460,12 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     want = std::max(1, std::min(want, ndev - first));
     Phase ph_sched("schedule");
     assign_classes(comp, reg);
+    pr.certs.clear();
+    pr.cert_off.clear();
+    if (mode == MODE_SOLVE && (opt.flags & OOB_F_FAST) && opt.timeout_s > 0) {
+        Phase ph_cert("certify");
+        build_certs(b, comp, reg, pr.certs, pr.cert_off);
+    }
     pr.qcls.assign(n, 0);
     for (int w = 0; w < 3; w++)
         for (int64_t q : reg[w]) pr.qcls[q] = comp[q].cls;
@@ -2389,6 +2561,8 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
     rc.passes = passes;
     rc.elapsed = elapsed;
     rc.errs = &pr.errs;
+    rc.certs = &pr.certs;
+    rc.cert_off = &pr.cert_off;
     std::string e = run_all(rc, pr.work);
     if (!e.empty()) {
         recycle();
@@ -2550,6 +2724,8 @@ int oob_host_bench(const oob_batch* b, const oob_options* opt, double* ms) {
     rc.qcls = &pr.qcls;
     rc.mode = MODE_SOLVE;
     rc.errs = &pr.errs;
+    rc.certs = &pr.certs;
+    rc.cert_off = &pr.cert_off;
     for (auto& wk : pr.work) {
         DevGroup G;
         G.dev = wk.dev;
@@ -2560,6 +2736,44 @@ int oob_host_bench(const oob_batch* b, const oob_options* opt, double* ms) {
     ms[0] = pr.compile_s * 1e3;
     ms[1] = std::chrono::duration<double, std::milli>(t1 - t0).count();
     ms[2] = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    return OOB_OK;
+}
+
+int oob_cert_compile(const oob_batch* b, const oob_options* opt, uint64_t* words, int64_t words_cap,
+                     int64_t* n_words, int64_t* cert_off, oob_i128* slots, int64_t slots_cap, int64_t* slot_begin) {
+    g_last_error.clear();
+    if (!b || !words || !n_words || !cert_off || !slots || !slot_begin) return fail(OOB_E_INVALID, "null argument");
+    const double timeout_s = opt ? opt->timeout_s : 30.0;
+    const int64_t n = b->n_queries;
+    std::vector<Compiled> comp(n);
+    std::vector<int64_t> reg[3];
+    for (int64_t q = 0; q < n; q++) {
+        std::string why = validate(b, q);
+        if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
+        comp[q] = compile_query(b, q, MODE_SOLVE, timeout_s, nullptr);
+        if (comp[q].regime >= R_W64 && comp[q].regime < R_W64 + 3) reg[comp[q].regime - R_W64].push_back(q);
+    }
+    assign_classes(comp, reg);
+    std::vector<uint64_t> certs;
+    std::vector<uint32_t> off;
+    build_certs(b, comp, reg, certs, off);
+    if ((int64_t)certs.size() > words_cap) return fail(OOB_E_NOMEM, "certificate words exceed the buffer");
+    std::copy(certs.begin(), certs.end(), words);
+    *n_words = (int64_t)certs.size();
+    int64_t at = 0;
+    for (int64_t q = 0; q < n; q++) {
+        slot_begin[q] = at;
+        const Compiled& c = comp[q];
+        const bool dev = c.regime >= R_W64 && c.regime < R_W64 + 3;
+        cert_off[q] = (dev && c.cls < off.size() && off[c.cls] != NO_CERT) ? (int64_t)off[c.cls] : -1;
+        if (!dev) continue;
+        if (at + c.nlit > slots_cap) return fail(OOB_E_NOMEM, "literal slots exceed the buffer");
+        for (uint32_t i = 0; i < c.nlit; i++) {
+            const i128 v = lit_value(b, q, *c.st, i);
+            slots[at++] = oob_i128{(uint64_t)v, (int64_t)(v >> 64)};
+        }
+    }
+    slot_begin[n] = at;
     return OOB_OK;
 }
 
@@ -2615,6 +2829,8 @@ int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** o
     rc.passes = p->passes.data();
     rc.elapsed = p->elapsed.data();
     rc.errs = &p->pr.errs;
+    rc.certs = &p->pr.certs;
+    rc.cert_off = &p->pr.cert_off;
     p->groups.resize(p->pr.work.size());
     for (size_t k = 0; k < p->pr.work.size(); k++) {
         DevGroup& G = p->groups[k];

@@ -337,8 +337,13 @@ struct Entry {
 std::mutex g_mu;
 std::map<std::string, std::shared_ptr<Entry>> g_cache;
 
-const char* kHeaderNames[] = {"types.h", "format.h", "wide.cuh", "engine.cuh", "frontier.cuh", "phases.cuh",
-                              "jit_lane.cuh"};
+// every device header the generated source reaches (same order in both lists)
+const char* kHeaderNames[] = {"types.h",      "format.h",   "wide.cuh",    "engine.cuh",
+                              "frontier.cuh", "symbolic.cuh", "phases.cuh", "jit_lane.cuh"};
+const char* kHeaderSrc[] = {kSrc_types_h,      kSrc_format_h,     kSrc_wide_cuh,   kSrc_engine_cuh,
+                            kSrc_frontier_cuh, kSrc_symbolic_cuh, kSrc_phases_cuh, kSrc_jit_lane_cuh};
+constexpr int kNumHeaders = sizeof(kHeaderNames) / sizeof(kHeaderNames[0]);
+static_assert(sizeof(kHeaderSrc) == sizeof(kHeaderNames), "one source per header name");
 
 // On-disk cubin cache shared by the processes of a box (one per GPU under
 // torchrun compile the same classes): $SCUBA_OOB_JIT_CACHE, else
@@ -367,9 +372,7 @@ std::string cache_path(const std::string& src, const std::string& opts) {
     const std::string d = cache_dir();
     if (d.empty()) return "";
     uint64_t h = fnv(src);
-    for (const char* hs : {kSrc_types_h, kSrc_format_h, kSrc_wide_cuh, kSrc_engine_cuh, kSrc_frontier_cuh,
-                           kSrc_phases_cuh, kSrc_jit_lane_cuh})
-        h = fnv(hs, h);
+    for (const char* hs : kHeaderSrc) h = fnv(hs, h);
     h = fnv(opts, h);
     int maj = 0, min = 0;
     nvrtcVersion(&maj, &min);
@@ -423,9 +426,8 @@ std::string compile_entry(Entry& e, const JitClass& c) {
         return "";
     }
     nvrtcProgram prog;
-    const char* hdr_src[7] = {kSrc_types_h, kSrc_format_h, kSrc_wide_cuh, kSrc_engine_cuh, kSrc_frontier_cuh,
-                              kSrc_phases_cuh, kSrc_jit_lane_cuh};
-    if (nvrtcCreateProgram(&prog, src.c_str(), "oob_jit_class.cu", 7, hdr_src, kHeaderNames) != NVRTC_SUCCESS)
+    if (nvrtcCreateProgram(&prog, src.c_str(), "oob_jit_class.cu", kNumHeaders, kHeaderSrc, kHeaderNames) !=
+        NVRTC_SUCCESS)
         return "nvrtcCreateProgram failed";
     std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DOOB_JIT=1",
                                      "--device-int128"};

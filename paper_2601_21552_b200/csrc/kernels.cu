@@ -23,6 +23,7 @@
 
 #include <cstdint>
 
+#include "cert.cuh"
 #include "engine.cuh"
 #include "format.h"
 #include "frontier.cuh"
@@ -183,6 +184,58 @@ __global__ void __launch_bounds__(THREADS) oob_root_kernel(LaunchArgs a) {
     }
 }
 
+// exact value of a job's element for the certificate check (a 256-bit value
+// beyond int128 becomes 2^126: "too big", which every check treats as unknown)
+__device__ __forceinline__ sym::i128 cert_value(long long x) { return x; }
+__device__ __forceinline__ sym::i128 cert_value(__int128 x) { return x; }
+__device__ __forceinline__ sym::i128 cert_value(const i256& x) {
+    const __int128 lo = x.low128();
+    const uint64_t s = lo < 0 ? ~0ull : 0ull;
+    return (x.w[2] == s && x.w[3] == s) ? lo : ((sym::i128)1 << 126);
+}
+
+// Fast mode (OOB_F_FAST): the Unsat certificate of each entry's structure
+// class (cert.cuh), checked numerically, one lane per entry, before the root
+// and solve kernels; a refuted entry is decided Unsat and never searched.
+// Entries are class-major, so a warp's lanes mostly share a certificate.
+template <typename T>
+__global__ void __launch_bounds__(128) oob_cert_kernel(LaunchArgs a) {
+    cert::BoxV B;
+    for (uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x; qi < a.n; qi += gridDim.x * blockDim.x) {
+        if (a.resume[qi] == RES_SKIP) continue;  // shadows
+        // the entry's class: the last class starting at or before qi
+        uint32_t lo = 0, hi = a.cert_nclasses;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (a.cert_classes[mid].q_begin <= qi) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t off = a.cert_classes[lo].cert;
+        if (off == NO_CERT) continue;
+        const QDesc d = a.qdesc[qi];
+        const uint32_t nv = d.nv_ncon & 0xFFFFu;
+        const T* src = reinterpret_cast<const T*>(a.data + d.data_off);
+        auto dom = [&](uint32_t i) -> sym::i128 { return cert_value(src[i]); };
+        auto lit = [&](uint32_t i) -> sym::i128 { return cert_value(src[2 * nv + i]); };
+        const uint64_t* c = a.certs + off;
+        const uint64_t ncerts = *c++;
+        bool refuted = false;
+        for (uint64_t k = 0; k < ncerts && !refuted; ++k) {
+            const uint64_t len = *c++;
+            refuted = cert::cert_check(c, dom, lit, B) == cert::C_REFUTED;
+            c += len;
+        }
+        if (!refuted) continue;
+        a.verdict[qi] = (int8_t)VERDICT_UNSAT;
+        a.err[qi] = (int8_t)ERR_NONE;
+        a.nodes[qi] = 0;
+        a.passes[qi] = 0;
+        a.elapsed[qi] = 0.f;
+        a.resume[qi] = RES_SKIP;
+        if (a.fast_stats) atomicAdd(a.fast_stats + 4, 1ull);
+    }
+}
+
 // propagate() / check_model() batches: one query per lane, no search
 template <typename T>
 __global__ void __launch_bounds__(THREADS) oob_aux_kernel(LaunchArgs a) {
@@ -263,6 +316,14 @@ cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t 
                              (int)smem);
         oob_root_kernel<__int128, 1><<<blocks, THREADS, smem, s>>>(a);
     }
+    return cudaGetLastError();
+}
+
+// fast mode certificate check of job `wide` (0 int64, 1 int128, 2 256-bit)
+cudaError_t launch_cert(const LaunchArgs& a, int wide, int blocks, cudaStream_t s) {
+    if (wide == 0) oob_cert_kernel<long long><<<blocks, 128, 0, s>>>(a);
+    else if (wide == 1) oob_cert_kernel<__int128><<<blocks, 128, 0, s>>>(a);
+    else if (wide == 2) oob_cert_kernel<i256><<<blocks, 128, 0, s>>>(a);
     return cudaGetLastError();
 }
 

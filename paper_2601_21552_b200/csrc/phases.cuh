@@ -7,6 +7,7 @@
 #pragma once
 #include "engine.cuh"
 #include "frontier.cuh"
+#include "symbolic.cuh"
 
 namespace oob {
 
@@ -253,6 +254,66 @@ __device__ __forceinline__ void release_slab(const LaunchArgs& a, uint32_t slot,
     }
 }
 
+// exact values of a job's value type for the symbolic prover (the 256-bit
+// regime stays with the exact emulation)
+template <typename T>
+struct SymVal {
+    static constexpr bool ok = false;
+    __device__ static sym::i128 get(const T&) { return 0; }
+};
+template <>
+struct SymVal<int> {
+    static constexpr bool ok = true;
+    __device__ static sym::i128 get(const int& x) { return x; }
+};
+template <>
+struct SymVal<long long> {
+    static constexpr bool ok = true;
+    __device__ static sym::i128 get(const long long& x) { return x; }
+};
+template <>
+struct SymVal<__int128> {
+    static constexpr bool ok = true;
+    __device__ static sym::i128 get(const __int128& x) { return x; }
+};
+
+// fast mode: the warp tries to refute query d symbolically (symbolic.cuh);
+// lane 0 builds the store, the lanes then search from one target each.  The
+// warp's frontier region is the scratch (the frontier re-initialises what it
+// uses).  src: the query's domains + literal slots in the job's layout.
+template <typename T>
+__device__ __noinline__ bool sym_refute_warp(const LaunchArgs& a, const QDesc& d, const T* src,
+                                             unsigned char* region, uint32_t lane) {
+    if (!SymVal<T>::ok) return false;
+    const unsigned FULL = 0xffffffffu;
+    sym::Store& S = *reinterpret_cast<sym::Store*>(region);
+    sym::LaneWork* W = reinterpret_cast<sym::LaneWork*>(region + sizeof(sym::Store));
+    const uint32_t nv = d.nv_ncon & 0xFFFFu, ncon = d.nv_ncon >> 16;
+    const uint32_t* cons = a.code + d.code_off;
+    const uint32_t* code = cons + ncon;
+    int r = sym::R_UNKNOWN;
+    const long long c0 = clock64();
+    if (lane == 0) {
+        auto dom = [&](uint32_t i) -> sym::i128 { return SymVal<T>::get(src[i]); };
+        auto lit = [&](uint32_t i) -> sym::i128 { return SymVal<T>::get(src[2 * nv + i]); };
+        r = sym::prepare(S, W[0], cons, code, nv, ncon, dom, lit);
+    }
+    r = __shfl_sync(FULL, r, 0);
+    __syncwarp();
+    const long long c1 = clock64();
+    if (a.fast_stats && lane == 0) atomicAdd(a.fast_stats + 2, (unsigned long long)(c1 - c0));
+    if (r != sym::R_CONTINUE) return r == sym::R_REFUTED;
+    const int nc = S.nc;
+    bool refuted = false;  // warp-uniform
+    for (int t0 = 0; t0 < nc && !refuted; t0 += 32) {
+        const int t = t0 + (int)lane;
+        const bool found = t < nc && sym::greedy_target(S, t, W[lane]);
+        refuted = __any_sync(FULL, found);
+    }
+    if (a.fast_stats && lane == 0) atomicAdd(a.fast_stats + 3, (unsigned long long)(clock64() - c1));
+    return refuted;
+}
+
 template <typename LaneT>
 __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, uint32_t warp, uint32_t lane) {
     const unsigned FULL = 0xffffffffu;
@@ -311,8 +372,34 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
         uint32_t region = 0;
         if (lane == 0) region = claim_region(a.fr_bitmap, a.fr_nregions, warp);
         region = __shfl_sync(FULL, region, 0);
-        R.bind((unsigned char*)a.fr_region + (size_t)region * a.fr_region_bytes, a.g.maxv, a.fr_ecap, a.fr_ucap,
-               a.fr_logcap);
+        unsigned char* rbase = (unsigned char*)a.fr_region + (size_t)region * a.fr_region_bytes;
+#if !defined(OOB_JIT)  // (the run-time compiled classes never run the frontier prover)
+        if (a.fast) {
+            typedef typename LaneT::T VT;
+            const VT* src = reinterpret_cast<const VT*>(((rs0 & RES_HANDOFF) && a.handoff ? a.handoff : a.data) +
+                                                        d.data_off);
+            const bool refuted = sym_refute_warp<VT>(a, d, src, rbase, lane);
+            if (lane == 0 && a.fast_stats) {
+                atomicAdd(a.fast_stats, 1ull);
+                if (refuted) atomicAdd(a.fast_stats + 1, 1ull);
+            }
+            if (refuted) {
+                if (lane == 0) {
+                    a.verdict[qi] = (int8_t)VERDICT_UNSAT;
+                    a.err[qi] = 0;
+                    a.nodes[qi] = 0;
+                    a.passes[qi] = 0;
+                    a.elapsed[qi] = (float)((double)(global_ns() - a.heavy_t0[qi]) * 1e-9);
+                    if (a.timeline) a.timeline[4 * (size_t)qi + 3] = global_ns();
+                    __threadfence();
+                    atomicAnd(a.fr_bitmap + (region >> 5), ~(1u << (region & 31)));
+                }
+                __syncwarp();
+                continue;
+            }
+        }
+#endif
+        R.bind(rbase, a.g.maxv, a.fr_ecap, a.fr_ucap, a.fr_logcap);
         frontier_query(L, a, R, qi, lane);
         __syncwarp();
         if (lane == 0) {

@@ -135,24 +135,35 @@ def solve_flat(fb: FlatBatch, timeout_s: float = 30.0, *, node_budget: int = 0,
     return out
 
 
+MODES = {"canonical": 0, "fast": _lib.F_FAST}
+
+
 def solve_batch(queries: Iterable, timeout_s: float = 30.0, *, node_budget: int = 0,
                 n_gpus: int = 0, device: int = 0, verdict_types=None,
-                stats: bool = False):
+                stats: bool = False, mode: str = "canonical"):
     """Decide many queries in one GPU batch.
 
     `queries`: iterable of `(variables, constraints)` pairs (reference-shaped
     objects or the JSON form).  Returns the list of verdicts in input order
-    (and the raw result arrays when `stats`)."""
+    (and the raw result arrays when `stats`).  `mode`: "canonical" (exact
+    emulation of the reference search: verdicts, models and node/pass
+    counters are the reference's) or "fast" (heavy queries first meet the
+    symbolic Unsat prover: verdicts and Sat models are the reference's,
+    counters of refuted queries are 0)."""
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r} (canonical, fast)")
     fb = flatten(list(queries))
-    out = solve_flat(fb, timeout_s, node_budget=node_budget, n_gpus=n_gpus, device=device)
+    out = solve_flat(fb, timeout_s, node_budget=node_budget, n_gpus=n_gpus, device=device,
+                     flags=MODES[mode])
     verdicts = _verdicts_from(out, fb, verdict_types or DEFAULT_VERDICT_TYPES)
     return (verdicts, out) if stats else verdicts
 
 
-def solve(variables, constraints, timeout_s: float = 30.0):
-    """Decide the conjunction over the given finite domains (solver.py:363)."""
+def solve(variables, constraints, timeout_s: float = 30.0, *, mode: str = "canonical"):
+    """Decide the conjunction over the given finite domains (solver.py:363).
+    One query runs on one device (n_gpus=1)."""
     types = DEFAULT_VERDICT_TYPES
-    return solve_batch([(variables, constraints)], timeout_s, verdict_types=types)[0]
+    return solve_batch([(variables, constraints)], timeout_s, n_gpus=1, verdict_types=types, mode=mode)[0]
 
 
 # ----- propagate / check_model ------------------------------------------------
