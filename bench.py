@@ -1,34 +1,44 @@
 """Benchmark of the OOB-query decision engine (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c3|c4|c5s] [--queries Q]
+                    [--config c3|c4|c5|c5s] [--queries Q] [--mode fast|canonical]
 
-One STEP = deciding one batch of Q synthetic analyzer-shaped queries (default
-config C3: 100K queries, M = 2^31-1, input caps 2^3..2^7, 30% buggy, seed
-2601215521) with verdicts and first models identical to the
-reference solver.  Under torchrun each rank decides its own Q-query slice of
-the stream on its own GPU (weak scaling, no data-path collective: queries are
-independent).
+One STEP = deciding one batch of synthetic analyzer-shaped queries with
+verdicts (and, for Sat, first models) identical to the reference solver.
 
-  value   queries/s with the compiled records resident in HBM: K launches of
-          the decision kernel(s), timed with CUDA events on the engine stream
-          (oob_plan_run), L2 flushed between steps, max over ranks.
-  e2e     queries/s through the public C-ABI call oob_solve_batch on host
-          buffers: host compile + H2D + kernels + D2H + scatter, every step.
-  corpus  the 110 solver queries of the reference's 20-program corpus decided
-          in one batch (wall time, verdicts vs the golden capture).
+  N = 1   config C3 (BASELINE configs[2]): 100K queries, M = 2^31-1, input caps
+          2^3..2^7, 30% buggy, seed 2601215521.
+  N > 1   config C4 (BASELINE configs[3]): 1M mixed 32/64-bit queries IN TOTAL,
+          sharded over the N ranks (strong scaling; one process per GPU, no
+          data-path collective: queries are independent).
+
+Modes: "fast" (default; OOB_F_FAST: per-class Unsat
+certificates checked on the device, then the exact emulation for the rest:
+verdicts and Sat models are the reference's) and "canonical" (exact emulation
+of every query, node/pass counters included).  The line carries both.
+
+  value     queries/s with the compiled records resident in HBM: K plan runs,
+            CUDA events on the engine stream (oob_plan_run), L2 flushed
+            between steps, max over ranks.
+  e2e       queries/s through the public C-ABI call oob_solve_batch on host
+            buffers (host compile + H2D + kernels + D2H + scatter, every step).
+  corpus    the 110 solver queries of the reference's 20-program corpus in one
+            batch; corpus_analysis: the reference ANALYZER (front end
+            unchanged) over the 20 programs with the GPU engine, warm and
+            cold, next to the reference's own analyze_source on this box.
+  c5_proper BASELINE configs[4]: the adversarial Unsat-by-construction family at
+            input caps 2^20 (2000 queries), where the reference times out.
+  strong_c4_1m (N = 1) the N > 1 workload on one GPU: the denominator of the
+            strong-scaling efficiency.
   cpu_baseline / --impl reference
-          the C restatement of the reference solver (oracle/, kind "port") on
-          the host cores, on a bounded sample of the same stream (N=1 only),
-          with verdict / node / pass / model-word parity on that sample.
-  witness_replay
-          every Sat model of the e2e step checked by the restated reference
-          evaluator (check_model over constraints + divisor side constraints).
-  roofline / roofline.issue
-          HBM (contract form: algorithmic bytes / kernel time vs the measured
-          copy bandwidth, ncu DRAM bytes as `traffic`) and the integer-issue
-          roofline (ncu warp instructions per step / live step time vs the SM
-          issue peak), from the committed profiles/ncu_summary.json.
+            the C restatement of the reference solver (oracle/, kind "port") on
+            all host cores over the SAME batch (C3: all 100K queries), with
+            parity on it; --impl reference also times the Python reference
+            itself (baseline/_ref) on a 10K-query sample of the stream.
+  roofline  the dominant kernel from the committed ncu capture of this exact
+            workload (profiles/ncu_summary.json): HBM form of the contract and
+            the integer-issue roofline (warp instructions / live step time vs
+            the SM issue peak).
 """
 from __future__ import annotations
 
@@ -60,8 +70,11 @@ WORKLOADS = {
           "2^3..2^7, 30% buggy, templates T1-T7, seed 2601215521",
     "c4": "C4: mixed 32/64-bit (M in {2^31-1, 2^59}), caps 2^3..2^10, templates T1-T8, "
           "seed 2601215522",
+    "c5": "C5 proper: adversarial bug-free templates (Unsat by construction), input caps 2^20, "
+          "seed 2601215523",
     "c5s": "C5 regenerated at caps 2^6 (bug-free, Unsat by construction), seed 2601215523",
 }
+C4_STRONG_TOTAL = 1_000_000
 
 
 def parse():
@@ -70,12 +83,39 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--config", default="c3", choices=tuple(WORKLOADS))
-    ap.add_argument("--queries", type=int, default=100_000)
+    ap.add_argument("--config", default=None, choices=tuple(WORKLOADS),
+                    help="default: c3 at N=1, c4 (1M total, strong scaling) at N>1")
+    ap.add_argument("--queries", type=int, default=None,
+                    help="queries per step in total (default: 100K per GPU for c3/c5s, 1M for c4, 2000 for c5)")
+    ap.add_argument("--mode", default="fast", choices=("fast", "canonical"))
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
-                    help="target CPU time of the bounded cpu_baseline sample")
+                    help="target CPU time of the reference arm's bounded samples")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="value + e2e only (quick runs)")
     return ap.parse_args()
+
+
+def workload(args, world):
+    """(config, total queries per step, per-rank slice size, scaling)."""
+    cfg = args.config or ("c3" if world == 1 else "c4")
+    if cfg == "c4" and args.config is None and world > 1:
+        total = args.queries or C4_STRONG_TOTAL
+        return cfg, total, (total + world - 1) // world, "strong"
+    if cfg == "c5":
+        per = args.queries or 2000
+    elif cfg == "c4" and world == 1:
+        per = args.queries or 100_000
+    else:
+        per = args.queries or 100_000
+    return cfg, per * world, per, "weak"
+
+
+def config_dict(cfg, total, per, scaling, world, mode):
+    """The `config` object of both arms' lines (identical for identical flags)."""
+    return {"workload": WORKLOADS[cfg], "config": cfg, "queries_per_step": total,
+            "queries_per_gpu": per, "mode": mode,
+            "scaling": scaling, "parallelism": f"dp{world} (query shards, no collective)",
+            "l2": "flushed (256 MiB write) between timed steps"}
 
 
 # ----- distributed plumbing ---------------------------------------------------
@@ -90,7 +130,6 @@ def dist_env():
 class Dist:
     def __init__(self, world, local, backend="nccl"):
         self.world = world
-        self.pg = None
         if world > 1:
             import torch
             import torch.distributed as td
@@ -105,19 +144,18 @@ class Dist:
         if self.world > 1:
             self.td.barrier()
 
-    def max(self, x: float) -> float:
+    def _reduce(self, x, op):
         if self.world == 1:
             return x
         t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
-        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        self.td.all_reduce(t, op=op)
         return float(t.item())
 
+    def max(self, x: float) -> float:
+        return self._reduce(x, self.td.ReduceOp.MAX) if self.world > 1 else x
+
     def sum(self, x: float) -> float:
-        if self.world == 1:
-            return x
-        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
-        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
-        return float(t.item())
+        return self._reduce(x, self.td.ReduceOp.SUM) if self.world > 1 else x
 
     def close(self):
         if self.world > 1:
@@ -148,7 +186,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t.start()
@@ -181,32 +219,65 @@ def flush_l2(torch_mod, device):
 flush_l2.buf = {}
 
 
-# ----- CPU baseline (oracle port; test-infrastructure restatement) ----------------
-
-def cpu_baseline(fb_all, target_s: float, threads: int):
-    """Bounded sample of the same stream on the host cores via the C oracle."""
-    from oracle import oracle
-    from paper_2601_21552_b200.wire import FlatBatch  # noqa: F401
-    probe = min(fb_all.n, 2000)
-    t0 = time.perf_counter()
-    oracle.solve_flat(fb_all.slice(0, probe), 30.0, threads=threads)
-    dt = max(time.perf_counter() - t0, 1e-6)
-    n = int(min(fb_all.n, max(probe, probe * target_s / dt)))
-    sample = fb_all.slice(0, n)
-    t0 = time.perf_counter()
-    out = oracle.solve_flat(sample, 30.0, threads=threads)
-    dt = time.perf_counter() - t0
-    return {"value": round(n / dt, 1), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {n} queries of the same stream ({dt:.1f} s on {threads} threads; "
-                      "oracle/oob_oracle.c restatement of solver.py)"}, out, n
-
-
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
 
+
+# ----- CPU legs (oracle = test-infrastructure restatement of the reference) ------
+
+def port_decide(fb, threads, timeout=30.0):
+    from oracle import oracle
+    t0 = time.perf_counter()
+    out = oracle.solve_flat(fb, timeout, threads=threads)
+    return out, time.perf_counter() - t0
+
+
+def port_sample_size(fb, threads, target_s):
+    """Queries of fb the port decides in about target_s (whole batch if less)."""
+    from oracle import oracle
+    probe = min(fb.n, 2000)
+    t0 = time.perf_counter()
+    oracle.solve_flat(fb.slice(0, probe), 30.0, threads=threads)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    return int(min(fb.n, max(probe, probe * target_s / dt)))
+
+
+def _py_solve(q):
+    import scuba_mini.solver as S
+    from paper_2601_21552_b200.terms import query_from_json
+    v, c = query_from_json(q, S)
+    r = S.solve(v, c, 30.0)
+    return {"Sat": 1, "Unsat": 0}.get(type(r).__name__, 2)
+
+
+def _py_init(pkg):
+    sys.path.insert(0, pkg)
+
+
+def python_reference(fb, n, threads):
+    """The Python reference's own solve() (baseline/_ref, unmodified) on the
+    first n queries of the stream, one process per host core."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from conftest import reference_paths
+    pkg, _ = reference_paths()
+    if pkg is None:
+        return None, None
+    import multiprocessing as mp
+    qs = [fb.query_json(q) for q in range(n)]
+    with mp.get_context("fork").Pool(threads, initializer=_py_init, initargs=(str(pkg),)) as pool:
+        pool.map(_py_solve, qs[: min(n, 4 * threads)], chunksize=1)  # import warm-up
+        t0 = time.perf_counter()
+        v = pool.map(_py_solve, qs, chunksize=16)
+        dt = time.perf_counter() - t0
+    return {"value": round(n / dt, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"first {n} queries of the same stream, scuba_mini.solver.solve from baseline/_ref "
+                      f"(unmodified Python reference), {dt:.1f} s on {threads} processes"}, np.array(v, np.int8)
+
+
+# ----- profiles ----------------------------------------------------------------------
 
 def load_peak_hbm():
     try:
@@ -215,86 +286,118 @@ def load_peak_hbm():
         return HBM_FALLBACK, "fallback"
 
 
-def ncu_alu(config: str):
-    """Issue / ALU-pipe utilisation of the dominant kernel from the committed
-    ncu --set full summary (profiles/ncu_summary.json), or None."""
+def ncu_entry(cfg, mode, per):
+    """The committed ncu launch-list summary of exactly this workload (config,
+    mode and queries per step; profiles/ncu_summary.json), or None."""
     try:
         d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
-        return d.get(config, {}).get("alu_evidence")
     except Exception:
         return None
+    return d.get(f"{cfg}/{mode}/{per}")
 
 
-def alu_roofline(config: str, launch_ms: float, sms: int = 148):
-    """Integer-pipe roofline of the decision kernels: warp instructions of one
-    step (ncu smsp__inst_executed.sum over all launches, committed in
-    profiles/ncu_summary.json) / the live device time of a step, against the
-    SM issue peak (4 schedulers x 1 warp-instruction/clock x sm_max_mhz x
-    SMs), next to the measured LOP3 peak (tools/alu_peak.cu,
-    profiles/alu_peak.jsonl)."""
-    try:
-        d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text()).get(config, {})
-        inst = float(d["warp_inst_per_step"])
-    except Exception:
-        return None
-    try:
-        mhz = float(json.loads(PEAKS.read_text())["sm_max_mhz"])
-    except Exception:
-        mhz = 1965.0
-    peak = sms * 4 * mhz * 1e6
-    lop3 = None
-    try:
-        for line in (ROOT / "profiles" / "alu_peak.jsonl").read_text().splitlines():
-            r = json.loads(line)
-            if r["kind"] == "lop3":
-                lop3 = r["warp_inst_per_s"]
-    except Exception:
-        pass
-    achieved = inst / (launch_ms / 1e3)
-    return {"bound": "issue (integer ALU / latency)", "unit": "warp-inst/s",
-            "warp_inst_per_step": inst, "achieved": round(achieved, 1), "issue_peak": peak,
-            "frac": round(achieved / peak, 4), "lop3_peak_measured": lop3}
-
-
-def ncu_traffic(config: str):
-    """DRAM bytes of one step (all launches of one plan run) from the
-    committed ncu launch-list summary (profiles/ncu_summary.json), or None."""
-    p = ROOT / "profiles" / "ncu_summary.json"
-    try:
-        d = json.loads(p.read_text())
-        return d.get(config, {}).get("dram_bytes_per_step")
-    except Exception:
-        return None
+def rooflines(cfg, mode, per, launch_ms, info):
+    peak, peak_kind = load_peak_hbm()
+    alg_bytes = info["record_bytes"] + info["result_bytes"]
+    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+    ent = ncu_entry(cfg, mode, per)
+    r = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+         "frac": round(achieved / peak, 5), "traffic": ent.get("dram_bytes_per_step") if ent else None,
+         "algorithmic_bytes_per_launch": alg_bytes,
+         "note": "the decision kernels are integer-ALU/latency bound: bytes = compiled records + results "
+                 "per step, all launches (DESIGN.md section 7); see `issue`"}
+    if ent:
+        try:
+            mhz = float(json.loads(PEAKS.read_text())["sm_max_mhz"])
+        except Exception:
+            mhz = 1965.0
+        ipeak = 148 * 4 * mhz * 1e6
+        inst = float(ent["warp_inst_per_step"])
+        ach = inst / (launch_ms / 1e3)
+        r["issue"] = {"bound": "issue (integer ALU / latency)", "unit": "warp-inst/s",
+                      "warp_inst_per_step": inst, "achieved": round(ach, 1), "issue_peak": ipeak,
+                      "frac": round(ach / ipeak, 4), "source": ent.get("source"),
+                      "dominant_kernel": ent.get("dominant_kernel")}
+        if ent.get("alu_evidence"):
+            r["alu"] = ent["alu_evidence"]
+    return r
 
 
 # ----- arms -------------------------------------------------------------------------
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU restatement of the reference solver (port) on
-    all host threads; rank 0 only."""
+    """--impl reference: the reference's own CPU implementation of the path on
+    the box's host cores: the C restatement (oracle/, "port") over the same
+    workload, plus the Python reference itself on a 10K sample.  Rank 0 only;
+    never loads the engine library (the generator is oracle/liboob_synth.so)."""
     if rank != 0:
         return
-    from paper_2601_21552_b200 import synth
+    from oracle import oracle
+    cfg, total, per, scaling = workload(args, world)
     threads = host_threads()
-    fb = synth.generate(args.config, args.queries, first=0, names=False)
-    per_step = []
+    fb = oracle.synth_generate(cfg, total)
+    # whole batch per step when the port gets through it in the budget
+    # (C3: 100K in ~2 s); otherwise a bounded prefix sample of the stream
+    n = port_sample_size(fb, threads, max(args.cpu_seconds / max(args.steps, 1), 2.0))
+    sample = fb if n >= fb.n else fb.slice(0, n)
+    vals = []
+    out = None
     for i in range(args.warmup + args.steps):
-        target = args.cpu_seconds / max(args.steps, 1)
-        res, _, n = cpu_baseline(fb, max(target, 2.0), threads)
+        out, dt = port_decide(sample, threads)
         if i >= args.warmup:
-            per_step.append(res["value"])
-    value = statistics.median(per_step)
+            vals.append(n / dt)
+    value = statistics.median(vals)
+    py, pyv = python_reference(fb, min(fb.n, 10_000 if cfg in ("c3", "c5s") else 2_000), threads)
+    if py is not None:
+        k = len(pyv)
+        decided = pyv != 2
+        py["verdicts_equal_port_where_decided"] = bool(np.array_equal(pyv[decided], out["verdict"][:k][decided]))
+        py["timeouts"] = int((~decided).sum())
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * args.queries / value, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "ms_per_step": round(1e3 * total / value, 3), "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": WORKLOADS[args.config], "queries_per_gpu": args.queries},
-        "cpu_baseline": {**res, "value": value},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": config_dict(cfg, total, per, scaling, world, args.mode),
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": (f"all {n} queries of the step" if n >= fb.n else
+                                    f"first {n} of the step's {fb.n} queries") +
+                         " per step, oracle/oob_oracle.cpp (C restatement of solver.py) on all host threads"},
+        "python_reference": py,
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def plan_runs(_lib, fb, flags, device, steps, warmup, torch, dist=None, clocks_dev=None):
+    plan = _lib.Plan(fb, 30.0, n_gpus=1, device=device, flags=flags)
+    for _ in range(warmup):
+        plan.run()
+    ms = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(clocks_dev) if clocks_dev is not None else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        for _ in range(steps):
+            flush_l2(torch, device)
+            torch.cuda.synchronize()
+            ms.append(plan.run())
+        torch.cuda.synchronize()
+    finally:
+        if sampler:
+            sampler.__exit__()
+    if dist:
+        dist.barrier()
+    res = plan.results()
+    if res["status"] != _lib.OOB_OK:
+        raise SystemExit(f"engine could not decide the batch: {_lib.last_error()}")
+    info = plan.info()
+    plan.close()
+    return ms, res, info, (sampler.summary() if sampler else None)
 
 
 def run_ours(args, rank, world, local):
@@ -308,133 +411,152 @@ def run_ours(args, rank, world, local):
     if ndev < 1:
         raise SystemExit("bench.py needs a CUDA device (the engine has no CPU path)")
     # one rank per GPU over NCCL; with fewer GPUs than ranks (a test of the
-    # multi-rank path on a small box) ranks share devices and the barrier /
-    # max-over-ranks reductions run over gloo
+    # multi-rank path on a small box) ranks share devices over gloo
     dist = Dist(world, local % ndev, backend="nccl" if ndev >= world else "gloo")
     device = local % ndev
-    Q = args.queries
-    fb = synth.generate(args.config, Q, first=rank * Q, names=False)
-
-    # ---- value: kernels on HBM-resident records --------------------------------
-    plan = _lib.Plan(fb, 30.0, n_gpus=1, device=device)
-    info = plan.info()
     torch.cuda.set_device(device)
-    for _ in range(args.warmup):
-        plan.run()
-    kernel_ms = []
-    dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(device) as clocks:
-        for _ in range(args.steps):
-            flush_l2(torch, device)
-            torch.cuda.synchronize()
-            kernel_ms.append(plan.run())
-        torch.cuda.synchronize()
-    dist.barrier()
-    total_ms = dist.max(sum(kernel_ms))
-    res = plan.results()
-    if res["status"] != _lib.OOB_OK:
-        raise SystemExit(f"engine could not decide the batch: {_lib.last_error()}")
-    info = plan.info()  # result bytes of a fetched run (Sat models packed on the device)
-    plan.close()  # its device pools are freed before the e2e leg allocates its own
-    value = dist.sum(Q) * args.steps / (total_ms / 1e3)
+    cfg, total, per, scaling = workload(args, world)
+    first = rank * per
+    n_mine = max(0, min(per, total - first))
+    fb = synth.generate(cfg, n_mine, first=first, names=False)
+    flags = _lib.F_FAST if args.mode == "fast" else 0
 
-    # ---- e2e: the public C-ABI call on host buffers ------------------------------
-    solve_flat(fb, 30.0, n_gpus=1, device=device)  # warm
+    # ---- value: kernels on HBM-resident records -----------------------------------
+    kernel_ms, res, info, clocks = plan_runs(_lib, fb, flags, device, args.steps, args.warmup, torch, dist,
+                                             clocks_dev=device)
+    total_ms = dist.max(sum(kernel_ms))
+    value = dist.sum(n_mine) * args.steps / (total_ms / 1e3)
+
+    # ---- the other mode, same batch (kernel-resident) ------------------------------
+    other = None
+    if not args.no_extras and cfg != "c5":
+        oflags = 0 if flags else _lib.F_FAST
+        oms, ores, _, _ = plan_runs(_lib, fb, oflags, device, args.steps, 1, torch, dist)
+        ototal = dist.max(sum(oms))
+        same = bool(np.array_equal(ores["verdict"], res["verdict"]) and np.array_equal(ores["model"], res["model"]))
+        other = {"mode": "canonical" if flags else "fast", "value": round(dist.sum(n_mine) * args.steps /
+                                                                          (ototal / 1e3), 1),
+                 "ms_per_step": round(ototal / args.steps, 3), "verdicts_and_models_identical": same}
+
+    # ---- e2e: the public C-ABI call on host buffers ----------------------------------
+    solve_flat(fb, 30.0, n_gpus=1, device=device, flags=flags)  # warm
     e2e_s = []
     dist.barrier()
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        out = solve_flat(fb, 30.0, n_gpus=1, device=device)
+        out = solve_flat(fb, 30.0, n_gpus=1, device=device, flags=flags)
         e2e_s.append(time.perf_counter() - t0)
     dist.barrier()
     e2e_total = dist.max(sum(e2e_s))
-    e2e_value = dist.sum(Q) * args.steps / e2e_total
+    e2e_value = dist.sum(n_mine) * args.steps / e2e_total
     assert np.array_equal(out["verdict"], res["verdict"]), "plan and solve_batch disagree"
-    assert np.array_equal(out["nodes"], res["nodes"])
+    assert np.array_equal(out["model"], res["model"])
 
-    # ---- corpus (config C2: the reference's 20 programs, 110 queries) -------------
-    corpus = None
-    if rank == 0:
-        recs = [json.loads(l) for l in open(ROOT / "tests/golden/corpus_m1048576.jsonl")]
-        cfb = flatten(recs)
-        solve_flat(cfb, 30.0, n_gpus=1, device=device)
-        walls = []
-        for _ in range(5):
-            t0 = time.perf_counter()
-            cout = solve_flat(cfb, 30.0, n_gpus=1, device=device)
-            walls.append(time.perf_counter() - t0)
-        want = np.array([{"unsat": 0, "sat": 1}[r["verdict"]] for r in recs])
-        corpus = {"queries": len(recs), "wall_ms_best": round(1e3 * min(walls), 3),
-                  "wall_ms_median": round(1e3 * statistics.median(walls), 3),
-                  "verdicts_identical": bool(np.array_equal(cout["verdict"], want)),
-                  "sat": int((cout["verdict"] == 1).sum()),
-                  "reference_python_ms": round(sum(r["ref_ms"] for r in recs), 1)}
-
-    # ---- CPU baseline + parity on its sample ---------------------------------------
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = host_threads()
-        cpu, cres, n = cpu_baseline(fb, args.cpu_seconds, threads)
-        mism = int((cres["verdict"][:n] != res["verdict"][:n]).sum())
-        mism += int((cres["nodes"][:n] != res["nodes"][:n]).sum())
-        mism += int((cres["passes"][:n] != res["passes"][:n]).sum())
-        vend = int(fb.var_begin[n])
-        model_mism = int((cres["model"][:vend] != out["model"][:vend]).any(axis=1).sum())
-        cpu["parity_sample"] = {"queries": n, "verdict_node_or_pass_mismatches": mism,
-                                "model_word_mismatches": model_mism}
-
-    # ---- witness replay: every Sat model of the step through the reference's
-    # evaluator (check_model over constraints + divisor side constraints,
-    # solver.py:319/:345, restated in oracle/) -------------------------------------
-    replay = None
-    if rank == 0:
-        from oracle import oracle
-        ok = oracle.check_model_flat(fb, out["model"])
-        sat = out["verdict"] == 1
-        replay = {"sat_witnesses": int(sat.sum()),
-                  "replayed_true": int((ok[sat] == 1).sum()),
-                  "evaluator": "check_model(constraints + divisor_side_constraints) restated "
-                               "in oracle/oob_oracle.cpp"}
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        extras = rank0_extras(args, cfg, fb, res, out, device, flags, world, _lib, synth, solve_flat, flatten, torch)
 
     dist.close()
     if rank != 0:
         return
-    peak, peak_kind = load_peak_hbm()
     launch_ms = sum(kernel_ms) / len(kernel_ms)
-    alg_bytes = info["record_bytes"] + info["result_bytes"]
-    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     n_sat = int((res["verdict"] == 1).sum())
+    conf = config_dict(cfg, total, per, scaling, world, args.mode)
+    conf.update({"classes": info["classes"], "wide_regime_queries": info["wide_queries"], "sat": n_sat,
+                 "unsat": int((res["verdict"] == 0).sum())})
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "scaling": scaling, "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (seeded analyzer-shaped query stream, generated natively)",
-        "config": {"workload": WORKLOADS[args.config], "queries_per_gpu": Q,
-                   "l2": "flushed (256 MiB write) between timed steps",
-                   "classes": info["classes"], "int128_regime_queries": info["wide_queries"],
-                   "sat": n_sat, "unsat": int((res["verdict"] == 0).sum()),
-                   "parallelism": f"dp{world} (query shards, no collective)"},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 5),
-                     "traffic": ncu_traffic(args.config),
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "note": "interval-propagation DFS is integer-ALU/latency bound; "
-                             "bytes = compiled records + results per step, all launches (DESIGN.md)",
-                     "alu": ncu_alu(args.config),
-                     "issue": alu_roofline(args.config, launch_ms)},
-        "cpu_baseline": cpu,
+        "config": conf,
+        "roofline": rooflines(cfg, args.mode, per, launch_ms, info),
+        "cpu_baseline": extras.get("cpu_baseline"),
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
                 "h2d_bytes_per_step": info["record_bytes"],
                 "d2h_bytes_per_step": info["result_bytes"]},
-        "clocks": clocks.summary(),
+        "clocks": clocks,
         "gpu_launches": info["launches_per_run"] * args.steps,
-        "corpus": corpus,
-        "witness_replay": replay,
+        "other_mode": other,
         "kernel_ms_per_step": [round(x, 3) for x in kernel_ms],
     }
+    for k in ("corpus", "corpus_analysis", "c5_proper", "strong_c4_1m", "witness_replay"):
+        if k in extras:
+            line[k] = extras[k]
     print(json.dumps(line), flush=True)
+
+
+def rank0_extras(args, cfg, fb, res, out, device, flags, world, _lib, synth, solve_flat, flatten, torch):
+    ex = {}
+    # corpus solver batch (config C2's 110 queries)
+    recs = [json.loads(l) for l in open(ROOT / "tests/golden/corpus_m1048576.jsonl")]
+    cfb = flatten(recs)
+    want = np.array([{"unsat": 0, "sat": 1}[r["verdict"]] for r in recs])
+    corpus = {"queries": len(recs), "reference_python_ms": round(sum(r["ref_ms"] for r in recs), 1)}
+    for name, fl in (("fast", _lib.F_FAST), ("canonical", 0)):
+        solve_flat(cfb, 30.0, n_gpus=1, device=device, flags=fl)
+        walls = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            cout = solve_flat(cfb, 30.0, n_gpus=1, device=device, flags=fl)
+            walls.append(time.perf_counter() - t0)
+        corpus[name] = {"wall_ms_median": round(1e3 * statistics.median(walls), 3),
+                        "verdicts_identical": bool(np.array_equal(cout["verdict"], want))}
+    ex["corpus"] = corpus
+    # the reference analyzer over the corpus with the GPU engine (config C2)
+    try:
+        r = subprocess.run([sys.executable, str(ROOT / "tools/corpus_wall.py"), args.mode],
+                           capture_output=True, text=True, timeout=300)
+        ex["corpus_analysis"] = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, not fatal
+        ex["corpus_analysis"] = {"unavailable": f"{type(e).__name__}: {e}"}
+    # C5 proper (configs[4]): fast mode decides the whole family
+    if world == 1 and cfg != "c5":
+        c5 = synth.generate("c5", 2000, names=False)
+        ms, c5res, _, _ = plan_runs(_lib, c5, _lib.F_FAST, device, 5, 2, torch)
+        v = c5res["verdict"]
+        ex["c5_proper"] = {"queries": 2000, "mode": "fast", "value": round(2000 / (statistics.median(ms) / 1e3), 1),
+                           "ms_per_step": round(statistics.median(ms), 3), "unsat": int((v == 0).sum()),
+                           "sat": int((v == 1).sum()), "timeout": int((v == 2).sum()),
+                           "reference": "Python reference and canonical mode time out on 674/2000 at the "
+                                        "30 s per-query timeout (profiles/r01_c5_probe.txt)"}
+    # N>1 workload on one GPU (strong-scaling denominator)
+    if world == 1 and cfg == "c3":
+        c4 = synth.generate("c4", C4_STRONG_TOTAL, names=False)
+        ms, _, _, _ = plan_runs(_lib, c4, flags, device, 3, 1, torch)
+        ex["strong_c4_1m"] = {"queries": C4_STRONG_TOTAL, "mode": args.mode,
+                              "value": round(C4_STRONG_TOTAL / (statistics.median(ms) / 1e3), 1),
+                              "ms_per_step": round(statistics.median(ms), 3)}
+        del c4
+    # CPU baseline: the port on the same batch, with parity
+    if world == 1 and not args.no_cpu_baseline:
+        threads = host_threads()
+        n = port_sample_size(fb, threads, args.cpu_seconds)
+        sample = fb if n >= fb.n else fb.slice(0, n)
+        cres, dt = port_decide(sample, threads)
+        vend = int(fb.var_begin[n])
+        cpu = {"value": round(n / dt, 1), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": (f"all {n} queries of the step" if n >= fb.n else f"first {n} queries of the step") +
+                         f" ({dt:.1f} s on {threads} threads; oracle/oob_oracle.cpp restatement of solver.py)",
+               "parity": {"queries": n,
+                          "verdict_mismatches": int((cres["verdict"] != res["verdict"][:n]).sum()),
+                          "sat_model_word_mismatches": int((cres["model"][:vend] != out["model"][:vend])
+                                                           .any(axis=1).sum())}}
+        if not flags:
+            cpu["parity"]["node_or_pass_mismatches"] = int((cres["nodes"] != res["nodes"][:n]).sum() +
+                                                           (cres["passes"] != res["passes"][:n]).sum())
+        ex["cpu_baseline"] = cpu
+    # witness replay: every Sat model of the e2e step through the reference's
+    # evaluator (check_model over constraints + divisor side constraints,
+    # solver.py:319/:345, restated in oracle/)
+    from oracle import oracle
+    ok = oracle.check_model_flat(fb, out["model"])
+    sat = out["verdict"] == 1
+    ex["witness_replay"] = {"sat_witnesses": int(sat.sum()), "replayed_true": int((ok[sat] == 1).sum()),
+                            "evaluator": "check_model(constraints + divisor_side_constraints) restated in "
+                                         "oracle/oob_oracle.cpp"}
+    return ex
 
 
 def main():

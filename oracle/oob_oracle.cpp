@@ -221,7 +221,7 @@ struct View {
     std::vector<uint8_t> rel;
     std::vector<int32_t> lhs, rhs;
     int nuser = 0;
-    int opc(int32_t n) const { return n == LIT_ONE ? OOB_NODE_LIT : op[n]; }
+    int opc(int32_t n) const { return n == LIT_ONE ? (int)OOB_NODE_LIT : (int)op[n]; }
     i128 litv(int32_t n) const { return n == LIT_ONE ? 1 : from_w(lit[na[n]]); }
     bool same(int32_t x, int32_t y) const {  // dataclass equality
         if (x == y) return true;

@@ -15,14 +15,37 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB = HERE / "liboob_oracle.so"
+SYNTH_LIB = HERE / "liboob_synth.so"
 
 _lib = None
 
 
 def build(force: bool = False) -> Path:
-    if force or not LIB.exists() or LIB.stat().st_mtime < (HERE / "oob_oracle.cpp").stat().st_mtime:
+    synth_src = HERE.parent / "paper_2601_21552_b200" / "csrc" / "synth.cpp"
+    stale = (not LIB.exists() or LIB.stat().st_mtime < (HERE / "oob_oracle.cpp").stat().st_mtime
+             or not SYNTH_LIB.exists() or SYNTH_LIB.stat().st_mtime < synth_src.stat().st_mtime)
+    if force or stale:
         subprocess.check_call(["make", "-s", "-C", str(HERE)])
     return LIB
+
+
+_synth = None
+
+
+def synth_lib():
+    """The seeded query generator (csrc/synth.cpp) built into oracle/ (no
+    engine library involved)."""
+    global _synth
+    if _synth is None:
+        if not SYNTH_LIB.exists():
+            build()
+        _synth = ctypes.CDLL(str(SYNTH_LIB))
+    return _synth
+
+
+def synth_generate(config: str, n: int, first: int = 0, names: bool = False):
+    from paper_2601_21552_b200 import synth
+    return synth.generate(config, n, first=first, names=names, lib=synth_lib())
 
 
 def lib():

@@ -34,6 +34,11 @@ namespace oob {
 namespace cert {
 
 using sym::i128;
+#if defined(__CUDA_ARCH__)
+#define CERT_INL __forceinline__
+#else
+#define CERT_INL inline
+#endif
 constexpr uint64_t MAGIC = 0x4345525431ull;  // "CERT1"
 constexpr int MAXB = 64;                     // box entries (variables + parameters + atoms)
 
@@ -43,7 +48,7 @@ struct BoxV {  // [0, np) parameters, [np, np + nv) variables, then atoms
     int np;
 };
 
-OOB_HD inline bool mono_iv_b(uint64_t k, const BoxV& B, i128& rl, i128& rh) {
+OOB_HD CERT_INL bool mono_iv_b(uint64_t k, const BoxV& B, i128& rl, i128& rh) {
     rl = rh = 1;
     while (k >> 56) {
         const int v = (int)(k >> 56) - 1;
@@ -59,7 +64,7 @@ OOB_HD inline bool mono_iv_b(uint64_t k, const BoxV& B, i128& rl, i128& rh) {
 }
 // interval of the blob polynomial at p (advances p past it); parameter runs
 // are collapsed first (sym::peval)
-OOB_HD inline bool peval_blob(const uint64_t*& p, const BoxV& B, i128& lo, i128& hi) {
+OOB_HD CERT_INL bool peval_blob(const uint64_t*& p, const BoxV& B, i128& lo, i128& hi) {
     const uint64_t n = *p++;
     const uint64_t* t = p;
     p += 3 * n;
@@ -90,13 +95,13 @@ OOB_HD inline bool peval_blob(const uint64_t*& p, const BoxV& B, i128& lo, i128&
     }
     return true;
 }
-OOB_HD inline void skip_poly(const uint64_t*& p) { p += 1 + 3 * p[0]; }
+OOB_HD CERT_INL void skip_poly(const uint64_t*& p) { p += 1 + 3 * p[0]; }
 
 enum : int { C_UNKNOWN = 0, C_REFUTED = 1 };
 
 // dom(i): declared domain word i (lo/hi interleaved), lit(slot): literal slot
 template <typename GetDom, typename GetLit>
-OOB_HD inline int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& B, int* why = nullptr) {
+OOB_HD CERT_INL int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& B, int* why = nullptr) {
     int dummy;
     int& reason = why ? *why : dummy;  // 1 header 2 values 3 atoms 4 guards0 5 guards1 6 final
     if (p[0] != MAGIC) return C_UNKNOWN;

@@ -1380,6 +1380,8 @@ size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
     return (b + 255) & ~(size_t)255;
 }
 
+constexpr size_t DEVICE_STACK_BYTES = 4096;
+
 std::string ensure_stream(DevicePool* P, int dev) {
     CK(cudaSetDevice(dev));
     if (!P->stream) {
@@ -1388,6 +1390,11 @@ std::string ensure_stream(DevicePool* P, int dev) {
         CK(cudaEventCreate(&P->ev1));
         CK(cudaEventCreateWithFlags(&P->evr, cudaEventDisableTiming));
         CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
+        // per-thread stack: the deepest kernels (root phase, certificate
+        // check, 256-bit solve) need up to ~2.2 KB; the default is 1 KB
+        size_t stack = 0;
+        CK(cudaDeviceGetLimit(&stack, cudaLimitStackSize));
+        if (stack < DEVICE_STACK_BYTES) CK(cudaDeviceSetLimit(cudaLimitStackSize, DEVICE_STACK_BYTES));
     }
     return "";
 }
@@ -2923,7 +2930,8 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
             if (w == 1 || w == 2) wide += own;
             jobs++;
             launches += 1 + (int64_t)j.jit_cls.size() + (j.tail_blocks ? 1 : 0) +
-                        ((!j.slot[0].empty() || !j.slot[1].empty() || !j.slot[2].empty()) ? 1 : 0);
+                        ((!j.slot[0].empty() || !j.slot[1].empty() || !j.slot[2].empty()) ? 1 : 0) +
+                        (j.a.certs ? 1 : 0);  // fast mode: the certificate check
         }
     info[0] = nq;
     info[1] = rec;

@@ -18,7 +18,7 @@ from .wire import FlatBatch
 SEEDS = {"c3": 2601215521, "c4": 2601215522, "c5": 2601215523, "c5s": 2601215523}
 CODES = {"c3": 3, "c4": 4, "c5": 5, "c5s": 5}
 CAP_LOG2 = {"c5s": 6}
-CONFIGS = ("c3", "c4", "c5s")
+CONFIGS = ("c3", "c4", "c5s")  # (c5 proper: caps 2^20, decided in fast mode only)
 
 AXES = ("TidX", "TidY", "TidZ", "BidX", "BidY", "BidZ",
         "GDimX", "GDimY", "GDimZ", "BDimX", "BDimY", "BDimZ")
@@ -53,9 +53,12 @@ def _setup(L):
 
 
 def generate(config: str, n: int, first: int = 0, seed: int | None = None,
-             names: bool = True) -> FlatBatch:
-    """Queries [first, first + n) of the config's stream."""
-    L = _lib.lib()
+             names: bool = True, lib=None) -> FlatBatch:
+    """Queries [first, first + n) of the config's stream.  `lib`: a library
+    exporting the generator (default: the engine's; bench.py's reference arm
+    passes the oracle-side build, oracle/liboob_synth.so, so that arm never
+    loads the engine)."""
+    L = lib if lib is not None else _lib.lib()
     _setup(L)
     code = CODES[config]
     seed = SEEDS[config] if seed is None else seed

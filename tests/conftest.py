@@ -27,8 +27,22 @@ def load_golden(name: str) -> list:
         return [json.loads(line) for line in f]
 
 
+BASELINE_REF = ROOT / "baseline" / "_ref"  # tools/install_reference.sh (travels to the GPU box)
+
+
+def reference_paths():
+    """(package dir, corpus dir) of the reference: the install under
+    baseline/_ref (present on the GPU box), else the mounted source tree
+    (build container); (None, None) when neither exists."""
+    if (BASELINE_REF / "scuba_mini" / "solver.py").exists() and (BASELINE_REF / "corpus").exists():
+        return BASELINE_REF, BASELINE_REF / "corpus"
+    if (REF_SRC / "scuba_mini" / "solver.py").exists():
+        return REF_SRC, REF_SRC.parent / "corpus"
+    return None, None
+
+
 def reference_available() -> bool:
-    return (REF_SRC / "scuba_mini" / "solver.py").exists()
+    return reference_paths()[0] is not None
 
 
 @pytest.fixture(scope="session")

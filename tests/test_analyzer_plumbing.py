@@ -1,10 +1,10 @@
 """Analyzer integration (paper_2601_21552_b200.analyzer) against the real
-reference front end, in THIS container (the reference is absent on the GPU
-box).  The engine call is stood in by the C oracle so the test runs without a
-GPU: it checks the plumbing -- record/replay, flattening of the reference's
-own objects, verdict objects of the reference's classes -- reproduces the
-reference's diagnostics byte for byte on the whole corpus.  The GPU side of
-the same queries is covered by tests/test_gpu_parity.py (corpus golden sets).
+reference front end (baseline/_ref, or the mounted reference).  The engine
+call is stood in by the C oracle so the test runs without a GPU: it checks the
+plumbing -- record/replay, flattening of the reference's own objects, verdict
+objects of the reference's classes -- reproduces the reference's diagnostics
+byte for byte on the whole corpus.  tests/test_gpu_analyzer.py runs the same
+analyses with the CUDA engine.
 """
 from __future__ import annotations
 
@@ -13,14 +13,14 @@ import sys
 
 import pytest
 
-from conftest import GOLDEN, REF_SRC, reference_available
+from conftest import GOLDEN, reference_available, reference_paths
 
 pytestmark = pytest.mark.skipif(not reference_available(), reason="reference not mounted")
 
 
 @pytest.fixture
 def ref(monkeypatch):
-    sys.path.insert(0, str(REF_SRC))
+    sys.path.insert(0, str(reference_paths()[0]))
     import scuba_mini.analyzer as An
     from oracle import oracle
     from paper_2601_21552_b200 import _lib
@@ -44,7 +44,7 @@ def test_batched_analysis_reproduces_reference_diagnostics(ref, m):
     from paper_2601_21552_b200.analyzer import analyze_batched
 
     want = json.loads((GOLDEN / "corpus_diags.json").read_text())
-    corpus = Path("/root/reference/pkg/corpus")
+    corpus = reference_paths()[1]
     total = 0
     for p in sorted(corpus.glob("*/*.mcu")):
         rel = f"{p.parent.name}/{p.name}"
@@ -64,7 +64,7 @@ def test_installed_solve_replaces_reference_binding(ref):
     from paper_2601_21552_b200.analyzer import installed
 
     want = json.loads((GOLDEN / "corpus_diags.json").read_text())
-    src = (REF_SRC.parent / "corpus/figs/sosfilt_intra.mcu").read_text()
+    src = (reference_paths()[1] / "figs/sosfilt_intra.mcu").read_text()
     with installed(ref):
         res = analyze_source(src, "sosfilt_intra.mcu")
     assert render_json_lines(res.diagnostics) == want["figs/sosfilt_intra.mcu"]["m1048576"]["json"]
@@ -81,7 +81,7 @@ def test_whole_corpus_in_one_batch(ref):
     from paper_2601_21552_b200.analyzer import analyze_many
 
     want = json.loads((GOLDEN / "corpus_diags.json").read_text())
-    progs = sorted(Path("/root/reference/pkg/corpus").glob("*/*.mcu"))
+    progs = sorted(reference_paths()[1].glob("*/*.mcu"))
     jobs = [((p.read_text(), p.name, AnalyzerConfig()), {}) for p in progs]
     stats = {}
     results = analyze_many(ref, analyze_source, jobs, stats=stats)
