@@ -40,7 +40,7 @@ using sym::i128;
 #define CERT_INL inline
 #endif
 constexpr uint64_t MAGIC = 0x4345525431ull;  // "CERT1"
-constexpr int MAXB = 64;                     // box entries (variables + parameters + atoms)
+constexpr int MAXB = 48;                     // box entries (variables + parameters + atoms)
 
 // ---- checker (one query; host build in tests, device in the cert kernel) ----
 struct BoxV {  // [0, np) parameters, [np, np + nv) variables, then atoms
@@ -49,6 +49,15 @@ struct BoxV {  // [0, np) parameters, [np, np + nv) variables, then atoms
 };
 
 OOB_HD CERT_INL bool mono_iv_b(uint64_t k, const BoxV& B, i128& rl, i128& rh) {
+    if (!(k << 8)) {  // a constant or a single variable (most terms)
+        if (!k) {
+            rl = rh = 1;
+        } else {
+            rl = B.lo[(k >> 56) - 1];
+            rh = B.hi[(k >> 56) - 1];
+        }
+        return true;
+    }
     rl = rh = 1;
     while (k >> 56) {
         const int v = (int)(k >> 56) - 1;
@@ -71,6 +80,20 @@ OOB_HD CERT_INL bool peval_blob(const uint64_t*& p, const BoxV& B, i128& lo, i12
     lo = hi = 0;
     sym::Box SB{const_cast<i128*>(B.lo), const_cast<i128*>(B.hi), B.np};
     auto coef = [&](uint64_t i) { return (i128)(((unsigned __int128)t[3 * i + 2] << 64) | t[3 * i + 1]); };
+    if (B.np == 0) {  // no parameters: one term per monomial
+        for (uint64_t i = 0; i < n; ++i) {
+            const i128 c = coef(i);
+            i128 a, b, x, y;
+            if (!mono_iv_b(t[3 * i], B, a, b) || !sym::smul(c, a, x) || !sym::smul(c, b, y)) return false;
+            if (c < 0) {
+                i128 w = x;
+                x = y;
+                y = w;
+            }
+            if (!sym::sadd(lo, x, lo) || !sym::sadd(hi, y, hi)) return false;
+        }
+        return true;
+    }
     for (uint64_t i = 0; i < n;) {
         bool ok = true;
         i128 pv, c = 0, u;

@@ -77,6 +77,12 @@ OOB_HD inline int bits(i128 x) {
 constexpr int LIMB = 120;  // |every stored value| < 2^120
 OOB_HD inline bool big(i128 x) { return bits(x) > LIMB; }
 OOB_HD inline bool smul(i128 a, i128 b, i128& r) {
+    // common case: both factors within int32 -- one 64-bit multiply, exact
+    const long long al = (long long)a, bl = (long long)b;
+    if ((i128)al == a && (i128)bl == b && al == (long long)(int)al && bl == (long long)(int)bl) {
+        r = (i128)(al * bl);
+        return true;
+    }
     if (a == 0 || b == 0) {
         r = 0;
         return true;

@@ -1,7 +1,10 @@
 """Per-step DRAM traffic and launch list of one plan run (ncu CSV) ->
 profiles/ncu_summary.json (read by bench.py for roofline.traffic).
 
-    python tools/ncu_traffic.py <config> <launches.csv> [profiles/ncu_summary.json]
+    python tools/ncu_traffic.py <cfg/mode/n> <launches.csv> [profiles/ncu_summary.json]
+
+The key names the workload exactly (config, mode, queries per step), as
+bench.py looks it up; the capture is tools/profile_kernels.py <cfg> <n> <mode>.
 """
 import collections
 import csv
@@ -38,7 +41,7 @@ keep = {k: v for k, v in summary.get(cfg, {}).items() if k == "alu_evidence"}
 summary[cfg] = {
     "source": f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
               f"smsp__inst_executed.sum "
-              f"--clock-control none, one plan run (tools/profile_kernels.py {cfg} 100000); "
+              f"--clock-control none, one plan run (tools/profile_kernels.py {' '.join(cfg.split('/'))}); "
               "launches serialised and cold-cache",
     "dram_bytes_per_step": tot["dram_bytes"],
     "warp_inst_per_step": tot["warp_inst"],
