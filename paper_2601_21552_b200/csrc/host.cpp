@@ -992,6 +992,21 @@ constexpr int NJOBS = 4;
 constexpr int W_X32 = 3;
 inline size_t tbytes_of(int w) { return w == 3 ? 4 : (w == 2 ? 32 : (w == 1 ? 16 : 8)); }
 
+// Logical devices (test knob SCUBA_OOB_VIRTUAL_DEVICES=k): one call deals its
+// queries over k logical devices -- k host threads, k sets of device pools --
+// that map onto the visible GPUs round-robin, so the multi-device dealing and
+// gather can be exercised (and shown to give identical results) on one B200.
+int env_virtual_devices() {
+    const char* e = std::getenv("SCUBA_OOB_VIRTUAL_DEVICES");
+    return (e && *e) ? std::max(0, std::min(64, std::atoi(e))) : 0;
+}
+int visible_devices();
+int phys_dev(int dev) {
+    if (env_virtual_devices() <= 0) return dev;
+    const int v = visible_devices();
+    return v > 0 ? dev % v : dev;
+}
+
 DevicePool* pool_for(int dev, int wide) {
     std::lock_guard<std::mutex> lk(g_pools_mu);
     size_t slot = ((size_t)tl_pool_slot * 64 + (size_t)dev) * NJOBS + (size_t)wide;
@@ -1383,13 +1398,13 @@ size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
 constexpr size_t DEVICE_STACK_BYTES = 4096;
 
 std::string ensure_stream(DevicePool* P, int dev) {
-    CK(cudaSetDevice(dev));
+    CK(cudaSetDevice(phys_dev(dev)));
     if (!P->stream) {
         CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
         CK(cudaEventCreate(&P->ev0));
         CK(cudaEventCreate(&P->ev1));
         CK(cudaEventCreateWithFlags(&P->evr, cudaEventDisableTiming));
-        CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, phys_dev(dev)));
         // per-thread stack: the deepest kernels (root phase, certificate
         // check, 256-bit solve) need up to ~2.2 KB; the default is 1 KB
         size_t stack = 0;
@@ -1867,7 +1882,7 @@ std::string stage_group(const RunCtx& rc, DevGroup& G, uint32_t depth_cap, uint3
 
 // one run of a group: resets, root kernels, then the lockstep kernels
 std::string launch_group(const RunCtx& rc, DevGroup& G) {
-    CK(cudaSetDevice(G.dev));
+    CK(cudaSetDevice(phys_dev(G.dev)));
     int first = -1;
     for (int w = 0; w < NJOBS; w++)
         if (present(G.job[w])) { first = w; break; }
@@ -1979,7 +1994,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
 
 // device time of the last run of a group: first start event to the last end
 std::string group_ms(DevGroup& G, float* ms) {
-    CK(cudaSetDevice(G.dev));
+    CK(cudaSetDevice(phys_dev(G.dev)));
     *ms = 0;
     int first = -1;
     for (int w = 0; w < NJOBS; w++)
@@ -1998,7 +2013,7 @@ std::string group_ms(DevGroup& G, float* ms) {
 // (by the query's own regime).  Entries a job does not own (shadows that were
 // not resumed, queries that were demoted) carry VERDICT_NONE.
 std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> retry[3]) {
-    CK(cudaSetDevice(j.dev));
+    CK(cudaSetDevice(phys_dev(j.dev)));
     const uint32_t n = (uint32_t)j.qs.size();
     cudaStream_t s = P->stream;
     HostArr<int8_t> verdict, err;
@@ -2456,6 +2471,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
             reg[c.regime - R_W64].push_back(q);
         }
     }
+    if (virtual_devices <= 0) virtual_devices = env_virtual_devices();
     int ndev = virtual_devices > 0 ? virtual_devices : visible_devices();
     const size_t n_dev_q = reg[0].size() + reg[1].size() + reg[2].size();
     if (n_dev_q > 0 && ndev == 0)
@@ -2854,7 +2870,7 @@ int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** o
     for (auto& G : p->groups)
         for (int w = 0; w < NJOBS; w++)
             if (present(G.job[w])) {
-                cudaSetDevice(G.dev);
+                cudaSetDevice(phys_dev(G.dev));
                 if (cudaStreamSynchronize(G.pool[w]->stream) != cudaSuccess)
                     return fail(OOB_E_CUDA, cudaGetErrorString(cudaGetLastError()));
             }
@@ -2948,7 +2964,7 @@ void oob_plan_destroy(oob_plan* p) {
     if (!p) return;
     for (auto& G : p->groups)
         for (int w = 0; w < NJOBS; w++) {
-            cudaSetDevice(G.dev);
+            cudaSetDevice(phys_dev(G.dev));
             DevicePool* P = G.pool[w];
             P->release_all();
             if (P->ev0) cudaEventDestroy(P->ev0);
