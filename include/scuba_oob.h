@@ -160,6 +160,14 @@ typedef struct {
 int oob_solve_batch(const oob_batch* batch, const oob_options* opt,
                     oob_result* out);
 
+/* A stream of independent batches: results[i] are exactly oob_solve_batch's
+ * for batches[i].  Consecutive batches are pipelined (the host compile and
+ * upload of batch i+1 overlap the kernels of batch i; two sets of device
+ * buffers alternate), so the throughput of a stream is bounded by the slower
+ * of the host and device phases instead of their sum. */
+int oob_solve_batches(const oob_batch* batches, int64_t n_batches, const oob_options* opt,
+                      oob_result* results);
+
 /* Batched propagate(domains, constraints): replaces solver.py:264-280.
  * Domains are var_lo/var_hi; constraints are used AS GIVEN (propagate() adds
  * no side constraints).  status[q] = 1 and out_lo/out_hi narrowed, or

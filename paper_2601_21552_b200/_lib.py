@@ -65,6 +65,7 @@ EXPORTS = (
     "oob_device_count",
     "oob_version",
     "oob_release",
+    "oob_solve_batches",
     "oob_plan_create",
     "oob_plan_run",
     "oob_plan_results",
@@ -88,6 +89,8 @@ def lib():
     vp = ctypes.c_void_p
     L.oob_solve_batch.argtypes = [vp, vp, vp]
     L.oob_solve_batch.restype = ctypes.c_int
+    L.oob_solve_batches.argtypes = [vp, ctypes.c_int64, vp, vp]
+    L.oob_solve_batches.restype = ctypes.c_int
     L.oob_propagate_batch.argtypes = [vp, vp, vp, vp, vp]
     L.oob_propagate_batch.restype = ctypes.c_int
     L.oob_check_model_batch.argtypes = [vp, vp, vp, vp]
@@ -151,8 +154,7 @@ def options(timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_no
     return o
 
 
-def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0, jit_min=0):
-    """Run oob_solve_batch on a FlatBatch -> dict of numpy result arrays."""
+def _result_arrays(fb):
     n = fb.n
     out = {
         "verdict": np.full(n, -1, dtype=np.int8),
@@ -165,12 +167,41 @@ def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, h
     r = oob_result(out["verdict"].ctypes.data, out["model"].ctypes.data,
                    out["nodes"].ctypes.data, out["passes"].ctypes.data,
                    out["elapsed"].ctypes.data)
+    return out, r
+
+
+def solve_flat(fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0, jit_min=0):
+    """Run oob_solve_batch on a FlatBatch -> dict of numpy result arrays."""
+    out, r = _result_arrays(fb)
     cb = fb.as_c()
     o = options(timeout_s, node_budget, n_gpus, device, flags, heavy_nodes, jit_min)
     rc = lib().oob_solve_batch(ctypes.byref(cb), ctypes.byref(o), ctypes.byref(r))
     out["status"] = rc
     out["error"] = last_error() if rc else ""
     return out
+
+
+def solve_flat_stream(fbs, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0,
+                      jit_min=0):
+    """oob_solve_batches: a list of FlatBatches decided as one pipelined
+    stream -> list of result dicts (each exactly solve_flat's)."""
+    outs, rs, cbs = [], [], []
+    for fb in fbs:
+        out, r = _result_arrays(fb)
+        outs.append(out)
+        rs.append(r)
+        cbs.append(fb.as_c())
+    if not fbs:
+        return []
+    ca = (type(cbs[0]) * len(cbs))(*cbs)
+    ra = (oob_result * len(rs))(*rs)
+    o = options(timeout_s, node_budget, n_gpus, device, flags, heavy_nodes, jit_min)
+    rc = lib().oob_solve_batches(ctypes.addressof(ca), len(fbs), ctypes.byref(o), ctypes.addressof(ra))
+    err = last_error() if rc else ""
+    for out in outs:
+        out["status"] = rc
+        out["error"] = err
+    return outs
 
 
 def propagate_flat(fb, device=0):

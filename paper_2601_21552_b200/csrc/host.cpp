@@ -1396,6 +1396,7 @@ size_t frontier_region_bytes(uint32_t maxv, size_t tbytes) {
 }
 
 constexpr size_t DEVICE_STACK_BYTES = 4096;
+constexpr uint64_t SLAB_BUDGET = 12ull << 30;  // per job, before the slabs are pooled
 
 std::string ensure_stream(DevicePool* P, int dev) {
     CK(cudaSetDevice(phys_dev(dev)));
@@ -1573,7 +1574,11 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         const char* e = std::getenv("SCUBA_OOB_SLAB_POOL");
         return e && *e == '1';
     }();
-    const bool pooled = rc.mode == MODE_SOLVE && slab_pool;
+    // large batches: one slab per warp of every launch would outgrow the
+    // device (C4 at 1M queries: ~100 K warps x ~0.7 MB); from SLAB_BUDGET on,
+    // the slabs come from the job pool (one per running warp)
+    const uint64_t slab_bytes = (uint64_t)n_warps * (j.g.slab_T_words * tbytes + j.g.slab_u32_words * 4);
+    const bool pooled = rc.mode == MODE_SOLVE && (slab_pool || slab_bytes > SLAB_BUDGET);
     j.slab_slots = pooled ? std::max(1u, std::min(n_warps, (uint32_t)P->sms * 64u)) : n_warps;
     j.root_blocks = std::max<uint32_t>(
         1u, std::min<uint64_t>((n + 32 * WARPS_PER_BLOCK - 1) / (32 * WARPS_PER_BLOCK), j.slab_slots / WARPS_PER_BLOCK));
@@ -2318,6 +2323,48 @@ void assign_classes(std::vector<Compiled>& comp, const std::vector<int64_t> reg[
 // host only COMPILES (symbolic algebra on a few representatives); every
 // query is decided by the device's numeric check of its class certificate.
 constexpr int CERT_REPS = 8;
+
+// Compiled certificates are kept per (structure, parameter slots, folded
+// constants) -- exactly what they are valid for -- so later batches of the
+// same structure classes (an analyzer re-run, the next chunk of a stream)
+// skip the symbolic compile.  The full key is compared on a hit.
+struct CertCache {
+    std::mutex mu;
+    std::unordered_map<uint64_t, std::vector<std::pair<std::vector<uint64_t>, std::vector<uint64_t>>>> map;
+    size_t entries = 0;
+};
+CertCache& cert_cache() {
+    static CertCache c;
+    return c;
+}
+uint64_t key_hash(const std::vector<uint64_t>& k) {
+    uint64_t h = 1469598103934665603ull;
+    for (uint64_t x : k) h = (h ^ x) * 1099511628211ull;
+    return h;
+}
+bool cert_cache_get(const std::vector<uint64_t>& key, std::vector<uint64_t>& out) {
+    CertCache& C = cert_cache();
+    std::lock_guard<std::mutex> lk(C.mu);
+    auto it = C.map.find(key_hash(key));
+    if (it == C.map.end()) return false;
+    for (const auto& e : it->second)
+        if (e.first == key) {
+            out = e.second;
+            return true;
+        }
+    return false;
+}
+void cert_cache_put(std::vector<uint64_t>&& key, const std::vector<uint64_t>& val) {
+    CertCache& C = cert_cache();
+    std::lock_guard<std::mutex> lk(C.mu);
+    if (C.entries >= 65536) {  // bounded: start over
+        C.map.clear();
+        C.entries = 0;
+    }
+    const uint64_t h = key_hash(key);
+    C.map[h].emplace_back(std::move(key), val);
+    ++C.entries;
+}
 void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const std::vector<int64_t> reg[3],
                  std::vector<uint64_t>& certs, std::vector<uint32_t>& cert_off) {
     uint32_t ncls = 0;
@@ -2327,15 +2374,43 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
     for (int w = 0; w < 3; w++)
         for (int64_t q : reg[w]) start[comp[q].cls + 1]++;
     for (uint32_t c = 0; c < ncls; c++) start[c + 1] += start[c];
+    // members of every class in ascending query order (one pass)
     std::vector<int64_t> mem(start[ncls]);
     {
         std::vector<uint32_t> at(start.begin(), start.end() - 1);
-        for (int w = 0; w < 3; w++)  // ascending query order within a class
-            for (int64_t q : reg[w]) mem[at[comp[q].cls]++] = q;
-        parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
-            for (size_t c = lo; c < hi; c++) std::sort(mem.begin() + start[c], mem.begin() + start[c + 1]);
-        });
+        const int64_t n = (int64_t)comp.size();
+        for (int64_t q = 0; q < n; q++)
+            if (comp[q].regime >= R_W64 && comp[q].regime <= R_W256) mem[at[comp[q].cls]++] = q;
     }
+    // literal slots whose value varies inside the class (the parameters):
+    // each query against its class's first member, in parallel over queries
+    // (every query through its own Structure: equal code words do not imply
+    // equal literal-slot sources)
+    std::vector<uint32_t> loff(ncls + 1, 0);
+    for (uint32_t c = 0; c < ncls; c++)
+        loff[c + 1] = loff[c] + (start[c + 1] > start[c] ? comp[mem[start[c]]].st->nlit : 0);
+    std::vector<i128> v0(loff[ncls]);
+    std::unique_ptr<std::atomic<uint8_t>[]> vary(new std::atomic<uint8_t>[std::max<uint32_t>(loff[ncls], 1)]);
+    for (uint32_t c = 0; c < ncls; c++) {
+        if (start[c + 1] == start[c]) continue;
+        const int64_t q0 = mem[start[c]];
+        for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
+            v0[loff[c] + i] = lit_value(b, q0, *comp[q0].st, i);
+            vary[loff[c] + i].store(0, std::memory_order_relaxed);
+        }
+    }
+    parallel_for(mem.size(), 4096, [&](size_t lo, size_t hi) {
+        for (size_t k = lo; k < hi; k++) {
+            const int64_t q = mem[k];
+            const uint32_t c = comp[q].cls;
+            const Structure& sk = *comp[q].st;
+            for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
+                std::atomic<uint8_t>& f = vary[loff[c] + i];
+                if (!f.load(std::memory_order_relaxed) && lit_value(b, q, sk, i) != v0[loff[c] + i])
+                    f.store(1, std::memory_order_relaxed);
+            }
+        }
+    });
     std::vector<std::vector<uint64_t>> per(ncls);
     parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
         static thread_local std::unique_ptr<sym::Store> S;
@@ -2354,23 +2429,29 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
             if (!nm) continue;
             const Structure& st = *comp[m[0]].st;
             if (!st.range_why.empty()) continue;
-            // literal slots whose value varies inside the class: parameters
             std::vector<int16_t> pmap(st.nlit, -1), pslot;
-            std::vector<i128> v0(st.nlit);
-            for (uint32_t i = 0; i < st.nlit; i++) v0[i] = lit_value(b, m[0], st, i);
-            std::vector<uint8_t> vary(st.nlit, 0);
-            // (each query through its own Structure: equal code words do not
-            // imply equal literal-slot sources)
-            for (size_t k = 1; k < nm; k++) {
-                const Structure& sk = *comp[m[k]].st;
-                for (uint32_t i = 0; i < st.nlit; i++)
-                    if (!vary[i] && lit_value(b, m[k], sk, i) != v0[i]) vary[i] = 1;
-            }
             for (uint32_t i = 0; i < st.nlit; i++)
-                if (vary[i]) {
+                if (vary[loff[c] + i].load(std::memory_order_relaxed)) {
                     pmap[i] = (int16_t)pslot.size();
                     pslot.push_back((int16_t)i);
                 }
+            // compiled before for this structure, parameter set and constants?
+            std::vector<uint64_t> ckey;
+            ckey.reserve(st.words.size() + 4 + 3 * st.nlit);
+            ckey.push_back(st.nv);
+            ckey.push_back(st.ncon);
+            ckey.push_back(st.nlit);
+            ckey.insert(ckey.end(), st.words.begin(), st.words.end());
+            for (uint32_t i = 0; i < st.nlit; i++) {
+                const bool var_i = pmap[i] >= 0;
+                ckey.push_back(var_i);
+                if (!var_i) {
+                    const i128 x = v0[loff[c] + i];
+                    ckey.push_back((uint64_t)x);
+                    ckey.push_back((uint64_t)((unsigned __int128)x >> 64));
+                }
+            }
+            if (cert_cache_get(ckey, per[c])) continue;
             std::vector<std::vector<uint64_t>> got;
             const size_t nr = std::min<size_t>(CERT_REPS, nm);
             for (size_t r = 0; r < nr; r++) {
@@ -2389,13 +2470,15 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
                 for (const auto& o : got) dup = dup || o == blob;
                 if (!dup) got.push_back(std::move(blob));
             }
-            if (got.empty()) continue;
             std::vector<uint64_t>& out = per[c];
-            out.push_back(got.size());
-            for (const auto& g : got) {
-                out.push_back(g.size());
-                out.insert(out.end(), g.begin(), g.end());
+            if (!got.empty()) {
+                out.push_back(got.size());
+                for (const auto& g : got) {
+                    out.push_back(g.size());
+                    out.insert(out.end(), g.begin(), g.end());
+                }
             }
+            cert_cache_put(std::move(ckey), out);
         }
     });
     certs.clear();
@@ -2657,6 +2740,47 @@ int oob_solve_batch(const oob_batch* batch, const oob_options* opt, oob_result* 
     for (auto& t : th) t.join();
     for (int c = 0; c < k; c++)
         if (rcs[c] != OOB_OK) return fail(rcs[c], "chunk " + std::to_string(c) + ": " + msgs[c]);
+    g_last_error.clear();
+    return OOB_OK;
+}
+
+int oob_solve_batches(const oob_batch* batches, int64_t n_batches, const oob_options* opt, oob_result* outs) {
+    if (!batches || !outs || n_batches < 0) return fail(OOB_E_INVALID, "null argument");
+    for (int64_t i = 0; i < n_batches; i++)
+        if (!outs[i].verdict) return fail(OOB_E_INVALID, "result arrays missing");
+    if (n_batches == 1) return oob_solve_batch(batches, opt, outs);
+    // two workers (pool slots 0/1) take the batches alternately; the gate
+    // hands the host phase (compile, certify, pack, upload, launch) to batch
+    // i + 1 as soon as batch i has launched its kernels, so host work and
+    // device work of consecutive batches overlap
+    HostGate gate;
+    std::vector<int> rcs(n_batches, OOB_OK);
+    std::vector<std::string> msgs(n_batches);
+    std::vector<std::thread> th;
+    for (int s = 0; s < 2 && s < n_batches; s++) {
+        th.emplace_back([&, s]() {
+            tl_pool_slot = s;
+            tl_gate = &gate;
+            for (int64_t i = s; i < n_batches; i += 2) {
+                tl_chunk = (int)i;
+                {
+                    std::unique_lock<std::mutex> lk(gate.mu);
+                    gate.cv.wait(lk, [&] { return gate.turn >= (int)i; });
+                }
+                tl_gate_held = true;
+                const oob_result& o = outs[i];
+                rcs[i] = drive(batches + i, opt, MODE_SOLVE, nullptr, o.model, o.verdict, o.nodes, o.passes,
+                               o.elapsed_s);
+                if (rcs[i] != OOB_OK) msgs[i] = g_last_error;
+                gate_release();  // also on early exits (no launch happened)
+            }
+            tl_gate = nullptr;
+            tl_pool_slot = 0;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int64_t i = 0; i < n_batches; i++)
+        if (rcs[i] != OOB_OK) return fail(rcs[i], "batch " + std::to_string(i) + ": " + msgs[i]);
     g_last_error.clear();
     return OOB_OK;
 }

@@ -12,7 +12,7 @@ from oracle import oracle
 from paper_2601_21552_b200 import _lib
 from paper_2601_21552_b200.solver import (
     BinE, Constraint, Lit, Sat, SolverVar, Timeout, Unsat, VarRef,
-    check_model, divisor_side_constraints, propagate, solve, solve_batch,
+    check_model, divisor_side_constraints, propagate, solve, solve_batch, solve_flat,
 )
 from paper_2601_21552_b200.terms import query_from_json
 from paper_2601_21552_b200.wire import flatten, words_to_ints
@@ -122,3 +122,18 @@ def test_every_model_row_is_written(gpu, golden):
         for q in np.flatnonzero(~sat)[:50]:
             vb, ve = int(fb.var_begin[q]), int(fb.var_begin[q + 1])
             assert not out["model"][vb:ve].any(), (name, q)
+
+
+@pytest.mark.parametrize("flags", [0, _lib.F_FAST])
+def test_stream_api_equals_single_calls(gpu, flags):
+    """oob_solve_batches (pipelined stream of batches) returns exactly what
+    one oob_solve_batch per batch returns."""
+    from paper_2601_21552_b200 import synth
+    from paper_2601_21552_b200._lib import solve_flat_stream
+    fbs = [synth.generate(c, 3000, first=k * 3000, names=False) for k, c in enumerate(("c3", "c4", "c3", "c5s", "c4"))]
+    outs = solve_flat_stream(fbs, 30.0, n_gpus=1, flags=flags)
+    for fb, o in zip(fbs, outs):
+        assert o["status"] == _lib.OOB_OK
+        ref = solve_flat(fb, 30.0, n_gpus=1, flags=flags)
+        for k in ("verdict", "model", "nodes", "passes"):
+            assert np.array_equal(o[k], ref[k]), k
