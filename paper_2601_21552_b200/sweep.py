@@ -634,5 +634,9 @@ def replay_witness(program, input_values: dict, default_value: int, line: int, c
 
 
 def load_programs(path) -> dict:
-    with open(path) as f:
-        return {k: SweepProgram.from_json(v) for k, v in json.load(f).items()}
+    """SweepPrograms from a JSON file (gzip-compressed when it ends in .gz)."""
+    import gzip
+    raw = open(path, "rb").read()
+    if str(path).endswith(".gz"):
+        raw = gzip.decompress(raw)
+    return {k: SweepProgram.from_json(v) for k, v in json.loads(raw).items()}

@@ -8,6 +8,7 @@ The GPU run of the same fixtures is tests/test_gpu_sweep.py."""
 from __future__ import annotations
 
 import ctypes
+import gzip
 import json
 import subprocess
 import sys
@@ -46,8 +47,8 @@ def host():
 
 
 def load():
-    progs = json.loads((GOLDEN / "sweep_programs.json").read_text())
-    expect = json.loads((GOLDEN / "sweep_expect.json").read_text())
+    progs = json.loads(gzip.decompress((GOLDEN / "sweep_programs.json.gz").read_bytes()))
+    expect = json.loads(gzip.decompress((GOLDEN / "sweep_expect.json.gz").read_bytes()))
     return {k: S.SweepProgram.from_json(v) for k, v in progs.items()}, expect
 
 
@@ -124,7 +125,7 @@ def test_first_witness_is_the_first_violating_tuple(host):
 def test_compiler_is_deterministic_on_reference_ast(name):
     sys.path.insert(0, str(REF_SRC))
     from scuba_mini.frontend import parse_source
-    src = json.loads((GOLDEN / "sweep_programs.json").read_text())[name]["source"]
+    src = json.loads(gzip.decompress((GOLDEN / "sweep_programs.json.gz").read_bytes()))[name]["source"]
     sp = S.compile_program(parse_source(src, name.split("/")[-1]))
     assert np.array_equal(sp.code, PROGS[name].code)
     assert np.array_equal(sp.sites, PROGS[name].sites)

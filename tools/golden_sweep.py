@@ -21,11 +21,12 @@ Programs: the 20 corpus files, the reference's own test_oracle.py sources
 their assert caps changed, and 70 seeded synthetic programs
 (tools/synth_programs.py) -- sources generated here, regenerated on every run.
 
-Usage:  python tools/golden_sweep.py      -> tests/golden/sweep_programs.json,
-                                             tests/golden/sweep_expect.json
+Usage:  python tools/golden_sweep.py      -> tests/golden/sweep_programs.json.gz,
+                                             tests/golden/sweep_expect.json.gz
 """
 from __future__ import annotations
 
+import gzip
 import json
 import random
 import re
@@ -136,8 +137,10 @@ def main():
         expect[name] = rec
         print(name, k, [(s["bound"], s["executions"], s["ref_s"]) for s in rec["sweeps"]], flush=True)
     OUT.mkdir(parents=True, exist_ok=True)
-    (OUT / "sweep_programs.json").write_text(json.dumps(programs, indent=0, sort_keys=True))
-    (OUT / "sweep_expect.json").write_text(json.dumps(expect, indent=0, sort_keys=True))
+    (OUT / "sweep_programs.json.gz").write_bytes(
+        gzip.compress(json.dumps(programs, indent=0, sort_keys=True).encode(), 9, mtime=0))
+    (OUT / "sweep_expect.json.gz").write_bytes(
+        gzip.compress(json.dumps(expect, indent=0, sort_keys=True).encode(), 9, mtime=0))
 
 
 if __name__ == "__main__":

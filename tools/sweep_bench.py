@@ -9,6 +9,7 @@ build container).  One JSON line per (program, B), then a summary line.
 """
 from __future__ import annotations
 
+import gzip
 import json
 import sys
 import time
@@ -23,8 +24,8 @@ from paper_2601_21552_b200 import sweep as S  # noqa: E402
 
 def main():
     bounds = [int(x) for x in sys.argv[1:]] or [64, 256, 1024]
-    progs = S.load_programs(ROOT / "tests" / "golden" / "sweep_programs.json")
-    expect = json.loads((ROOT / "tests" / "golden" / "sweep_expect.json").read_text())
+    progs = S.load_programs(ROOT / "tests" / "golden" / "sweep_programs.json.gz")
+    expect = json.loads(gzip.decompress((ROOT / "tests" / "golden" / "sweep_expect.json.gz").read_bytes()))
     tot = {b: [0, 0.0, 0.0] for b in bounds}
     for name in sorted(k for k in progs if k.startswith("corpus/")):
         sp = progs[name]
