@@ -5,13 +5,20 @@
 // Each thread runs 8 independent dependency chains of LOP3 (and, separately,
 // IADD3 and IMNMX compare/select) for ITER rounds; the grid fills every SM
 // with 64 warps.  Reported: thread-instructions per second over the
-// whole GPU and per SM per cycle (at the SM clock measured by clock64 over the
-// same kernel), for each instruction kind.  The chains are unrolled so the
+// whole GPU and per SM per cycle, at the SM clock measured INSIDE the kernel
+// (block 0's clock64 cycles over its %globaltimer nanoseconds, the same
+// interval), for each instruction kind.  The chains are unrolled so the
 // loop overhead is < 3% of the issued instructions (checked in the SASS).
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o alu_peak tools/alu_peak.cu && ./alu_peak
 #include <cstdio>
 #include <cuda_runtime.h>
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 constexpr int ITER = 4096;
 constexpr int CH = 8;
@@ -20,6 +27,7 @@ __global__ void lop3_kernel(unsigned* out, unsigned seed, long long* cycles) {
     unsigned a[CH];
     for (int c = 0; c < CH; c++) a[c] = seed ^ (threadIdx.x * 0x9E3779B9u + c);
     const unsigned b = seed * 3u + 1u, d = seed * 7u + 5u;
+    const unsigned long long g0 = gtimer();
     long long t0 = clock64();
 #pragma unroll 16
     for (int i = 0; i < ITER; i++) {
@@ -31,16 +39,21 @@ __global__ void lop3_kernel(unsigned* out, unsigned seed, long long* cycles) {
         }
     }
     long long t1 = clock64();
+    const unsigned long long g1 = gtimer();
     unsigned x = 0;
     for (int c = 0; c < CH; c++) x ^= a[c];
     out[blockIdx.x * blockDim.x + threadIdx.x] = x;
-    if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = t1 - t0;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        cycles[0] = t1 - t0;
+        cycles[1] = (long long)(g1 - g0);
+    }
 }
 
 __global__ void iadd3_kernel(unsigned* out, unsigned seed, long long* cycles) {
     unsigned a[CH];
     for (int c = 0; c < CH; c++) a[c] = seed + threadIdx.x * 17u + c;
     const unsigned b = seed * 3u + 1u, d = seed * 7u + 5u;
+    const unsigned long long g0 = gtimer();
     long long t0 = clock64();
 #pragma unroll 16
     for (int i = 0; i < ITER; i++) {
@@ -52,10 +65,14 @@ __global__ void iadd3_kernel(unsigned* out, unsigned seed, long long* cycles) {
         }
     }
     long long t1 = clock64();
+    const unsigned long long g1 = gtimer();
     unsigned x = 0;
     for (int c = 0; c < CH; c++) x ^= a[c];
     out[blockIdx.x * blockDim.x + threadIdx.x] = x;
-    if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = t1 - t0;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        cycles[0] = t1 - t0;
+        cycles[1] = (long long)(g1 - g0);
+    }
 }
 
 __global__ void setp_sel_kernel(unsigned* out, unsigned seed, long long* cycles) {
@@ -63,6 +80,7 @@ __global__ void setp_sel_kernel(unsigned* out, unsigned seed, long long* cycles)
     int a[CH];
     for (int c = 0; c < CH; c++) a[c] = (int)(seed + threadIdx.x * 13u + c);
     const int b = (int)(seed * 3u + 1u);
+    const unsigned long long g0 = gtimer();
     long long t0 = clock64();
 #pragma unroll 16
     for (int i = 0; i < ITER; i++) {
@@ -74,10 +92,14 @@ __global__ void setp_sel_kernel(unsigned* out, unsigned seed, long long* cycles)
         }
     }
     long long t1 = clock64();
+    const unsigned long long g1 = gtimer();
     int x = 0;
     for (int c = 0; c < CH; c++) x ^= a[c];
     out[blockIdx.x * blockDim.x + threadIdx.x] = (unsigned)x;
-    if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = t1 - t0;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        cycles[0] = t1 - t0;
+        cycles[1] = (long long)(g1 - g0);
+    }
 }
 
 template <typename K>
@@ -86,13 +108,13 @@ void run(const char* name, K kernel, int insts_per_chain_step, int sms) {
     unsigned* out;
     long long* cyc;
     cudaMalloc(&out, (size_t)threads * blocks * 4);
-    cudaMalloc(&cyc, 8);
+    cudaMalloc(&cyc, 16);
     kernel<<<blocks, threads>>>(out, 1u, cyc);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     float best = 1e30f;
-    long long cycles = 0;
+    long long cyc_ns[2] = {0, 1};
     for (int r = 0; r < 5; r++) {
         cudaEventRecord(e0);
         kernel<<<blocks, threads>>>(out, (unsigned)r + 2u, cyc);
@@ -102,14 +124,14 @@ void run(const char* name, K kernel, int insts_per_chain_step, int sms) {
         cudaEventElapsedTime(&ms, e0, e1);
         if (ms < best) {
             best = ms;
-            cudaMemcpy(&cycles, cyc, 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(cyc_ns, cyc, 16, cudaMemcpyDeviceToHost);
         }
     }
     const double insts = (double)threads * blocks * ITER * CH * insts_per_chain_step;
     const double per_s = insts / (best * 1e-3);
-    const double mhz = cycles / (best * 1e3);  // block 0's clock64 span over the whole kernel time
+    const double mhz = (double)cyc_ns[0] / (double)cyc_ns[1] * 1e3;  // cycles per ns of the same interval
     std::printf("{\"kind\": \"%s\", \"thread_inst_per_s\": %.4e, \"warp_inst_per_s\": %.4e, "
-                "\"thread_inst_per_sm_per_clk\": %.1f, \"sm_mhz_est\": %.0f, \"ms\": %.3f, \"sms\": %d}\n",
+                "\"thread_inst_per_sm_per_clk\": %.1f, \"sm_mhz_in_kernel\": %.0f, \"ms\": %.3f, \"sms\": %d}\n",
                 name, per_s, per_s / 32, per_s / sms / (mhz * 1e6), mhz, best, sms);
     cudaFree(out);
     cudaFree(cyc);
