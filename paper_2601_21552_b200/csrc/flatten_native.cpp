@@ -12,6 +12,8 @@
 //    (lo > hi) is stored into slot 0 so that the query is Unsat before search;
 //  * terms are hash-consed per query in post-order (children first), literals
 //    deduplicated by value, so structural equality is node-id equality;
+//  * a query with an empty domain whose constraints do not resolve keeps no
+//    constraints (Unsat before search; the reference never evaluates them)
 //  * errors: KeyError(name) for an undeclared variable, ValueError for an
 //    unknown operator / relation or a boolean term, OverflowError (raised after
 //    the whole batch, as finish() does) for a value outside int128.
@@ -164,13 +166,33 @@ class Query {
         n_b_.clear();
         q_lits_.clear();
         if (!add_vars(variables)) return false;
-        PyObject* seq = PySequence_Fast(constraints, "constraints must be iterable");
-        if (!seq) return false;
-        bool ok = true;
-        const Py_ssize_t nc = PySequence_Fast_GET_SIZE(seq);
-        for (Py_ssize_t k = 0; k < nc && ok; k++) ok = add_con(PySequence_Fast_GET_ITEM(seq, k));
-        Py_DECREF(seq);
-        if (!ok) return false;
+        // a query with an empty domain is Unsat before its constraints are
+        // ever evaluated (solver.py:374): if they do not resolve (undeclared
+        // variable, unknown operator -- the reference raises nothing then),
+        // the query keeps no constraints
+        {
+            const size_t c0 = o_.con_rel.size();
+            PyObject* seq = PySequence_Fast(constraints, "constraints must be iterable");
+            if (!seq) return false;
+            bool ok = true;
+            const Py_ssize_t nc = PySequence_Fast_GET_SIZE(seq);
+            for (Py_ssize_t k = 0; k < nc && ok; k++) ok = add_con(PySequence_Fast_GET_ITEM(seq, k));
+            Py_DECREF(seq);
+            if (!ok && q_empty_) {
+                PyErr_Clear();
+                o_.con_rel.resize(c0);
+                o_.con_lhs.resize(c0);
+                o_.con_rhs.resize(c0);
+                nodes_.clear();
+                lit_index_.clear();
+                n_op_.clear();
+                n_a_.clear();
+                n_b_.clear();
+                q_lits_.clear();
+                ok = true;
+            }
+            if (!ok) return false;
+        }
         // append (finish() range-checks the stored values: var_lo, var_hi, lits)
         for (size_t i = 0; i < lo_.size(); i++) {
             o_.var_lo.push_back(lo_[i]);
@@ -204,6 +226,7 @@ class Query {
     std::vector<i128> lo_, hi_;
     std::vector<PyObject*> bad_lo_, bad_hi_;  // stored out-of-range values (or null)
     PyObject *e_blo = nullptr, *e_bhi = nullptr;
+    bool q_empty_ = false;  // the current query has an empty domain
     static int sign_of(PyObject* big) {  // sign of an int beyond the long long range
         int ovf = 0;
         PyLong_AsLongLongAndOverflow(big, &ovf);
@@ -316,6 +339,7 @@ class Query {
             Py_XDECREF(name);
         }
         Py_DECREF(seq);
+        q_empty_ = ok && have_empty;
         if (ok && have_empty) {  // Unsat before search (solver.py:374)
             lo_[0] = e_lo;
             hi_[0] = e_hi;

@@ -267,14 +267,25 @@ class _Builder:
         rels = []
         lhs = []
         rhs = []
-        for c in constraints:
-            rel, l, r = _con_fields(c)
-            code = REL_CODE.get(rel)
-            if code is None:
-                raise ValueError(f"unknown relation {rel!r}")
-            rels.append(code)
-            lhs.append(walk(l))
-            rhs.append(walk(r))
+        try:
+            for c in constraints:
+                rel, l, r = _con_fields(c)
+                code = REL_CODE.get(rel)
+                if code is None:
+                    raise ValueError(f"unknown relation {rel!r}")
+                rels.append(code)
+                lhs.append(walk(l))
+                rhs.append(walk(r))
+        except (KeyError, ValueError):
+            if empty is None:
+                raise
+            # an empty domain: Unsat before search (solver.py:374); the
+            # reference never evaluates these constraints, so it raises nothing
+            rels, lhs, rhs = [], [], []
+            n_ops.clear()
+            n_a.clear()
+            n_b.clear()
+            q_lits.clear()
         # --- append ---
         self.var_names.append(names)
         self.var_lo.extend(lo)

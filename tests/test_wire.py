@@ -60,3 +60,15 @@ def test_undeclared_variable_and_unknown_op():
         flatten([{"vars": [["x", 0, 1]], "cons": [["<", ["^", "x", 1], 2]]}])
     with pytest.raises(ValueError):
         flatten([{"vars": [["x", 0, 1]], "cons": [["!=", "x", 1]]}])
+
+
+def test_empty_domain_query_is_unsat_without_resolving_terms():
+    """solver.py:374: any lo > hi is Unsat before the constraints are touched,
+    so an undeclared variable or unknown operator there raises nothing."""
+    from paper_2601_21552_b200.wire import flatten_py
+    from paper_2601_21552_b200.wire import flatten as flatten_any
+    q = {"vars": [["x", 0, 5], ["y", 3, 1]],
+         "cons": [["<", "undeclared", 3], ["=", ["^", "x", 2], 1]]}
+    for fl in (flatten_py, flatten_any):
+        fb = fl([q])
+        assert fb.n == 1 and int(fb.con_begin[1]) == 0
