@@ -385,11 +385,13 @@ class HostPool {
         static HostPool* p = new HostPool(host_threads() - 1);  // never destroyed (detached workers)
         return *p;
     }
-    // runs body(lo, hi) over [0, n) in chunks of `grain`; false if busy
+    // runs body(lo, hi) over [0, n) in chunks of `grain`; false from inside a
+    // pool worker (nested sections run serially).  Concurrent callers (the
+    // stream API's two workers: one batch's fetch beside the next one's
+    // compile) take the pool in turn instead of falling back to one thread.
     bool run(size_t n, size_t grain, const std::function<void(size_t, size_t)>& body) {
         if (workers_.empty() || tl_in_pool) return false;
-        std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
-        if (!busy.owns_lock()) return false;
+        std::unique_lock<std::mutex> busy(run_mu_);
         {
             std::lock_guard<std::mutex> lk(mu_);
             body_ = &body;
