@@ -1372,19 +1372,27 @@ bool fast_frontier() {
     }();
     return v;
 }
+// Fast mode hand-off thresholds.  With the Unsat bulk refuted up front, the
+// queries left are mostly Sat with a few dozen DFS nodes; handing them to the
+// frontier after 24 nodes only queues them behind the few warps that serve a
+// class's heavy list (B200 A/B, identical results, plan-run ms, 128-pass
+// hand-off: C3 24 nodes 7.6, 96 nodes 6.4, never 5.3; C4 24 13.3, 96 13.0,
+// never 25.0 -- C4's long Sat chains still need the frontier): 96 nodes.
+// With the frontier prover (SCUBA_OOB_FAST_FRONTIER=1) heavy queries should
+// meet it early: 8 nodes / 32 passes.
 uint32_t fast_heavy_nodes() {
     static const uint32_t v = [] {
         const char* e = std::getenv("SCUBA_OOB_FAST_HEAVY_NODES");
-        return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : 8);
+        return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : (fast_frontier() ? 8 : 96));
     }();
     return v;
 }
-uint32_t fast_heavy_passes() {
-    static const uint32_t v = [] {
+uint32_t fast_heavy_passes(uint32_t canonical) {
+    static const int v = [] {
         const char* e = std::getenv("SCUBA_OOB_FAST_HEAVY_PASSES");
-        return (uint32_t)std::max(1, (e && *e) ? std::atoi(e) : 32);
+        return (e && *e) ? std::max(1, std::atoi(e)) : 0;
     }();
-    return v;
+    return v > 0 ? (uint32_t)v : (fast_frontier() ? 32u : canonical);
 }
 // the symbolic prover's scratch at the start of a frontier region: the
 // query's store plus one working set per lane
@@ -1550,7 +1558,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     int64_t hn = rc.opt.heavy_nodes;
     const bool fast = rc.mode == MODE_SOLVE && (rc.opt.flags & OOB_F_FAST);
     uint32_t heavy_nodes = (rc.mode == MODE_SOLVE && heavy && hn >= 0) ? (hn ? (uint32_t)hn : HEAVY_NODES_DEFAULT) : 0;
-    if (fast && fast_frontier()) heavy_nodes = hn > 0 ? (uint32_t)hn : fast_heavy_nodes();
+    if (fast && heavy_nodes) heavy_nodes = hn > 0 ? (uint32_t)hn : fast_heavy_nodes();
     // wide jobs: a frontier-only tail launch with a full grid serves their
     // heavy list once the int64 kernel has freed the SMs
     const uint32_t own_warps = n_warps;  // slabs [0, own_warps): the interpreting kernel + class kernels
@@ -1663,7 +1671,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
             const char* e = std::getenv("SCUBA_OOB_HEAVY_PASSES");
             return (uint32_t)((e && *e) ? std::atoi(e) : (int)HEAVY_PASSES_DEFAULT);
         }();
-        a.heavy_passes = (fast && fast_frontier()) ? fast_heavy_passes() : hp;
+        a.heavy_passes = fast ? fast_heavy_passes(hp) : hp;
     }
     a.fast = (fast && fast_frontier()) ? 1u : 0u;
     a.fast_stats = nullptr;
