@@ -42,6 +42,7 @@ namespace oob {
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s);
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
 cudaError_t launch_cert(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
+cudaError_t grow_smem_limit(const void* fn, size_t smem);
 cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm);
 cudaError_t launch_gather_sat(const int8_t* verdict, const QDesc* qd, const int64_t* model, uint32_t n,
                               unsigned long long* counter, uint32_t* sat_off, int64_t* compact, int sms,
@@ -1524,7 +1525,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         }
         if (!occ) {
             if (jit_smem())
-                cudaFuncSetAttribute(j.jit_fn[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jit_smem());
+                grow_smem_limit(j.jit_fn[i], jit_smem());
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, j.jit_fn[i], jw * 32, jit_smem()) != cudaSuccess) {
                 cudaGetLastError();
                 occ = 4;

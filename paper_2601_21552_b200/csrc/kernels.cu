@@ -1,4 +1,6 @@
 #include <algorithm>
+#include <map>
+#include <mutex>
 // kernels.cu -- sm_100a kernels of the OOB-query engine.
 //
 //   oob_lockstep_kernel<T>  K1: exact solve() emulation (solver.py:363-416)
@@ -292,10 +294,28 @@ static cudaError_t launch_impl(const LaunchArgs& a, int blocks, int fblocks, cud
     return cudaGetLastError();
 }
 
+// The dynamic shared memory limit of a kernel is a per-function attribute
+// of the device: several host threads staging jobs on one device (logical
+// devices, the stream API's workers) must never LOWER it under another's
+// launch, so it only ever grows (per function and device).
+cudaError_t grow_smem_limit(const void* fn, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> set;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = set[{fn, dev}];
+    if (smem <= cur && cur) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max(smem, cur));
+    if (e == cudaSuccess) cur = std::max(smem, cur);
+    return e;
+}
+
 template <typename T>
 static cudaError_t occupancy_impl(int mode, size_t smem, int* blocks_per_sm) {
     const void* fn = kernel_ptr<T>(mode);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = grow_smem_limit(fn, smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, THREADS, smem);
 }
@@ -304,16 +324,13 @@ static cudaError_t occupancy_impl(int mode, size_t smem, int* blocks_per_sm) {
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s) {
     size_t smem = (size_t)a.g.smem_per_warp * (THREADS / 32);
     if (wide == 0) {
-        cudaFuncSetAttribute((const void*)oob_root_kernel<long long, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        grow_smem_limit((const void*)oob_root_kernel<long long, 0>, smem);
         oob_root_kernel<long long, 0><<<blocks, THREADS, smem, s>>>(a);
     } else if (wide == 2) {
-        cudaFuncSetAttribute((const void*)oob_root_kernel<i256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        grow_smem_limit((const void*)oob_root_kernel<i256, 2>, smem);
         oob_root_kernel<i256, 2><<<blocks, THREADS, smem, s>>>(a);
     } else {
-        cudaFuncSetAttribute((const void*)oob_root_kernel<__int128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        grow_smem_limit((const void*)oob_root_kernel<__int128, 1>, smem);
         oob_root_kernel<__int128, 1><<<blocks, THREADS, smem, s>>>(a);
     }
     return cudaGetLastError();
