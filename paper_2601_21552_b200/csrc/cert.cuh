@@ -41,12 +41,17 @@ using sym::i128;
 #endif
 constexpr uint64_t MAGIC = 0x4345525431ull;  // "CERT1"
 constexpr int MAXB = 48;                     // box entries (variables + parameters + atoms)
+constexpr uint64_t KCONST = 1ull << 32;      // tighten entry flag: the coefficient K is a constant
 
 // ---- checker (one query; host build in tests, device in the cert kernel) ----
 struct BoxV {  // [0, np) parameters, [np, np + nv) variables, then atoms
-    i128 lo[MAXB], hi[MAXB];
+    // int64 storage (half the per-lane local memory of __int128): a query
+    // with a bound beyond int64 is left to the search (never refuted here);
+    // every product and sum is still exact __int128 (sym::smul / sadd)
+    long long lo[MAXB], hi[MAXB];
     int np;
 };
+OOB_HD CERT_INL bool fits64(i128 x) { return x == (i128)(long long)x; }
 
 OOB_HD CERT_INL bool mono_iv_b(uint64_t k, const BoxV& B, i128& rl, i128& rh) {
     if (!(k << 8)) {  // a constant or a single variable (most terms)
@@ -71,6 +76,23 @@ OOB_HD CERT_INL bool mono_iv_b(uint64_t k, const BoxV& B, i128& rl, i128& rh) {
     }
     return true;
 }
+// key without its parameter bytes; pv = the product of the parameters' values
+OOB_HD CERT_INL uint64_t kstrip_b(uint64_t k, const BoxV& B, i128& pv, bool& ok) {
+    uint64_t r = 0;
+    int n = 0;
+    pv = 1;
+    while (k >> 56) {
+        const uint64_t x = k >> 56;
+        k <<= 8;
+        if ((int)x <= B.np) {
+            if (!sym::smul(pv, B.lo[x - 1], pv)) ok = false;
+        } else {
+            r |= x << (56 - 8 * n);
+            ++n;
+        }
+    }
+    return r;
+}
 // interval of the blob polynomial at p (advances p past it); parameter runs
 // are collapsed first (sym::peval)
 OOB_HD CERT_INL bool peval_blob(const uint64_t*& p, const BoxV& B, i128& lo, i128& hi) {
@@ -78,7 +100,6 @@ OOB_HD CERT_INL bool peval_blob(const uint64_t*& p, const BoxV& B, i128& lo, i12
     const uint64_t* t = p;
     p += 3 * n;
     lo = hi = 0;
-    sym::Box SB{const_cast<i128*>(B.lo), const_cast<i128*>(B.hi), B.np};
     auto coef = [&](uint64_t i) { return (i128)(((unsigned __int128)t[3 * i + 2] << 64) | t[3 * i + 1]); };
     if (B.np == 0) {  // no parameters: one term per monomial
         for (uint64_t i = 0; i < n; ++i) {
@@ -97,11 +118,11 @@ OOB_HD CERT_INL bool peval_blob(const uint64_t*& p, const BoxV& B, i128& lo, i12
     for (uint64_t i = 0; i < n;) {
         bool ok = true;
         i128 pv, c = 0, u;
-        const uint64_t rk = sym::kstrip(t[3 * i], B.np, pv, SB, ok);
+        const uint64_t rk = kstrip_b(t[3 * i], B, pv, ok);
         if (!ok || !sym::smul(coef(i), pv, u) || !sym::sadd(c, u, c)) return false;
         ++i;
         while (i < n) {
-            const uint64_t rk2 = sym::kstrip(t[3 * i], B.np, pv, SB, ok);
+            const uint64_t rk2 = kstrip_b(t[3 * i], B, pv, ok);
             if (rk2 != rk) break;
             if (!ok || !sym::smul(coef(i), pv, u) || !sym::sadd(c, u, c)) return false;
             ++i;
@@ -137,8 +158,8 @@ OOB_HD CERT_INL int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& 
     B.np = np;
     for (int q = 0; q < np; ++q) {
         const i128 x = lit((uint32_t)p[q]);
-        if (sym::big(x)) return C_UNKNOWN;
-        B.lo[q] = B.hi[q] = x;
+        if (!fits64(x)) return C_UNKNOWN;
+        B.lo[q] = B.hi[q] = (long long)x;
     }
     p += np;
     // literal slots the certificate folded as numbers must hold exactly those
@@ -149,9 +170,10 @@ OOB_HD CERT_INL int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& 
         if (lit((uint32_t)p[0]) != want) return C_UNKNOWN;
     }
     for (int v = 0; v < nv; ++v) {
-        B.lo[np + v] = dom(2 * v);
-        B.hi[np + v] = dom(2 * v + 1);
-        if (sym::big(B.lo[np + v]) || sym::big(B.hi[np + v])) return C_UNKNOWN;
+        const i128 a = dom(2 * v), b = dom(2 * v + 1);
+        if (!fits64(a) || !fits64(b)) return C_UNKNOWN;
+        B.lo[np + v] = (long long)a;
+        B.hi[np + v] = (long long)b;
     }
     reason = 3;
     // atoms, in creation order (each may use the earlier ones)
@@ -161,26 +183,30 @@ OOB_HD CERT_INL int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& 
         const int d = nv + np + t;
         i128 al, ah, bl, bh;
         if (!peval_blob(p, B, al, ah) || !peval_blob(p, B, bl, bh)) return C_UNKNOWN;
+        i128 rlo, rhi;
         if (litdiv) {
             if (bl != bh || bl < 1) return C_UNKNOWN;  // guards0 also checks it
-            B.lo[d] = sym::tdiv(al, bl);
-            B.hi[d] = sym::tdiv(ah, bl);
+            rlo = sym::tdiv(al, bl);
+            rhi = sym::tdiv(ah, bl);
         } else if (op == NODE_DIV) {
             if (al >= 0 && bl >= 1) {
-                B.lo[d] = sym::tdiv(al, bh);
-                B.hi[d] = sym::tdiv(ah, bl);
+                rlo = sym::tdiv(al, bh);
+                rhi = sym::tdiv(ah, bl);
             } else {
                 const i128 m = sym::imax(sym::iabs(al), sym::iabs(ah));
-                B.lo[d] = -m;
-                B.hi[d] = m;
+                rlo = -m;
+                rhi = m;
             }
         } else {
             i128 m = sym::imax(sym::iabs(bl), sym::iabs(bh)) - 1;
             if (m < 0) m = 0;
             m = sym::imin(m, sym::imax(sym::iabs(al), sym::iabs(ah)));
-            B.lo[d] = al < 0 ? -m : 0;
-            B.hi[d] = ah > 0 ? m : 0;
+            rlo = al < 0 ? -m : 0;
+            rhi = ah > 0 ? m : 0;
         }
+        if (!fits64(rlo) || !fits64(rhi)) return C_UNKNOWN;
+        B.lo[d] = (long long)rlo;
+        B.hi[d] = (long long)rhi;
     }
     // guards0 on the build box
     reason = 4;
@@ -188,32 +214,47 @@ OOB_HD CERT_INL int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& 
         i128 lo, hi;
         if (!peval_blob(p, B, lo, hi) || lo < 0) return C_UNKNOWN;
     }
-    // tighten
+    // tighten (entry: v | KCONST flag, then the constant K or K's polynomial,
+    // then s)
     const uint64_t ne = *p++;
     const uint64_t* ent = p;
     for (uint64_t e = 0; e < ne; ++e) {  // skip to the end of the entries
-        p += 1;
-        skip_poly(p);
+        const uint64_t w = *p++;
+        if (w & KCONST) p += 1;
+        else skip_poly(p);
         skip_poly(p);
     }
     for (int r = 0; r < sym::ROUNDS; ++r) {
         bool changed = false;
         const uint64_t* q = ent;
         for (uint64_t e = 0; e < ne; ++e) {
-            const int v = (int)q[0];
-            q += 1;
-            i128 klo, khi, slo, shi;
-            const bool kok = peval_blob(q, B, klo, khi);
-            if (!peval_blob(q, B, slo, shi) || !kok || klo != khi || klo == 0) continue;
-            const i128 k = klo;
+            const uint64_t w = *q++;
+            const int v = (int)(w & 0xFFFFu);
+            i128 k;
+            if (w & KCONST) {
+                k = (i128)(long long)*q++;
+            } else {
+                i128 klo, khi;
+                const bool kok = peval_blob(q, B, klo, khi);
+                k = (kok && klo == khi) ? klo : 0;
+            }
+            i128 slo, shi;
+            if (!peval_blob(q, B, slo, shi) || k == 0) continue;
             if (k > 0) {
                 const i128 nlo = -sym::fdiv(shi, k);
-                if (nlo > B.lo[v]) B.lo[v] = nlo, changed = true;
+                if (nlo > B.lo[v]) {
+                    if (nlo > B.hi[v]) return C_REFUTED;
+                    B.lo[v] = (long long)nlo;
+                    changed = true;
+                }
             } else {
                 const i128 nhi = sym::fdiv(shi, -k);
-                if (nhi < B.hi[v]) B.hi[v] = nhi, changed = true;
+                if (nhi < B.hi[v]) {
+                    if (nhi < B.lo[v]) return C_REFUTED;
+                    B.hi[v] = (long long)nhi;
+                    changed = true;
+                }
             }
-            if (B.lo[v] > B.hi[v]) return C_REFUTED;
         }
         if (!changed) break;
     }
@@ -336,8 +377,13 @@ inline size_t cert_build(sym::Store& S, sym::LaneWork& W, sym::Moves& M, const u
         for (int v = 0; v < S.nv; ++v) {
             PV K = w[1], s = w[0];
             if (!pcoef(g, v, 0, S.np, K, s)) continue;
-            b.put((uint64_t)v);
-            b.poly(K);
+            if (K.n == 1 && K.k[0] == 0 && K.c[0] == (i128)(long long)K.c[0]) {
+                b.put((uint64_t)v | KCONST);
+                b.put((uint64_t)(long long)K.c[0]);
+            } else {
+                b.put((uint64_t)v);
+                b.poly(K);
+            }
             b.poly(s);
             ++ne;
             covered[j] = true;
