@@ -85,8 +85,10 @@ def test_node_budget_is_deterministic_timeout(gpu, heavy):
 
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
 def test_frontier_matches_sequential_on_synthetic_streams(gpu, cfg):
-    """20K queries of each stream: the frontier path (every query handed off)
-    and the one-lane path agree on every verdict, model and counter."""
+    """20K queries of each stream: the frontier path (every query handed off),
+    the one-lane path, the default hand-off, no demotion and no x32 agree on
+    every verdict, model and counter -- with each other and with the C
+    restatement of the reference."""
     from paper_2601_21552_b200 import synth
     fb = synth.generate(cfg, 20000, names=False)
     a = solve_flat(fb, 30.0, heavy_nodes=-1)
@@ -97,3 +99,8 @@ def test_frontier_matches_sequential_on_synthetic_streams(gpu, cfg):
     for o in (b, c, d, e):
         for k in ("verdict", "nodes", "passes", "model"):
             assert np.array_equal(a[k], o[k]), k
+    # and against the C restatement of the reference on the whole stream
+    from oracle import oracle
+    r = oracle.solve_flat(fb, 30.0, threads=oracle.cpu_count())
+    for k in ("verdict", "nodes", "passes", "model"):
+        assert np.array_equal(a[k], r[k]), k
