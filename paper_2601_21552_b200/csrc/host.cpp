@@ -224,6 +224,7 @@ struct Structure {
     std::vector<int32_t> lit_src; // per literal slot: the query's input literal index (-1: the constant 1)
     uint64_t key = 0;             // structure-class hash (words, nv, ncon)
     std::string range_why;        // non-empty: the structure alone is beyond the engine (R_RANGE)
+    int w128_log2 = -1;           // ... and <= 2^w128_log2: the int128 regime (fast mode's shortcut)
     int w64_log2 = -1;            // every query of this structure whose domain bounds and literals
                                   // are <= 2^w64_log2 in magnitude is in the int64 regime (-1: none)
     const uint32_t* code() const { return words.data() + ncon; }
@@ -757,6 +758,24 @@ std::shared_ptr<Structure> build_structure(const QView& v, int mode) {
                 else hi = mid;
             }
         st.w64_log2 = lo;
+        // the same for the int128 regime (2^127 = 1.7e38; the double bound's
+        // relative rounding error is below 1e-12)
+        auto ok128 = [&](int k) {
+            const i128 D = (i128)1 << k;
+            for (uint32_t i = 0; i < st.nv; i++) { dlo[i] = -D; dhi[i] = D; }
+            for (uint32_t i = 0; i < st.nlit; i++) lits[i] = D;
+            return prove_bound_mag(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits) < 1.6e38;
+        };
+        lo = -1;
+        hi = 125;
+        if (ok128(hi)) lo = hi;
+        else
+            while (hi - lo > 1) {
+                int mid = lo + (hi - lo) / 2;
+                if (mid >= 0 && ok128(mid)) lo = mid;
+                else hi = mid;
+            }
+        st.w128_log2 = lo;
     }
     return out;
 }
@@ -833,8 +852,13 @@ struct StructCache {
 };
 
 // mode: MODE_SOLVE (side constraints), MODE_PROPAGATE / MODE_CHECK (as given)
+// fast: the fast mode's regime shortcut -- a query the double-precision
+// bound does not admit to int64 but whose magnitudes are within the
+// structure's int128 threshold goes to the int128 job without the exact
+// proof (which would move some of them to int64: a scheduling choice only;
+// every regime is exact for the query it holds)
 Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s,
-                       const oob_i128* model_in) {
+                       const oob_i128* model_in, bool fast = false) {
     Compiled out;
     QView v = view_of(b, q);
     out.nv = (uint32_t)v.nv;
@@ -901,6 +925,10 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
     const double mag = prove_bound_mag(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits);
     if (mag < 9.2e18 && Dmax <= D64MAX) {
         out.regime = R_W64;
+        return out;
+    }
+    if (fast && st.w128_log2 >= 0 && imax(Dmax, Lmax) <= ((i128)1 << st.w128_log2) && Dmax <= D128MAX) {
+        out.regime = R_W128;
         return out;
     }
     i128 B = prove_bound(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits);
@@ -1290,7 +1318,7 @@ void pack(const RunCtx& rc, DevJob& j, bool inline_fill = false) {
         }
     };
     if (inline_fill) fill(0, n);
-    else parallel_for(n, 4096, fill);
+    else parallel_for(n, 1024, fill);  // (the wide jobs hold 10-30K entries: small grains spread them)
     if (n == 0) std::fill(j.data.data(), j.data.data() + j.data.size(), 0);
     if (j.code.empty()) j.code.push_back(0);
     if (j.cls.empty()) j.cls.push_back(ClassDesc{});
@@ -1856,14 +1884,20 @@ void pack_group(const RunCtx& rc, DevGroup& G, bool upload = false) {
         if (T.shadows.empty()) continue;
         static thread_local std::vector<uint32_t> at;  // query id -> shadow index in T
         if (at.size() < (size_t)rc.b->n_queries) at.resize((size_t)rc.b->n_queries);
-        for (size_t i = 0; i < T.qs.size(); i++)
-            if (T.is_shadow[i]) at[T.qs[i]] = (uint32_t)i;
+        uint32_t* atp = at.data();
+        parallel_for(T.qs.size(), 8192, [&](size_t lo, size_t hi) {
+            for (size_t i = lo; i < hi; i++)
+                if (T.is_shadow[i]) atp[T.qs[i]] = (uint32_t)i;
+        });
         for (int w = 0; w < 3; w++) {
             if (t == 2 ? w != 0 : w <= t) continue;  // x32: from the int64 job; else from the wider jobs
             DevJob& W = G.job[w];
             if (W.qs.empty()) continue;
             W.slot[t].resize(W.qs.size());
-            for (size_t i = 0; i < W.qs.size(); i++) W.slot[t][i] = at[W.qs[i]];
+            uint32_t* sl = W.slot[t].data();
+            parallel_for(W.qs.size(), 8192, [&](size_t lo, size_t hi) {
+                for (size_t i = lo; i < hi; i++) sl[i] = atp[W.qs[i]];
+            });
         }
     }
 }
@@ -2110,7 +2144,7 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
     std::vector<uint8_t> is_retry(n, 0);
-    parallel_for(n, 8192, [&](size_t lo, size_t hi) {
+    parallel_for(n, 2048, [&](size_t lo, size_t hi) {
         for (size_t i = lo; i < hi; i++) {
             if (verdict[i] == VERDICT_NONE) continue;
             int64_t q = j.qs[i];
@@ -2378,20 +2412,32 @@ void cert_cache_put(std::vector<uint64_t>&& key, const std::vector<uint64_t>& va
 }
 void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const std::vector<int64_t> reg[3],
                  std::vector<uint64_t>& certs, std::vector<uint32_t>& cert_off) {
+    // compact per-device-query views (class id, structure): the loops below
+    // then stream 12 bytes per query instead of whole Compiled records
+    size_t ndq = 0;
+    for (int w = 0; w < 3; w++) ndq += reg[w].size();
+    std::vector<int64_t> dq;
+    dq.reserve(ndq);
+    for (int w = 0; w < 3; w++) dq.insert(dq.end(), reg[w].begin(), reg[w].end());
+    std::vector<uint32_t> qc(ndq);
+    std::vector<const Structure*> qs(ndq);
+    parallel_for(ndq, 8192, [&](size_t lo, size_t hi) {
+        for (size_t k = lo; k < hi; k++) {
+            qc[k] = comp[dq[k]].cls;
+            qs[k] = comp[dq[k]].st.get();
+        }
+    });
     uint32_t ncls = 0;
-    for (int w = 0; w < 3; w++)
-        for (int64_t q : reg[w]) ncls = std::max(ncls, comp[q].cls + 1);
+    for (uint32_t c : qc) ncls = std::max(ncls, c + 1);
     std::vector<uint32_t> start(ncls + 1, 0);
-    for (int w = 0; w < 3; w++)
-        for (int64_t q : reg[w]) start[comp[q].cls + 1]++;
+    for (uint32_t c : qc) start[c + 1]++;
     for (uint32_t c = 0; c < ncls; c++) start[c + 1] += start[c];
-    // members of every class in ascending query order (one pass)
-    std::vector<int64_t> mem(start[ncls]);
+    // members of every class (regime-major, ascending within a regime):
+    // positions k into dq / qc / qs
+    std::vector<uint32_t> mem(ndq);
     {
         std::vector<uint32_t> at(start.begin(), start.end() - 1);
-        const int64_t n = (int64_t)comp.size();
-        for (int64_t q = 0; q < n; q++)
-            if (comp[q].regime >= R_W64 && comp[q].regime <= R_W256) mem[at[comp[q].cls]++] = q;
+        for (size_t k = 0; k < ndq; k++) mem[at[qc[k]]++] = (uint32_t)k;
     }
     // literal slots whose value varies inside the class (the parameters):
     // each query against its class's first member, in parallel over queries
@@ -2399,22 +2445,22 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
     // equal literal-slot sources)
     std::vector<uint32_t> loff(ncls + 1, 0);
     for (uint32_t c = 0; c < ncls; c++)
-        loff[c + 1] = loff[c] + (start[c + 1] > start[c] ? comp[mem[start[c]]].st->nlit : 0);
+        loff[c + 1] = loff[c] + (start[c + 1] > start[c] ? qs[mem[start[c]]]->nlit : 0);
     std::vector<i128> v0(loff[ncls]);
     std::unique_ptr<std::atomic<uint8_t>[]> vary(new std::atomic<uint8_t>[std::max<uint32_t>(loff[ncls], 1)]);
     for (uint32_t c = 0; c < ncls; c++) {
         if (start[c + 1] == start[c]) continue;
-        const int64_t q0 = mem[start[c]];
+        const uint32_t k0 = mem[start[c]];
         for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
-            v0[loff[c] + i] = lit_value(b, q0, *comp[q0].st, i);
+            v0[loff[c] + i] = lit_value(b, dq[k0], *qs[k0], i);
             vary[loff[c] + i].store(0, std::memory_order_relaxed);
         }
     }
-    parallel_for(mem.size(), 4096, [&](size_t lo, size_t hi) {
+    parallel_for(ndq, 4096, [&](size_t lo, size_t hi) {
         for (size_t k = lo; k < hi; k++) {
-            const int64_t q = mem[k];
-            const uint32_t c = comp[q].cls;
-            const Structure& sk = *comp[q].st;
+            const uint32_t c = qc[k];
+            const Structure& sk = *qs[k];
+            const int64_t q = dq[k];
             for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
                 std::atomic<uint8_t>& f = vary[loff[c] + i];
                 if (!f.load(std::memory_order_relaxed) && lit_value(b, q, sk, i) != v0[loff[c] + i])
@@ -2435,10 +2481,10 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
             buf.resize(1 << 15);
         }
         for (size_t c = lo; c < hi; c++) {
-            const int64_t* m = mem.data() + start[c];
+            const uint32_t* m = mem.data() + start[c];
             const size_t nm = start[c + 1] - start[c];
             if (!nm) continue;
-            const Structure& st = *comp[m[0]].st;
+            const Structure& st = *qs[m[0]];
             if (!st.range_why.empty()) continue;
             std::vector<int16_t> pmap(st.nlit, -1), pslot;
             for (uint32_t i = 0; i < st.nlit; i++)
@@ -2466,10 +2512,11 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
             std::vector<std::vector<uint64_t>> got;
             const size_t nr = std::min<size_t>(CERT_REPS, nm);
             for (size_t r = 0; r < nr; r++) {
-                const int64_t q = m[r * nm / nr];
+                const uint32_t kq = m[r * nm / nr];
+                const int64_t q = dq[kq];
                 const int64_t vb = b->var_begin[q];
                 auto dom = [&](uint32_t i) -> i128 { return from_w(i % 2 ? b->var_hi[vb + i / 2] : b->var_lo[vb + i / 2]); };
-                const Structure& sq = *comp[q].st;
+                const Structure& sq = *qs[kq];
                 auto lit = [&](uint32_t i) -> i128 { return lit_value(b, q, sq, i); };
                 const size_t n = cert::cert_build(*S, *W, *M, st.words.data(), st.code(), st.nv, st.ncon, st.nlit,
                                                   dom, lit,
@@ -2542,10 +2589,12 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     }
     std::vector<Compiled>& comp = pr.comp;
     comp.assign(n, Compiled{});
+    const bool fast_shortcut = mode == MODE_SOLVE && (opt.flags & OOB_F_FAST);
     {
         Phase ph("compile");
         parallel_for((size_t)n, 256, [&](size_t lo, size_t hi) {
-            for (size_t q = lo; q < hi; q++) comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in);
+            for (size_t q = lo; q < hi; q++)
+                comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, fast_shortcut);
         });
     }
     pr.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -2576,7 +2625,10 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     int want = opt.n_gpus > 0 ? opt.n_gpus : ndev - first;
     want = std::max(1, std::min(want, ndev - first));
     Phase ph_sched("schedule");
-    assign_classes(comp, reg);
+    {
+        Phase ph_cls("schedule.classes");
+        assign_classes(comp, reg);
+    }
     pr.certs.clear();
     pr.cert_off.clear();
     if (mode == MODE_SOLVE && (opt.flags & OOB_F_FAST) && opt.timeout_s > 0) {
@@ -2590,25 +2642,45 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         pr.work.resize(want);
         for (int d = 0; d < want; d++) pr.work[d].dev = first + d;
     }
+    Phase ph_sort("schedule.sort");
     for (int w = 0; w < 3; w++) {
         auto& qs = reg[w];
         if (qs.empty()) continue;
         if (!(opt.flags & OOB_F_NO_SORT)) {
             // class-major (counting sort, stable), cost-minor: expensive first,
             // ties by query index (per-class sorts run in parallel)
+            const std::vector<uint32_t>& qcls = pr.qcls;
             uint32_t ncls = 0;
-            for (int64_t q : qs) ncls = std::max(ncls, comp[q].cls + 1);
+            for (int64_t q : qs) ncls = std::max(ncls, qcls[q] + 1);
             std::vector<uint32_t> start(ncls + 1, 0);
-            for (int64_t q : qs) start[comp[q].cls + 1]++;
+            for (int64_t q : qs) start[qcls[q] + 1]++;
             for (uint32_t c = 0; c < ncls; c++) start[c + 1] += start[c];
             std::vector<std::pair<uint32_t, int64_t>> keyed(qs.size());  // (inverted cost, query)
             {
                 std::vector<uint32_t> at(start.begin(), start.end() - 1);
                 for (int64_t q : qs)
-                    keyed[at[comp[q].cls]++] = {0xFFFFu - (uint32_t)std::min(comp[q].cost, 65535.0), q};
+                    keyed[at[qcls[q]]++] = {0xFFFFu - (uint32_t)std::min(comp[q].cost, 65535.0), q};
             }
+            // per class: a stable counting sort on the key (ties stay in
+            // ascending query order, as the sort on (key, query) had them)
             parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
-                for (size_t c = lo; c < hi; c++) std::sort(keyed.begin() + start[c], keyed.begin() + start[c + 1]);
+                std::vector<uint32_t> cnt;
+                std::vector<std::pair<uint32_t, int64_t>> tmp;
+                for (size_t c = lo; c < hi; c++) {
+                    const size_t a = start[c], z = start[c + 1];
+                    if (z - a < 2) continue;
+                    uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
+                    for (size_t i = a; i < z; i++) {
+                        kmin = std::min(kmin, keyed[i].first);
+                        kmax = std::max(kmax, keyed[i].first);
+                    }
+                    cnt.assign(kmax - kmin + 2, 0);
+                    for (size_t i = a; i < z; i++) cnt[keyed[i].first - kmin + 1]++;
+                    for (size_t k = 1; k < cnt.size(); k++) cnt[k] += cnt[k - 1];
+                    tmp.resize(z - a);
+                    for (size_t i = a; i < z; i++) tmp[cnt[keyed[i].first - kmin]++] = keyed[i];
+                    std::copy(tmp.begin(), tmp.end(), keyed.begin() + a);
+                }
             });
             for (size_t i = 0; i < qs.size(); i++) qs[i] = keyed[i].second;
         }
