@@ -2570,32 +2570,30 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     const oob_options& opt = pr.opt;
     const int64_t n = b->n_queries;
     auto t0 = std::chrono::steady_clock::now();
+    std::vector<Compiled>& comp = pr.comp;
+    comp.resize(n);  // every entry is overwritten below (recycled vectors keep their storage)
+    const bool fast_shortcut = mode == MODE_SOLVE && (opt.flags & OOB_F_FAST);
     {
-        Phase ph("validate");
+        // validation and compilation in one pass over the batch: a query is
+        // compiled only once it has validated; the lowest invalid query is
+        // reported (nothing is decided for an invalid batch)
+        Phase ph("validate+compile");
         std::atomic<int64_t> bad{INT64_MAX};
-        parallel_for((size_t)n, 8192, [&](size_t lo, size_t hi) {
-            for (size_t q = lo; q < hi; q++)
+        parallel_for((size_t)n, 256, [&](size_t lo, size_t hi) {
+            for (size_t q = lo; q < hi; q++) {
                 if (!validate(b, (int64_t)q).empty()) {
                     int64_t cur = bad.load();
                     while ((int64_t)q < cur && !bad.compare_exchange_weak(cur, (int64_t)q)) {
                     }
                     break;
                 }
+                comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, fast_shortcut);
+            }
         });
         if (bad.load() != INT64_MAX) {
             int64_t q = bad.load();
             return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + validate(b, q));
         }
-    }
-    std::vector<Compiled>& comp = pr.comp;
-    comp.assign(n, Compiled{});
-    const bool fast_shortcut = mode == MODE_SOLVE && (opt.flags & OOB_F_FAST);
-    {
-        Phase ph("compile");
-        parallel_for((size_t)n, 256, [&](size_t lo, size_t hi) {
-            for (size_t q = lo; q < hi; q++)
-                comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, fast_shortcut);
-        });
     }
     pr.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     pr.errs.assign(n, 0);
