@@ -39,6 +39,9 @@
 #include <thread>
 #include <vector>
 
+#include <cerrno>
+#include <ctime>
+#include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -425,6 +428,44 @@ std::string compile_entry(Entry& e, const JitClass& c) {
         e.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         return "";
     }
+    // one compiler per class per box: the ranks of a torchrun job compile the
+    // same classes at the same moment; the first takes `<cubin>.lock`, the
+    // others wait for its cubin (a lock older than 120 s is presumed dead)
+    int lock_fd = -1;
+    if (!cpath.empty()) {
+        const std::string dir = cpath.substr(0, cpath.rfind('/'));
+        for (size_t i = 1; i <= dir.size(); i++)  // mkdir -p
+            if (i == dir.size() || dir[i] == '/') ::mkdir(dir.substr(0, i).c_str(), 0755);
+        const std::string lpath = cpath + ".lock";
+        for (int waited = 0;; waited += 50) {
+            lock_fd = ::open(lpath.c_str(), O_CREAT | O_EXCL | O_WRONLY, 0644);
+            if (lock_fd >= 0) break;
+            if (read_file(cpath, e.cubin)) {
+                e.from_disk = true;
+                e.compile_ms =
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                return "";
+            }
+            struct stat st;
+            if (waited > 120000 || (::stat(lpath.c_str(), &st) == 0 && ::time(nullptr) - st.st_mtime > 120)) {
+                std::remove(lpath.c_str());  // stale
+                waited = 0;
+                continue;
+            }
+            if (errno != EEXIST) break;  // no lock possible here: just compile
+            ::usleep(50000);
+        }
+    }
+    struct LockRelease {
+        int fd;
+        std::string path;
+        ~LockRelease() {
+            if (fd >= 0) {
+                ::close(fd);
+                std::remove(path.c_str());
+            }
+        }
+    } lock_release{lock_fd, cpath + ".lock"};
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, src.c_str(), "oob_jit_class.cu", kNumHeaders, kHeaderSrc, kHeaderNames) !=
         NVRTC_SUCCESS)
