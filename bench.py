@@ -483,9 +483,9 @@ def run_ours(args, rank, world, local):
         return
     launch_ms = sum(kernel_ms) / len(kernel_ms)
     n_sat = int((res["verdict"] == 1).sum())
-    conf = config_dict(cfg, total, per, scaling, world, args.mode)
-    conf.update({"classes": info["classes"], "wide_regime_queries": info["wide_queries"], "sat": n_sat,
-                 "unsat": int((res["verdict"] == 0).sum())})
+    conf = config_dict(cfg, total, per, scaling, world, args.mode)  # identical to the reference arm's
+    stats = {"classes": info["classes"], "wide_regime_queries": info["wide_queries"], "sat": n_sat,
+             "unsat": int((res["verdict"] == 0).sum()), "timeout": int((res["verdict"] == 2).sum())}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -493,6 +493,7 @@ def run_ours(args, rank, world, local):
         "scaling": scaling, "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (seeded analyzer-shaped query stream, generated natively)",
         "config": conf,
+        "workload_stats": stats,
         "roofline": rooflines(cfg, args.mode, per, launch_ms, info),
         "cpu_baseline": extras.get("cpu_baseline"),
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
