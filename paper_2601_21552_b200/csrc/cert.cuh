@@ -24,8 +24,9 @@
 // query whose guards fail is simply not refuted here.
 //
 // Blob layout (u64 words): see cert_check() -- header, parameter slots,
-// folded constant slots (slot, value: checked per query), atoms, guards0,
-// tighten entries, direct constraints, guards1, final.
+// folded constant slots (slot, value: checked per query), atoms, domain
+// guards of eliminated variables, guards0, tighten entries, direct
+// constraints, guards1, final.
 // Polynomial: n, then n x (key, coef lo, coef hi).
 #pragma once
 #include "symbolic.cuh"
@@ -208,6 +209,15 @@ OOB_HD CERT_INL int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& 
         B.lo[d] = (long long)rlo;
         B.hi[d] = (long long)rhi;
     }
+    // eliminated variables: their domain constraints were compiled with the
+    // representative's bounds, valid for a query whose domain lies within them
+    for (uint64_t g = *p++; g > 0; --g, p += 5) {
+        const int v = (int)(p[0] & 0xFFFF), flags = (int)(p[0] >> 16);
+        const i128 lo = (i128)(((unsigned __int128)p[2] << 64) | p[1]);
+        const i128 hi = (i128)(((unsigned __int128)p[4] << 64) | p[3]);
+        if ((flags & 1) && (i128)B.lo[v] < lo) return C_UNKNOWN;
+        if ((flags & 2) && (i128)B.hi[v] > hi) return C_UNKNOWN;
+    }
     // guards0 on the build box
     reason = 4;
     for (uint64_t g = *p++; g > 0; --g) {
@@ -361,10 +371,19 @@ inline size_t cert_build(sym::Store& S, sym::LaneWork& W, sym::Moves& M, const u
             }
         }
     }
-    b.put((uint64_t)ng0);
-    for (int i = 0; i < ng0; ++i) b.poly(guards0[i]);
     PV w[4] = {work(W, 0), work(W, 1), work(W, 2), work(W, 3)};
     if (!eliminate(S, w) || S.nc > 64) CERT_FAIL();
+    // domain-containment guards of the eliminated variables, then guards0
+    b.put((uint64_t)S.nelim);
+    for (int i = 0; i < S.nelim; ++i) {
+        b.put((uint64_t)(uint16_t)S.elim_v[i] | (uint64_t)(uint8_t)S.elim_flags[i] << 16);
+        b.put((uint64_t)S.elim_lo[i]);
+        b.put((uint64_t)((unsigned __int128)S.elim_lo[i] >> 64));
+        b.put((uint64_t)S.elim_hi[i]);
+        b.put((uint64_t)((unsigned __int128)S.elim_hi[i] >> 64));
+    }
+    b.put((uint64_t)ng0);
+    for (int i = 0; i < ng0; ++i) b.poly(guards0[i]);
     // tighten entries: every constraint, every variable with a (parametric)
     // constant coefficient: (v, K, s) for g = K*v + s
     size_t at_ne = b.n;

@@ -2508,11 +2508,31 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
                     ckey.push_back((uint64_t)((unsigned __int128)x >> 64));
                 }
             }
+            // representatives: the member with the widest domains first (a
+            // certificate holds for every member whose domains of the
+            // eliminated variables lie within the representative's, and its
+            // sign conditions only get easier on sub-boxes), then members
+            // spread over the class
+            uint32_t widest = m[0];
+            for (size_t i = 1; i < nm; i++)
+                if (comp[dq[m[i]]].cost > comp[dq[widest]].cost) widest = m[i];
+            // ... so the cache key also carries the widest member's domains
+            {
+                const int64_t vb = b->var_begin[dq[widest]];
+                for (uint32_t v = 0; v < st.nv; v++) {
+                    const i128 lo = from_w(b->var_lo[vb + v]), hi = from_w(b->var_hi[vb + v]);
+                    ckey.push_back((uint64_t)lo);
+                    ckey.push_back((uint64_t)((unsigned __int128)lo >> 64));
+                    ckey.push_back((uint64_t)hi);
+                    ckey.push_back((uint64_t)((unsigned __int128)hi >> 64));
+                }
+            }
             if (cert_cache_get(ckey, per[c])) continue;
             std::vector<std::vector<uint64_t>> got;
             const size_t nr = std::min<size_t>(CERT_REPS, nm);
-            for (size_t r = 0; r < nr; r++) {
-                const uint32_t kq = m[r * nm / nr];
+            for (size_t r = 0; r <= nr; r++) {
+                const uint32_t kq = r == 0 ? widest : m[(r - 1) * nm / nr];
+                if (r > 0 && kq == widest) continue;
                 const int64_t q = dq[kq];
                 const int64_t vb = b->var_begin[q];
                 auto dom = [&](uint32_t i) -> i128 { return from_w(i % 2 ? b->var_hi[vb + i / 2] : b->var_lo[vb + i / 2]); };

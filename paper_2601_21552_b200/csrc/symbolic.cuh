@@ -405,6 +405,13 @@ struct Store {
     int8_t acase[MAXA];   // dividend sign on the build box: 0 >= 0, 1 <= 0, 2 mixed
     int8_t alitdiv[MAXA]; // divisor is a literal >= 1 (constant or parameter)
     int natoms;
+    // eliminated variables whose domain became constraints (certificate
+    // compilation: those constraints hold for a query only if its domain of
+    // the variable lies within the bounds used here -- cert.cuh checks it)
+    int nelim;
+    int16_t elim_v[MAXC];
+    int8_t elim_flags[MAXC];  // 1: lower bound used, 2: upper bound used
+    i128 elim_lo[MAXC], elim_hi[MAXC];
     // literal parameters (certificate compilation): box entries 0 .. np-1
     // hold literal slots whose value varies inside the structure class; the
     // query's variables follow (np .. np+nv-1), then the atoms
@@ -653,6 +660,7 @@ OOB_HD inline bool build(Store& S, const uint32_t* cons, const uint32_t* code, u
     if (nv + (uint32_t)np > (uint32_t)MAXV) return false;
     S.np = pmap ? np : 0;
     S.nv = S.np + (int)nv;
+    S.nelim = 0;
     S.nc = 0;
     S.cur = 0;
     S.used = 0;
@@ -787,8 +795,18 @@ OOB_HD SYM_NI inline bool eliminate(Store& S, PV* w) {
         // they hold on the whole box)
         i128 elo, ehi;
         const bool ev_ok = peval(ex, B, elo, ehi);
-        if ((!ev_ok || elo < S.lo[ev]) && !add_con(S, ex, 1, -S.lo[ev], false, -1)) return false;
-        if ((!ev_ok || ehi > S.hi[ev]) && !add_con(S, ex, -1, S.hi[ev], false, -1)) return false;
+        const bool use_lo = !ev_ok || elo < S.lo[ev], use_hi = !ev_ok || ehi > S.hi[ev];
+        if (use_lo && !add_con(S, ex, 1, -S.lo[ev], false, -1)) return false;
+        if (use_hi && !add_con(S, ex, -1, S.hi[ev], false, -1)) return false;
+        if ((use_lo || use_hi) && S.nelim < MAXC) {
+            S.elim_v[S.nelim] = (int16_t)ev;
+            S.elim_flags[S.nelim] = (int8_t)((use_lo ? 1 : 0) | (use_hi ? 2 : 0));
+            S.elim_lo[S.nelim] = S.lo[ev];
+            S.elim_hi[S.nelim] = S.hi[ev];
+            ++S.nelim;
+        } else if (use_lo || use_hi) {
+            return false;
+        }
     }
     // remaining equalities -> e >= 0 and -e >= 0
     const int nc0 = S.nc;

@@ -72,6 +72,7 @@ extern "C" int sym_host_refute(const oob_batch* b, int8_t* refuted) {
 // checked numerically for every query of the class (the device's job).
 // refuted[q] = 1: refuted by its class certificate.  stats[0] classes,
 // [1] classes with a certificate, [2] total certificate words.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -123,8 +124,21 @@ extern "C" int sym_host_cert(const oob_batch* b, int32_t reps, int8_t* refuted, 
                 }
         std::vector<std::vector<uint64_t>> certs;
         const int nr = std::max(1, std::min<int>(reps, (int)mem.size()));
-        for (int ri = 0; ri < nr; ++ri) {
-            const int64_t rq = mem[(size_t)ri * mem.size() / nr];
+        // the member with the widest domains first (as the engine does)
+        int64_t widest = mem[0];
+        auto width_bits = [&](int64_t q) {
+            double w = 0;
+            for (int64_t v = b->var_begin[q]; v < b->var_begin[q + 1]; ++v) {
+                const i128 d = w128(b->var_hi[v]) - w128(b->var_lo[v]);
+                w += d > 0 ? std::log2((double)d + 1.0) : 0.0;
+            }
+            return w;
+        };
+        for (int64_t q : mem)
+            if (width_bits(q) > width_bits(widest)) widest = q;
+        for (int ri = 0; ri <= nr; ++ri) {
+            const int64_t rq = ri == 0 ? widest : mem[(size_t)(ri - 1) * mem.size() / nr];
+            if (ri > 0 && rq == widest) continue;
             const Q& r = qs[rq];
             const int64_t vb = b->var_begin[rq];
             auto dom = [&](uint32_t i) -> i128 { return w128(i % 2 ? b->var_hi[vb + i / 2] : b->var_lo[vb + i / 2]); };
