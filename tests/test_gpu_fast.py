@@ -88,3 +88,36 @@ def test_fast_timeout_zero_is_timeout_before_search(gpu):
     assert set(np.unique(out["verdict"])) <= {_lib.UNSAT, _lib.TIMEOUT}
     ref = solve_flat(fb, 0.0)
     assert np.array_equal(out["verdict"], ref["verdict"])
+
+
+def test_fast_frontier_prover_option(gpu, tmp_path):
+    """SCUBA_OOB_FAST_FRONTIER=1 (read once per process, hence a subprocess):
+    heavy queries also meet the symbolic prover itself in the interpreting
+    frontier; verdicts and models stay the golden ones."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    script = tmp_path / "ff.py"
+    script.write_text(
+        "import sys, json\n"
+        f"sys.path.insert(0, {str(ROOT)!r}); sys.path.insert(0, {str(ROOT / 'tests')!r})\n"
+        "from conftest import GOLDEN_SETS, VCODE, load_golden\n"
+        "from paper_2601_21552_b200 import _lib, synth\n"
+        "from paper_2601_21552_b200.solver import solve_flat\n"
+        "from paper_2601_21552_b200.wire import flatten\n"
+        "bad = 0\n"
+        "for name in GOLDEN_SETS:\n"
+        "    recs = [r for r in load_golden(name) if r['verdict'] != 'timeout' and r['timeout'] == 30.0]\n"
+        "    fb = flatten(recs)\n"
+        "    out = solve_flat(fb, 30.0, flags=_lib.F_FAST | _lib.F_NO_JIT, n_gpus=1)\n"
+        "    bad += sum(int(out['verdict'][q]) != VCODE[r['verdict']] for q, r in enumerate(recs))\n"
+        "c5 = synth.generate('c5', 500, names=False)\n"
+        "f5 = solve_flat(c5, 30.0, flags=_lib.F_FAST, n_gpus=1)\n"
+        "print(json.dumps({'bad': bad, 'c5_unsat': int((f5['verdict'] == 0).sum())}))\n")
+    env = dict(os.environ, SCUBA_OOB_FAST_FRONTIER="1")
+    r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res == {"bad": 0, "c5_unsat": 500}
