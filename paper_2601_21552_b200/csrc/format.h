@@ -137,9 +137,11 @@ struct LaunchArgs {
     // heavy_nodes DFS nodes and queues it for the frontier kernel
     uint32_t heavy_nodes;     // 0 = never hand off
     uint32_t heavy_passes;    // also hand off after this many propagation passes (0 = no)
+    uint32_t handoff_gate;    // hand off only while a frontier warp of the launch waits (fast mode)
     uint32_t frontier_only;   // a tail launch: skip the lockstep phase, serve the heavy list
     uint32_t frontier_wait_us;  // bound on an idle frontier warp's wait for its launch's producers
-    uint32_t* heavy_count;    // [0] listed [1] claimed [2] lockstep warps started [3] done
+    uint32_t* heavy_count;    // [0] listed [1] claimed [2] lockstep warps started [3] done [4] frontier
+                              // warps waiting (8 words per launch)
     uint32_t* heavy_list;     // query index + 1 (0 = not yet published)
     uint64_t* heavy_t0;       // start time of each scheduled query (ns)
     uint32_t* heavy_next;     // frontier kernel work cursor

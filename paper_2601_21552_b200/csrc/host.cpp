@@ -1409,6 +1409,14 @@ bool fast_frontier() {
 // never 25.0 -- C4's long Sat chains still need the frontier): 96 nodes.
 // With the frontier prover (SCUBA_OOB_FAST_FRONTIER=1) heavy queries should
 // meet it early: 8 nodes / 32 passes.
+// SCUBA_OOB_HANDOFF_GATE=0 disables the fast mode's hand-off gate
+bool handoff_gate_env() {
+    static const bool v = [] {
+        const char* e = std::getenv("SCUBA_OOB_HANDOFF_GATE");
+        return !(e && *e == '0');
+    }();
+    return v;
+}
 uint32_t fast_heavy_nodes() {
     static const uint32_t v = [] {
         const char* e = std::getenv("SCUBA_OOB_FAST_HEAVY_NODES");
@@ -1641,7 +1649,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(P->class_next.ensure(j.cls.size() * 4));
     CK(P->class_init.ensure(j.cls.size() * 4));
     CK(P->warp_class.ensure((size_t)n_warps * 4));
-    CK(P->heavy_count.ensure(16 * (1 + j.jit_cls.size())));
+    CK(P->heavy_count.ensure(32 * (1 + j.jit_cls.size())));
     CK(P->heavy_list.ensure((size_t)n * 8));  // [0, n): per compiled class at its q range; [n, 2n): interpreter
     CK(P->heavy_t0.ensure((size_t)n * 8));
     if (j.fr_regions) {
@@ -1703,6 +1711,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         a.heavy_passes = fast ? fast_heavy_passes(hp) : hp;
     }
     a.fast = (fast && fast_frontier()) ? 1u : 0u;
+    a.handoff_gate = (fast && !fast_frontier() && handoff_gate_env()) ? 1u : 0u;
     a.fast_stats = nullptr;
     a.cert_classes = nullptr;
     a.certs = nullptr;
@@ -1756,7 +1765,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         CK(P->stats.ensure(128));
         CK(cudaMemsetAsync(P->stats.p, 0, 128, s));
         a.stats = (unsigned long long*)P->stats.p;
-        if (fast) a.fast_stats = a.stats + 10;  // [10..14]
+        if (fast) a.fast_stats = a.stats + 10;  // [10..14] (certificate kernel: [14])
     }
     a.timeline = nullptr;
     if (timeline_path() && rc.mode == MODE_SOLVE) {
@@ -1787,7 +1796,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         b.n_classes = 1;
         b.class_next = (uint32_t*)P->class_next.p + c;
         b.warp_class = nullptr;
-        b.heavy_count = (uint32_t*)P->heavy_count.p + 4 * (1 + i);
+        b.heavy_count = (uint32_t*)P->heavy_count.p + 8 * (1 + i);
         b.heavy_list = (uint32_t*)P->heavy_list.p + j.cls[c].q_begin;
         j.jit_args.push_back(b);
     }
@@ -1947,7 +1956,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         const size_t n = j.qs.size();
         CK(cudaMemsetAsync(P->next.p, 0, 4, s0));
         CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s0));
-        CK(cudaMemsetAsync(P->heavy_count.p, 0, 16 * (1 + j.jit_cls.size()), s0));
+        CK(cudaMemsetAsync(P->heavy_count.p, 0, 32 * (1 + j.jit_cls.size()), s0));
         if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 8, s0));
         if (j.fr_regions) CK(cudaMemsetAsync(P->fr_map.p, 0, ((size_t)j.fr_regions + 31) / 32 * 4, s0));
         if (j.a.slab_bitmap) CK(cudaMemsetAsync(P->slab_map.p, 0, ((size_t)j.slab_slots + 31) / 32 * 4, s0));
@@ -2134,7 +2143,7 @@ std::string fetch(RunCtx& rc, DevJob& j, DevicePool* P, std::vector<int64_t> ret
                      st[4] ? 100.0 * st[5] / st[4] : 0.0);
         std::fprintf(stderr, "[oob] job w%d: frontier Sat passes expanded %llu / reference %llu; Unsat %llu / %llu\n",
                      j.wide, st[6], st[7], st[8], st[9]);
-        if (j.a.fast)
+        if (j.a.fast || j.a.certs)
             std::fprintf(stderr,
                          "[oob] job w%d: fast mode: %llu entries refuted by their class certificate; %llu heavy "
                          "queries met the frontier prover, %llu refuted; cycles per query: prepare %.0f search %.0f\n",

@@ -88,8 +88,14 @@ __device__ __forceinline__ void lockstep_phase(const LaunchArgs& a, LaneT& L, ui
         if (!active) break;
 
         // ---- node start (_search, solver.py:391-393) ----
+        // (fast mode: only while some frontier warp of this launch waits for
+        // an entry -- a queue behind busy frontier warps is slower than
+        // staying here; the check repeats every pass)
         if ((phase == PH_NODE || phase == PH_PASS) && a.heavy_nodes &&
-            ((phase == PH_NODE && nodes >= a.heavy_nodes) || (a.heavy_passes && passes >= a.heavy_passes))) {
+            ((phase == PH_NODE && nodes >= a.heavy_nodes) || (a.heavy_passes && passes >= a.heavy_passes)) &&
+            (!a.handoff_gate ||
+             ((volatile uint32_t*)a.heavy_count)[4] > ((volatile uint32_t*)a.heavy_count)[0] -
+                                                          ((volatile uint32_t*)a.heavy_count)[1])) {
             // a heavy search (many nodes, or a long propagation chain): hand
             // it to the warp-cooperative frontier phase, which restarts it
             // from the root in a warp of its own (so a long chain no longer
@@ -318,6 +324,7 @@ template <typename LaneT>
 __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, uint32_t warp, uint32_t lane) {
     const unsigned FULL = 0xffffffffu;
     volatile uint32_t* ctl = a.heavy_count;  // [0] listed [1] claimed [2] lockstep started [3] lockstep done
+                                             // [4] frontier warps waiting for an entry
     if (!a.frontier_only && lane == 0) {
         __threadfence();
         atomicAdd(a.heavy_count + 3, 1u);
@@ -329,6 +336,7 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
     for (;;) {
         int idx = -1;
         if (lane == 0) {
+            bool waiting = false;
             for (;;) {
                 const uint32_t done = ctl[3], started = ctl[2];
                 __threadfence();
@@ -342,11 +350,16 @@ __device__ __forceinline__ void frontier_phase(const LaunchArgs& a, LaneT& L, ui
                     continue;
                 }
                 if (done >= started || !WAIT_NS) break;  // no producer of this launch left
+                if (!waiting) {
+                    waiting = true;
+                    atomicAdd(a.heavy_count + 4, 1u);
+                }
                 const uint64_t now = global_ns();
                 if (!idle_since) idle_since = now;
                 else if (now - idle_since > WAIT_NS) break;
                 __nanosleep(4000);
             }
+            if (waiting) atomicSub(a.heavy_count + 4, 1u);
         }
         idx = __shfl_sync(FULL, idx, 0);
         if (idx < 0) break;
