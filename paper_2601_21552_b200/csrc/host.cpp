@@ -1038,6 +1038,17 @@ int phys_dev(int dev) {
     return v > 0 ? dev % v : dev;
 }
 
+// frees the device buffers of one pool slot (every device)
+void release_slot_pools(int slot) {
+    std::lock_guard<std::mutex> lk(g_pools_mu);
+    for (size_t i = 0; i < g_pools.size(); i++) {
+        if (!g_pools[i] || (int)(i / NJOBS / 64) != slot) continue;
+        std::lock_guard<std::mutex> lk2(g_pools[i]->mu);
+        cudaSetDevice(phys_dev((int)((i / NJOBS) % 64)));
+        g_pools[i]->release_all();
+    }
+}
+
 DevicePool* pool_for(int dev, int wide) {
     std::lock_guard<std::mutex> lk(g_pools_mu);
     size_t slot = ((size_t)tl_pool_slot * 64 + (size_t)dev) * NJOBS + (size_t)wide;
@@ -2881,6 +2892,17 @@ int oob_solve_batches(const oob_batch* batches, int64_t n_batches, const oob_opt
                 const oob_result& o = outs[i];
                 rcs[i] = drive(batches + i, opt, MODE_SOLVE, nullptr, o.model, o.verdict, o.nodes, o.passes,
                                o.elapsed_s);
+                if (rcs[i] == OOB_E_CUDA && tl_pool_slot != 0 &&
+                    g_last_error.find("out of memory") != std::string::npos) {
+                    // no room for a second set of device buffers: this worker
+                    // frees its own and shares slot 0's from here on (the pool
+                    // locks serialise the device phases; host phases still overlap)
+                    release_slot_pools(tl_pool_slot);
+                    tl_pool_slot = 0;
+                    cudaGetLastError();
+                    rcs[i] = drive(batches + i, opt, MODE_SOLVE, nullptr, o.model, o.verdict, o.nodes, o.passes,
+                                   o.elapsed_s);
+                }
                 if (rcs[i] != OOB_OK) msgs[i] = g_last_error;
                 gate_release();  // also on early exits (no launch happened)
             }
