@@ -312,11 +312,11 @@ def jit_compile(fb, q: int, cap: int = 1 << 22):
     return buf.value.decode(), ms.value
 
 
-def host_bench(fb, timeout_s=30.0):
+def host_bench(fb, timeout_s=30.0, flags=0):
     """Host pipeline timings without a device: [validate+compile, prepare
     (compile + schedule), pack] in ms (diagnostics)."""
     ms = np.zeros(3, dtype=np.float64)
     cb = fb.as_c()
-    o = options(timeout_s)
+    o = options(timeout_s, flags=flags)
     check(lib().oob_host_bench(ctypes.byref(cb), ctypes.byref(o), ms.ctypes.data), "oob_host_bench")
     return ms

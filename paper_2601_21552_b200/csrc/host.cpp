@@ -75,14 +75,21 @@ static int trace_level() {
     return lv;
 }
 static bool trace_on() { return trace_level() > 0; }
+static const std::chrono::steady_clock::time_point g_trace_epoch = std::chrono::steady_clock::now();
+thread_local int tl_pool_slot = 0;  // stream API pool slot of this thread (see HostGate)
 struct Phase {
     const char* name;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     explicit Phase(const char* n) : name(n) {}
     ~Phase() {
-        if (trace_on())
-            std::fprintf(stderr, "[oob] %-10s %9.3f ms\n", name,
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        if (!trace_on()) return;
+        using ms = std::chrono::duration<double, std::milli>;
+        if (trace_level() >= 3)  // start time + pool slot: shows the overlap of stream batches
+            std::fprintf(stderr, "[oob] %-10s %9.3f ms  @%10.3f slot %d\n", name,
+                         ms(std::chrono::steady_clock::now() - t0).count(), ms(t0 - g_trace_epoch).count(),
+                         tl_pool_slot);
+        else
+            std::fprintf(stderr, "[oob] %-10s %9.3f ms\n", name, ms(std::chrono::steady_clock::now() - t0).count());
     }
 };
 
@@ -230,20 +237,39 @@ struct Structure {
     const uint32_t* code() const { return words.data() + ncon; }
 };
 
+// Structures referenced by one call's Compiled records, which hold plain
+// pointers: a reference per distinct structure and compile chunk instead of
+// an atomic reference-count update per query (the counts of a few shared
+// structures are contended by every compile thread)
+struct Pins {
+    std::vector<std::shared_ptr<const Structure>> v;
+    const Structure* add(const std::shared_ptr<const Structure>& p) {
+        const Structure* r = p.get();
+        if (last < v.size() && v[last].get() == r) return r;
+        const size_t k0 = v.size() > 64 ? v.size() - 64 : 0;  // (a bounded look-back)
+        for (size_t k = v.size(); k > k0; k--)
+            if (v[k - 1].get() == r) {
+                last = k - 1;
+                return r;
+            }
+        last = v.size();
+        v.push_back(p);
+        return r;
+    }
+    size_t last = 0;
+};
+
 struct Compiled {
     int8_t regime = R_IMMEDIATE;
     int8_t immediate = OOB_UNSAT;
-    std::shared_ptr<const Structure> st;
+    const Structure* st = nullptr;  // kept alive by the call's Pins
     uint32_t nv = 0, ncon = 0, ncode = 0, nlit = 0;
     uint32_t maxcsize = 1, maxdepth = 1;
     double cost = 0;
     uint64_t key = 0;             // structure-class hash (words, nv, ncon)
     uint32_t cls = UINT32_MAX;    // batch-wide structure class id (prepare)
-    std::string why;              // reason for R_RANGE
+    const char* why = nullptr;    // reason for R_RANGE (static text or the pinned structure's)
     const std::vector<uint32_t>& words() const { return st->words; }
-    bool same_class(const Compiled& o) const {
-        return key == o.key && nv == o.nv && ncon == o.ncon && (st == o.st || st->words == o.st->words);
-    }
 };
 
 // literal slot i of query q (values are read from the caller's batch)
@@ -339,31 +365,6 @@ inline uint64_t class_hash(const std::vector<uint32_t>& w, uint32_t nv, uint32_t
         h *= 1099511628211ull;
     }
     return h;
-}
-
-// Groups items by structure class.  Returns the class id of every item
-// (ids in order of first appearance) and the representative of each class.
-template <typename GetComp>
-void group_classes(size_t n, GetComp get, std::vector<uint32_t>& cls, std::vector<size_t>& rep) {
-    std::unordered_multimap<uint64_t, uint32_t> seen;
-    cls.resize(n);
-    rep.clear();
-    for (size_t i = 0; i < n; i++) {
-        const Compiled& c = get(i);
-        uint32_t id = UINT32_MAX;
-        auto range = seen.equal_range(c.key);
-        for (auto it = range.first; it != range.second; ++it)
-            if (get(rep[it->second]).same_class(c)) {
-                id = it->second;
-                break;
-            }
-        if (id == UINT32_MAX) {
-            id = (uint32_t)rep.size();
-            rep.push_back(i);
-            seen.emplace(c.key, id);
-        }
-        cls[i] = id;
-    }
 }
 
 // host worker threads (SCUBA_OOB_HOST_THREADS caps them; default: cores, <= 32)
@@ -822,15 +823,16 @@ struct StructCache {
                std::memcmp(e.lhs.data(), v.lhs, v.ncon * 4) == 0 &&
                std::memcmp(e.rhs.data(), v.rhs, v.ncon * 4) == 0 && e.divok == divok;
     }
-    std::shared_ptr<const Structure> get(const QView& v, int mode) {
+    const Structure* get(const QView& v, int mode, Pins& pins) {
         static thread_local std::vector<uint8_t> divok;
         bool cacheable;
         uint64_t h = fingerprint(v, mode, divok, cacheable);
-        if (!cacheable) return build_structure(v, mode);
+        if (!cacheable) return pins.add(build_structure(v, mode));
         auto range = map.equal_range(h);
         for (auto it = range.first; it != range.second; ++it)
-            if (same(it->second, v, mode, divok)) return it->second.st;
+            if (same(it->second, v, mode, divok)) return pins.add(it->second.st);
         std::shared_ptr<const Structure> st = build_structure(v, mode);
+        pins.add(st);
         if (map.size() > 4096) map.clear();  // bounded
         Entry e;
         e.mode = mode;
@@ -845,9 +847,10 @@ struct StructCache {
         e.lhs.assign(v.lhs, v.lhs + v.ncon);
         e.rhs.assign(v.rhs, v.rhs + v.ncon);
         e.divok = divok;
-        e.st = st;
+        const Structure* st_ptr = st.get();
+        e.st = std::move(st);
         map.emplace(h, std::move(e));
-        return st;
+        return st_ptr;
     }
 };
 
@@ -858,7 +861,7 @@ struct StructCache {
 // proof (which would move some of them to int64: a scheduling choice only;
 // every regime is exact for the query it holds)
 Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s,
-                       const oob_i128* model_in, bool fast = false) {
+                       const oob_i128* model_in, Pins& pins, bool fast = false) {
     Compiled out;
     QView v = view_of(b, q);
     out.nv = (uint32_t)v.nv;
@@ -886,7 +889,7 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
         if (empty) { out.immediate = OOB_UNSAT; return out; }          // solver.py:374-375
         if (!(timeout_s > 0)) { out.immediate = OOB_TIMEOUT; return out; }  // deadline passed (:391)
     }
-    out.st = cache.get(v, mode);
+    out.st = cache.get(v, mode, pins);
     const Structure& st = *out.st;
     out.ncon = st.ncon;
     out.ncode = st.ncode;
@@ -896,7 +899,7 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
     out.key = st.key;
     if (!st.range_why.empty()) {
         out.regime = R_RANGE;
-        out.why = st.range_why;
+        out.why = st.range_why.c_str();
         return out;
     }
     lits.resize(st.nlit);
@@ -1003,10 +1006,23 @@ struct HostGate {
     std::condition_variable cv;
     int turn = 0;  // the chunk whose host phase may run
 };
-thread_local int tl_pool_slot = 0;
 thread_local HostGate* tl_gate = nullptr;
 thread_local int tl_chunk = 0;
 thread_local bool tl_gate_held = false;
+// stream API: the host phase after which the next batch's host work may
+// start (SCUBA_OOB_GATE = compile | schedule | pack | launch; default
+// compile: the next batch compiles while this one schedules, packs and runs)
+enum { GATE_COMPILE = 0, GATE_SCHEDULE = 1, GATE_PACK = 2, GATE_LAUNCH = 3 };
+int gate_point() {
+    static const int g = [] {
+        const char* e = std::getenv("SCUBA_OOB_GATE");
+        if (!e || !*e) return (int)GATE_COMPILE;
+        std::string v(e);
+        return v == "compile" ? (int)GATE_COMPILE : v == "schedule" ? (int)GATE_SCHEDULE
+                                                  : v == "pack" ? (int)GATE_PACK : (int)GATE_LAUNCH;
+    }();
+    return g;
+}
 void gate_release() {
     if (!tl_gate || !tl_gate_held) return;
     {
@@ -1834,7 +1850,6 @@ struct DevGroup {
     int dev = 0;
     DevJob job[NJOBS];
     DevicePool* pool[NJOBS] = {nullptr, nullptr, nullptr, nullptr};
-    bool has(int w) const { return !job[w].qs.empty(); }
 };
 
 // start the upload of a packed job's records at once (caller holds P->mu):
@@ -2256,6 +2271,7 @@ std::string run_group(RunCtx& rc, int dev, std::vector<int64_t> qs[3]) {
                 Phase ph("pack");
                 pack_group(rc, G, true);  // each job's upload overlaps the next job's packing
             }
+            if (gate_point() == GATE_PACK) gate_release();
             std::string e;
             {
                 Phase ph("stage");
@@ -2325,60 +2341,153 @@ int visible_devices() {
     return n;
 }
 
-// Batch-wide structure-class ids of the device-bound queries: by hash, then
-// verified word for word in parallel (on a hash collision the exact grouping
-// is used instead).
-void assign_classes(std::vector<Compiled>& comp, const std::vector<int64_t> reg[3]) {
-    // queries share Structure objects (one per structure and compile thread):
-    // number the distinct pointers with a small open-addressing table, then
-    // merge pointers whose structures are equal word for word
-    const size_t TB = 1u << 14;
-    std::vector<const Structure*> slot_ptr(TB, nullptr);
-    std::vector<uint32_t> slot_id(TB, 0);
-    std::vector<const Structure*> ptrs;
-    std::unordered_map<const Structure*, uint32_t> overflow;  // only if the table fills up
-    auto pid_of = [&](const Structure* p) -> uint32_t {
-        size_t h = (std::hash<const void*>{}(p) * 0x9E3779B97F4A7C15ull) >> 50;
-        for (size_t k = 0; k < 64; k++) {
-            size_t i = (h + k) & (TB - 1);
-            if (slot_ptr[i] == p) return slot_id[i];
-            if (!slot_ptr[i]) {
-                slot_ptr[i] = p;
-                slot_id[i] = (uint32_t)ptrs.size();
-                ptrs.push_back(p);
-                return slot_id[i];
-            }
+// Device-bound queries by regime, grouped by structure class.  A class is a
+// structure word for word (queries compiled on different threads hold
+// different Structure objects of one class); classes are numbered densely in
+// order of first appearance (lowest query index), and each regime's list is
+// class-major with ascending query indices inside a class.  The class table
+// is built from the call's pins (a few entries per structure); the per-query
+// passes run in parallel over query chunks.
+struct Classes {
+    std::vector<int64_t> reg[3];
+    std::vector<uint32_t> start[3];  // class c of regime w: reg[w][start[w][c] .. start[w][c + 1])
+    uint32_t ncls = 0;
+    size_t members(uint32_t c) const {
+        size_t m = 0;
+        for (int w = 0; w < 3; w++) m += start[w][c + 1] - start[w][c];
+        return m;
+    }
+    int64_t member(uint32_t c, size_t i) const {  // regime-major, ascending query index
+        for (int w = 0; w < 3; w++) {
+            const size_t k = start[w][c + 1] - start[w][c];
+            if (i < k) return reg[w][start[w][c] + i];
+            i -= k;
         }
-        auto it = overflow.emplace(p, (uint32_t)ptrs.size());
-        if (it.second) ptrs.push_back(p);
-        return it.first->second;
-    };
-    for (int w = 0; w < 3; w++)
-        for (int64_t q : reg[w]) comp[q].cls = pid_of(comp[q].st.get());
-    // canonical class per pointer
-    std::vector<uint32_t> canon(ptrs.size());
-    std::unordered_multimap<uint64_t, uint32_t> by_key;  // key -> class id (first pointer index)
-    std::vector<uint32_t> first_ptr;
-    for (uint32_t i = 0; i < ptrs.size(); i++) {
-        const Structure& st = *ptrs[i];
+        return -1;
+    }
+};
+inline bool device_regime(const Compiled& c) { return c.regime >= R_W64 && c.regime < R_W64 + 3; }
+
+// other(q, comp[q]) is called (concurrently) for every query that is not
+// device-bound; qcls[q] = class of a device query, 0 otherwise
+template <typename Other>
+void classify(std::vector<Compiled>& comp, int64_t n, const std::vector<std::shared_ptr<const Structure>>& pins,
+              std::vector<uint32_t>& qcls, Classes& K, Other other) {
+    // distinct structure objects -> canonical class (word-for-word equality)
+    size_t TB = 1024;
+    while (TB < 2 * pins.size()) TB *= 2;
+    std::vector<const Structure*> slot_ptr(TB, nullptr);
+    std::vector<uint32_t> slot_canon(TB, 0);
+    std::unordered_multimap<uint64_t, const Structure*> by_key;  // key -> first structure of a class
+    std::unordered_map<const Structure*, uint32_t> canon_of_first;
+    uint32_t nct = 0;
+    auto hash_slot = [&](const Structure* p) { return (size_t)((std::hash<const void*>{}(p) * 0x9E3779B97F4A7C15ull) >> 20) & (TB - 1); };
+    for (const auto& sp : pins) {
+        const Structure* p = sp.get();
+        size_t i = hash_slot(p);
+        while (slot_ptr[i] && slot_ptr[i] != p) i = (i + 1) & (TB - 1);
+        if (slot_ptr[i]) continue;
         uint32_t id = UINT32_MAX;
-        auto range = by_key.equal_range(st.key);
+        auto range = by_key.equal_range(p->key);
         for (auto it = range.first; it != range.second; ++it) {
-            const Structure& o = *ptrs[first_ptr[it->second]];
-            if (o.nv == st.nv && o.ncon == st.ncon && o.words == st.words) {
-                id = it->second;
+            const Structure& o = *it->second;
+            if (o.nv == p->nv && o.ncon == p->ncon && o.words == p->words) {
+                id = canon_of_first[it->second];
                 break;
             }
         }
         if (id == UINT32_MAX) {
-            id = (uint32_t)first_ptr.size();
-            first_ptr.push_back(i);
-            by_key.emplace(st.key, id);
+            id = nct++;
+            by_key.emplace(p->key, p);
+            canon_of_first[p] = id;
         }
-        canon[i] = id;
+        slot_ptr[i] = p;
+        slot_canon[i] = id;
     }
-    for (int w = 0; w < 3; w++)
-        for (int64_t q : reg[w]) comp[q].cls = canon[comp[q].cls];
+    auto canon = [&](const Structure* p) -> uint32_t {
+        size_t i = hash_slot(p);
+        while (slot_ptr[i] != p) i = (i + 1) & (TB - 1);  // every compiled structure is pinned
+        return slot_canon[i];
+    };
+    qcls.resize(n);
+    // chunks: per-chunk tables of 3 * classes entries stay within 2^22 words
+    const size_t per = std::max<size_t>(1, ((size_t)1 << 22) / std::max<size_t>(1, 3 * (size_t)nct));
+    const size_t G = std::max<size_t>(8192, ((size_t)n + per - 1) / per);
+    const size_t nch = ((size_t)n + G - 1) / G;
+    std::vector<int64_t> firstq(nch * (size_t)std::max(nct, 1u), INT64_MAX);
+    parallel_for(nch, 1, [&](size_t c0, size_t c1) {
+        for (size_t ch = c0; ch < c1; ch++) {
+            int64_t* fq = firstq.data() + ch * nct;
+            const int64_t q1 = std::min<int64_t>(n, (int64_t)((ch + 1) * G));
+            for (int64_t q = (int64_t)(ch * G); q < q1; q++) {
+                const Compiled& c = comp[q];
+                if (!device_regime(c)) {
+                    qcls[q] = 0;
+                    other(q, c);
+                    continue;
+                }
+                const uint32_t cc = canon(c.st);
+                qcls[q] = cc;
+                if (fq[cc] == INT64_MAX) fq[cc] = q;
+            }
+        }
+    });
+    // dense ids in order of first appearance
+    std::vector<std::pair<int64_t, uint32_t>> order;
+    for (uint32_t cc = 0; cc < nct; cc++) {
+        int64_t m = INT64_MAX;
+        for (size_t ch = 0; ch < nch; ch++) m = std::min(m, firstq[ch * nct + cc]);
+        if (m != INT64_MAX) order.push_back({m, cc});
+    }
+    std::sort(order.begin(), order.end());
+    std::vector<uint32_t> dense(std::max(nct, 1u), UINT32_MAX);
+    for (uint32_t i = 0; i < order.size(); i++) dense[order[i].second] = i;
+    const uint32_t ncls = (uint32_t)order.size();
+    K.ncls = ncls;
+    const size_t W = 3 * (size_t)ncls;
+    std::vector<uint32_t> cnt(nch * std::max<size_t>(W, 1), 0);
+    parallel_for(nch, 1, [&](size_t c0, size_t c1) {
+        for (size_t ch = c0; ch < c1; ch++) {
+            uint32_t* ct = cnt.data() + ch * W;
+            const int64_t q1 = std::min<int64_t>(n, (int64_t)((ch + 1) * G));
+            for (int64_t q = (int64_t)(ch * G); q < q1; q++) {
+                Compiled& c = comp[q];
+                if (!device_regime(c)) continue;
+                const uint32_t id = dense[qcls[q]];
+                qcls[q] = id;
+                c.cls = id;
+                ct[(size_t)(c.regime - R_W64) * ncls + id]++;
+            }
+        }
+    });
+    // offsets: regime, then class, then chunk
+    for (int w = 0; w < 3; w++) {
+        K.start[w].assign(ncls + 1, 0);
+        uint32_t at = 0;
+        for (uint32_t c = 0; c < ncls; c++) {
+            K.start[w][c] = at;
+            for (size_t ch = 0; ch < nch; ch++) {
+                uint32_t& x = cnt[ch * W + (size_t)w * ncls + c];
+                const uint32_t k = x;
+                x = at;
+                at += k;
+            }
+        }
+        K.start[w][ncls] = at;
+        K.reg[w].resize(at);
+    }
+    parallel_for(nch, 1, [&](size_t c0, size_t c1) {
+        for (size_t ch = c0; ch < c1; ch++) {
+            uint32_t* ct = cnt.data() + ch * W;
+            const int64_t q1 = std::min<int64_t>(n, (int64_t)((ch + 1) * G));
+            for (int64_t q = (int64_t)(ch * G); q < q1; q++) {
+                const Compiled& c = comp[q];
+                if (!device_regime(c)) continue;
+                const int w = c.regime - R_W64;
+                K.reg[w][ct[(size_t)w * ncls + qcls[q]]++] = q;
+            }
+        }
+    });
 }
 
 // Fast mode: compile the Unsat certificates of every structure class
@@ -2430,64 +2539,41 @@ void cert_cache_put(std::vector<uint64_t>&& key, const std::vector<uint64_t>& va
     C.map[h].emplace_back(std::move(key), val);
     ++C.entries;
 }
-void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const std::vector<int64_t> reg[3],
-                 std::vector<uint64_t>& certs, std::vector<uint32_t>& cert_off) {
-    // compact per-device-query views (class id, structure): the loops below
-    // then stream 12 bytes per query instead of whole Compiled records
-    size_t ndq = 0;
-    for (int w = 0; w < 3; w++) ndq += reg[w].size();
-    std::vector<int64_t> dq;
-    dq.reserve(ndq);
-    for (int w = 0; w < 3; w++) dq.insert(dq.end(), reg[w].begin(), reg[w].end());
-    std::vector<uint32_t> qc(ndq);
-    std::vector<const Structure*> qs(ndq);
-    parallel_for(ndq, 8192, [&](size_t lo, size_t hi) {
-        for (size_t k = lo; k < hi; k++) {
-            qc[k] = comp[dq[k]].cls;
-            qs[k] = comp[dq[k]].st.get();
-        }
-    });
-    uint32_t ncls = 0;
-    for (uint32_t c : qc) ncls = std::max(ncls, c + 1);
-    std::vector<uint32_t> start(ncls + 1, 0);
-    for (uint32_t c : qc) start[c + 1]++;
-    for (uint32_t c = 0; c < ncls; c++) start[c + 1] += start[c];
-    // members of every class (regime-major, ascending within a regime):
-    // positions k into dq / qc / qs
-    std::vector<uint32_t> mem(ndq);
-    {
-        std::vector<uint32_t> at(start.begin(), start.end() - 1);
-        for (size_t k = 0; k < ndq; k++) mem[at[qc[k]]++] = (uint32_t)k;
-    }
+void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const Classes& K,
+                 const std::vector<uint32_t>& qcls, std::vector<uint64_t>& certs, std::vector<uint32_t>& cert_off) {
+    const uint32_t ncls = K.ncls;
     // literal slots whose value varies inside the class (the parameters):
     // each query against its class's first member, in parallel over queries
     // (every query through its own Structure: equal code words do not imply
     // equal literal-slot sources)
     std::vector<uint32_t> loff(ncls + 1, 0);
-    for (uint32_t c = 0; c < ncls; c++)
-        loff[c + 1] = loff[c] + (start[c + 1] > start[c] ? qs[mem[start[c]]]->nlit : 0);
+    std::vector<int64_t> first(ncls, -1);
+    for (uint32_t c = 0; c < ncls; c++) {
+        first[c] = K.member(c, 0);
+        loff[c + 1] = loff[c] + (first[c] >= 0 ? comp[first[c]].st->nlit : 0);
+    }
     std::vector<i128> v0(loff[ncls]);
     std::unique_ptr<std::atomic<uint8_t>[]> vary(new std::atomic<uint8_t>[std::max<uint32_t>(loff[ncls], 1)]);
     for (uint32_t c = 0; c < ncls; c++) {
-        if (start[c + 1] == start[c]) continue;
-        const uint32_t k0 = mem[start[c]];
+        if (first[c] < 0) continue;
         for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
-            v0[loff[c] + i] = lit_value(b, dq[k0], *qs[k0], i);
+            v0[loff[c] + i] = lit_value(b, first[c], *comp[first[c]].st, i);
             vary[loff[c] + i].store(0, std::memory_order_relaxed);
         }
     }
-    parallel_for(ndq, 4096, [&](size_t lo, size_t hi) {
-        for (size_t k = lo; k < hi; k++) {
-            const uint32_t c = qc[k];
-            const Structure& sk = *qs[k];
-            const int64_t q = dq[k];
-            for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
-                std::atomic<uint8_t>& f = vary[loff[c] + i];
-                if (!f.load(std::memory_order_relaxed) && lit_value(b, q, sk, i) != v0[loff[c] + i])
-                    f.store(1, std::memory_order_relaxed);
+    for (int w = 0; w < 3; w++)
+        parallel_for(K.reg[w].size(), 4096, [&](size_t lo, size_t hi) {
+            for (size_t k = lo; k < hi; k++) {
+                const int64_t q = K.reg[w][k];
+                const uint32_t c = qcls[q];
+                const Structure& sk = *comp[q].st;
+                for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
+                    std::atomic<uint8_t>& f = vary[loff[c] + i];
+                    if (!f.load(std::memory_order_relaxed) && lit_value(b, q, sk, i) != v0[loff[c] + i])
+                        f.store(1, std::memory_order_relaxed);
+                }
             }
-        }
-    });
+        });
     std::vector<std::vector<uint64_t>> per(ncls);
     parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
         static thread_local std::unique_ptr<sym::Store> S;
@@ -2501,10 +2587,9 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
             buf.resize(1 << 15);
         }
         for (size_t c = lo; c < hi; c++) {
-            const uint32_t* m = mem.data() + start[c];
-            const size_t nm = start[c + 1] - start[c];
+            const size_t nm = K.members((uint32_t)c);
             if (!nm) continue;
-            const Structure& st = *qs[m[0]];
+            const Structure& st = *comp[first[c]].st;
             if (!st.range_why.empty()) continue;
             std::vector<int16_t> pmap(st.nlit, -1), pslot;
             for (uint32_t i = 0; i < st.nlit; i++)
@@ -2533,12 +2618,22 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
             // eliminated variables lie within the representative's, and its
             // sign conditions only get easier on sub-boxes), then members
             // spread over the class
-            uint32_t widest = m[0];
-            for (size_t i = 1; i < nm; i++)
-                if (comp[dq[m[i]]].cost > comp[dq[widest]].cost) widest = m[i];
+            int64_t widest = first[c];
+            {
+                double wc = comp[widest].cost;
+                size_t i = 0;
+                for (int w = 0; w < 3; w++)
+                    for (uint32_t k = K.start[w][c]; k < K.start[w][c + 1]; k++, i++) {
+                        const int64_t q = K.reg[w][k];
+                        if (i > 0 && comp[q].cost > wc) {
+                            widest = q;
+                            wc = comp[q].cost;
+                        }
+                    }
+            }
             // ... so the cache key also carries the widest member's domains
             {
-                const int64_t vb = b->var_begin[dq[widest]];
+                const int64_t vb = b->var_begin[widest];
                 for (uint32_t v = 0; v < st.nv; v++) {
                     const i128 lo = from_w(b->var_lo[vb + v]), hi = from_w(b->var_hi[vb + v]);
                     ckey.push_back((uint64_t)lo);
@@ -2551,12 +2646,11 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
             std::vector<std::vector<uint64_t>> got;
             const size_t nr = std::min<size_t>(CERT_REPS, nm);
             for (size_t r = 0; r <= nr; r++) {
-                const uint32_t kq = r == 0 ? widest : m[(r - 1) * nm / nr];
-                if (r > 0 && kq == widest) continue;
-                const int64_t q = dq[kq];
+                const int64_t q = r == 0 ? widest : K.member((uint32_t)c, (r - 1) * nm / nr);
+                if (r > 0 && q == widest) continue;
                 const int64_t vb = b->var_begin[q];
                 auto dom = [&](uint32_t i) -> i128 { return from_w(i % 2 ? b->var_hi[vb + i / 2] : b->var_lo[vb + i / 2]); };
-                const Structure& sq = *qs[kq];
+                const Structure& sq = *comp[q].st;
                 auto lit = [&](uint32_t i) -> i128 { return lit_value(b, q, sq, i); };
                 const size_t n = cert::cert_build(*S, *W, *M, st.words.data(), st.code(), st.nv, st.ncon, st.nlit,
                                                   dom, lit,
@@ -2591,6 +2685,8 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const st
 // Compile + schedule: fills immediate verdicts and returns the device jobs.
 struct Prepared {
     std::vector<Compiled> comp;
+    std::vector<std::shared_ptr<const Structure>> pins;  // every structure comp[] points to
+    Classes classes;
     std::vector<uint32_t> qcls;  // comp[q].cls, compact
     std::vector<uint64_t> certs;     // fast mode: Unsat certificates (cert.cuh)
     std::vector<uint32_t> cert_off;  // per structure class: offset in certs, NO_CERT: none
@@ -2611,15 +2707,18 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     const int64_t n = b->n_queries;
     auto t0 = std::chrono::steady_clock::now();
     std::vector<Compiled>& comp = pr.comp;
-    comp.resize(n);  // every entry is overwritten below (recycled vectors keep their storage)
+    if ((int64_t)comp.size() != n) comp.resize(n);  // every entry is overwritten below (recycled storage)
     const bool fast_shortcut = mode == MODE_SOLVE && (opt.flags & OOB_F_FAST);
+    pr.pins.clear();
     {
         // validation and compilation in one pass over the batch: a query is
         // compiled only once it has validated; the lowest invalid query is
         // reported (nothing is decided for an invalid batch)
         Phase ph("validate+compile");
         std::atomic<int64_t> bad{INT64_MAX};
+        std::mutex pins_mu;
         parallel_for((size_t)n, 256, [&](size_t lo, size_t hi) {
+            Pins pins;
             for (size_t q = lo; q < hi; q++) {
                 if (!validate(b, (int64_t)q).empty()) {
                     int64_t cur = bad.load();
@@ -2627,8 +2726,10 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
                     }
                     break;
                 }
-                comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, fast_shortcut);
+                comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, pins, fast_shortcut);
             }
+            std::lock_guard<std::mutex> lk(pins_mu);
+            for (auto& p : pins.v) pr.pins.push_back(std::move(p));
         });
         if (bad.load() != INT64_MAX) {
             int64_t q = bad.load();
@@ -2636,25 +2737,35 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         }
     }
     pr.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (gate_point() == GATE_COMPILE) gate_release();
     pr.errs.assign(n, 0);
-    std::vector<int64_t> reg[3];
-    for (int64_t q = 0; q < n; q++) {
-        const Compiled& c = comp[q];
-        if (c.regime == R_IMMEDIATE) {
-            verdict[q] = c.immediate;
-            if (nodes) nodes[q] = 0;
-            if (passes) passes[q] = 0;
-            if (elapsed) elapsed[q] = std::max(pr.compile_s / std::max<int64_t>(n, 1), 1e-9);
-        } else if (c.regime == R_RANGE) {
-            verdict[q] = OOB_ERROR;
-            if (pr.range_msg.empty()) pr.range_msg = "query " + std::to_string(q) + ": " + c.why;
-        } else {
-            reg[c.regime - R_W64].push_back(q);
-        }
-    }
     if (virtual_devices <= 0) virtual_devices = env_virtual_devices();
-    int ndev = virtual_devices > 0 ? virtual_devices : visible_devices();
-    const size_t n_dev_q = reg[0].size() + reg[1].size() + reg[2].size();
+    const int ndev = virtual_devices > 0 ? virtual_devices : visible_devices();
+    Phase ph_sched("schedule");
+    Classes& K = pr.classes;
+    {
+        // immediate verdicts and range errors on the way (the lowest
+        // out-of-range query is reported)
+        Phase ph_cls("schedule.classes");
+        std::atomic<int64_t> range_q{INT64_MAX};
+        const double el = std::max(pr.compile_s / std::max<int64_t>(n, 1), 1e-9);
+        classify(comp, n, pr.pins, pr.qcls, K, [&](int64_t q, const Compiled& c) {
+            if (c.regime == R_IMMEDIATE) {
+                verdict[q] = c.immediate;
+                if (nodes) nodes[q] = 0;
+                if (passes) passes[q] = 0;
+                if (elapsed) elapsed[q] = el;
+            } else {  // R_RANGE
+                verdict[q] = OOB_ERROR;
+                int64_t cur = range_q.load();
+                while (q < cur && !range_q.compare_exchange_weak(cur, q)) {
+                }
+            }
+        });
+        if (range_q.load() != INT64_MAX)
+            pr.range_msg = "query " + std::to_string(range_q.load()) + ": " + comp[range_q.load()].why;
+    }
+    const size_t n_dev_q = K.reg[0].size() + K.reg[1].size() + K.reg[2].size();
     if (n_dev_q > 0 && ndev == 0)
         return fail(OOB_E_CUDA, "no CUDA device visible: the OOB engine has no CPU fallback");
     int first = std::max(0, opt.device);
@@ -2662,66 +2773,53 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         return fail(OOB_E_CUDA, "device ordinal out of range");
     int want = opt.n_gpus > 0 ? opt.n_gpus : ndev - first;
     want = std::max(1, std::min(want, ndev - first));
-    Phase ph_sched("schedule");
-    {
-        Phase ph_cls("schedule.classes");
-        assign_classes(comp, reg);
-    }
     pr.certs.clear();
     pr.cert_off.clear();
     if (mode == MODE_SOLVE && (opt.flags & OOB_F_FAST) && opt.timeout_s > 0) {
         Phase ph_cert("certify");
-        build_certs(b, comp, reg, pr.certs, pr.cert_off);
+        build_certs(b, comp, K, pr.qcls, pr.certs, pr.cert_off);
     }
-    pr.qcls.assign(n, 0);
-    for (int w = 0; w < 3; w++)
-        for (int64_t q : reg[w]) pr.qcls[q] = comp[q].cls;
     if (n_dev_q > 0) {
         pr.work.resize(want);
         for (int d = 0; d < want; d++) pr.work[d].dev = first + d;
     }
+    struct GateAtEnd {
+        ~GateAtEnd() { if (gate_point() == GATE_SCHEDULE) gate_release(); }
+    } gate_at_end;
     Phase ph_sort("schedule.sort");
-    for (int w = 0; w < 3; w++) {
-        auto& qs = reg[w];
-        if (qs.empty()) continue;
-        if (!(opt.flags & OOB_F_NO_SORT)) {
-            // class-major (counting sort, stable), cost-minor: expensive first,
-            // ties by query index (per-class sorts run in parallel)
-            const std::vector<uint32_t>& qcls = pr.qcls;
-            uint32_t ncls = 0;
-            for (int64_t q : qs) ncls = std::max(ncls, qcls[q] + 1);
-            std::vector<uint32_t> start(ncls + 1, 0);
-            for (int64_t q : qs) start[qcls[q] + 1]++;
-            for (uint32_t c = 0; c < ncls; c++) start[c + 1] += start[c];
-            std::vector<std::pair<uint32_t, int64_t>> keyed(qs.size());  // (inverted cost, query)
-            {
-                std::vector<uint32_t> at(start.begin(), start.end() - 1);
-                for (int64_t q : qs)
-                    keyed[at[qcls[q]]++] = {0xFFFFu - (uint32_t)std::min(comp[q].cost, 65535.0), q};
-            }
-            // per class: a stable counting sort on the key (ties stay in
-            // ascending query order, as the sort on (key, query) had them)
-            parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
-                std::vector<uint32_t> cnt;
-                std::vector<std::pair<uint32_t, int64_t>> tmp;
-                for (size_t c = lo; c < hi; c++) {
-                    const size_t a = start[c], z = start[c + 1];
-                    if (z - a < 2) continue;
-                    uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
-                    for (size_t i = a; i < z; i++) {
-                        kmin = std::min(kmin, keyed[i].first);
-                        kmax = std::max(kmax, keyed[i].first);
-                    }
-                    cnt.assign(kmax - kmin + 2, 0);
-                    for (size_t i = a; i < z; i++) cnt[keyed[i].first - kmin + 1]++;
-                    for (size_t k = 1; k < cnt.size(); k++) cnt[k] += cnt[k - 1];
-                    tmp.resize(z - a);
-                    for (size_t i = a; i < z; i++) tmp[cnt[keyed[i].first - kmin]++] = keyed[i];
-                    std::copy(tmp.begin(), tmp.end(), keyed.begin() + a);
+    // class-major (classify), cost-minor: expensive first, ties by query
+    // index -- a stable counting sort per (regime, class) range, in parallel
+    if (!(opt.flags & OOB_F_NO_SORT)) {
+        std::vector<std::pair<int, uint32_t>> ranges;
+        for (int w = 0; w < 3; w++)
+            for (uint32_t c = 0; c < K.ncls; c++)
+                if (K.start[w][c + 1] - K.start[w][c] >= 2) ranges.push_back({w, c});
+        parallel_for(ranges.size(), 1, [&](size_t lo, size_t hi) {
+            std::vector<uint32_t> cnt;
+            std::vector<std::pair<uint32_t, int64_t>> tmp;
+            for (size_t r = lo; r < hi; r++) {
+                std::vector<int64_t>& qs = K.reg[ranges[r].first];
+                const uint32_t c = ranges[r].second;
+                const size_t a = K.start[ranges[r].first][c], z = K.start[ranges[r].first][c + 1];
+                tmp.resize(z - a);
+                uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
+                for (size_t i = a; i < z; i++) {
+                    const uint32_t key = 0xFFFFu - (uint32_t)std::min(comp[qs[i]].cost, 65535.0);
+                    tmp[i - a] = {key, qs[i]};
+                    kmin = std::min(kmin, key);
+                    kmax = std::max(kmax, key);
                 }
-            });
-            for (size_t i = 0; i < qs.size(); i++) qs[i] = keyed[i].second;
-        }
+                if (kmin == kmax) continue;  // one key: already in query order
+                cnt.assign(kmax - kmin + 2, 0);
+                for (const auto& t : tmp) cnt[t.first - kmin + 1]++;
+                for (size_t k = 1; k < cnt.size(); k++) cnt[k] += cnt[k - 1];
+                for (const auto& t : tmp) qs[a + cnt[t.first - kmin]++] = t.second;
+            }
+        });
+    }
+    for (int w = 0; w < 3; w++) {
+        const auto& qs = K.reg[w];
+        if (qs.empty()) continue;
         if (want == 1) {
             pr.work[0].qs[w] = qs;
         } else {
@@ -2766,8 +2864,7 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
     pr.qcls.swap(tl_qcls);
     pr.errs.swap(tl_errs);
     auto recycle = [&]() {
-        pr.comp.clear();
-        pr.comp.swap(tl_comp);
+        pr.comp.swap(tl_comp);  // (kept sized: entries are overwritten by the next call)
         pr.qcls.swap(tl_qcls);
         pr.errs.swap(tl_errs);
     };
@@ -2804,6 +2901,23 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
     return rcode;
 }
 
+// SOLVE through drive().  A device allocation failure frees the device
+// buffers of the other pool slots (stream API workers keep theirs between
+// calls) and retries once; a worker of another slot falls back to slot 0's
+// buffers for good (the pool locks serialise the device phases).
+int drive_solve(const oob_batch* b, const oob_options* opt, const oob_result& o) {
+    int rc = drive(b, opt, MODE_SOLVE, nullptr, o.model, o.verdict, o.nodes, o.passes, o.elapsed_s);
+    if (rc != OOB_E_CUDA || g_last_error.find("out of memory") == std::string::npos) return rc;
+    cudaGetLastError();
+    if (tl_pool_slot != 0) {
+        release_slot_pools(tl_pool_slot);
+        tl_pool_slot = 0;
+    } else {
+        for (int s = 1; s < 4; s++) release_slot_pools(s);
+    }
+    return drive(b, opt, MODE_SOLVE, nullptr, o.model, o.verdict, o.nodes, o.passes, o.elapsed_s);
+}
+
 }  // namespace
 
 // ============================================================================
@@ -2824,9 +2938,7 @@ int oob_solve_batch(const oob_batch* batch, const oob_options* opt, oob_result* 
         return (int64_t)((e && *e) ? std::atoll(e) : 0);  // off by default: measured slower
     }();
     const bool one_dev = (opt && opt->n_gpus == 1) || visible_devices() <= 1;
-    if (chunk_q <= 0 || n < 2 * chunk_q || !one_dev || tl_gate)
-        return drive(batch, opt, MODE_SOLVE, nullptr, out->model, out->verdict, out->nodes, out->passes,
-                     out->elapsed_s);
+    if (chunk_q <= 0 || n < 2 * chunk_q || !one_dev || tl_gate) return drive_solve(batch, opt, *out);
     const int k = (int)std::min<int64_t>(4, (n + chunk_q - 1) / chunk_q);
     HostGate gate;
     std::vector<int> rcs(k, OOB_OK);
@@ -2849,9 +2961,12 @@ int oob_solve_batch(const oob_batch* batch, const oob_options* opt, oob_result* 
                 gate.cv.wait(lk, [&] { return gate.turn >= c; });
             }
             tl_gate_held = true;
-            rcs[c] = drive(&sub, opt, MODE_SOLVE, nullptr, out->model, out->verdict + q0,
-                           out->nodes ? out->nodes + q0 : nullptr, out->passes ? out->passes + q0 : nullptr,
-                           out->elapsed_s ? out->elapsed_s + q0 : nullptr);
+            oob_result part = *out;
+            part.verdict = out->verdict + q0;
+            part.nodes = out->nodes ? out->nodes + q0 : nullptr;
+            part.passes = out->passes ? out->passes + q0 : nullptr;
+            part.elapsed_s = out->elapsed_s ? out->elapsed_s + q0 : nullptr;
+            rcs[c] = drive_solve(&sub, opt, part);
             if (rcs[c] != OOB_OK) msgs[c] = g_last_error;
             gate_release();  // also on early exits (no launch happened)
             tl_gate = nullptr;
@@ -2878,11 +2993,15 @@ int oob_solve_batches(const oob_batch* batches, int64_t n_batches, const oob_opt
     std::vector<int> rcs(n_batches, OOB_OK);
     std::vector<std::string> msgs(n_batches);
     std::vector<std::thread> th;
-    for (int s = 0; s < 2 && s < n_batches; s++) {
+    static const int n_slots = [] {
+        const char* e = std::getenv("SCUBA_OOB_STREAM_SLOTS");
+        return (e && *e) ? std::max(1, std::min(4, std::atoi(e))) : 3;
+    }();
+    for (int s = 0; s < n_slots && s < n_batches; s++) {
         th.emplace_back([&, s]() {
             tl_pool_slot = s;
             tl_gate = &gate;
-            for (int64_t i = s; i < n_batches; i += 2) {
+            for (int64_t i = s; i < n_batches; i += n_slots) {
                 tl_chunk = (int)i;
                 {
                     std::unique_lock<std::mutex> lk(gate.mu);
@@ -2890,19 +3009,7 @@ int oob_solve_batches(const oob_batch* batches, int64_t n_batches, const oob_opt
                 }
                 tl_gate_held = true;
                 const oob_result& o = outs[i];
-                rcs[i] = drive(batches + i, opt, MODE_SOLVE, nullptr, o.model, o.verdict, o.nodes, o.passes,
-                               o.elapsed_s);
-                if (rcs[i] == OOB_E_CUDA && tl_pool_slot != 0 &&
-                    g_last_error.find("out of memory") != std::string::npos) {
-                    // no room for a second set of device buffers: this worker
-                    // frees its own and shares slot 0's from here on (the pool
-                    // locks serialise the device phases; host phases still overlap)
-                    release_slot_pools(tl_pool_slot);
-                    tl_pool_slot = 0;
-                    cudaGetLastError();
-                    rcs[i] = drive(batches + i, opt, MODE_SOLVE, nullptr, o.model, o.verdict, o.nodes, o.passes,
-                                   o.elapsed_s);
-                }
+                rcs[i] = drive_solve(batches + i, opt, o);
                 if (rcs[i] != OOB_OK) msgs[i] = g_last_error;
                 gate_release();  // also on early exits (no launch happened)
             }
@@ -2968,7 +3075,8 @@ int oob_jit_compile(const oob_batch* b, int64_t q, char* src, int64_t src_cap, d
     if (!b || q < 0 || q >= b->n_queries) return fail(OOB_E_INVALID, "bad query index");
     std::string why = validate(b, q);
     if (!why.empty()) return fail(OOB_E_INVALID, why);
-    Compiled c = compile_query(b, q, MODE_SOLVE, 30.0, nullptr);
+    Pins pins;
+    Compiled c = compile_query(b, q, MODE_SOLVE, 30.0, nullptr, pins);
     if (c.regime == R_IMMEDIATE || c.regime == R_RANGE) return fail(OOB_E_INVALID, "query has no search");
     JitClass jc{c.words().data(), c.nv, c.ncon, c.ncode, c.nlit, c.regime == R_W128 ? 128 : 64};
     std::string text = jit_source(jc);
@@ -3025,17 +3133,18 @@ int oob_cert_compile(const oob_batch* b, const oob_options* opt, uint64_t* words
     const double timeout_s = opt ? opt->timeout_s : 30.0;
     const int64_t n = b->n_queries;
     std::vector<Compiled> comp(n);
-    std::vector<int64_t> reg[3];
+    Pins pins;
     for (int64_t q = 0; q < n; q++) {
         std::string why = validate(b, q);
         if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
-        comp[q] = compile_query(b, q, MODE_SOLVE, timeout_s, nullptr);
-        if (comp[q].regime >= R_W64 && comp[q].regime < R_W64 + 3) reg[comp[q].regime - R_W64].push_back(q);
+        comp[q] = compile_query(b, q, MODE_SOLVE, timeout_s, nullptr, pins);
     }
-    assign_classes(comp, reg);
+    Classes K;
+    std::vector<uint32_t> qcls;
+    classify(comp, n, pins.v, qcls, K, [](int64_t, const Compiled&) {});
     std::vector<uint64_t> certs;
     std::vector<uint32_t> off;
-    build_certs(b, comp, reg, certs, off);
+    build_certs(b, comp, K, qcls, certs, off);
     if ((int64_t)certs.size() > words_cap) return fail(OOB_E_NOMEM, "certificate words exceed the buffer");
     std::copy(certs.begin(), certs.end(), words);
     *n_words = (int64_t)certs.size();
@@ -3063,7 +3172,8 @@ int oob_query_regime(const oob_batch* b, const oob_options* opt, int8_t* regime)
     for (int64_t q = 0; q < b->n_queries; q++) {
         std::string why = validate(b, q);
         if (!why.empty()) return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + why);
-        regime[q] = compile_query(b, q, MODE_SOLVE, timeout_s, nullptr).regime;
+        Pins pins;
+        regime[q] = compile_query(b, q, MODE_SOLVE, timeout_s, nullptr, pins).regime;
     }
     return OOB_OK;
 }
