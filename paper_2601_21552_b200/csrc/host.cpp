@@ -379,9 +379,12 @@ unsigned host_threads() {
 }
 
 // Persistent host worker pool (thread creation per parallel loop cost ~0.5 ms
-// a call, and a solve runs about ten such loops).  One loop at a time; a
-// caller that finds the pool busy -- or a loop nested inside a worker -- runs
-// its loop inline.
+// a call, and a solve runs about ten such loops).  Several loops may run at
+// once -- the stream API's workers (one batch packing while the next one
+// compiles) -- and idle workers take chunks from the oldest loop with work
+// left, so one batch's short loop is not queued behind another's long one.
+// Each caller works on its own loop too; a loop nested inside a worker runs
+// inline.
 class HostPool {
   public:
     static HostPool& get() {
@@ -389,66 +392,77 @@ class HostPool {
         return *p;
     }
     // runs body(lo, hi) over [0, n) in chunks of `grain`; false from inside a
-    // pool worker (nested sections run serially).  Concurrent callers (the
-    // stream API's two workers: one batch's fetch beside the next one's
-    // compile) take the pool in turn instead of falling back to one thread.
+    // pool worker (nested sections run serially)
     bool run(size_t n, size_t grain, const std::function<void(size_t, size_t)>& body) {
         if (workers_.empty() || tl_in_pool) return false;
-        std::unique_lock<std::mutex> busy(run_mu_);
+        Loop L;
+        L.body = &body;
+        L.n = n;
+        L.grain = std::max<size_t>(grain, 1);
         {
             std::lock_guard<std::mutex> lk(mu_);
-            body_ = &body;
-            n_ = n;
-            grain_ = grain;
-            next_.store(0);
-            active_ = (int)workers_.size();
-            ++gen_;
+            active_.push_back(&L);
         }
         cv_.notify_all();
-        work();  // the caller takes chunks too
+        work_on(L);  // the caller takes chunks too
         std::unique_lock<std::mutex> lk(mu_);
-        done_cv_.wait(lk, [&] { return active_ == 0; });
-        body_ = nullptr;
+        active_.erase(std::find(active_.begin(), active_.end(), &L));
+        done_cv_.wait(lk, [&] { return L.done == L.n && L.users == 0; });
         return true;
     }
 
   private:
+    struct Loop {
+        const std::function<void(size_t, size_t)>* body = nullptr;
+        size_t n = 0, grain = 1;
+        std::atomic<size_t> next{0};
+        std::atomic<size_t> done{0};  // items finished
+        int users = 0;     // workers holding a pointer to this loop (under mu_)
+    };
     explicit HostPool(unsigned n) {
         for (unsigned i = 0; i < n; i++) {
             workers_.emplace_back([this] { loop(); });
             workers_.back().detach();
         }
     }
-    void work() {
+    void work_on(Loop& L) {
         for (;;) {
-            size_t a = next_.fetch_add(grain_);
-            if (a >= n_) break;
-            (*body_)(a, std::min(n_, a + grain_));
+            const size_t a = L.next.fetch_add(L.grain);
+            if (a >= L.n) break;
+            const size_t z = std::min(L.n, a + L.grain);
+            (*L.body)(a, z);
+            if (L.done.fetch_add(z - a) + (z - a) == L.n) {
+                std::lock_guard<std::mutex> lk(mu_);  // (the waiter tests under mu_: no lost wake-up)
+                done_cv_.notify_all();
+            }
         }
     }
     void loop() {
         tl_in_pool = true;
-        uint64_t seen = 0;
         for (;;) {
+            Loop* L = nullptr;
             {
                 std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
-                seen = gen_;
+                cv_.wait(lk, [&] {
+                    for (Loop* x : active_)
+                        if (x->next.load() < x->n) {
+                            L = x;
+                            return true;
+                        }
+                    return false;
+                });
+                L->users++;
             }
-            work();
+            work_on(*L);
             std::lock_guard<std::mutex> lk(mu_);
-            if (--active_ == 0) done_cv_.notify_all();
+            if (--L->users == 0 && L->done == L->n) done_cv_.notify_all();
         }
     }
     static thread_local bool tl_in_pool;
     std::vector<std::thread> workers_;
-    std::mutex mu_, run_mu_;
+    std::mutex mu_;
     std::condition_variable cv_, done_cv_;
-    const std::function<void(size_t, size_t)>* body_ = nullptr;
-    size_t n_ = 0, grain_ = 1;
-    std::atomic<size_t> next_{0};
-    int active_ = 0;
-    uint64_t gen_ = 0;
+    std::vector<Loop*> active_;
 };
 thread_local bool HostPool::tl_in_pool = false;
 
@@ -1205,147 +1219,176 @@ void pack(const RunCtx& rc, DevJob& j, bool inline_fill = false) {
     const auto pack_t0 = std::chrono::steady_clock::now();
     const std::vector<Compiled>& comp = *rc.comp;
     const oob_batch* b = rc.b;
-    // group the job's entries (own queries, then shadows) by structure class
-    // (batch-wide ids from prepare), keeping their order within a class (the
-    // lockstep kernel runs each warp on one class)
-    // scratch reused across calls (per thread): fresh vectors of this size
-    // would be page-faulted in on every call
-    // (local references: thread_local names inside the parallel lambdas below
-    // would resolve to the worker threads' own instances)
-    static thread_local std::vector<int64_t> tl_entries, tl_order;
-    static thread_local std::vector<uint32_t> tl_cls, tl_ocls;
-    static thread_local std::vector<uint64_t> tl_doff, tl_moff;
-    std::vector<int64_t>& entries = tl_entries;
-    std::vector<int64_t>& order = tl_order;
-    std::vector<uint32_t>& cls = tl_cls;
-    std::vector<uint32_t>& ocls = tl_ocls;
-    std::vector<uint64_t>& doff = tl_doff;
-    std::vector<uint64_t>& moff = tl_moff;
-    entries.assign(j.qs.begin(), j.qs.end());  // query id, or ~id for a shadow
-    entries.reserve(j.qs.size() + j.shadows.size());
-    for (int64_t q : j.shadows) entries.push_back(~q);
-    auto qid = [](int64_t e) { return e < 0 ? ~e : e; };
-    std::unordered_map<uint32_t, uint32_t> local;
-    cls.resize(entries.size());
-    std::vector<size_t> rep;
-    uint32_t last_g = UINT32_MAX, last_l = 0;  // entries arrive in class runs
     const std::vector<uint32_t>& qcls = *rc.qcls;  // 4 bytes per query: cache-resident, unlike comp[]
-    for (size_t i = 0; i < entries.size(); i++) {
-        const uint32_t g = qcls[qid(entries[i])];
-        if (g != last_g) {
-            auto it = local.emplace(g, (uint32_t)rep.size());
-            if (it.second) rep.push_back(i);
-            last_g = g;
-            last_l = it.first->second;
+    // The job's entries are its own queries, then its shadows, each list in
+    // class runs (prepare's class-major schedule).  Entries are grouped by
+    // structure class (batch-wide ids) keeping their order within a class
+    // (the lockstep kernel runs each warp on one class): the runs are found
+    // in parallel, placed serially (a few per class), and copied + filled in
+    // parallel.  Scratch is reused across calls (per calling thread).
+    static thread_local std::vector<int64_t> tl_own;
+    std::vector<int64_t>& own = tl_own;
+    own.swap(j.qs);
+    const size_t n_own = own.size(), n = n_own + j.shadows.size();
+    const int64_t* shp = j.shadows.data();
+    auto entry = [&](size_t i) -> int64_t { return i < n_own ? own[i] : ~shp[i - n_own]; };
+    auto qid = [](int64_t e) { return e < 0 ? ~e : e; };
+    struct Run {
+        uint32_t g;
+        size_t at, len;
+    };
+    const size_t RCH = 16384;
+    const size_t nrch = (n + RCH - 1) / RCH;
+    std::vector<std::vector<Run>> chunk_runs(nrch);
+    auto find_runs = [&](size_t c0, size_t c1) {
+        for (size_t ch = c0; ch < c1; ch++) {
+            std::vector<Run>& R = chunk_runs[ch];
+            const size_t z = std::min(n, (ch + 1) * RCH);
+            for (size_t i = ch * RCH; i < z; i++) {
+                const uint32_t g = qcls[qid(entry(i))];
+                if (R.empty() || R.back().g != g) R.push_back({g, i, 0});
+                R.back().len++;
+            }
         }
-        cls[i] = last_l;
+    };
+    find_runs(0, nrch);  // (serial: ~2 ns an entry, less than waking the pool)
+    std::vector<Run> runs;
+    for (const auto& R : chunk_runs)
+        for (const Run& r : R) {
+            if (!runs.empty() && runs.back().g == r.g) runs.back().len += r.len;
+            else runs.push_back(r);
+        }
+    // local class ids in order of first appearance
+    std::unordered_map<uint32_t, uint32_t> local;
+    std::vector<size_t> rep;  // first entry of every local class
+    std::vector<uint32_t> run_cls(runs.size());
+    for (size_t r = 0; r < runs.size(); r++) {
+        auto it = local.emplace(runs[r].g, (uint32_t)rep.size());
+        if (it.second) rep.push_back(runs[r].at);
+        run_cls[r] = it.first->second;
     }
     const size_t nc = rep.size();
-    std::vector<uint32_t> count(nc + 1, 0);
-    for (uint32_t c : cls) count[c + 1]++;
+    std::vector<uint64_t> count(nc + 1, 0);
+    for (size_t r = 0; r < runs.size(); r++) count[run_cls[r] + 1] += runs[r].len;
     for (size_t c = 0; c < nc; c++) count[c + 1] += count[c];
-    const size_t n = entries.size();
-    order.resize(n);
-    ocls.resize(n);
-    {
-        std::vector<uint32_t> at(count.begin(), count.end() - 1);
-        for (size_t i = 0; i < n; i++) {
-            uint32_t k = at[cls[i]]++;
-            order[k] = entries[i];
-            ocls[k] = cls[i];
-        }
-    }
     j.code.clear();
     j.cls.assign(nc, ClassDesc{});
+    // data layout: per entry (2 nv + nlit) values of the job's width, padded
+    // to 16 bytes (x32/int64/int128) or 32 bytes (256-bit); every entry of a
+    // class has the same data size, so offsets follow from the class bases
+    const size_t tb = tbytes_of(j.wide);
+    const size_t vw = tb >= 8 ? tb / 8 : 1;  // int64 words per value (x32 entries are shadows only)
+    const size_t align = j.wide == 2 ? 4 : 2;
+    std::vector<uint64_t> dbase(nc), dsz(nc), mbase(nc);
+    uint64_t dtot = 0, mtot = 0;
     for (size_t id = 0; id < nc; id++) {
-        const Compiled& c = comp[qid(entries[rep[id]])];
+        const Compiled& c = comp[qid(entry(rep[id]))];
         ClassDesc& cd = j.cls[id];
         cd.code_off = (uint32_t)j.code.size();
         j.code.insert(j.code.end(), c.words().begin(), c.words().end());
         cd.nv_ncon = c.nv | (c.ncon << 16);
         cd.ncode_nlit = c.ncode | (c.nlit << 16);
-        cd.q_begin = count[id];
-        cd.q_end = count[id + 1];
+        cd.q_begin = (uint32_t)count[id];
+        cd.q_end = (uint32_t)count[id + 1];
         cd.cert = (rc.cert_off && c.cls < rc.cert_off->size()) ? (*rc.cert_off)[c.cls] : NO_CERT;
         j.maxv = std::max(j.maxv, c.nv);
         j.maxcode = std::max(j.maxcode, c.ncode);
         j.maxlit = std::max(j.maxlit, c.nlit);
         j.maxcsize = std::max(j.maxcsize, c.maxcsize);
         j.maxdepth = std::max(j.maxdepth, c.maxdepth);
+        const uint64_t words = ((2 * (uint64_t)c.nv + c.nlit) * tb + 7) / 8;
+        dsz[id] = ((words + align - 1) / align) * align;
+        dbase[id] = dtot;
+        mbase[id] = mtot;
+        dtot += dsz[id] * (count[id + 1] - count[id]);
+        mtot += (uint64_t)c.nv * (count[id + 1] - count[id]);
     }
     j.n_classes = (uint32_t)nc;
+    j.model_words = mtot;
+    // copy segments: every run at its place in its class, cut into pieces
+    struct Seg {
+        size_t src, dst, len;
+        uint32_t cls;
+    };
+    std::vector<Seg> segs;
+    {
+        std::vector<uint64_t> at(count.begin(), count.end() - 1);
+        const size_t PIECE = 2048;
+        for (size_t r = 0; r < runs.size(); r++) {
+            const uint32_t c = run_cls[r];
+            for (size_t k = 0; k < runs[r].len; k += PIECE)
+                segs.push_back({runs[r].at + k, at[c] + k, std::min(PIECE, runs[r].len - k), c});
+            at[c] += runs[r].len;
+        }
+    }
+    if (trace_level() >= 2)
+        std::fprintf(stderr, "[oob]   pack w%d: %zu entries, %zu classes, %zu runs, serial part %.3f ms\n", j.wide, n,
+                     nc, runs.size(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pack_t0).count());
     j.qs.resize(n);
     j.is_shadow.resize(n);
     j.resume_init.resize(n);
     j.mo.resize(n);
     j.qd.alloc(n);
-    // data layout: per entry (2 nv + nlit) values of the job's width, padded
-    // to 16 bytes (x32/int64/int128) or 32 bytes (256-bit)
-    const size_t tb = tbytes_of(j.wide);
-    const size_t vw = tb >= 8 ? tb / 8 : 1;  // int64 words per value (x32 entries are shadows only)
-    const size_t align = j.wide == 2 ? 4 : 2;
-    // every entry of a class has the same data size: offsets per class run
-    doff.assign(n + 1, 0);
-    moff.assign(n + 1, 0);
-    for (size_t id = 0; id < nc; id++) {
-        const Compiled& c = comp[qid(entries[rep[id]])];
-        const uint64_t words = ((2 * (uint64_t)c.nv + c.nlit) * tb + 7) / 8;
-        const uint64_t dsz = ((words + align - 1) / align) * align;
-        for (uint32_t i = j.cls[id].q_begin; i < j.cls[id].q_end; i++) {
-            doff[i + 1] = doff[i] + dsz;
-            moff[i + 1] = moff[i] + c.nv;
-        }
-    }
-    j.model_words = moff[n];
-    if (trace_level() >= 2)
-        std::fprintf(stderr, "[oob]   pack w%d: %zu entries, %zu classes, serial part %.3f ms\n", j.wide, n, nc,
-                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pack_t0).count());
-    j.data.alloc(std::max<uint64_t>(doff[n], 4));
-    auto fill = [&](size_t lo, size_t hi) {
-        for (size_t i = lo; i < hi; i++) {
-            const int64_t e = order[i];
-            const int64_t q = qid(e);
-            const Compiled& c = comp[q];
-            j.qs[i] = q;
-            j.is_shadow[i] = e < 0;
-            j.resume_init[i] = e < 0 ? RES_SKIP : 0u;
-            QDesc& d = j.qd[i];
-            d.code_off = j.cls[ocls[i]].code_off;
-            d.nv_ncon = c.nv | (c.ncon << 16);
-            d.ncode_nlit = c.ncode | (c.nlit << 16);
-            d.out_q = (uint32_t)i;
-            d.data_off = doff[i];
-            d.out_v = moff[i];
-            j.mo[i] = moff[i];
-            int64_t* out = j.data.data() + doff[i];
-            int64_t* end = j.data.data() + doff[i + 1];
-            if (e < 0) continue;  // a shadow: written on the device before it is ever read
-            auto put = [&](i128 x) {
-                *out++ = (int64_t)(uint64_t)x;
-                if (vw >= 2) *out++ = (int64_t)(x >> 64);
-                if (vw == 4) {
-                    int64_t sgn = x < 0 ? -1 : 0;
-                    *out++ = sgn;
-                    *out++ = sgn;
+    j.data.alloc(std::max<uint64_t>(dtot, 4));
+    auto fill = [&](size_t s0, size_t s1) {
+        for (size_t si = s0; si < s1; si++) {
+            const Seg& sg = segs[si];
+            const ClassDesc& cd = j.cls[sg.cls];
+            const uint64_t ds = dsz[sg.cls];
+            for (size_t k = 0; k < sg.len; k++) {
+                const int64_t e = entry(sg.src + k);
+                const int64_t q = qid(e);
+                const size_t i = sg.dst + k;
+                const uint64_t rank = i - cd.q_begin;
+                j.qs[i] = q;
+                j.is_shadow[i] = e < 0;
+                j.resume_init[i] = e < 0 ? RES_SKIP : 0u;
+                QDesc& d = j.qd[i];
+                d.code_off = cd.code_off;
+                d.nv_ncon = cd.nv_ncon;
+                d.ncode_nlit = cd.ncode_nlit;
+                d.out_q = (uint32_t)i;
+                d.data_off = dbase[sg.cls] + rank * ds;
+                const uint32_t nv = cd.nv_ncon & 0xFFFFu;
+                d.out_v = mbase[sg.cls] + rank * nv;
+                j.mo[i] = d.out_v;
+                if (e < 0) continue;  // a shadow: written on the device before it is ever read
+                int64_t* out = j.data.data() + d.data_off;
+                int64_t* end = out + ds;
+                auto put = [&](i128 x) {
+                    *out++ = (int64_t)(uint64_t)x;
+                    if (vw >= 2) *out++ = (int64_t)(x >> 64);
+                    if (vw == 4) {
+                        int64_t sgn = x < 0 ? -1 : 0;
+                        *out++ = sgn;
+                        *out++ = sgn;
+                    }
+                };
+                const Compiled& c = comp[q];
+                const int64_t vb = b->var_begin[q];
+                for (uint32_t v = 0; v < nv; v++) {
+                    if (rc.mode == MODE_CHECK) {
+                        i128 m = from_w(rc.model[vb + v]);
+                        put(m);
+                        put(m);
+                    } else {
+                        put(from_w(b->var_lo[vb + v]));
+                        put(from_w(b->var_hi[vb + v]));
+                    }
                 }
-            };
-            const int64_t vb = b->var_begin[q];
-            for (uint32_t v = 0; v < c.nv; v++) {
-                if (rc.mode == MODE_CHECK) {
-                    i128 m = from_w(rc.model[vb + v]);
-                    put(m);
-                    put(m);
-                } else {
-                    put(from_w(b->var_lo[vb + v]));
-                    put(from_w(b->var_hi[vb + v]));
+                const Structure& st = *c.st;
+                const int64_t lb = b->lit_begin[q];
+                for (uint32_t li = 0; li < c.nlit; li++) {
+                    const int32_t src = st.lit_src[li];
+                    put(src < 0 ? (i128)1 : from_w(b->lits[lb + src]));
                 }
+                std::fill(out, end, 0);
             }
-            for (uint32_t i = 0; i < c.nlit; i++) put(lit_value(b, q, *c.st, i));
-            std::fill(out, end, 0);
         }
     };
-    if (inline_fill) fill(0, n);
-    else parallel_for(n, 1024, fill);  // (the wide jobs hold 10-30K entries: small grains spread them)
+    if (inline_fill) fill(0, segs.size());
+    else parallel_for(segs.size(), 1, fill);
     if (n == 0) std::fill(j.data.data(), j.data.data() + j.data.size(), 0);
     if (j.code.empty()) j.code.push_back(0);
     if (j.cls.empty()) j.cls.push_back(ClassDesc{});
