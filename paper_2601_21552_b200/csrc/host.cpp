@@ -31,6 +31,11 @@
 #include <unordered_map>
 #include <vector>
 
+#include <dlfcn.h>
+#include <signal.h>
+#include <sys/time.h>
+#include <ucontext.h>
+
 #include "../../include/scuba_oob.h"
 #include "format.h"
 #include "jit.h"
@@ -105,6 +110,52 @@ static const char* timeline_path() {
 // queues than the default 8 so that independent streams do not serialise.
 // Only effective before the process creates its CUDA context; never
 // overrides a value the user set.
+// SCUBA_OOB_PROF=<file>: sampling profile of the host pipeline -- SIGPROF
+// every 0.5 ms of process CPU time records the interrupted program counter;
+// at exit the counters inside this library are written to <file> as offsets
+// from its load address (tools/host_profile.sh symbolizes them with
+// addr2line).  A diagnostics hook only.
+namespace prof {
+constexpr size_t CAP = 1 << 20;
+std::atomic<size_t> n{0};
+uintptr_t pc[CAP];
+const char* path = nullptr;
+void on_sigprof(int, siginfo_t*, void* uc) {
+    const size_t i = n.fetch_add(1, std::memory_order_relaxed);
+    if (i < CAP) pc[i] = (uintptr_t)((ucontext_t*)uc)->uc_mcontext.gregs[REG_RIP];
+}
+void dump() {
+    Dl_info info{};
+    if (!dladdr((void*)&dump, &info)) return;
+    FILE* f = std::fopen(path, "w");
+    if (!f) return;
+    const uintptr_t base = (uintptr_t)info.dli_fbase;
+    const size_t m = std::min(n.load(), CAP);
+    size_t outside = 0;
+    for (size_t i = 0; i < m; i++) {
+        Dl_info d{};
+        if (dladdr((void*)pc[i], &d) && d.dli_fbase == info.dli_fbase) std::fprintf(f, "%lx\n", (unsigned long)(pc[i] - base));
+        else outside++;
+    }
+    std::fprintf(f, "# samples %zu outside %zu\n", m, outside);
+    std::fclose(f);
+}
+__attribute__((constructor)) void init() {
+    path = std::getenv("SCUBA_OOB_PROF");
+    if (!path || !*path) return;
+    struct sigaction sa {};
+    sa.sa_sigaction = on_sigprof;
+    sa.sa_flags = SA_SIGINFO | SA_RESTART;
+    sigemptyset(&sa.sa_mask);
+    sigaction(SIGPROF, &sa, nullptr);
+    itimerval t{};
+    t.it_interval.tv_usec = 500;
+    t.it_value.tv_usec = 500;
+    setitimer(ITIMER_PROF, &t, nullptr);
+    std::atexit(dump);
+}
+}  // namespace prof
+
 __attribute__((constructor)) static void oob_default_connections() {
     setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
 }
@@ -520,8 +571,10 @@ i128 prove_bound(const uint32_t* code, size_t n, const std::vector<std::pair<uin
                  const std::vector<uint8_t>& rels, const std::vector<i128>& dlo,
                  const std::vector<i128>& dhi, const std::vector<i128>& lits) {
     Chk c;
-    static thread_local std::vector<i128> flo, fhi, gm;  // scratch reused across queries
-    static thread_local std::vector<char> none;
+    static thread_local std::vector<i128> tl_flo, tl_fhi, tl_gm, tl_tgt;  // scratch reused across queries
+    static thread_local std::vector<char> tl_none, tl_has;
+    std::vector<i128>&flo = tl_flo, &fhi = tl_fhi, &gm = tl_gm, &tgt = tl_tgt;
+    std::vector<char>&none = tl_none, &has = tl_has;
     flo.resize(n);
     fhi.resize(n);
     gm.resize(n);
@@ -584,8 +637,11 @@ i128 prove_bound(const uint32_t* code, size_t n, const std::vector<std::pair<uin
     // per relation (solver.py:240-259): the one-sided ones are +-INF and the
     // other side's forward bound +-1; for "=" arithmetic only happens when the
     // target [max(l0,r0), min(l1,r1)] is non-empty, i.e. inside both sides.
-    static thread_local std::vector<std::pair<uint32_t, i128>> stack;
-    stack.clear();
+    // Every node of the expanded code has one parent (constraint terms are
+    // emitted separately), so one reverse sweep over the postfix code hands
+    // each node its parent's target.
+    tgt.resize(n);
+    has.assign(n, 0);
     for (size_t k = 0; k < cons.size(); k++) {
         i128 fl = fmag(cons[k].first), fr = fmag(cons[k].second), tl, tr;
         switch (rels[k]) {
@@ -601,26 +657,29 @@ i128 prove_bound(const uint32_t* code, size_t n, const std::vector<std::pair<uin
             tl = tr = imin(fl, fr);
             break;
         }
-        stack.push_back({cons[k].first, tl});
-        stack.push_back({cons[k].second, tr});
-        while (!stack.empty()) {
-            auto [i, T] = stack.back();
-            stack.pop_back();
-            B = imax(B, T);
-            uint32_t op = w_op(code[i]);
-            if (op < NODE_ADD) continue;
-            uint32_t R = i - 1, L = R - size_of(R);
-            if (op == NODE_ADD || op == NODE_SUB) {
-                stack.push_back({L, c.add(T, fmag(R))});
-                stack.push_back({R, c.add(T, fmag(L))});
-            } else if (op == NODE_MUL) {
-                stack.push_back({L, imax(T, INF_R)});
-                stack.push_back({R, imax(T, INF_R)});
-            } else if (op == NODE_DIV && w_op(code[R]) == NODE_LIT && lits[w_arg(code[R])] >= 1) {
-                i128 cc = lits[w_arg(code[R])];
-                stack.push_back({L, c.add(c.mul(T, cc), cc)});
-            }
-            if (c.ovf) return -1;
+        tgt[cons[k].first] = tl;
+        has[cons[k].first] = 1;
+        tgt[cons[k].second] = tr;
+        has[cons[k].second] = 1;
+    }
+    for (size_t i = n; i-- > 0;) {
+        if (!has[i]) continue;
+        const i128 T = tgt[i];
+        B = imax(B, T);
+        uint32_t op = w_op(code[i]);
+        if (op < NODE_ADD) continue;
+        uint32_t R = (uint32_t)i - 1, L = R - size_of(R);
+        if (op == NODE_ADD || op == NODE_SUB) {
+            tgt[L] = c.add(T, fmag(R));
+            tgt[R] = c.add(T, fmag(L));
+            has[L] = has[R] = 1;
+        } else if (op == NODE_MUL) {
+            tgt[L] = tgt[R] = imax(T, INF_R);
+            has[L] = has[R] = 1;
+        } else if (op == NODE_DIV && w_op(code[R]) == NODE_LIT && lits[w_arg(code[R])] >= 1) {
+            i128 cc = lits[w_arg(code[R])];
+            tgt[L] = c.add(c.mul(T, cc), cc);
+            has[L] = 1;
         }
     }
     return c.ovf ? -1 : B;
@@ -637,7 +696,8 @@ double prove_bound_mag(const uint32_t* code, size_t n, const std::vector<std::pa
         if (v == (int64_t)v) return std::fabs((double)(int64_t)v);  // one conversion in the common case
         return (double)(v < 0 ? -(long double)v : (long double)v);
     };
-    static thread_local std::vector<double> m;
+    static thread_local std::vector<double> tl_m, tl_t;
+    std::vector<double>&m = tl_m, &tg = tl_t;
     m.resize(n);
     double B = 0;
     auto size_of = [&](uint32_t i) { return w_op(code[i]) >= NODE_ADD ? w_arg(code[i]) : 1u; };
@@ -655,31 +715,31 @@ double prove_bound_mag(const uint32_t* code, size_t n, const std::vector<std::pa
         B = std::max(B, m[j]);
     }
     const double INF_D = 1e18;
-    static thread_local std::vector<std::pair<uint32_t, double>> st;
-    st.clear();
+    // targets: one reverse sweep (every node has one parent; prove_bound);
+    // -1 = no target
+    tg.assign(n, -1.0);
     for (size_t k = 0; k < cons.size(); k++) {
         double fl = m[cons[k].first], fr = m[cons[k].second], tl, tr;
         if (rels[k] == OOB_REL_EQ) tl = tr = std::min(fl, fr);
         else { tl = std::max(INF_D, fr + 1); tr = std::max(INF_D, fl + 1); }
-        st.push_back({cons[k].first, tl});
-        st.push_back({cons[k].second, tr});
-        while (!st.empty()) {
-            auto [i, T] = st.back();
-            st.pop_back();
-            B = std::max(B, T);
-            uint32_t op = w_op(code[i]);
-            if (op < NODE_ADD) continue;
-            uint32_t R = i - 1, L = R - size_of(R);
-            if (op == NODE_ADD || op == NODE_SUB) {
-                st.push_back({L, T + m[R]});
-                st.push_back({R, T + m[L]});
-            } else if (op == NODE_MUL) {
-                st.push_back({L, std::max(T, INF_D)});
-                st.push_back({R, std::max(T, INF_D)});
-            } else if (op == NODE_DIV && w_op(code[R]) == NODE_LIT && lits[w_arg(code[R])] >= 1) {
-                double cc = mag(lits[w_arg(code[R])]);
-                st.push_back({L, T * cc + cc});
-            }
+        tg[cons[k].first] = tl;
+        tg[cons[k].second] = tr;
+    }
+    for (size_t i = n; i-- > 0;) {
+        const double T = tg[i];
+        if (T < 0) continue;
+        B = std::max(B, T);
+        uint32_t op = w_op(code[i]);
+        if (op < NODE_ADD) continue;
+        uint32_t R = (uint32_t)i - 1, L = R - size_of(R);
+        if (op == NODE_ADD || op == NODE_SUB) {
+            tg[L] = T + m[R];
+            tg[R] = T + m[L];
+        } else if (op == NODE_MUL) {
+            tg[L] = tg[R] = std::max(T, INF_D);
+        } else if (op == NODE_DIV && w_op(code[R]) == NODE_LIT && lits[w_arg(code[R])] >= 1) {
+            double cc = mag(lits[w_arg(code[R])]);
+            tg[L] = T * cc + cc;
         }
     }
     return B;
