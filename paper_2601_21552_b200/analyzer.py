@@ -8,12 +8,16 @@ checks).  Two integrations, both leaving the reference front end untouched:
 * `install(analyzer_module)` -- replace that binding with the GPU `solve`
   (one device call per query; simplest, launch-latency bound).
 
-* `analyze_batched(analyze, *args)` -- two-pass record/replay.  Constraint
+* `analyze_batched(analyze, *args)` -- record/replay.  Constraint
   generation never depends on an earlier verdict (analyzer.py:160-243), so
-  pass 1 runs the analysis with a recording stub, ONE GPU batch decides every
-  recorded query, and pass 2 re-runs the analysis replaying the verdicts in
-  call order.  Diagnostics are identical to the reference's because verdicts
-  and models are.
+  pass 1 runs the analysis with a recording stub that answers Unsat, ONE GPU
+  batch decides every recorded query, and pass 2 re-runs the analysis
+  replaying the verdicts in call order.  Diagnostics are identical to the
+  reference's because verdicts and models are.  Pass 2 is skipped when every
+  recorded query is decided Unsat: the analysis is deterministic, so pass 1
+  -- which saw exactly those verdicts -- already is the reference's result
+  (most programs: an access is reported only when a query is Sat or times
+  out).
 """
 from __future__ import annotations
 
@@ -105,18 +109,40 @@ class _Replay:
                                f"(pass 2 made {self.i} of the {len(self.calls)} recorded solver calls)")
 
 
+def _parse_once(analyzer_module, analyze, args, kwargs):
+    """analyze_source(text, filename, config) is parse_source + analyze_program
+    (analyzer.py:263-267): parse once, so a replayed pass re-runs only the
+    analysis (the passes build new objects from the AST and never modify it)."""
+    if analyze is not getattr(analyzer_module, "analyze_source", None):
+        return analyze, args, kwargs
+    import inspect
+
+    bound = inspect.signature(analyze).bind(*args, **kwargs)
+    bound.apply_defaults()
+    a = bound.arguments
+    program = analyzer_module.parse_source(a["text"], a["filename"])
+    return analyzer_module.analyze_program, (program, a["config"]), {}
+
+
 def analyze_batched(analyzer_module, analyze, *args, stats=None, mode="canonical", **kwargs):
     """Run `analyze(*args, **kwargs)` (e.g. analyzer_module.analyze_source)
     with all of its solver queries decided in one GPU batch."""
     types = _types(analyzer_module)
+    analyze, args, kwargs = _parse_once(analyzer_module, analyze, args, kwargs)
     saved = analyzer_module.solve
     rec = _Recorder(types[1])
     analyzer_module.solve = rec
     try:
-        analyze(*args, **kwargs)
+        first = analyze(*args, **kwargs)
     finally:
         analyzer_module.solve = saved
-    replay = _Replay(rec.calls, decide_calls(rec.calls, types, mode=mode))
+    verdicts = decide_calls(rec.calls, types, mode=mode)
+    if stats is not None:
+        stats["queries"] = len(rec.calls)
+        stats["replayed"] = 0
+    if all(isinstance(v, types[1]) for v in verdicts):
+        return first  # pass 1 saw exactly these verdicts
+    replay = _Replay(rec.calls, verdicts)
     analyzer_module.solve = replay
     try:
         result = analyze(*args, **kwargs)
@@ -124,7 +150,7 @@ def analyze_batched(analyzer_module, analyze, *args, stats=None, mode="canonical
         analyzer_module.solve = saved
     replay.finish()
     if stats is not None:
-        stats["queries"] = len(rec.calls)
+        stats["replayed"] = 1
     return result
 
 
@@ -138,12 +164,13 @@ def analyze_many(analyzer_module, analyze, jobs, stats=None, mode="canonical"):
     verdicts in call order.  Returns the list of results, in job order."""
     types = _types(analyzer_module)
     saved = analyzer_module.solve
-    recs = []
+    prepared = [_parse_once(analyzer_module, analyze, args, kwargs) for args, kwargs in jobs]
+    recs, firsts = [], []
     try:
-        for args, kwargs in jobs:
+        for analyze, args, kwargs in prepared:
             rec = _Recorder(types[1])
             analyzer_module.solve = rec
-            analyze(*args, **kwargs)
+            firsts.append(analyze(*args, **kwargs))
             recs.append(rec)
     finally:
         analyzer_module.solve = saved
@@ -151,16 +178,23 @@ def analyze_many(analyzer_module, analyze, jobs, stats=None, mode="canonical"):
     verdicts = decide_calls(calls, types, mode=mode)
     results = []
     base = 0
-    for (args, kwargs), rec in zip(jobs, recs):
-        replay = _Replay(rec.calls, verdicts[base:base + len(rec.calls)])
+    replayed = 0
+    for (analyze, args, kwargs), rec, first in zip(prepared, recs, firsts):
+        mine = verdicts[base:base + len(rec.calls)]
+        base += len(rec.calls)
+        if all(isinstance(v, types[1]) for v in mine):
+            results.append(first)  # pass 1 saw exactly these verdicts
+            continue
+        replay = _Replay(rec.calls, mine)
         analyzer_module.solve = replay
         try:
             results.append(analyze(*args, **kwargs))
         finally:
             analyzer_module.solve = saved
         replay.finish()
-        base += len(rec.calls)
+        replayed += 1
     if stats is not None:
         stats["queries"] = len(calls)
         stats["batches"] = len({c[2] for c in calls})
+        stats["replayed"] = replayed
     return results
