@@ -454,7 +454,12 @@ def run_ours(args, rank, world, local):
     stream_fbs = [synth.generate(cfg, n_mine, first=total * (k + 1) + first, names=False)
                   for k in range(k_stream)]
     from paper_2601_21552_b200._lib import solve_flat_stream
-    solve_flat_stream(stream_fbs[:2], 30.0, n_gpus=1, device=device, flags=flags)  # warm (pools, JIT)
+    # warm: every pool slot of the stream workers (device buffers, JIT) on
+    # other batches of the stream
+    warm_fbs = [synth.generate(cfg, n_mine, first=total * (k_stream + 1 + k) + first, names=False)
+                for k in range(3)]
+    solve_flat_stream(warm_fbs, 30.0, n_gpus=1, device=device, flags=flags)
+    del warm_fbs
     dist.barrier()
     t0 = time.perf_counter()
     souts = solve_flat_stream(stream_fbs, 30.0, n_gpus=1, device=device, flags=flags)
@@ -531,7 +536,10 @@ def rank0_extras(args, cfg, fb, res, out, device, flags, world, _lib, synth, sol
         corpus[name] = {"wall_ms_median": round(1e3 * statistics.median(walls), 3),
                         "verdicts_identical": bool(np.array_equal(cout["verdict"], want))}
     ex["corpus"] = corpus
-    # the reference analyzer over the corpus with the GPU engine (config C2)
+    # the reference analyzer over the corpus with the GPU engine (config C2);
+    # this process's pooled device buffers are freed first, so the fresh
+    # process's cold start does not run against a nearly full device
+    _lib.release()
     try:
         r = subprocess.run([sys.executable, str(ROOT / "tools/corpus_wall.py"), args.mode],
                            capture_output=True, text=True, timeout=300)

@@ -142,6 +142,12 @@ def device_count() -> int:
     return int(lib().oob_device_count())
 
 
+def release() -> None:
+    """Free the pooled device buffers of the solve paths (the stream API keeps
+    one set per worker between calls); the next call allocates again."""
+    lib().oob_release()
+
+
 def options(timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0, jit_min=0):
     o = oob_options()
     o.jit_min = int(jit_min)

@@ -3295,9 +3295,30 @@ struct oob_plan {
     int64_t runs = 0;
 };
 
-int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** out) {
-    if (!out) return fail(OOB_E_INVALID, "null plan pointer");
-    std::unique_ptr<oob_plan> p(new oob_plan());
+// frees a plan's device buffers, streams and events (also a partly built one)
+static void plan_free(oob_plan* p) {
+    if (!p) return;
+    for (auto& G : p->groups)
+        for (int w = 0; w < NJOBS; w++) {
+            DevicePool* P = G.pool[w];
+            if (!P) continue;
+            cudaSetDevice(phys_dev(G.dev));
+            P->release_all();
+            if (P->ev0) cudaEventDestroy(P->ev0);
+            if (P->ev1) cudaEventDestroy(P->ev1);
+            if (P->evr) cudaEventDestroy(P->evr);
+            for (auto x : P->xs) cudaStreamDestroy(x);
+            for (auto x : P->xev) cudaEventDestroy(x);
+            if (P->stream) cudaStreamDestroy(P->stream);
+        }
+    delete p;
+}
+struct PlanFree {
+    void operator()(oob_plan* p) const { plan_free(p); }
+};
+
+static int plan_create_once(const oob_batch* batch, const oob_options* opt, oob_plan** out) {
+    std::unique_ptr<oob_plan, PlanFree> p(new oob_plan());
     p->b = batch;
     if (!batch) return fail(OOB_E_INVALID, "null batch");
     int64_t n = batch->n_queries;
@@ -3345,6 +3366,19 @@ int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** o
             }
     *out = p.release();
     return OOB_OK;
+}
+
+int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** out) {
+    if (!out) return fail(OOB_E_INVALID, "null plan pointer");
+    int rc = plan_create_once(batch, opt, out);
+    if (rc == OOB_E_CUDA && g_last_error.find("out of memory") != std::string::npos) {
+        // the solve paths' pooled buffers (stream workers keep theirs
+        // between calls) make room for the plan's own
+        cudaGetLastError();
+        for (int s = 0; s < 4; s++) release_slot_pools(s);
+        rc = plan_create_once(batch, opt, out);
+    }
+    return rc;
 }
 
 int oob_plan_run(oob_plan* p, float* device_ms) {
@@ -3429,22 +3463,7 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
     return OOB_OK;
 }
 
-void oob_plan_destroy(oob_plan* p) {
-    if (!p) return;
-    for (auto& G : p->groups)
-        for (int w = 0; w < NJOBS; w++) {
-            cudaSetDevice(phys_dev(G.dev));
-            DevicePool* P = G.pool[w];
-            P->release_all();
-            if (P->ev0) cudaEventDestroy(P->ev0);
-            if (P->ev1) cudaEventDestroy(P->ev1);
-            if (P->evr) cudaEventDestroy(P->evr);
-            for (auto x : P->xs) cudaStreamDestroy(x);
-            for (auto x : P->xev) cudaEventDestroy(x);
-            if (P->stream) cudaStreamDestroy(P->stream);
-        }
-    delete p;
-}
+void oob_plan_destroy(oob_plan* p) { plan_free(p); }
 
 // Host-side self-test of the 256-bit regime arithmetic (tests/test_wide.py
 // compares it with Python integers).  op: 0 + 1 - 2 * 3 / 4 % 5 < 6 >>1
@@ -3476,12 +3495,7 @@ int oob_device_count(void) { return visible_devices(); }
 const char* oob_version(void) { return "scuba-oob-b200 0.1 (sm_100a)"; }
 
 void oob_release(void) {
-    std::lock_guard<std::mutex> lk(g_pools_mu);
-    for (auto& p : g_pools) {
-        if (!p) continue;
-        std::lock_guard<std::mutex> lk2(p->mu);
-        p->release_all();
-    }
+    for (int s = 0; s < 4; s++) release_slot_pools(s);
 }
 
 }  // extern "C"
