@@ -18,11 +18,18 @@ checks).  Two integrations, both leaving the reference front end untouched:
   -- which saw exactly those verdicts -- already is the reference's result
   (most programs: an access is reported only when a query is Sat or times
   out).
+
+Both batched entry points also build the queries natively (`emit.py`,
+SURVEY.md 8(f) rank 1): the analyzer's two constraint-set generators are
+bound to `csrc/emit_native.cpp`, which creates objects equal to the
+reference's `_SetBuilder` output, field for field (`native=False` keeps the
+reference's Python generators).
 """
 from __future__ import annotations
 
 import contextlib
 
+from .emit import native_emission
 from .solver import solve_batch
 from .terms import query_to_json
 
@@ -124,9 +131,14 @@ def _parse_once(analyzer_module, analyze, args, kwargs):
     return analyzer_module.analyze_program, (program, a["config"]), {}
 
 
-def analyze_batched(analyzer_module, analyze, *args, stats=None, mode="canonical", **kwargs):
+def analyze_batched(analyzer_module, analyze, *args, stats=None, mode="canonical", native=True, **kwargs):
     """Run `analyze(*args, **kwargs)` (e.g. analyzer_module.analyze_source)
     with all of its solver queries decided in one GPU batch."""
+    with (native_emission(analyzer_module) if native else contextlib.nullcontext()):
+        return _analyze_batched(analyzer_module, analyze, args, kwargs, stats, mode)
+
+
+def _analyze_batched(analyzer_module, analyze, args, kwargs, stats, mode):
     types = _types(analyzer_module)
     analyze, args, kwargs = _parse_once(analyzer_module, analyze, args, kwargs)
     saved = analyzer_module.solve
@@ -154,7 +166,7 @@ def analyze_batched(analyzer_module, analyze, *args, stats=None, mode="canonical
     return result
 
 
-def analyze_many(analyzer_module, analyze, jobs, stats=None, mode="canonical"):
+def analyze_many(analyzer_module, analyze, jobs, stats=None, mode="canonical", native=True):
     """a whole set of analyses (e.g. the 20-program
     corpus) with ALL their solver queries decided in ONE device batch.
 
@@ -162,6 +174,11 @@ def analyze_many(analyzer_module, analyze, jobs, stats=None, mode="canonical"):
     analysis with a recording stub, one batch decides the union of the
     recorded queries, pass 2 re-runs each analysis replaying its own slice of
     verdicts in call order.  Returns the list of results, in job order."""
+    with (native_emission(analyzer_module) if native else contextlib.nullcontext()):
+        return _analyze_many(analyzer_module, analyze, jobs, stats, mode)
+
+
+def _analyze_many(analyzer_module, analyze, jobs, stats, mode):
     types = _types(analyzer_module)
     saved = analyzer_module.solve
     prepared = [_parse_once(analyzer_module, analyze, args, kwargs) for args, kwargs in jobs]
