@@ -17,7 +17,8 @@ import numpy as np
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "libscuba_oob.so"
+# (SCUBA_OOB_LIB_PATH: another build of the library, for A/B measurements)
+LIB_PATH = Path(os.environ["SCUBA_OOB_LIB_PATH"]) if os.environ.get("SCUBA_OOB_LIB_PATH") else HERE / "libscuba_oob.so"
 
 OOB_OK, OOB_E_INVALID, OOB_E_CUDA, OOB_E_RANGE, OOB_E_NOMEM = 0, 1, 2, 3, 4
 UNSAT, SAT, TIMEOUT, ERROR = 0, 1, 2, 3

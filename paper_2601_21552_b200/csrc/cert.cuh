@@ -53,6 +53,24 @@ struct BoxV {  // [0, np) parameters, [np, np + nv) variables, then atoms
     int np;
 };
 OOB_HD CERT_INL bool fits64(i128 x) { return x == (i128)(long long)x; }
+// sym::fdiv / sym::tdiv with a 64-bit path: the 128-bit division is a long
+// software loop on the device, and the checked values are mostly small
+OOB_HD CERT_INL i128 fdiv64(i128 a, i128 b) {  // floor(a / b), b > 0
+    if (b == 1) return a;
+    const long long al = (long long)a, bl = (long long)b;
+    if ((i128)al == a && (i128)bl == b) {
+        long long q = al / bl;
+        if ((al % bl != 0) && (al < 0)) --q;
+        return q;
+    }
+    return sym::fdiv(a, b);
+}
+OOB_HD CERT_INL i128 tdiv64(i128 a, i128 b) {  // C truncation, b != 0
+    if (b == 1) return a;
+    const long long al = (long long)a, bl = (long long)b;
+    if ((i128)al == a && (i128)bl == b && !(bl == -1 && al == (long long)(1ull << 63))) return al / bl;
+    return sym::tdiv(a, b);
+}
 
 OOB_HD CERT_INL bool mono_iv_b(uint64_t k, const BoxV& B, i128& rl, i128& rh) {
     if (!(k << 8)) {  // a constant or a single variable (most terms)
@@ -187,12 +205,12 @@ OOB_HD CERT_INL int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& 
         i128 rlo, rhi;
         if (litdiv) {
             if (bl != bh || bl < 1) return C_UNKNOWN;  // guards0 also checks it
-            rlo = sym::tdiv(al, bl);
-            rhi = sym::tdiv(ah, bl);
+            rlo = tdiv64(al, bl);
+            rhi = tdiv64(ah, bl);
         } else if (op == NODE_DIV) {
             if (al >= 0 && bl >= 1) {
-                rlo = sym::tdiv(al, bh);
-                rhi = sym::tdiv(ah, bl);
+                rlo = tdiv64(al, bh);
+                rhi = tdiv64(ah, bl);
             } else {
                 const i128 m = sym::imax(sym::iabs(al), sym::iabs(ah));
                 rlo = -m;
@@ -251,14 +269,14 @@ OOB_HD CERT_INL int cert_check(const uint64_t* p, GetDom dom, GetLit lit, BoxV& 
             i128 slo, shi;
             if (!peval_blob(q, B, slo, shi) || k == 0) continue;
             if (k > 0) {
-                const i128 nlo = -sym::fdiv(shi, k);
+                const i128 nlo = -fdiv64(shi, k);
                 if (nlo > B.lo[v]) {
                     if (nlo > B.hi[v]) return C_REFUTED;
                     B.lo[v] = (long long)nlo;
                     changed = true;
                 }
             } else {
-                const i128 nhi = sym::fdiv(shi, -k);
+                const i128 nhi = fdiv64(shi, -k);
                 if (nhi < B.hi[v]) {
                     if (nhi < B.lo[v]) return C_REFUTED;
                     B.hi[v] = (long long)nhi;

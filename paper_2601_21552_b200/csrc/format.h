@@ -183,6 +183,7 @@ struct LaunchArgs {
     // table (ClassDesc::cert) and the certificate words
     const ClassDesc* cert_classes;
     uint32_t cert_nclasses;
+    uint32_t cert_kmax;       // most certificates of any class of the job
     const uint64_t* certs;
 };
 

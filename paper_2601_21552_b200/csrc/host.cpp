@@ -46,7 +46,7 @@
 namespace oob {
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s);
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
-cudaError_t launch_cert(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
+cudaError_t launch_cert(const LaunchArgs& a, int wide, uint32_t k0, uint32_t k1, int sms, cudaStream_t s);
 cudaError_t grow_smem_limit(const void* fn, size_t smem);
 cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm);
 cudaError_t launch_gather_sat(const int8_t* verdict, const QDesc* qd, const int64_t* model, uint32_t n,
@@ -1846,7 +1846,11 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     a.cert_classes = nullptr;
     a.certs = nullptr;
     a.cert_nclasses = (uint32_t)j.cls.size();
+    a.cert_kmax = 0;
     if (fast && rc.certs && !rc.certs->empty() && j.wide != W_X32) {
+        for (const ClassDesc& cd : j.cls)
+            if (cd.cert != NO_CERT && cd.q_end > cd.q_begin)
+                a.cert_kmax = std::max<uint32_t>(a.cert_kmax, (uint32_t)(*rc.certs)[cd.cert]);
         CK(P->certs.ensure(rc.certs->size() * 8));
         CK(cudaMemcpyAsync(P->certs.p, rc.certs->data(), rc.certs->size() * 8, cudaMemcpyHostToDevice, s));
         a.certs = (const uint64_t*)P->certs.p;
@@ -2105,9 +2109,9 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         for (int w = 0; w < 3; w++) {
             if (!present(G.job[w]) || !G.job[w].a.certs) continue;
             const DevJob& j = G.job[w];
-            const uint32_t n = (uint32_t)j.qs.size();
-            const int blocks = (int)std::max<uint32_t>(1, std::min<uint32_t>((n + 127) / 128, (uint32_t)G.pool[w]->sms * 8));
-            CK(launch_cert(j.a, w, blocks, G.pool[w]->stream));
+            if (!j.a.cert_kmax) continue;
+            CK(launch_cert(j.a, w, 0, 1, G.pool[w]->sms, G.pool[w]->stream));
+            if (j.a.cert_kmax > 1) CK(launch_cert(j.a, w, 1, j.a.cert_kmax, G.pool[w]->sms, G.pool[w]->stream));
         }
         // root phases, widest first: 256-bit -> int128 -> int64 -> x32
         for (int w = 2; w >= 0; w--) {
@@ -3450,7 +3454,7 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
             jobs++;
             launches += 1 + (int64_t)j.jit_cls.size() + (j.tail_blocks ? 1 : 0) +
                         ((!j.slot[0].empty() || !j.slot[1].empty() || !j.slot[2].empty()) ? 1 : 0) +
-                        (j.a.certs ? 1 : 0);  // fast mode: the certificate check
+                        (j.a.certs && j.a.cert_kmax ? (j.a.cert_kmax > 1 ? 2 : 1) : 0);  // fast mode: certificates
         }
     info[0] = nq;
     info[1] = rec;

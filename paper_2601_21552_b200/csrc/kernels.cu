@@ -196,15 +196,24 @@ __device__ __forceinline__ sym::i128 cert_value(const i256& x) {
     return (x.w[2] == s && x.w[3] == s) ? lo : ((sym::i128)1 << 126);
 }
 
-// Fast mode (OOB_F_FAST): the Unsat certificate of each entry's structure
-// class (cert.cuh), checked numerically, one lane per entry, before the root
-// and solve kernels; a refuted entry is decided Unsat and never searched.
-// Entries are class-major, so a warp's lanes mostly share a certificate.
+// Fast mode (OOB_F_FAST): the Unsat certificates of each entry's structure
+// class (cert.cuh), checked numerically before the root and solve kernels; a
+// refuted entry is decided Unsat and never searched.  Two launches: every
+// entry's first certificate (the one from the class's widest member, which
+// refutes most entries), then one thread per (entry, later certificate) pair
+// for the entries still open -- so an entry no certificate refutes (a Sat
+// query) costs two certificates of latency instead of all of them in
+// sequence.  Entries are class-major, so a warp's lanes share a certificate.
 template <typename T>
-__global__ void __launch_bounds__(128) oob_cert_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(128) oob_cert_kernel(LaunchArgs a, uint32_t k0, uint32_t k1) {
     cert::BoxV B;
-    for (uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x; qi < a.n; qi += gridDim.x * blockDim.x) {
-        if (a.resume[qi] == RES_SKIP) continue;  // shadows
+    const uint64_t items = (uint64_t)a.n * (k1 - k0);
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+         it += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t kk = (uint32_t)(it / a.n), qi = (uint32_t)(it - (uint64_t)kk * a.n);
+        const uint32_t k = k0 + kk;
+        const uint32_t r0 = __ldcg(a.resume + qi);
+        if (r0 == RES_SKIP) continue;  // a shadow, or refuted by another certificate already
         // the entry's class: the last class starting at or before qi
         uint32_t lo = 0, hi = a.cert_nclasses;
         while (hi - lo > 1) {
@@ -214,26 +223,23 @@ __global__ void __launch_bounds__(128) oob_cert_kernel(LaunchArgs a) {
         }
         const uint32_t off = a.cert_classes[lo].cert;
         if (off == NO_CERT) continue;
+        const uint64_t* c = a.certs + off;
+        const uint64_t ncerts = *c++;
+        if (k >= ncerts) continue;
+        for (uint32_t s = 0; s < k; s++) c += 1 + c[0];  // [length][words] per certificate
+        ++c;
         const QDesc d = a.qdesc[qi];
         const uint32_t nv = d.nv_ncon & 0xFFFFu;
         const T* src = reinterpret_cast<const T*>(a.data + d.data_off);
         auto dom = [&](uint32_t i) -> sym::i128 { return cert_value(src[i]); };
         auto lit = [&](uint32_t i) -> sym::i128 { return cert_value(src[2 * nv + i]); };
-        const uint64_t* c = a.certs + off;
-        const uint64_t ncerts = *c++;
-        bool refuted = false;
-        for (uint64_t k = 0; k < ncerts && !refuted; ++k) {
-            const uint64_t len = *c++;
-            refuted = cert::cert_check(c, dom, lit, B) == cert::C_REFUTED;
-            c += len;
-        }
-        if (!refuted) continue;
+        if (cert::cert_check(c, dom, lit, B) != cert::C_REFUTED) continue;
+        if (atomicCAS(a.resume + qi, r0, RES_SKIP) != r0) continue;  // another certificate was first
         a.verdict[qi] = (int8_t)VERDICT_UNSAT;
         a.err[qi] = (int8_t)ERR_NONE;
         a.nodes[qi] = 0;
         a.passes[qi] = 0;
         a.elapsed[qi] = 0.f;
-        a.resume[qi] = RES_SKIP;
         if (a.fast_stats) atomicAdd(a.fast_stats + 4, 1ull);
     }
 }
@@ -337,10 +343,13 @@ cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t 
 }
 
 // fast mode certificate check of job `wide` (0 int64, 1 int128, 2 256-bit)
-cudaError_t launch_cert(const LaunchArgs& a, int wide, int blocks, cudaStream_t s) {
-    if (wide == 0) oob_cert_kernel<long long><<<blocks, 128, 0, s>>>(a);
-    else if (wide == 1) oob_cert_kernel<__int128><<<blocks, 128, 0, s>>>(a);
-    else if (wide == 2) oob_cert_kernel<i256><<<blocks, 128, 0, s>>>(a);
+// certificates [k0, k1) of every entry: one thread per (entry, certificate)
+cudaError_t launch_cert(const LaunchArgs& a, int wide, uint32_t k0, uint32_t k1, int sms, cudaStream_t s) {
+    const uint64_t items = (uint64_t)a.n * (k1 - k0);
+    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((items + 127) / 128, (uint64_t)sms * 16));
+    if (wide == 0) oob_cert_kernel<long long><<<blocks, 128, 0, s>>>(a, k0, k1);
+    else if (wide == 1) oob_cert_kernel<__int128><<<blocks, 128, 0, s>>>(a, k0, k1);
+    else if (wide == 2) oob_cert_kernel<i256><<<blocks, 128, 0, s>>>(a, k0, k1);
     return cudaGetLastError();
 }
 
