@@ -457,7 +457,7 @@ def run_ours(args, rank, world, local):
     # warm: every pool slot of the stream workers (device buffers, JIT) on
     # other batches of the stream
     warm_fbs = [synth.generate(cfg, n_mine, first=total * (k_stream + 1 + k) + first, names=False)
-                for k in range(3)]
+                for k in range(3 if n_mine > 200_000 else 6)]
     solve_flat_stream(warm_fbs, 30.0, n_gpus=1, device=device, flags=flags)
     del warm_fbs
     dist.barrier()
@@ -504,7 +504,7 @@ def run_ours(args, rank, world, local):
         "cpu_baseline": extras.get("cpu_baseline"),
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
                 "api": f"oob_solve_batches: {k_stream} different batches of the stream, pipelined",
-                "h2d_bytes_per_step": info["record_bytes"], "d2h_bytes_per_step": info["result_bytes"],
+                "h2d_bytes_per_step": info["h2d_bytes"], "d2h_bytes_per_step": info["result_bytes"],
                 "caller_batch_bytes_per_step": int(fb.nbytes if isinstance(fb.nbytes, int) else fb.nbytes()),
                 "single_call": {"value": round(e2e_single, 1), "unit": UNIT,
                                 "api": "one synchronous oob_solve_batch per step"}},

@@ -212,13 +212,15 @@ int oob_jit_compile(const oob_batch* batch, int64_t q, char* src, int64_t src_ca
  *                     class code + per-query data)  [2] result bytes
  *                     [3] structure classes  [4] device jobs  [5] kernel
  *                     launches per run  [6] queries in the int128 regime
- *                     [7] host compile time (us)
+ *                     [7] host compile time (us)  [8] bytes one solve call
+ *                     copies host -> device (raw values or records,
+ *                     descriptors, class code)
  */
 typedef struct oob_plan oob_plan;
 int oob_plan_create(const oob_batch* batch, const oob_options* opt, oob_plan** plan);
 int oob_plan_run(oob_plan* plan, float* device_ms);
 int oob_plan_results(oob_plan* plan, oob_result* out);
-int oob_plan_info(const oob_plan* plan, int64_t info[8]);
+int oob_plan_info(const oob_plan* plan, int64_t info[9]);
 void oob_plan_destroy(oob_plan* plan);
 
 /* Diagnostics: host-side evaluation of the 256-bit regime arithmetic

@@ -247,7 +247,7 @@ class Plan:
     """oob_plan_*: compile + upload once, run kernels on HBM-resident records."""
 
     INFO = ("queries", "record_bytes", "result_bytes", "classes", "jobs",
-            "launches_per_run", "wide_queries", "compile_us")
+            "launches_per_run", "wide_queries", "compile_us", "h2d_bytes")
 
     def __init__(self, fb, timeout_s=30.0, node_budget=0, n_gpus=0, device=0, flags=0, heavy_nodes=0,
                  jit_min=0):
@@ -264,7 +264,7 @@ class Plan:
         return float(ms.value)
 
     def info(self) -> dict:
-        a = np.zeros(8, dtype=np.int64)
+        a = np.zeros(len(self.INFO), dtype=np.int64)
         check(lib().oob_plan_info(self._p, a.ctypes.data), "oob_plan_info")
         return dict(zip(self.INFO, (int(x) for x in a)))
 

@@ -48,6 +48,8 @@ cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks,
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
 cudaError_t launch_cert(const LaunchArgs& a, int wide, uint32_t k0, uint32_t k1, int sms, cudaStream_t s);
 cudaError_t grow_smem_limit(const void* fn, size_t smem);
+cudaError_t launch_expand(int wide, const QDesc* qd, uint32_t n, const void* rawoff, const void* vlo, const void* vhi,
+                          const void* lits, const int32_t* litsrc, int64_t* data, int sms, cudaStream_t s);
 cudaError_t kernel_occupancy(int wide, int mode, size_t smem, int* blocks_per_sm);
 cudaError_t launch_gather_sat(const int8_t* verdict, const QDesc* qd, const int64_t* model, uint32_t n,
                               unsigned long long* counter, uint32_t* sat_off, int64_t* compact, int sms,
@@ -319,6 +321,7 @@ struct Compiled {
     double cost = 0;
     uint64_t key = 0;             // structure-class hash (words, nv, ncon)
     uint32_t cls = UINT32_MAX;    // batch-wide structure class id (prepare)
+    uint32_t lsrc = 0;            // offset of its structure's literal-slot sources in the call's table
     const char* why = nullptr;    // reason for R_RANGE (static text or the pinned structure's)
     const std::vector<uint32_t>& words() const { return st->words; }
 };
@@ -1029,6 +1032,8 @@ struct DevBuf {
     size_t cap = 0;
     cudaError_t ensure(size_t bytes) {
         if (bytes <= cap) return cudaSuccess;
+        if (trace_level() >= 3)
+            std::fprintf(stderr, "[oob]   device buffer grows %.1f -> %.1f MiB\n", cap / 1048576.0, bytes / 1048576.0);
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
@@ -1051,16 +1056,19 @@ struct DevicePool {
     DevBuf fr_map;                   // frontier region pool: held bits
     DevBuf slab_map;                 // slab pool (SOLVE kernels): held bits
     DevBuf handoff;                  // root states of queries handed off at their root
+    DevBuf raw_vlo, raw_vhi, raw_l, litsrc;  // SOLVE: the call's raw values (device-side records)
+    DevBuf rawoff;                   // per entry: raw var / literal offsets, literal-source table offset
     std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
     std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evr = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evr = nullptr, evraw = nullptr;
     int sms = 148;
     void release_all() {
         for (DevBuf* b : {&qdesc, &code, &data, &slabT, &slabU, &next, &verdict, &model, &nodes, &passes,
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
                           &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &slotx32, &timeline,
-                          &classes_interp, &stats, &certs, &satcnt, &satoff, &compact, &fr_map, &slab_map, &handoff})
+                          &classes_interp, &stats, &certs, &satcnt, &satoff, &compact, &fr_map, &slab_map, &handoff,
+                          &raw_vlo, &raw_vhi, &raw_l, &litsrc, &rawoff})
             b->release();
     }
 };
@@ -1163,6 +1171,15 @@ struct RunCtx {
     // fast mode: Unsat certificates per batch-wide structure class (cert.cuh)
     const std::vector<uint64_t>* certs = nullptr;
     const std::vector<uint32_t>* cert_off = nullptr;  // per class, NO_CERT: none
+    // SOLVE: the records are written on the device from the caller's raw
+    // values (copied to page-locked memory by the compile pass): domains and
+    // input literals at their batch offsets minus raw_v0 / raw_l0, and the
+    // literal-slot sources of every structure the call uses
+    bool raw = false;
+    const oob_i128 *raw_vlo = nullptr, *raw_vhi = nullptr, *raw_l = nullptr;
+    uint64_t raw_nv = 0, raw_nl = 0;
+    int64_t raw_v0 = 0, raw_l0 = 0;
+    const std::vector<int32_t>* litsrc = nullptr;
 };
 
 constexpr size_t SMEM_WARP_MAX = 48 * 1024;  // hot state per warp kept on chip up to this
@@ -1268,10 +1285,14 @@ struct DevJob {
     int64_t last_sat_vars = -1;  // packed Sat-model vars of the last fetch (SOLVE), -1: unpacked
     bool data_uploaded = false;  // records already on their way (uploaded right after pack)
     std::string upload_err;
+    bool dev_fill = false;       // SOLVE: records written on the device (oob_expand_kernel) from the raw values
+    uint64_t data_words = 0;     // record words of the job (data[] on the device)
+    HostArr<uint32_t> rawoff;    // dev_fill: per entry {var offset, literal offset, literal-source offset, 0}
+    DevicePool* raw_pool = nullptr;  // dev_fill: the pool holding the call's raw values on this device
 
     uint64_t record_bytes() const {  // algorithmic input bytes of one launch (x32 records: written on device)
         return qd.size() * sizeof(QDesc) + cls.size() * sizeof(ClassDesc) + code.size() * 4 +
-               (wide == W_X32 ? 0 : data.size() * 8);
+               (wide == W_X32 ? 0 : data_words * 8);
     }
 };
 
@@ -1390,7 +1411,10 @@ void pack(const RunCtx& rc, DevJob& j, bool inline_fill = false) {
     j.resume_init.resize(n);
     j.mo.resize(n);
     j.qd.alloc(n);
-    j.data.alloc(std::max<uint64_t>(dtot, 4));
+    j.dev_fill = rc.raw && rc.mode == MODE_SOLVE && j.wide != W_X32;
+    j.data_words = std::max<uint64_t>(dtot, 4);
+    if (j.dev_fill) j.rawoff.alloc(4 * std::max<size_t>(n, 1));
+    else j.data.alloc(j.data_words);
     auto fill = [&](size_t s0, size_t s1) {
         for (size_t si = s0; si < s1; si++) {
             const Seg& sg = segs[si];
@@ -1413,6 +1437,15 @@ void pack(const RunCtx& rc, DevJob& j, bool inline_fill = false) {
                 const uint32_t nv = cd.nv_ncon & 0xFFFFu;
                 d.out_v = mbase[sg.cls] + rank * nv;
                 j.mo[i] = d.out_v;
+                const Compiled& c = comp[q];
+                if (j.dev_fill) {  // the device writes the record (oob_expand_kernel)
+                    uint32_t* ro = j.rawoff.data() + 4 * i;
+                    ro[0] = e < 0 ? UINT32_MAX : (uint32_t)(b->var_begin[q] - rc.raw_v0);
+                    ro[1] = e < 0 ? 0u : (uint32_t)(b->lit_begin[q] - rc.raw_l0);
+                    ro[2] = c.lsrc;
+                    ro[3] = 0;
+                    continue;
+                }
                 if (e < 0) continue;  // a shadow: written on the device before it is ever read
                 int64_t* out = j.data.data() + d.data_off;
                 int64_t* end = out + ds;
@@ -1425,7 +1458,6 @@ void pack(const RunCtx& rc, DevJob& j, bool inline_fill = false) {
                         *out++ = sgn;
                     }
                 };
-                const Compiled& c = comp[q];
                 const int64_t vb = b->var_begin[q];
                 for (uint32_t v = 0; v < nv; v++) {
                     if (rc.mode == MODE_CHECK) {
@@ -1449,7 +1481,7 @@ void pack(const RunCtx& rc, DevJob& j, bool inline_fill = false) {
     };
     if (inline_fill) fill(0, segs.size());
     else parallel_for(segs.size(), 1, fill);
-    if (n == 0) std::fill(j.data.data(), j.data.data() + j.data.size(), 0);
+    if (n == 0 && !j.dev_fill) std::fill(j.data.data(), j.data.data() + j.data.size(), 0);
     if (j.code.empty()) j.code.push_back(0);
     if (j.cls.empty()) j.cls.push_back(ClassDesc{});
 }
@@ -1582,6 +1614,7 @@ std::string ensure_stream(DevicePool* P, int dev) {
         CK(cudaEventCreate(&P->ev0));
         CK(cudaEventCreate(&P->ev1));
         CK(cudaEventCreateWithFlags(&P->evr, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->evraw, cudaEventDisableTiming));
         CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, phys_dev(dev)));
         // per-thread stack: the deepest kernels (root phase, certificate
         // check, 256-bit solve) need up to ~2.2 KB; the default is 1 KB
@@ -1764,7 +1797,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     j.out_model_words = j.model_words * (rc.mode == MODE_PROPAGATE ? 4 : 2);
     CK(P->qdesc.ensure(j.qd.size() * sizeof(QDesc)));
     CK(P->code.ensure(j.code.size() * 4));
-    CK(P->data.ensure(j.data.size() * 8));
+    CK(P->data.ensure(j.data_words * 8));
     CK(P->slabT.ensure((size_t)j.slab_slots * j.g.slab_T_words * tbytes));
     CK(P->slabU.ensure((size_t)j.slab_slots * j.g.slab_u32_words * 4));
     if (pooled) CK(P->slab_map.ensure(((size_t)j.slab_slots + 31) / 32 * 4));
@@ -1812,8 +1845,17 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     CK(cudaMemcpyAsync(P->code.p, j.code.data(), j.code.size() * 4, cudaMemcpyHostToDevice, s));
     // the x32 job holds shadows only: their records are written on the device
     // (by the int64 root phase) before they are ever read -- nothing to upload
-    if ((j.wide != W_X32 || rc.mode != MODE_SOLVE) && !j.data_uploaded)
+    if ((j.wide != W_X32 || rc.mode != MODE_SOLVE) && !j.data_uploaded && !j.dev_fill)
         CK(cudaMemcpyAsync(P->data.p, j.data.data(), j.data.size() * 8, cudaMemcpyHostToDevice, s));
+    if (j.dev_fill && n > 0) {  // the records, written on the device from the call's raw values
+        DevicePool* R = j.raw_pool;
+        if (!R || !R->raw_vlo.p) return "device-side records: the raw values were not uploaded";
+        CK(P->rawoff.ensure((size_t)n * 16));
+        CK(cudaMemcpyAsync(P->rawoff.p, j.rawoff.data(), (size_t)n * 16, cudaMemcpyHostToDevice, s));
+        if (R != P) CK(cudaStreamWaitEvent(s, R->evraw, 0));
+        CK(launch_expand(j.wide, (const QDesc*)P->qdesc.p, n, P->rawoff.p, R->raw_vlo.p, R->raw_vhi.p, R->raw_l.p,
+                         (const int32_t*)R->litsrc.p, (int64_t*)P->data.p, P->sms, s));
+    }
     LaunchArgs& a = j.a;
     a = LaunchArgs{};
     a.qdesc = (const QDesc*)P->qdesc.p;
@@ -1874,7 +1916,7 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     }();
     a.handoff = nullptr;
     if (rc.mode == MODE_SOLVE && heavy_nodes && handoff_resume) {
-        CK(P->handoff.ensure(j.data.size() * 8));
+        CK(P->handoff.ensure(j.data_words * 8));
         a.handoff = (int64_t*)P->handoff.p;
     }
     a.fr_ecap = FR_ECAP;
@@ -1957,11 +1999,39 @@ struct DevGroup {
     int dev = 0;
     DevJob job[NJOBS];
     DevicePool* pool[NJOBS] = {nullptr, nullptr, nullptr, nullptr};
+    bool raw_uploaded = false;
 };
+
+// SOLVE: the call's raw domains / literals and the literal-source table go to
+// the device once per group (into the int64 job's pool, on its stream); the
+// jobs' record kernels wait for them (evraw)
+std::string upload_raw(const RunCtx& rc, DevGroup& G) {
+    if (!rc.raw || G.raw_uploaded) return "";
+    DevicePool* R = G.pool[0];
+    if (!R) return "device-side records: no pool for the raw values";
+    std::string e = ensure_stream(R, G.dev);
+    if (!e.empty()) return e;
+    CK(R->raw_vlo.ensure(std::max<uint64_t>(rc.raw_nv, 1) * 16));
+    CK(R->raw_vhi.ensure(std::max<uint64_t>(rc.raw_nv, 1) * 16));
+    CK(R->raw_l.ensure(std::max<uint64_t>(rc.raw_nl, 1) * 16));
+    CK(R->litsrc.ensure(std::max<size_t>(rc.litsrc->size(), 1) * 4));
+    if (rc.raw_nv) {
+        CK(cudaMemcpyAsync(R->raw_vlo.p, rc.raw_vlo, rc.raw_nv * 16, cudaMemcpyHostToDevice, R->stream));
+        CK(cudaMemcpyAsync(R->raw_vhi.p, rc.raw_vhi, rc.raw_nv * 16, cudaMemcpyHostToDevice, R->stream));
+    }
+    if (rc.raw_nl) CK(cudaMemcpyAsync(R->raw_l.p, rc.raw_l, rc.raw_nl * 16, cudaMemcpyHostToDevice, R->stream));
+    if (!rc.litsrc->empty())
+        CK(cudaMemcpyAsync(R->litsrc.p, rc.litsrc->data(), rc.litsrc->size() * 4, cudaMemcpyHostToDevice, R->stream));
+    CK(cudaEventRecord(R->evraw, R->stream));
+    for (int w = 0; w < NJOBS; w++) G.job[w].raw_pool = R;
+    G.raw_uploaded = true;
+    return "";
+}
 
 // start the upload of a packed job's records at once (caller holds P->mu):
 // the copy overlaps the packing of the next jobs instead of following it
 std::string upload_data(DevJob& j, DevicePool* P) {
+    if (j.dev_fill) return "";  // written on the device at staging (oob_expand_kernel)
     std::string e = ensure_stream(P, j.dev);
     if (!e.empty()) return e;
     CK(P->data.ensure(j.data.size() * 8));
@@ -1994,6 +2064,11 @@ void pack_group(const RunCtx& rc, DevGroup& G, bool upload = false) {
     for (int w = 0; w < NJOBS; w++) {
         G.job[w].data_uploaded = false;
         G.job[w].upload_err.clear();
+    }
+    if (upload) {  // the raw values travel while the jobs are packed
+        const std::string e = upload_raw(rc, G);
+        if (!e.empty())
+            for (int w = 0; w < NJOBS; w++) G.job[w].upload_err = e;
     }
     auto has = [&](int w) { return !G.job[w].qs.empty() || !G.job[w].shadows.empty(); };
     // the x32 job (shadows only: descriptors, no record data) is packed on a
@@ -2048,6 +2123,10 @@ void pack_group(const RunCtx& rc, DevGroup& G, bool upload = false) {
 inline bool present(const DevJob& j) { return !j.qs.empty(); }
 
 std::string stage_group(const RunCtx& rc, DevGroup& G, uint32_t depth_cap, uint32_t trail_cap, bool heavy) {
+    {
+        const std::string e = upload_raw(rc, G);  // (once per group)
+        if (!e.empty()) return e;
+    }
     for (int w = 0; w < NJOBS; w++) {
         if (!present(G.job[w])) continue;
         std::string e = stage(rc, G.job[w], G.pool[w], depth_cap, trail_cap, heavy);
@@ -2479,12 +2558,13 @@ inline bool device_regime(const Compiled& c) { return c.regime >= R_W64 && c.reg
 // device-bound; qcls[q] = class of a device query, 0 otherwise
 template <typename Other>
 void classify(std::vector<Compiled>& comp, int64_t n, const std::vector<std::shared_ptr<const Structure>>& pins,
-              std::vector<uint32_t>& qcls, Classes& K, Other other) {
+              std::vector<uint32_t>& qcls, Classes& K, Other other, std::vector<int32_t>* litsrc = nullptr) {
     // distinct structure objects -> canonical class (word-for-word equality)
     size_t TB = 1024;
     while (TB < 2 * pins.size()) TB *= 2;
     std::vector<const Structure*> slot_ptr(TB, nullptr);
-    std::vector<uint32_t> slot_canon(TB, 0);
+    std::vector<uint32_t> slot_canon(TB, 0), slot_lsrc(TB, 0);
+    if (litsrc) litsrc->clear();
     std::unordered_multimap<uint64_t, const Structure*> by_key;  // key -> first structure of a class
     std::unordered_map<const Structure*, uint32_t> canon_of_first;
     uint32_t nct = 0;
@@ -2510,11 +2590,15 @@ void classify(std::vector<Compiled>& comp, int64_t n, const std::vector<std::sha
         }
         slot_ptr[i] = p;
         slot_canon[i] = id;
+        if (litsrc) {  // this structure's literal-slot sources (device-side records)
+            slot_lsrc[i] = (uint32_t)litsrc->size();
+            litsrc->insert(litsrc->end(), p->lit_src.begin(), p->lit_src.end());
+        }
     }
-    auto canon = [&](const Structure* p) -> uint32_t {
+    auto slot_of = [&](const Structure* p) -> size_t {
         size_t i = hash_slot(p);
         while (slot_ptr[i] != p) i = (i + 1) & (TB - 1);  // every compiled structure is pinned
-        return slot_canon[i];
+        return i;
     };
     qcls.resize(n);
     // chunks: per-chunk tables of 3 * classes entries stay within 2^22 words
@@ -2527,13 +2611,15 @@ void classify(std::vector<Compiled>& comp, int64_t n, const std::vector<std::sha
             int64_t* fq = firstq.data() + ch * nct;
             const int64_t q1 = std::min<int64_t>(n, (int64_t)((ch + 1) * G));
             for (int64_t q = (int64_t)(ch * G); q < q1; q++) {
-                const Compiled& c = comp[q];
+                Compiled& c = comp[q];
                 if (!device_regime(c)) {
                     qcls[q] = 0;
                     other(q, c);
                     continue;
                 }
-                const uint32_t cc = canon(c.st);
+                const size_t si = slot_of(c.st);
+                const uint32_t cc = slot_canon[si];
+                c.lsrc = slot_lsrc[si];
                 qcls[q] = cc;
                 if (fq[cc] == INT64_MAX) fq[cc] = q;
             }
@@ -2792,6 +2878,13 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const Cl
 // Compile + schedule: fills immediate verdicts and returns the device jobs.
 struct Prepared {
     std::vector<Compiled> comp;
+    // SOLVE: the caller's raw domains and literals in page-locked memory,
+    // copied by the compile pass (device-side records, RunCtx::raw)
+    bool raw = false;
+    HostArr<oob_i128> raw_vlo, raw_vhi, raw_l;
+    int64_t raw_v0 = 0, raw_l0 = 0;
+    uint64_t raw_nv = 0, raw_nl = 0;
+    std::vector<int32_t> litsrc;  // literal-slot sources of every structure (Compiled::lsrc)
     std::vector<std::shared_ptr<const Structure>> pins;  // every structure comp[] points to
     Classes classes;
     std::vector<uint32_t> qcls;  // comp[q].cls, compact
@@ -2817,6 +2910,29 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     if ((int64_t)comp.size() != n) comp.resize(n);  // every entry is overwritten below (recycled storage)
     const bool fast_shortcut = mode == MODE_SOLVE && (opt.flags & OOB_F_FAST);
     pr.pins.clear();
+    // device-side records (SOLVE): the compile pass also copies each chunk's
+    // raw domains and literals into page-locked arrays (one H2D per call
+    // instead of ~2x their size in regime-width records filled on the host)
+    {
+        static const bool env_on = [] {
+            const char* e = std::getenv("SCUBA_OOB_DEVICE_RECORDS");
+            return !(e && *e == '0');
+        }();
+        pr.raw = false;
+        if (mode == MODE_SOLVE && env_on && n > 0) {
+            const int64_t v0 = b->var_begin[0], v1 = b->var_begin[n], l0 = b->lit_begin[0], l1 = b->lit_begin[n];
+            if (v1 >= v0 && l1 >= l0 && v1 - v0 < (int64_t)UINT32_MAX && l1 - l0 < (int64_t)UINT32_MAX) {
+                pr.raw = true;
+                pr.raw_v0 = v0;
+                pr.raw_l0 = l0;
+                pr.raw_nv = (uint64_t)(v1 - v0);
+                pr.raw_nl = (uint64_t)(l1 - l0);
+                pr.raw_vlo.alloc(std::max<uint64_t>(pr.raw_nv, 1));
+                pr.raw_vhi.alloc(std::max<uint64_t>(pr.raw_nv, 1));
+                pr.raw_l.alloc(std::max<uint64_t>(pr.raw_nl, 1));
+            }
+        }
+    }
     {
         // validation and compilation in one pass over the batch: a query is
         // compiled only once it has validated; the lowest invalid query is
@@ -2826,14 +2942,25 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         std::mutex pins_mu;
         parallel_for((size_t)n, 256, [&](size_t lo, size_t hi) {
             Pins pins;
+            bool valid = true;
             for (size_t q = lo; q < hi; q++) {
                 if (!validate(b, (int64_t)q).empty()) {
                     int64_t cur = bad.load();
                     while ((int64_t)q < cur && !bad.compare_exchange_weak(cur, (int64_t)q)) {
                     }
+                    valid = false;
                     break;
                 }
                 comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, pins, fast_shortcut);
+            }
+            if (valid && pr.raw) {  // this chunk's raw values (contiguous: offsets validated)
+                const int64_t va = b->var_begin[lo], vz = b->var_begin[hi];
+                const int64_t la = b->lit_begin[lo], lz = b->lit_begin[hi];
+                if (vz > va) {
+                    std::memcpy(pr.raw_vlo.data() + (va - pr.raw_v0), b->var_lo + va, (size_t)(vz - va) * 16);
+                    std::memcpy(pr.raw_vhi.data() + (va - pr.raw_v0), b->var_hi + va, (size_t)(vz - va) * 16);
+                }
+                if (lz > la) std::memcpy(pr.raw_l.data() + (la - pr.raw_l0), b->lits + la, (size_t)(lz - la) * 16);
             }
             std::lock_guard<std::mutex> lk(pins_mu);
             for (auto& p : pins.v) pr.pins.push_back(std::move(p));
@@ -2868,7 +2995,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
                 while (q < cur && !range_q.compare_exchange_weak(cur, q)) {
                 }
             }
-        });
+        }, pr.raw ? &pr.litsrc : nullptr);
         if (range_q.load() != INT64_MAX)
             pr.range_msg = "query " + std::to_string(range_q.load()) + ": " + comp[range_q.load()].why;
     }
@@ -2947,6 +3074,19 @@ int finish(Prepared& pr, int64_t n) {
     return OOB_OK;
 }
 
+// device-side records: the prepared call's raw values (RunCtx::raw)
+void set_raw(RunCtx& rc, const Prepared& pr) {
+    rc.raw = pr.raw;
+    rc.raw_vlo = pr.raw_vlo.data();
+    rc.raw_vhi = pr.raw_vhi.data();
+    rc.raw_l = pr.raw_l.data();
+    rc.raw_nv = pr.raw_nv;
+    rc.raw_nl = pr.raw_nl;
+    rc.raw_v0 = pr.raw_v0;
+    rc.raw_l0 = pr.raw_l0;
+    rc.litsrc = &pr.litsrc;
+}
+
 // Common driver of the three batched entry points.
 int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i128* model_in, oob_i128* model_out,
           int8_t* verdict, int64_t* nodes, int64_t* passes, double* elapsed) {
@@ -2994,6 +3134,7 @@ int drive(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i12
     rc.errs = &pr.errs;
     rc.certs = &pr.certs;
     rc.cert_off = &pr.cert_off;
+    set_raw(rc, pr);
     std::string e = run_all(rc, pr.work);
     if (!e.empty()) {
         recycle();
@@ -3220,6 +3361,7 @@ int oob_host_bench(const oob_batch* b, const oob_options* opt, double* ms) {
     rc.errs = &pr.errs;
     rc.certs = &pr.certs;
     rc.cert_off = &pr.cert_off;
+    set_raw(rc, pr);
     for (auto& wk : pr.work) {
         DevGroup G;
         G.dev = wk.dev;
@@ -3348,6 +3490,7 @@ static int plan_create_once(const oob_batch* batch, const oob_options* opt, oob_
     rc.errs = &p->pr.errs;
     rc.certs = &p->pr.certs;
     rc.cert_off = &p->pr.cert_off;
+    set_raw(rc, p->pr);
     p->groups.resize(p->pr.work.size());
     for (size_t k = 0; k < p->pr.work.size(); k++) {
         DevGroup& G = p->groups[k];
@@ -3432,13 +3575,18 @@ int oob_plan_results(oob_plan* p, oob_result* out) {
     return finish(p->pr, n);
 }
 
-int oob_plan_info(const oob_plan* p, int64_t info[8]) {
+int oob_plan_info(const oob_plan* p, int64_t info[9]) {
     if (!p || !info) return fail(OOB_E_INVALID, "null argument");
-    int64_t nq = 0, rec = 0, res = 0, cls = 0, wide = 0, jobs = 0, launches = 0;
-    for (auto& G : p->groups)
+    int64_t nq = 0, rec = 0, res = 0, cls = 0, wide = 0, jobs = 0, launches = 0, h2d = 0;
+    for (auto& G : p->groups) {
+        if (p->rc.raw)  // the raw values and literal sources, once per device
+            h2d += (int64_t)(p->rc.raw_nv * 2 + p->rc.raw_nl) * 16 + (int64_t)p->rc.litsrc->size() * 4;
         for (int w = 0; w < NJOBS; w++) {
             const DevJob& j = G.job[w];
             if (!present(j)) continue;
+            h2d += (int64_t)(j.qd.size() * sizeof(QDesc) + 2 * j.cls.size() * sizeof(ClassDesc) + j.code.size() * 4 +
+                             j.qs.size() * 4 + (j.slot[0].size() + j.slot[1].size() + j.slot[2].size()) * 4) +
+                   (j.dev_fill ? (int64_t)j.qs.size() * 16 : (j.wide == W_X32 ? 0 : (int64_t)j.data_words * 8));
             int64_t own = 0;
             for (uint8_t sh : j.is_shadow) own += !sh;
             nq += own;
@@ -3456,6 +3604,7 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
                         ((!j.slot[0].empty() || !j.slot[1].empty() || !j.slot[2].empty()) ? 1 : 0) +
                         (j.a.certs && j.a.cert_kmax ? (j.a.cert_kmax > 1 ? 2 : 1) : 0);  // fast mode: certificates
         }
+    }
     info[0] = nq;
     info[1] = rec;
     info[2] = res;
@@ -3464,6 +3613,7 @@ int oob_plan_info(const oob_plan* p, int64_t info[8]) {
     info[5] = launches;  // kernel launches per run
     info[6] = wide;
     info[7] = (int64_t)(p->pr.compile_s * 1e6);
+    info[8] = h2d;
     return OOB_OK;
 }
 

@@ -244,6 +244,67 @@ __global__ void __launch_bounds__(128) oob_cert_kernel(LaunchArgs a, uint32_t k0
     }
 }
 
+// Device-side records (SOLVE): every own entry's domains and literal slots,
+// written in its job's width (VW int64 words per value: 1 int64, 2 int128,
+// 4 256-bit, sign-extended) from the caller's raw int128 values uploaded once
+// per call; the host only writes the entry's offsets {raw var offset, raw
+// literal offset, literal-source table offset} (shadows: UINT32_MAX).  One
+// thread per entry; the record's padding is zeroed as the host did.
+struct RawWord {
+    uint64_t lo;
+    int64_t hi;
+};
+template <int VW>
+__global__ void __launch_bounds__(256) oob_expand_kernel(const QDesc* __restrict__ qd, uint32_t n,
+                                                         const uint4* __restrict__ rawoff,
+                                                         const RawWord* __restrict__ vlo,
+                                                         const RawWord* __restrict__ vhi,
+                                                         const RawWord* __restrict__ lits,
+                                                         const int32_t* __restrict__ litsrc, int64_t* data,
+                                                         uint32_t align) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint4 ro = rawoff[i];
+        if (ro.x == 0xFFFFFFFFu) continue;  // a shadow: written by the root phases
+        const QDesc d = qd[i];
+        const uint32_t nv = d.nv_ncon & 0xFFFFu, nlit = d.ncode_nlit >> 16;
+        int64_t* out = data + d.data_off;
+        auto put = [&](uint64_t lo, int64_t hi) {
+            out[0] = (int64_t)lo;
+            if (VW >= 2) out[1] = hi;
+            if (VW == 4) out[2] = out[3] = hi < 0 ? -1 : 0;
+            out += VW;
+        };
+        for (uint32_t v = 0; v < nv; v++) {
+            const RawWord a = vlo[ro.x + v], b = vhi[ro.x + v];
+            put(a.lo, a.hi);
+            put(b.lo, b.hi);
+        }
+        for (uint32_t s = 0; s < nlit; s++) {
+            const int32_t src = litsrc[ro.z + s];
+            if (src < 0) put(1, 0);
+            else {
+                const RawWord l = lits[ro.y + src];
+                put(l.lo, l.hi);
+            }
+        }
+        const uint64_t words = (uint64_t)(2 * nv + nlit) * VW;
+        const uint64_t dsz = (words + align - 1) / align * align;
+        for (uint64_t k = words; k < dsz; k++) data[d.data_off + k] = 0;
+    }
+}
+
+cudaError_t launch_expand(int wide, const QDesc* qd, uint32_t n, const void* rawoff, const void* vlo, const void* vhi,
+                          const void* lits, const int32_t* litsrc, int64_t* data, int sms, cudaStream_t s) {
+    const int blocks = (int)std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, (uint32_t)sms * 8));
+    const uint4* ro = (const uint4*)rawoff;
+    const RawWord *a = (const RawWord*)vlo, *b = (const RawWord*)vhi, *l = (const RawWord*)lits;
+    if (wide == 0) oob_expand_kernel<1><<<blocks, 256, 0, s>>>(qd, n, ro, a, b, l, litsrc, data, 2);
+    else if (wide == 1) oob_expand_kernel<2><<<blocks, 256, 0, s>>>(qd, n, ro, a, b, l, litsrc, data, 2);
+    else if (wide == 2) oob_expand_kernel<4><<<blocks, 256, 0, s>>>(qd, n, ro, a, b, l, litsrc, data, 4);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
 // propagate() / check_model() batches: one query per lane, no search
 template <typename T>
 __global__ void __launch_bounds__(THREADS) oob_aux_kernel(LaunchArgs a) {

@@ -11,7 +11,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
 k = int(sys.argv[3]) if len(sys.argv) > 3 else 6
 fbs = [synth.generate(cfg, n, first=(i + 1) * n, names=False) for i in range(k)]
-solve_flat_stream(fbs[:2], 30.0, n_gpus=1, flags=_lib.F_FAST)
+solve_flat_stream([synth.generate(cfg, n, first=(k + 1) * n + 10**8, names=False) for k in range(3)], 30.0, n_gpus=1, flags=_lib.F_FAST)
 for rep in range(3):
     t = time.perf_counter()
     solve_flat_stream(fbs, 30.0, n_gpus=1, flags=_lib.F_FAST)
