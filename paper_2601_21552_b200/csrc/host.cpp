@@ -1033,7 +1033,8 @@ struct DevBuf {
     cudaError_t ensure(size_t bytes) {
         if (bytes <= cap) return cudaSuccess;
         if (trace_level() >= 3)
-            std::fprintf(stderr, "[oob]   device buffer grows %.1f -> %.1f MiB\n", cap / 1048576.0, bytes / 1048576.0);
+            std::fprintf(stderr, "[oob]   device buffer %p grows %.1f -> %.1f MiB\n", (const void*)this, cap / 1048576.0,
+                         bytes / 1048576.0);
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
