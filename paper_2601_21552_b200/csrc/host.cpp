@@ -307,7 +307,27 @@ struct Pins {
             }
         last = v.size();
         v.push_back(p);
+        first.emplace_back();
+        vary.emplace_back();
+        seen.push_back(0);
         return r;
+    }
+    // fast mode: per pinned structure, the literal-slot values of its first
+    // device query in the chunk and which slots took another value since
+    // (the certificates' parameter scan, done while the values are at hand)
+    std::vector<std::vector<i128>> first;
+    std::vector<std::vector<uint8_t>> vary;
+    std::vector<uint8_t> seen;
+    void note_lits(const std::vector<i128>& lits, size_t nlit) {  // for the structure added or hit last
+        if (!seen[last]) {
+            seen[last] = 1;
+            first[last].assign(lits.begin(), lits.begin() + nlit);
+            vary[last].assign(nlit, 0);
+            return;
+        }
+        const i128* f = first[last].data();
+        uint8_t* y = vary[last].data();
+        for (size_t i = 0; i < nlit; i++) y[i] |= lits[i] != f[i];
     }
     size_t last = 0;
 };
@@ -937,13 +957,17 @@ struct StructCache {
 // structure's int128 threshold goes to the int128 job without the exact
 // proof (which would move some of them to int64: a scheduling choice only;
 // every regime is exact for the query it holds)
+// literal-slot values of the last query compile_query got that far with (per thread)
+thread_local std::vector<i128> tl_cq_lits;
+
 Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s,
                        const oob_i128* model_in, Pins& pins, bool fast = false) {
     Compiled out;
     QView v = view_of(b, q);
     out.nv = (uint32_t)v.nv;
     // per-thread scratch reused across queries (no allocation per query)
-    static thread_local std::vector<i128> dlo, dhi, lits;
+    static thread_local std::vector<i128> dlo, dhi;
+    std::vector<i128>& lits = tl_cq_lits;
     static thread_local StructCache cache;
     dlo.resize(v.nv);
     dhi.resize(v.nv);
@@ -2559,7 +2583,8 @@ inline bool device_regime(const Compiled& c) { return c.regime >= R_W64 && c.reg
 // device-bound; qcls[q] = class of a device query, 0 otherwise
 template <typename Other>
 void classify(std::vector<Compiled>& comp, int64_t n, const std::vector<std::shared_ptr<const Structure>>& pins,
-              std::vector<uint32_t>& qcls, Classes& K, Other other, std::vector<int32_t>* litsrc = nullptr) {
+              std::vector<uint32_t>& qcls, Classes& K, Other other, std::vector<int32_t>* litsrc = nullptr,
+              std::vector<uint32_t>* pin_cls = nullptr) {
     // distinct structure objects -> canonical class (word-for-word equality)
     size_t TB = 1024;
     while (TB < 2 * pins.size()) TB *= 2;
@@ -2638,6 +2663,10 @@ void classify(std::vector<Compiled>& comp, int64_t n, const std::vector<std::sha
     for (uint32_t i = 0; i < order.size(); i++) dense[order[i].second] = i;
     const uint32_t ncls = (uint32_t)order.size();
     K.ncls = ncls;
+    if (pin_cls) {  // the class of every pins entry (UINT32_MAX: no device query)
+        pin_cls->resize(pins.size());
+        for (size_t k = 0; k < pins.size(); k++) (*pin_cls)[k] = dense[slot_canon[slot_of(pins[k].get())]];
+    }
     const size_t W = 3 * (size_t)ncls;
     std::vector<uint32_t> cnt(nch * std::max<size_t>(W, 1), 0);
     parallel_for(nch, 1, [&](size_t c0, size_t c1) {
@@ -2733,8 +2762,16 @@ void cert_cache_put(std::vector<uint64_t>&& key, const std::vector<uint64_t>& va
     C.map[h].emplace_back(std::move(key), val);
     ++C.entries;
 }
+// the parameter scan's inputs gathered during compilation (Pins::note_lits)
+struct VaryInput {
+    const std::vector<std::vector<i128>>* first;
+    const std::vector<std::vector<uint8_t>>* vary;
+    const std::vector<uint8_t>* seen;
+    const std::vector<uint32_t>* cls;
+};
 void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const Classes& K,
-                 const std::vector<uint32_t>& qcls, std::vector<uint64_t>& certs, std::vector<uint32_t>& cert_off) {
+                 const std::vector<uint32_t>& qcls, std::vector<uint64_t>& certs, std::vector<uint32_t>& cert_off,
+                 const VaryInput* vin = nullptr) {
     const uint32_t ncls = K.ncls;
     // literal slots whose value varies inside the class (the parameters):
     // each query against its class's first member, in parallel over queries
@@ -2755,19 +2792,34 @@ void build_certs(const oob_batch* b, const std::vector<Compiled>& comp, const Cl
             vary[loff[c] + i].store(0, std::memory_order_relaxed);
         }
     }
-    for (int w = 0; w < 3; w++)
-        parallel_for(K.reg[w].size(), 4096, [&](size_t lo, size_t hi) {
-            for (size_t k = lo; k < hi; k++) {
-                const int64_t q = K.reg[w][k];
-                const uint32_t c = qcls[q];
-                const Structure& sk = *comp[q].st;
-                for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
-                    std::atomic<uint8_t>& f = vary[loff[c] + i];
-                    if (!f.load(std::memory_order_relaxed) && lit_value(b, q, sk, i) != v0[loff[c] + i])
-                        f.store(1, std::memory_order_relaxed);
+    if (vin) {
+        // from the compile pass: a slot varies in a class if it varied within
+        // one of the class's pinned structures (per compile chunk) or two of
+        // them started with different values
+        for (size_t k = 0; k < vin->seen->size(); k++) {
+            const uint32_t c = (*vin->cls)[k];
+            if (!(*vin->seen)[k] || c >= ncls) continue;
+            const std::vector<i128>& f = (*vin->first)[k];
+            const std::vector<uint8_t>& y = (*vin->vary)[k];
+            const uint32_t ns = std::min<uint32_t>(loff[c + 1] - loff[c], (uint32_t)f.size());
+            for (uint32_t i = 0; i < ns; i++)
+                if (y[i] || f[i] != v0[loff[c] + i]) vary[loff[c] + i].store(1, std::memory_order_relaxed);
+        }
+    } else {
+        for (int w = 0; w < 3; w++)
+            parallel_for(K.reg[w].size(), 4096, [&](size_t lo, size_t hi) {
+                for (size_t k = lo; k < hi; k++) {
+                    const int64_t q = K.reg[w][k];
+                    const uint32_t c = qcls[q];
+                    const Structure& sk = *comp[q].st;
+                    for (uint32_t i = 0; i < loff[c + 1] - loff[c]; i++) {
+                        std::atomic<uint8_t>& f = vary[loff[c] + i];
+                        if (!f.load(std::memory_order_relaxed) && lit_value(b, q, sk, i) != v0[loff[c] + i])
+                            f.store(1, std::memory_order_relaxed);
+                    }
                 }
-            }
-        });
+            });
+    }
     std::vector<std::vector<uint64_t>> per(ncls);
     parallel_for(ncls, 1, [&](size_t lo, size_t hi) {
         static thread_local std::unique_ptr<sym::Store> S;
@@ -2887,6 +2939,12 @@ struct Prepared {
     uint64_t raw_nv = 0, raw_nl = 0;
     std::vector<int32_t> litsrc;  // literal-slot sources of every structure (Compiled::lsrc)
     std::vector<std::shared_ptr<const Structure>> pins;  // every structure comp[] points to
+    // fast mode, per pins entry (Pins::note_lits): first literal-slot values,
+    // varying slots, whether a device query was seen; the class of each entry
+    std::vector<std::vector<i128>> pin_first;
+    std::vector<std::vector<uint8_t>> pin_vary;
+    std::vector<uint8_t> pin_seen;
+    std::vector<uint32_t> pin_cls;
     Classes classes;
     std::vector<uint32_t> qcls;  // comp[q].cls, compact
     std::vector<uint64_t> certs;     // fast mode: Unsat certificates (cert.cuh)
@@ -2911,6 +2969,9 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     if ((int64_t)comp.size() != n) comp.resize(n);  // every entry is overwritten below (recycled storage)
     const bool fast_shortcut = mode == MODE_SOLVE && (opt.flags & OOB_F_FAST);
     pr.pins.clear();
+    pr.pin_first.clear();
+    pr.pin_vary.clear();
+    pr.pin_seen.clear();
     // device-side records (SOLVE): the compile pass also copies each chunk's
     // raw domains and literals into page-locked arrays (one H2D per call
     // instead of ~2x their size in regime-width records filled on the host)
@@ -2941,6 +3002,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         Phase ph("validate+compile");
         std::atomic<int64_t> bad{INT64_MAX};
         std::mutex pins_mu;
+        std::unordered_map<const Structure*, size_t> pin_at;  // structure -> its pins entry
         parallel_for((size_t)n, 256, [&](size_t lo, size_t hi) {
             Pins pins;
             bool valid = true;
@@ -2953,6 +3015,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
                     break;
                 }
                 comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, pins, fast_shortcut);
+                if (fast_shortcut && device_regime(comp[q])) pins.note_lits(tl_cq_lits, comp[q].nlit);
             }
             if (valid && pr.raw) {  // this chunk's raw values (contiguous: offsets validated)
                 const int64_t va = b->var_begin[lo], vz = b->var_begin[hi];
@@ -2964,7 +3027,31 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
                 if (lz > la) std::memcpy(pr.raw_l.data() + (la - pr.raw_l0), b->lits + la, (size_t)(lz - la) * 16);
             }
             std::lock_guard<std::mutex> lk(pins_mu);
-            for (auto& p : pins.v) pr.pins.push_back(std::move(p));
+            for (size_t k = 0; k < pins.v.size(); k++) {
+                // one parameter-scan entry per distinct structure: merge this chunk's
+                const Structure* sp = pins.v[k].get();
+                auto it = pin_at.find(sp);
+                if (it == pin_at.end()) {
+                    pin_at.emplace(sp, pr.pins.size());
+                    pr.pins.push_back(std::move(pins.v[k]));
+                    pr.pin_first.push_back(std::move(pins.first[k]));
+                    pr.pin_vary.push_back(std::move(pins.vary[k]));
+                    pr.pin_seen.push_back(pins.seen[k]);
+                    continue;
+                }
+                if (!pins.seen[k]) continue;
+                const size_t g = it->second;
+                if (!pr.pin_seen[g]) {
+                    pr.pin_seen[g] = 1;
+                    pr.pin_first[g] = std::move(pins.first[k]);
+                    pr.pin_vary[g] = std::move(pins.vary[k]);
+                    continue;
+                }
+                const std::vector<i128>& f = pins.first[k];
+                std::vector<uint8_t>& y = pr.pin_vary[g];
+                for (size_t i = 0; i < f.size() && i < y.size(); i++)
+                    y[i] |= pins.vary[k][i] | (f[i] != pr.pin_first[g][i]);
+            }
         });
         if (bad.load() != INT64_MAX) {
             int64_t q = bad.load();
@@ -2996,7 +3083,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
                 while (q < cur && !range_q.compare_exchange_weak(cur, q)) {
                 }
             }
-        }, pr.raw ? &pr.litsrc : nullptr);
+        }, pr.raw ? &pr.litsrc : nullptr, &pr.pin_cls);
         if (range_q.load() != INT64_MAX)
             pr.range_msg = "query " + std::to_string(range_q.load()) + ": " + comp[range_q.load()].why;
     }
@@ -3012,7 +3099,8 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
     pr.cert_off.clear();
     if (mode == MODE_SOLVE && (opt.flags & OOB_F_FAST) && opt.timeout_s > 0) {
         Phase ph_cert("certify");
-        build_certs(b, comp, K, pr.qcls, pr.certs, pr.cert_off);
+        const VaryInput vin{&pr.pin_first, &pr.pin_vary, &pr.pin_seen, &pr.pin_cls};
+        build_certs(b, comp, K, pr.qcls, pr.certs, pr.cert_off, fast_shortcut ? &vin : nullptr);
     }
     if (n_dev_q > 0) {
         pr.work.resize(want);
