@@ -169,7 +169,7 @@ static i128 from_w(oob_i128 w) { return (i128)(((unsigned __int128)(uint64_t)w.h
 // ============================================================================
 namespace {
 
-enum Regime : int8_t { R_IMMEDIATE = 0, R_W64 = 1, R_W128 = 2, R_W256 = 3, R_RANGE = 4 };
+enum Regime : int8_t { R_IMMEDIATE = 0, R_W64 = 1, R_W128 = 2, R_W256 = 3, R_RANGE = 4, R_INVALID = 5 };
 
 struct QView {
     int nv, ncon, nn, nl;
@@ -199,12 +199,10 @@ QView view_of(const oob_batch* b, int64_t q) {
     return v;
 }
 
-std::string validate(const oob_batch* b, int64_t q) {
-    if (b->var_begin[q + 1] < b->var_begin[q] || b->con_begin[q + 1] < b->con_begin[q] ||
-        b->node_begin[q + 1] < b->node_begin[q] || b->lit_begin[q + 1] < b->lit_begin[q])
-        return "decreasing offsets";
-    QView v = view_of(b, q);
-    if (v.nv > 65535 || v.ncon > 65535) return "more than 65535 variables or constraints";
+// the checks on the query's terms and constraints (validate); the compile
+// pass runs them only for a query whose terms are not word-for-word those of
+// an already validated query (StructCache)
+std::string validate_terms(const QView& v) {
     for (int i = 0; i < v.nn; i++) {
         int op = v.op[i];
         if (op > OOB_NODE_MOD) return "unknown operator code " + std::to_string(op);
@@ -219,6 +217,19 @@ std::string validate(const oob_batch* b, int64_t q) {
             return "constraint root out of range";
     }
     return "";
+}
+// the checks on the query's offsets and sizes (validate)
+const char* validate_offsets(const oob_batch* b, int64_t q) {
+    if (b->var_begin[q + 1] < b->var_begin[q] || b->con_begin[q + 1] < b->con_begin[q] ||
+        b->node_begin[q + 1] < b->node_begin[q] || b->lit_begin[q + 1] < b->lit_begin[q])
+        return "decreasing offsets";
+    if (b->var_begin[q + 1] - b->var_begin[q] > 65535 || b->con_begin[q + 1] - b->con_begin[q] > 65535)
+        return "more than 65535 variables or constraints";
+    return nullptr;
+}
+std::string validate(const oob_batch* b, int64_t q) {
+    if (const char* e = validate_offsets(b, q)) return e;
+    return validate_terms(view_of(b, q));
 }
 
 // structural equality of two input terms (dataclass equality in the reference)
@@ -891,7 +902,7 @@ struct StructCache {
     };
     std::unordered_multimap<uint64_t, Entry> map;
 
-    static uint64_t fingerprint(const QView& v, int mode, std::vector<uint8_t>& divok, bool& cacheable) {
+    static uint64_t fingerprint(const QView& v, int mode, std::vector<uint8_t>& divok, bool& cacheable, bool& bad) {
         uint64_t h = 1469598103934665603ull ^ ((uint64_t)mode << 56) ^ ((uint64_t)v.nv << 40) ^
                      ((uint64_t)v.ncon << 20) ^ (uint64_t)v.nn;
         auto mix = [&](uint64_t x) {
@@ -900,12 +911,24 @@ struct StructCache {
         };
         divok.clear();
         cacheable = true;
+        bad = false;
         for (int i = 0; i < v.nn; i++) {
             mix((uint64_t)v.op[i] | ((uint64_t)(uint32_t)v.na[i] << 8) | ((uint64_t)(uint32_t)v.nb[i] << 36));
             if (v.op[i] == OOB_NODE_DIV || v.op[i] == OOB_NODE_MOD) {
-                int r = v.nb[i];
-                if (v.op[r] == OOB_NODE_LIT) divok.push_back(from_w(v.lits[v.na[r]]) >= 1);
-                else cacheable = false;
+                const int r = v.nb[i];
+                if (r < 0 || r >= i) {  // (not yet validated: invalid indices are not followed)
+                    bad = true;
+                    continue;
+                }
+                if (v.op[r] == OOB_NODE_LIT) {
+                    if (v.na[r] < 0 || v.na[r] >= v.nl) {
+                        bad = true;
+                        continue;
+                    }
+                    divok.push_back(from_w(v.lits[v.na[r]]) >= 1);
+                } else {
+                    cacheable = false;
+                }
             }
         }
         for (int k = 0; k < v.ncon; k++) mix((uint64_t)v.rel[k] | ((uint64_t)(uint32_t)v.lhs[k] << 8) |
@@ -920,14 +943,22 @@ struct StructCache {
                std::memcmp(e.lhs.data(), v.lhs, v.ncon * 4) == 0 &&
                std::memcmp(e.rhs.data(), v.rhs, v.ncon * 4) == 0 && e.divok == divok;
     }
+    // null: the query's terms are invalid (validate_terms).  A query equal
+    // word for word to a cached one is valid like it: only the others are
+    // checked here
     const Structure* get(const QView& v, int mode, Pins& pins) {
         static thread_local std::vector<uint8_t> divok;
-        bool cacheable;
-        uint64_t h = fingerprint(v, mode, divok, cacheable);
-        if (!cacheable) return pins.add(build_structure(v, mode));
+        bool cacheable, bad;
+        uint64_t h = fingerprint(v, mode, divok, cacheable, bad);
+        if (bad) return nullptr;
+        if (!cacheable) {
+            if (!validate_terms(v).empty()) return nullptr;
+            return pins.add(build_structure(v, mode));
+        }
         auto range = map.equal_range(h);
         for (auto it = range.first; it != range.second; ++it)
             if (same(it->second, v, mode, divok)) return pins.add(it->second.st);
+        if (!validate_terms(v).empty()) return nullptr;
         std::shared_ptr<const Structure> st = build_structure(v, mode);
         pins.add(st);
         if (map.size() > 4096) map.clear();  // bounded
@@ -986,11 +1017,19 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
             out.cost += hi64 ? 128 - __builtin_clzll(hi64) : (lo64 ? 64 - __builtin_clzll(lo64) : 0);
         }
     }
-    if (mode == MODE_SOLVE) {
-        if (empty) { out.immediate = OOB_UNSAT; return out; }          // solver.py:374-375
-        if (!(timeout_s > 0)) { out.immediate = OOB_TIMEOUT; return out; }  // deadline passed (:391)
+    if (mode == MODE_SOLVE && (empty || !(timeout_s > 0))) {
+        if (!validate_terms(v).empty()) {  // (the structure cache is not consulted on this path)
+            out.regime = R_INVALID;
+            return out;
+        }
+        out.immediate = empty ? OOB_UNSAT : OOB_TIMEOUT;  // solver.py:374-375 / deadline passed (:391)
+        return out;
     }
     out.st = cache.get(v, mode, pins);
+    if (!out.st) {  // invalid terms (the caller reports validate()'s message)
+        out.regime = R_INVALID;
+        return out;
+    }
     const Structure& st = *out.st;
     out.ncon = st.ncon;
     out.ncode = st.ncode;
@@ -3007,14 +3046,17 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
             Pins pins;
             bool valid = true;
             for (size_t q = lo; q < hi; q++) {
-                if (!validate(b, (int64_t)q).empty()) {
+                // offsets here; the terms inside compile_query, only for terms
+                // not already validated in an equal query (StructCache::get)
+                if (validate_offsets(b, (int64_t)q) ||
+                    (comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, pins, fast_shortcut))
+                            .regime == R_INVALID) {
                     int64_t cur = bad.load();
                     while ((int64_t)q < cur && !bad.compare_exchange_weak(cur, (int64_t)q)) {
                     }
                     valid = false;
                     break;
                 }
-                comp[q] = compile_query(b, (int64_t)q, mode, opt.timeout_s, model_in, pins, fast_shortcut);
                 if (fast_shortcut && device_regime(comp[q])) pins.note_lits(tl_cq_lits, comp[q].nlit);
             }
             if (valid && pr.raw) {  // this chunk's raw values (contiguous: offsets validated)
