@@ -13,7 +13,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
 fb = synth.generate(cfg, n, names=False)
 base = None
-for hn in (0, 48, 96, 192, -1):
+for hn in [int(x) for x in os.environ.get("HN", "0,48,96,192,-1").split(",")]:
     p = _lib.Plan(fb, 30.0, flags=_lib.F_FAST, heavy_nodes=hn)
     ms = sorted(p.run() for _ in range(7))
     r = p.results()
