@@ -1240,7 +1240,7 @@ struct RunCtx {
     // input literals at their batch offsets minus raw_v0 / raw_l0, and the
     // literal-slot sources of every structure the call uses
     bool raw = false;
-    const oob_i128 *raw_vlo = nullptr, *raw_vhi = nullptr, *raw_l = nullptr;
+    const int64_t *raw_vlo = nullptr, *raw_vhi = nullptr, *raw_l = nullptr;  // int64 (the call's values fit)
     uint64_t raw_nv = 0, raw_nl = 0;
     int64_t raw_v0 = 0, raw_l0 = 0;
     const std::vector<int32_t>* litsrc = nullptr;
@@ -2075,15 +2075,15 @@ std::string upload_raw(const RunCtx& rc, DevGroup& G) {
     if (!R) return "device-side records: no pool for the raw values";
     std::string e = ensure_stream(R, G.dev);
     if (!e.empty()) return e;
-    CK(R->raw_vlo.ensure(std::max<uint64_t>(rc.raw_nv, 1) * 16));
-    CK(R->raw_vhi.ensure(std::max<uint64_t>(rc.raw_nv, 1) * 16));
-    CK(R->raw_l.ensure(std::max<uint64_t>(rc.raw_nl, 1) * 16));
+    CK(R->raw_vlo.ensure(std::max<uint64_t>(rc.raw_nv, 1) * 8));
+    CK(R->raw_vhi.ensure(std::max<uint64_t>(rc.raw_nv, 1) * 8));
+    CK(R->raw_l.ensure(std::max<uint64_t>(rc.raw_nl, 1) * 8));
     CK(R->litsrc.ensure(std::max<size_t>(rc.litsrc->size(), 1) * 4));
     if (rc.raw_nv) {
-        CK(cudaMemcpyAsync(R->raw_vlo.p, rc.raw_vlo, rc.raw_nv * 16, cudaMemcpyHostToDevice, R->stream));
-        CK(cudaMemcpyAsync(R->raw_vhi.p, rc.raw_vhi, rc.raw_nv * 16, cudaMemcpyHostToDevice, R->stream));
+        CK(cudaMemcpyAsync(R->raw_vlo.p, rc.raw_vlo, rc.raw_nv * 8, cudaMemcpyHostToDevice, R->stream));
+        CK(cudaMemcpyAsync(R->raw_vhi.p, rc.raw_vhi, rc.raw_nv * 8, cudaMemcpyHostToDevice, R->stream));
     }
-    if (rc.raw_nl) CK(cudaMemcpyAsync(R->raw_l.p, rc.raw_l, rc.raw_nl * 16, cudaMemcpyHostToDevice, R->stream));
+    if (rc.raw_nl) CK(cudaMemcpyAsync(R->raw_l.p, rc.raw_l, rc.raw_nl * 8, cudaMemcpyHostToDevice, R->stream));
     if (!rc.litsrc->empty())
         CK(cudaMemcpyAsync(R->litsrc.p, rc.litsrc->data(), rc.litsrc->size() * 4, cudaMemcpyHostToDevice, R->stream));
     CK(cudaEventRecord(R->evraw, R->stream));
@@ -2973,7 +2973,7 @@ struct Prepared {
     // SOLVE: the caller's raw domains and literals in page-locked memory,
     // copied by the compile pass (device-side records, RunCtx::raw)
     bool raw = false;
-    HostArr<oob_i128> raw_vlo, raw_vhi, raw_l;
+    HostArr<int64_t> raw_vlo, raw_vhi, raw_l;  // narrowed to int64 (else no device-side records)
     int64_t raw_v0 = 0, raw_l0 = 0;
     uint64_t raw_nv = 0, raw_nl = 0;
     std::vector<int32_t> litsrc;  // literal-slot sources of every structure (Compiled::lsrc)
@@ -3040,6 +3040,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
         // reported (nothing is decided for an invalid batch)
         Phase ph("validate+compile");
         std::atomic<int64_t> bad{INT64_MAX};
+        std::atomic<bool> raw_wide{false};  // a raw value beyond int64: the records are filled on the host
         std::mutex pins_mu;
         std::unordered_map<const Structure*, size_t> pin_at;  // structure -> its pins entry
         parallel_for((size_t)n, 256, [&](size_t lo, size_t hi) {
@@ -3059,14 +3060,21 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
                 }
                 if (fast_shortcut && device_regime(comp[q])) pins.note_lits(tl_cq_lits, comp[q].nlit);
             }
-            if (valid && pr.raw) {  // this chunk's raw values (contiguous: offsets validated)
+            if (valid && pr.raw) {  // this chunk's raw values (contiguous: offsets validated), as int64
                 const int64_t va = b->var_begin[lo], vz = b->var_begin[hi];
                 const int64_t la = b->lit_begin[lo], lz = b->lit_begin[hi];
-                if (vz > va) {
-                    std::memcpy(pr.raw_vlo.data() + (va - pr.raw_v0), b->var_lo + va, (size_t)(vz - va) * 16);
-                    std::memcpy(pr.raw_vhi.data() + (va - pr.raw_v0), b->var_hi + va, (size_t)(vz - va) * 16);
-                }
-                if (lz > la) std::memcpy(pr.raw_l.data() + (la - pr.raw_l0), b->lits + la, (size_t)(lz - la) * 16);
+                bool fits = true;
+                auto narrow = [&](int64_t* dst, const oob_i128* src, int64_t k) {
+                    for (int64_t i = 0; i < k; i++) {
+                        const int64_t w = (int64_t)src[i].lo;
+                        fits &= src[i].hi == (w >> 63);
+                        dst[i] = w;
+                    }
+                };
+                narrow(pr.raw_vlo.data() + (va - pr.raw_v0), b->var_lo + va, vz - va);
+                narrow(pr.raw_vhi.data() + (va - pr.raw_v0), b->var_hi + va, vz - va);
+                narrow(pr.raw_l.data() + (la - pr.raw_l0), b->lits + la, lz - la);
+                if (!fits) raw_wide.store(true, std::memory_order_relaxed);
             }
             std::lock_guard<std::mutex> lk(pins_mu);
             for (size_t k = 0; k < pins.v.size(); k++) {
@@ -3099,6 +3107,7 @@ int prepare(const oob_batch* b, const oob_options* opt_in, int mode, const oob_i
             int64_t q = bad.load();
             return fail(OOB_E_INVALID, "query " + std::to_string(q) + ": " + validate(b, q));
         }
+        if (raw_wide.load()) pr.raw = false;  // (values beyond int64: records filled on the host)
     }
     pr.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (gate_point() == GATE_COMPILE) gate_release();
@@ -3711,7 +3720,7 @@ int oob_plan_info(const oob_plan* p, int64_t info[9]) {
     int64_t nq = 0, rec = 0, res = 0, cls = 0, wide = 0, jobs = 0, launches = 0, h2d = 0;
     for (auto& G : p->groups) {
         if (p->rc.raw)  // the raw values and literal sources, once per device
-            h2d += (int64_t)(p->rc.raw_nv * 2 + p->rc.raw_nl) * 16 + (int64_t)p->rc.litsrc->size() * 4;
+            h2d += (int64_t)(p->rc.raw_nv * 2 + p->rc.raw_nl) * 8 + (int64_t)p->rc.litsrc->size() * 4;
         for (int w = 0; w < NJOBS; w++) {
             const DevJob& j = G.job[w];
             if (!present(j)) continue;

@@ -246,13 +246,13 @@ __global__ void __launch_bounds__(128) oob_cert_kernel(LaunchArgs a, uint32_t k0
 
 // Device-side records (SOLVE): every own entry's domains and literal slots,
 // written in its job's width (VW int64 words per value: 1 int64, 2 int128,
-// 4 256-bit, sign-extended) from the caller's raw int128 values uploaded once
-// per call; the host only writes the entry's offsets {raw var offset, raw
-// literal offset, literal-source table offset} (shadows: UINT32_MAX).  One
-// thread per entry; the record's padding is zeroed as the host did.
+// 4 256-bit, sign-extended) from the caller's raw values, narrowed to int64
+// by the host (a call with a value beyond int64 keeps the host fill) and
+// uploaded once per call; the host only writes the entry's offsets {raw var
+// offset, raw literal offset, literal-source table offset} (shadows:
+// UINT32_MAX).  One thread per entry; the padding is zeroed as the host did.
 struct RawWord {
-    uint64_t lo;
-    int64_t hi;
+    int64_t v;
 };
 template <int VW>
 __global__ void __launch_bounds__(256) oob_expand_kernel(const QDesc* __restrict__ qd, uint32_t n,
@@ -268,24 +268,19 @@ __global__ void __launch_bounds__(256) oob_expand_kernel(const QDesc* __restrict
         const QDesc d = qd[i];
         const uint32_t nv = d.nv_ncon & 0xFFFFu, nlit = d.ncode_nlit >> 16;
         int64_t* out = data + d.data_off;
-        auto put = [&](uint64_t lo, int64_t hi) {
-            out[0] = (int64_t)lo;
-            if (VW >= 2) out[1] = hi;
-            if (VW == 4) out[2] = out[3] = hi < 0 ? -1 : 0;
+        auto put = [&](int64_t x) {
+            out[0] = x;
+            if (VW >= 2) out[1] = x < 0 ? -1 : 0;
+            if (VW == 4) out[2] = out[3] = x < 0 ? -1 : 0;
             out += VW;
         };
         for (uint32_t v = 0; v < nv; v++) {
-            const RawWord a = vlo[ro.x + v], b = vhi[ro.x + v];
-            put(a.lo, a.hi);
-            put(b.lo, b.hi);
+            put(vlo[ro.x + v].v);
+            put(vhi[ro.x + v].v);
         }
         for (uint32_t s = 0; s < nlit; s++) {
             const int32_t src = litsrc[ro.z + s];
-            if (src < 0) put(1, 0);
-            else {
-                const RawWord l = lits[ro.y + src];
-                put(l.lo, l.hi);
-            }
+            put(src < 0 ? 1 : lits[ro.y + src].v);
         }
         const uint64_t words = (uint64_t)(2 * nv + nlit) * VW;
         const uint64_t dsz = (words + align - 1) / align * align;
