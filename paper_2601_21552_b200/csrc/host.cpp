@@ -723,9 +723,11 @@ i128 prove_bound(const uint32_t* code, size_t n, const std::vector<std::pair<uin
 // 128-bit proof overflows): |x + y| <= |x| + |y|, |x * y| <= |x||y|,
 // |tdiv(a, d)| <= |a|, |a % d| <= min(|a|, |d|); targets as in prove_bound.
 // Relative rounding error is far below the 2^250 vs 2^255 margin.
+// stop: return as soon as the bound exceeds it (the value is then a lower
+// bound of the full one, above `stop`)
 double prove_bound_mag(const uint32_t* code, size_t n, const std::vector<std::pair<uint32_t, uint32_t>>& cons,
                        const std::vector<uint8_t>& rels, const std::vector<i128>& dlo, const std::vector<i128>& dhi,
-                       const std::vector<i128>& lits) {
+                       const std::vector<i128>& lits, double stop = HUGE_VAL) {
     auto mag = [](i128 v) -> double {
         if (v == (int64_t)v) return std::fabs((double)(int64_t)v);  // one conversion in the common case
         return (double)(v < 0 ? -(long double)v : (long double)v);
@@ -747,6 +749,7 @@ double prove_bound_mag(const uint32_t* code, size_t n, const std::vector<std::pa
             else m[j] = std::min(m[L], m[R]);
         }
         B = std::max(B, m[j]);
+        if (B > stop) return B;
     }
     const double INF_D = 1e18;
     // targets: one reverse sweep (every node has one parent; prove_bound);
@@ -763,6 +766,7 @@ double prove_bound_mag(const uint32_t* code, size_t n, const std::vector<std::pa
         const double T = tg[i];
         if (T < 0) continue;
         B = std::max(B, T);
+        if (B > stop) return B;
         uint32_t op = w_op(code[i]);
         if (op < NODE_ADD) continue;
         uint32_t R = (uint32_t)i - 1, L = R - size_of(R);
@@ -1065,7 +1069,9 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
     // error over < 2^14 operations is below 1e-12 relative, so a value under
     // 9.2e18 (I64MAX = 9.223e18) proves the int64 regime.  Otherwise the exact
     // checked 128-bit proof decides.
-    const double mag = prove_bound_mag(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits);
+    // (fast mode: only whether the bound stays under 9.2e18 matters before the
+    // int128 shortcut, so its computation stops as soon as it does not)
+    double mag = prove_bound_mag(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits, fast ? 9.2e18 : HUGE_VAL);
     if (mag < 9.2e18 && Dmax <= D64MAX) {
         out.regime = R_W64;
         return out;
@@ -1074,6 +1080,7 @@ Compiled compile_query(const oob_batch* b, int64_t q, int mode, double timeout_s
         out.regime = R_W128;
         return out;
     }
+    if (fast && mag >= 9.2e18) mag = prove_bound_mag(st.code(), st.ncode, st.roots, st.rels, dlo, dhi, lits);
     // (fast mode: a magnitude bound beyond 2^127 goes to the 256-bit regime
     // without the exact proof -- on C3 the proof admits 14 of 14 000 such
     // queries to int128; a scheduling choice, every regime is exact)
