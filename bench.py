@@ -172,8 +172,46 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.samples = []
+        self.source = "nvidia-smi"
         self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:  # NVML in-process: ~1 ms per sample, so a timed region of a few
+            # ms steps still gets many samples (nvidia-smi takes ~50 ms each)
+            import pynvml
+            pynvml.nvmlInit()
+            idx = device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                ids = [v.strip() for v in vis.split(",") if v.strip()]
+                if device < len(ids) and ids[device].isdigit():
+                    idx = int(ids[device])
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx))
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+        self._t = threading.Thread(target=self._run_nvml if self._nvml else self._run, daemon=True)
+
+    def _nvml_sample(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        self.samples.append([str(sm), str(mx), hex(r)] + ["Active" if r & b else "Not Active" for b in bits])
+
+    def _run_nvml(self):
+        while not self._stop.is_set():
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
+            self._stop.wait(0.001)
+        try:  # at least one sample even for a region shorter than one period
+            if not self.samples:
+                self._nvml_sample()
+        except Exception:
+            pass
 
     def _run(self):
         while not self._stop.is_set():
@@ -205,7 +243,8 @@ class ClockSampler:
         reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7]) if v == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(self.samples), "reasons": reasons}
+                "sm_mhz_min": min(sm) if sm else None,
+                "samples": len(self.samples), "source": self.source, "reasons": reasons}
 
 
 def flush_l2(torch_mod, device):
