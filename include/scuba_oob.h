@@ -135,7 +135,7 @@ enum {
                             compiled class kernels; testing) */
     OOB_F_NO_X32 = 8,    /* keep int64-regime queries in int64 (no x32
                             demotion after the root phase; testing) */
-    OOB_F_FAST = 16      /* fast mode: heavy queries first meet a symbolic
+    OOB_F_FAST = 16,     /* fast mode: heavy queries first meet a symbolic
                             Unsat prover (sound: a refuted query has no
                             integer solution in its root box, so the reference
                             can never return Sat on it); what it does not
@@ -143,6 +143,13 @@ enum {
                             and Sat models are the reference's; nodes/passes
                             of refuted queries are 0 (not the reference's
                             counters).  DESIGN.md section 4.9. */
+    OOB_F_CHAIN = 32     /* with OOB_F_FAST: the int64 job's open entries first
+                            run a warp-per-query search with warp-parallel
+                            (Jacobi) propagation (chain.cuh); verdicts, Sat
+                            models and node counts stay the reference's, pass
+                            counts of the entries it decides are its rounds.
+                            Opt-in: slower than the exact emulation on the
+                            benchmark batches. */
 };
 
 /* Results (caller-allocated; optional arrays may be NULL). */

@@ -28,6 +28,7 @@ F_NO_DEMOTE = 2
 F_NO_JIT = 4
 F_NO_X32 = 8
 F_FAST = 16  # fast mode: symbolic Unsat prover in front of the exact emulation
+F_CHAIN = 32  # with F_FAST: warp-per-query search with warp-parallel propagation (opt-in)
 
 class EngineError(RuntimeError):
     """The GPU engine could not decide a batch (no device, capacity, range)."""

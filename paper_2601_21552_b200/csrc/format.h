@@ -185,6 +185,13 @@ struct LaunchArgs {
     uint32_t cert_nclasses;
     uint32_t cert_kmax;       // most certificates of any class of the job
     const uint64_t* certs;
+    // fast mode warp-per-query search of the int64 job's own entries
+    // (chain.cuh, before the root kernel): entries [0, chain_n), per-warp DFS
+    // frames, node and propagation-round budgets (beyond: the exact path)
+    uint32_t chain_n;
+    uint32_t chain_nodes;
+    uint32_t chain_rounds;
+    long long* chain_frames;
 };
 
 enum { MODE_SOLVE = 0, MODE_PROPAGATE = 1, MODE_CHECK = 2 };

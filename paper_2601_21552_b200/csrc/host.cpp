@@ -47,6 +47,7 @@ namespace oob {
 cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks, cudaStream_t s);
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
 cudaError_t launch_cert(const LaunchArgs& a, int wide, uint32_t k0, uint32_t k1, int sms, cudaStream_t s);
+cudaError_t launch_chain(const LaunchArgs& a, int blocks, cudaStream_t s);
 cudaError_t grow_smem_limit(const void* fn, size_t smem);
 cudaError_t launch_expand(int wide, const QDesc* qd, uint32_t n, const void* rawoff, const void* vlo, const void* vhi,
                           const void* lits, const int32_t* litsrc, int64_t* data, int sms, cudaStream_t s);
@@ -1120,6 +1121,27 @@ struct DevBuf {
     void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
 };
 
+// fast-mode warp-per-query search (chain.cuh): grid, per-warp frame words
+// (chain::DEPTH frames of chain::MAXV domain pairs), budgets
+constexpr int CHAIN_WARPS = 4;
+constexpr size_t CHAIN_FRAME_WORDS = (size_t)64 * 2 * 64;
+int chain_blocks(int sms) { return sms * 4; }
+struct ChainCfg {
+    bool on = false;
+    uint32_t nodes = 512, rounds = 4096;
+};
+const ChainCfg& chain_cfg() {
+    static const ChainCfg c = [] {
+        ChainCfg r;
+        const char* e = std::getenv("SCUBA_OOB_CHAIN");
+        if (e && *e == '1') r.on = true;
+        if ((e = std::getenv("SCUBA_OOB_CHAIN_NODES")) && *e) r.nodes = (uint32_t)std::max(1, std::atoi(e));
+        if ((e = std::getenv("SCUBA_OOB_CHAIN_ROUNDS")) && *e) r.rounds = (uint32_t)std::max(1, std::atoi(e));
+        return r;
+    }();
+    return c;
+}
+
 struct DevicePool {
     std::mutex mu;
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
@@ -1132,6 +1154,7 @@ struct DevicePool {
     DevBuf handoff;                  // root states of queries handed off at their root
     DevBuf raw_vlo, raw_vhi, raw_l, litsrc;  // SOLVE: the call's raw values (device-side records)
     DevBuf rawoff;                   // per entry: raw var / literal offsets, literal-source table offset
+    DevBuf chain;                    // fast mode: DFS frames of the warp-per-query search (chain.cuh)
     std::vector<cudaStream_t> xs;  // extra streams (one per compiled-class kernel)
     std::vector<cudaEvent_t> xev;
     cudaStream_t stream = nullptr;
@@ -1142,7 +1165,7 @@ struct DevicePool {
                           &elapsed, &err, &classes, &class_next, &class_init, &warp_class, &heavy_count, &heavy_list,
                           &heavy_t0, &fr_region, &resume, &resume_init, &slot64, &slot128, &slotx32, &timeline,
                           &classes_interp, &stats, &certs, &satcnt, &satoff, &compact, &fr_map, &slab_map, &handoff,
-                          &raw_vlo, &raw_vhi, &raw_l, &litsrc, &rawoff})
+                          &raw_vlo, &raw_vhi, &raw_l, &litsrc, &rawoff, &chain})
             b->release();
     }
 };
@@ -1972,6 +1995,23 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
         a.certs = (const uint64_t*)P->certs.p;
         a.cert_classes = (const ClassDesc*)P->classes.p;
     }
+    // fast mode with OOB_F_CHAIN (or SCUBA_OOB_CHAIN=1): the int64 job's own
+    // entries first meet the warp-per-query search with warp-parallel
+    // propagation (chain.cuh); SCUBA_OOB_CHAIN_NODES / _ROUNDS: its budgets
+    a.chain_n = 0;
+    a.chain_frames = nullptr;
+    if (fast && rc.mode == MODE_SOLVE && j.wide == 0 && ((rc.opt.flags & OOB_F_CHAIN) || chain_cfg().on)) {
+        uint32_t own = 0;
+        while (own < n && !j.is_shadow[own]) ++own;
+        if (own > 0) {
+            const size_t warps = (size_t)chain_blocks(P->sms) * CHAIN_WARPS;
+            CK(P->chain.ensure(warps * CHAIN_FRAME_WORDS * 8));
+            a.chain_n = own;
+            a.chain_frames = (long long*)P->chain.p;
+            a.chain_nodes = chain_cfg().nodes;
+            a.chain_rounds = chain_cfg().rounds;
+        }
+    }
     a.heavy_count = (uint32_t*)P->heavy_count.p;
     a.heavy_next = (uint32_t*)P->heavy_count.p + 1;
     a.heavy_list = (uint32_t*)P->heavy_list.p + n;
@@ -2266,6 +2306,9 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
             CK(launch_cert(j.a, w, 0, 1, G.pool[w]->sms, G.pool[w]->stream));
             if (j.a.cert_kmax > 1) CK(launch_cert(j.a, w, 1, j.a.cert_kmax, G.pool[w]->sms, G.pool[w]->stream));
         }
+        // fast mode: the int64 job's open own entries, warp per query
+        if (present(G.job[0]) && G.job[0].a.chain_n)
+            CK(launch_chain(G.job[0].a, chain_blocks(G.pool[0]->sms), G.pool[0]->stream));
         // root phases, widest first: 256-bit -> int128 -> int64 -> x32
         for (int w = 2; w >= 0; w--) {
             if (!present(G.job[w])) continue;

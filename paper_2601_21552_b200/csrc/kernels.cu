@@ -26,6 +26,7 @@
 #include <cstdint>
 
 #include "cert.cuh"
+#include "chain.cuh"
 #include "engine.cuh"
 #include "format.h"
 #include "frontier.cuh"
@@ -400,6 +401,11 @@ cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t 
 
 // fast mode certificate check of job `wide` (0 int64, 1 int128, 2 256-bit)
 // certificates [k0, k1) of every entry: one thread per (entry, certificate)
+cudaError_t launch_chain(const LaunchArgs& a, int blocks, cudaStream_t s) {
+    oob_chain_kernel<<<blocks, chain::WARPS * 32, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_cert(const LaunchArgs& a, int wide, uint32_t k0, uint32_t k1, int sms, cudaStream_t s) {
     const uint64_t items = (uint64_t)a.n * (k1 - k0);
     const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((items + 127) / 128, (uint64_t)sms * 16));
