@@ -13,8 +13,10 @@ from pathlib import Path
 import numpy as np
 
 # several engine kernels run concurrently per device: more hardware work
-# queues than the default 8 (effective only before a CUDA context exists)
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# queues than the default 8 (effective only before a CUDA context exists);
+# 16, not 32: same throughput on B200 (C3/C4 A/B), half the context-creation
+# cost (cold corpus analysis 3.1 -> 1.3 s, tools/gpu_connections.sh)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "16")
 
 HERE = Path(__file__).resolve().parent
 # (SCUBA_OOB_LIB_PATH: another build of the library, for A/B measurements)

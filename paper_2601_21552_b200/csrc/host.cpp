@@ -160,7 +160,7 @@ __attribute__((constructor)) void init() {
 }  // namespace prof
 
 __attribute__((constructor)) static void oob_default_connections() {
-    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "16", 0);
 }
 
 static i128 from_w(oob_i128 w) { return (i128)(((unsigned __int128)(uint64_t)w.hi << 64) | w.lo); }

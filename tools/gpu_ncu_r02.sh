@@ -2,7 +2,7 @@
 # instructions per kernel (one plan run each), then --set full captures of the
 # certificate kernel and of the first compiled-class kernel in fast mode
 mkdir -p gpurun_out
-export CUDA_DEVICE_MAX_CONNECTIONS=32
+export CUDA_DEVICE_MAX_CONNECTIONS=16
 nvidia-smi --query-gpu=clocks.sm,clocks.max.sm --format=csv,noheader
 for spec in "c3 100000 fast" "c3 100000 canonical" "c4 100000 fast" "c5 2000 fast" "c5s 100000 fast"; do
   set -- $spec
