@@ -120,7 +120,8 @@ typedef struct {
     int32_t flags;        /* OOB_F_* below                                        */
     int32_t heavy_nodes;  /* DFS nodes after which a query moves to the warp-
                              cooperative frontier kernel; 0 = default (24;
-                             fast mode: SCUBA_OOB_FAST_HEAVY_NODES, 8),
+                             fast mode: 96, SCUBA_OOB_FAST_HEAVY_NODES; 8 with
+                             SCUBA_OOB_FAST_FRONTIER=1),
                              <0 = never (one lane per query throughout)      */
     int32_t jit_min;      /* structure classes with at least this many queries
                              in an int64 job run as run-time compiled kernels;
