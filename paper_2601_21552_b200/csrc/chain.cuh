@@ -538,3 +538,100 @@ __global__ void __launch_bounds__(chain::WARPS * 32) oob_chain_kernel(LaunchArgs
 }
 
 }  // namespace oob
+
+namespace oob {
+
+// Fast mode, K3: exhaustive enumeration of the small boxes.  An own entry of
+// the int64 job that no certificate refuted and whose declared box holds at
+// most a.enum_max points is enumerated point by point (lanes stride over the
+// mixed-radix point index; each lane evaluates every constraint exactly at
+// its point, _eval_exact / check_model :286-328, divisor side constraints
+// included).  The reference only ever answers Sat with a point of the box
+// that passes check_model (:405-407), so a box without such a point is the
+// reference's Unsat: decided here (nodes/passes 0, like a certificate
+// refutation).  The first satisfying point any lane meets (warp ballot) ends
+// the enumeration and leaves the entry to the exact emulation, which finds
+// the reference's first model.  int64 arithmetic is exact here: the job's
+// bound proof covers every value of the box.
+__global__ void __launch_bounds__(chain::WARPS * 32) oob_enum_kernel(LaunchArgs a) {
+    using namespace chain;
+    __shared__ ll s_lo[WARPS][MAXV];
+    __shared__ uint64_t s_size[WARPS][MAXV];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    const uint32_t nwarps = gridDim.x * WARPS;
+    // 32 consecutive entries per warp and step: each lane screens one (open,
+    // box within enum_max), then the warp enumerates the admitted ones
+    for (uint32_t base = (blockIdx.x * WARPS + wib) * 32u; base < a.enum_n; base += nwarps * 32u) {
+        const uint32_t qi = base + lane;
+        bool cand = false;
+        if (qi < a.enum_n && __ldcg(a.resume + qi) == 0u) {
+            const QDesc d = a.qdesc[qi];
+            const uint32_t nv = d.nv_ncon & 0xFFFFu;
+            if (nv > 0 && nv <= MAXV && (d.nv_ncon >> 16) > 0) {
+                const ll* src = reinterpret_cast<const ll*>(a.data + d.data_off);
+                uint64_t box = 1;
+                cand = true;
+                for (uint32_t v = 0; v < nv && cand; ++v) {
+                    const ll lo = src[2 * v], hi = src[2 * v + 1];
+                    const uint64_t sz = hi >= lo ? (uint64_t)hi - (uint64_t)lo + 1 : 0;
+                    if (sz == 0 || sz > a.enum_max || box * sz > a.enum_max) cand = false;
+                    else box *= sz;
+                }
+            }
+        }
+        uint32_t todo = __ballot_sync(0xFFFFFFFFu, cand);
+        while (todo) {
+            const uint32_t e = base + (uint32_t)(__ffs(todo) - 1);
+            todo &= todo - 1;
+            const QDesc d = a.qdesc[e];
+            Query q;
+            q.nv = d.nv_ncon & 0xFFFFu;
+            q.ncon = d.nv_ncon >> 16;
+            q.ncode = d.ncode_nlit & 0xFFFFu;
+            q.cons = a.code + d.code_off;
+            q.code = q.cons + q.ncon;
+            const ll* src = reinterpret_cast<const ll*>(a.data + d.data_off);
+            q.lit = src + 2 * q.nv;
+            uint64_t box = 1;
+            for (uint32_t v = lane; v < q.nv; v += 32) {
+                s_lo[wib][v] = src[2 * v];
+                s_size[wib][v] = (uint64_t)src[2 * v + 1] - (uint64_t)src[2 * v] + 1;
+            }
+            __syncwarp();
+            for (uint32_t v = 0; v < q.nv; ++v) box *= s_size[wib][v];
+            ll pt[MAXV];
+            Overlay ov;
+            ov.n = 0;
+            ov.full = false;
+            Ctx c{q, pt, pt, ov};
+            bool found = false;
+            for (uint64_t b0 = 0; b0 < box && !found; b0 += 32) {
+                const uint64_t idx = b0 + lane;
+                bool ok = false;
+                if (idx < box) {
+                    uint64_t r = idx;
+                    for (uint32_t v = 0; v < q.nv; ++v) {  // variable 0 varies slowest
+                        const uint32_t w = q.nv - 1 - v;
+                        const uint64_t sz = s_size[wib][w];
+                        pt[w] = s_lo[wib][w] + (ll)(r % sz);
+                        r /= sz;
+                    }
+                    ok = true;
+                    for (uint32_t k = 0; k < q.ncon && ok; ++k) ok = c.exact(k);
+                }
+                found = __any_sync(0xFFFFFFFFu, ok);
+            }
+            if (!found && lane == 0) {
+                a.verdict[e] = (int8_t)VERDICT_UNSAT;
+                a.err[e] = (int8_t)ERR_NONE;
+                a.nodes[e] = 0;
+                a.passes[e] = 0;
+                a.elapsed[e] = 0.f;
+                a.resume[e] = RES_SKIP;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace oob

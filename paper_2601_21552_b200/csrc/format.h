@@ -192,6 +192,10 @@ struct LaunchArgs {
     uint32_t chain_nodes;
     uint32_t chain_rounds;
     long long* chain_frames;
+    // fast mode K3 (chain.cuh oob_enum_kernel): entries [0, enum_n) whose
+    // declared box holds at most enum_max points are enumerated
+    uint32_t enum_n;
+    uint32_t enum_max;
 };
 
 enum { MODE_SOLVE = 0, MODE_PROPAGATE = 1, MODE_CHECK = 2 };

@@ -48,6 +48,7 @@ cudaError_t launch_solve(const LaunchArgs& a, int wide, int blocks, int fblocks,
 cudaError_t launch_root(const LaunchArgs& a, int wide, int blocks, cudaStream_t s);
 cudaError_t launch_cert(const LaunchArgs& a, int wide, uint32_t k0, uint32_t k1, int sms, cudaStream_t s);
 cudaError_t launch_chain(const LaunchArgs& a, int blocks, cudaStream_t s);
+cudaError_t launch_enum(const LaunchArgs& a, int blocks, cudaStream_t s);
 cudaError_t grow_smem_limit(const void* fn, size_t smem);
 cudaError_t launch_expand(int wide, const QDesc* qd, uint32_t n, const void* rawoff, const void* vlo, const void* vhi,
                           const void* lits, const int32_t* litsrc, int64_t* data, int sms, cudaStream_t s);
@@ -1142,6 +1143,14 @@ const ChainCfg& chain_cfg() {
     return c;
 }
 
+uint32_t enum_max_points() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("SCUBA_OOB_ENUM_MAX");
+        return (uint32_t)((e && *e) ? std::max(0, std::atoi(e)) : 4096);
+    }();
+    return v;
+}
+
 struct DevicePool {
     std::mutex mu;
     DevBuf qdesc, code, data, slabT, slabU, next, verdict, model, nodes, passes, elapsed, err;
@@ -2000,6 +2009,17 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     // propagation (chain.cuh); SCUBA_OOB_CHAIN_NODES / _ROUNDS: its budgets
     a.chain_n = 0;
     a.chain_frames = nullptr;
+    // fast mode, K3: the int64 job's own entries with small declared boxes are
+    // enumerated (chain.cuh oob_enum_kernel); SCUBA_OOB_ENUM_MAX points
+    // (default 4096, 0 = off)
+    a.enum_n = 0;
+    a.enum_max = 0;
+    if (fast && rc.mode == MODE_SOLVE && j.wide == 0 && enum_max_points() > 0) {
+        uint32_t own = 0;
+        while (own < n && !j.is_shadow[own]) ++own;
+        a.enum_n = own;
+        a.enum_max = enum_max_points();
+    }
     if (fast && rc.mode == MODE_SOLVE && j.wide == 0 && ((rc.opt.flags & OOB_F_CHAIN) || chain_cfg().on)) {
         uint32_t own = 0;
         while (own < n && !j.is_shadow[own]) ++own;
@@ -2280,7 +2300,7 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
         DevicePool* P = G.pool[w];
         const DevJob& j = G.job[w];
         const size_t n = j.qs.size();
-        CK(cudaMemsetAsync(P->next.p, 0, 4, s0));
+        CK(cudaMemsetAsync(P->next.p, 0, 4, s0));  // work cursor (aux kernel / opt-in chain search)
         CK(cudaMemcpyAsync(P->class_next.p, P->class_init.p, j.cls.size() * 4, cudaMemcpyDeviceToDevice, s0));
         CK(cudaMemsetAsync(P->heavy_count.p, 0, 32 * (1 + j.jit_cls.size()), s0));
         if (rc.mode == MODE_SOLVE) CK(cudaMemsetAsync(P->heavy_list.p, 0, n * 8, s0));
@@ -2306,7 +2326,10 @@ std::string launch_group(const RunCtx& rc, DevGroup& G) {
             CK(launch_cert(j.a, w, 0, 1, G.pool[w]->sms, G.pool[w]->stream));
             if (j.a.cert_kmax > 1) CK(launch_cert(j.a, w, 1, j.a.cert_kmax, G.pool[w]->sms, G.pool[w]->stream));
         }
-        // fast mode: the int64 job's open own entries, warp per query
+        // fast mode: the int64 job's small boxes (K3), then (opt-in) its
+        // open own entries, warp per query
+        if (present(G.job[0]) && G.job[0].a.enum_n)
+            CK(launch_enum(G.job[0].a, chain_blocks(G.pool[0]->sms), G.pool[0]->stream));
         if (present(G.job[0]) && G.job[0].a.chain_n)
             CK(launch_chain(G.job[0].a, chain_blocks(G.pool[0]->sms), G.pool[0]->stream));
         // root phases, widest first: 256-bit -> int128 -> int64 -> x32

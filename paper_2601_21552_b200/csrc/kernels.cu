@@ -406,6 +406,11 @@ cudaError_t launch_chain(const LaunchArgs& a, int blocks, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+cudaError_t launch_enum(const LaunchArgs& a, int blocks, cudaStream_t s) {
+    oob_enum_kernel<<<blocks, chain::WARPS * 32, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_cert(const LaunchArgs& a, int wide, uint32_t k0, uint32_t k1, int sms, cudaStream_t s) {
     const uint64_t items = (uint64_t)a.n * (k1 - k0);
     const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((items + 127) / 128, (uint64_t)sms * 16));

@@ -157,3 +157,25 @@ def test_chain_search_equals_canonical_on_streams(gpu, cfg):
     assert np.array_equal(a["nodes"][sat], b["nodes"][sat])
     if cfg == "c3":  # the search decided a share of the Sat entries itself
         assert int((sat & (a["passes"] != b["passes"])).sum()) > 100
+
+
+@pytest.mark.parametrize("name", ["random_solver", "random_accept", "crafted", "corpus_m64"])
+def test_fast_enumeration_decides_uncertified_small_boxes(gpu, name):
+    """K3 (chain.cuh oob_enum_kernel): in fast mode an int64-regime entry that
+    no certificate refutes and whose declared box has <= 4096 points is
+    enumerated; a box without a check_model point is the reference's Unsat.
+    Every entry decided without search (nodes 0) is golden Unsat, and on the
+    reference's randomized sets some of them had no certificate (so the
+    enumeration decided them)."""
+    import test_symbolic_host as H
+    H.prover.__wrapped__()  # host build of the certificate checker
+    recs = [r for r in load_golden(name) if r["verdict"] != "timeout" and r["timeout"] >= 1.0]
+    fb = flatten(recs)
+    out = solve_flat(fb, 30.0, flags=FAST)
+    gold = np.array([VCODE[r["verdict"]] for r in recs])
+    assert np.array_equal(out["verdict"], gold)
+    no_search = (out["nodes"] == 0) & (np.array([r["nodes"] for r in recs]) > 0)
+    assert (gold[no_search] == _lib.UNSAT).all()
+    by_enum = no_search & ~H._engine_cert_refutes(fb)
+    if name.startswith("random"):
+        assert int(by_enum.sum()) > 0, "no entry decided by enumeration"
