@@ -140,7 +140,11 @@ enum {
                             Unsat prover (sound: a refuted query has no
                             integer solution in its root box, so the reference
                             can never return Sat on it); what it does not
-                            refute is decided by the exact emulation.  Verdicts
+                            refute is decided by the exact emulation (an
+                            int64-regime query with a declared box of at most
+                            SCUBA_OOB_ENUM_MAX = 4096 points is first
+                            enumerated exhaustively: no check_model point =
+                            Unsat).  Verdicts
                             and Sat models are the reference's; nodes/passes
                             of refuted queries are 0 (not the reference's
                             counters).  DESIGN.md section 4.9. */

@@ -274,7 +274,10 @@ struct Ctx {
             for (uint32_t j = root + 1 - q.size_of(root); j <= root; ++j) {
                 const uint32_t ww = __ldg(q.code + j);
                 const uint32_t op = op_of(ww);
-                if (op < NODE_ADD && sp == VST) return false;  // (never admitted: eval bailed first)
+                if (op < NODE_ADD && sp == VST) {  // unreachable (host: depth <= 30); callers treat as unknown
+                    ov.full = true;
+                    return false;
+                }
                 if (op == NODE_LIT) {
                     st[sp++] = q.lit[arg_of(ww)];
                 } else if (op == NODE_VAR) {
@@ -448,7 +451,9 @@ __global__ void __launch_bounds__(chain::WARPS * 32) oob_chain_kernel(LaunchArgs
                     ov.n = 0;
                     Ctx c{q, cur_lo, cur_hi, ov};
                     bool ok = true;
+                    ov.full = false;
                     for (uint32_t k = lane; k < q.ncon && ok; k += 32) ok = c.exact(k);
+                    if (__any_sync(0xFFFFFFFFu, ov.full)) break;  // (unreachable) exact path
                     if (__all_sync(0xFFFFFFFFu, ok)) {
                         outcome = 1;
                         break;
@@ -618,6 +623,7 @@ __global__ void __launch_bounds__(chain::WARPS * 32) oob_enum_kernel(LaunchArgs 
                     }
                     ok = true;
                     for (uint32_t k = 0; k < q.ncon && ok; ++k) ok = c.exact(k);
+                    ok = ok || ov.full;  // (unreachable) an unevaluated point counts as found
                 }
                 found = __any_sync(0xFFFFFFFFu, ok);
             }
