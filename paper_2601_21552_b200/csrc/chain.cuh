@@ -1,5 +1,11 @@
-// chain.cuh -- fast mode (OOB_F_FAST): warp-per-query search of the int64
-// job's open entries with warp-parallel propagation.
+// chain.cuh -- fast mode (OOB_F_FAST), warp-per-query kernels of the int64
+// job's open own entries (after the certificate kernels, before the root
+// kernel):
+//   oob_enum_kernel   K3, on by default: exhaustive enumeration of declared
+//                     boxes of at most SCUBA_OOB_ENUM_MAX points (bottom of
+//                     this file);
+//   oob_chain_kernel  opt-in (OOB_F_CHAIN): the reference's DFS with
+//                     warp-parallel propagation, below.
 //
 // The exact emulation (engine.cuh) runs a query's propagation passes in ONE
 // lane: a pass visits the constraints in order (solver.py:271-277), so a Sat
