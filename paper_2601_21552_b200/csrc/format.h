@@ -196,6 +196,9 @@ struct LaunchArgs {
     // declared box holds at most enum_max points are enumerated
     uint32_t enum_n;
     uint32_t enum_max;
+    // frontier: speculative lanes stop after fr_abort x the leftmost lane's
+    // passes (+16) once it has finished (frontier.cuh); 0 = never
+    uint32_t fr_abort;
 };
 
 enum { MODE_SOLVE = 0, MODE_PROPAGATE = 1, MODE_CHECK = 2 };

@@ -110,10 +110,10 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
         }
         const bool has = lane < k;
         uint64_t p0 = 0, p1 = 0;
-        uint32_t depth = 0, freed = 0xFFFFFFFFu;
+        uint32_t depth = 0, freed = 0xFFFFFFFFu, u = 0;
         bool resumed_root = false;
         if (has) {
-            uint32_t u = R.units[nunits - 1 - lane];
+            u = R.units[nunits - 1 - lane];
             L.depth = 0;  // no trail: every lane owns its node's domains
             L.clean0 = L.clean1 = 0;
             L.err = ERR_NONE;
@@ -142,12 +142,6 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
         }
         __syncwarp();
         nunits -= k;
-        // free the entries whose right unit was consumed
-        {
-            unsigned fm = __ballot_sync(FULL, freed != 0xFFFFFFFFu);
-            if (freed != 0xFFFFFFFFu) R.freel[nfree + __popc(fm & ((1u << lane) - 1u))] = freed;
-            nfree += __popc(fm);
-        }
         // ---- expand: node start + pass-synchronous propagate() ----
         int outcome = FN_NONE;
         int64_t my_passes = resumed_root ? (int64_t)(rs & RES_PASSES) : 0;
@@ -158,7 +152,22 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
             break;
         }
         bool dead = false;
+        // speculative lanes (right of the leftmost) stop once the leftmost
+        // lane has finished and the round has run fr_abort times its passes
+        // (+16): their units go back on the stack unexpanded, so a creeping
+        // right sibling no longer holds up the leftmost path (a.fr_abort 0:
+        // every lane runs to its fixpoint)
+        bool aborted = false;
+        int l0_end = -1;
         for (int pin = 0; __any_sync(FULL, prop); ++pin) {
+            if (a.fr_abort) {
+                if (l0_end < 0 && !__shfl_sync(FULL, prop ? 1 : 0, 0)) l0_end = pin;
+                if (l0_end >= 0 && pin >= (int)a.fr_abort * l0_end + 16 && prop) {
+                    aborted = true;
+                    prop = false;
+                }
+                if (!__any_sync(FULL, prop)) break;
+            }
             if (prop) {
                 if (pin + pin0 >= PASS_CAP) {
                     prop = false;
@@ -176,8 +185,21 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
             }
         }
         if (status == VERDICT_TIMEOUT) break;
+        // lanes from the first aborted one on are re-pushed unexpanded (a Sat
+        // leaf right of an unexpanded unit need not be the leftmost one)
+        const unsigned abm = __ballot_sync(FULL, aborted);
+        const uint32_t cut = abm ? (uint32_t)(__ffs(abm) - 1) : 32u;
+        const bool live = has && lane < cut;
+        const bool repush = has && lane >= cut;
+        // free the entries whose right unit was consumed
+        {
+            const bool fr = live && freed != 0xFFFFFFFFu;
+            unsigned fm = __ballot_sync(FULL, fr);
+            if (fr) R.freel[nfree + __popc(fm & ((1u << lane) - 1u))] = freed;
+            nfree += __popc(fm);
+        }
         uint32_t pick = 0;
-        if (has) {
+        if (live) {
             if (L.err) {
                 outcome = FN_DEAD;
                 err = L.err;
@@ -193,7 +215,7 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
                 }
             }
         }
-        if (__any_sync(FULL, has && L.err != ERR_NONE)) {
+        if (__any_sync(FULL, live && L.err != ERR_NONE)) {
             status = VERDICT_ERROR;
             err = ERR_STACK;
             break;
@@ -202,23 +224,23 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
         // paths hold 128 levels and the log `logcap` nodes: beyond that the
         // query ends with ERR_DEPTH and the host decides it again on the
         // sequential path with more scratch (counters stay exact)
-        if (__any_sync(FULL, has && depth >= 128) || nlog + k > logcap) {
+        if (__any_sync(FULL, live && depth >= 128) || nlog + k > logcap) {
             status = VERDICT_ERROR;
             err = ERR_DEPTH;
             break;
         }
         {
-            unsigned hm = __ballot_sync(FULL, has);
-            if (has) {
+            unsigned hm = __ballot_sync(FULL, live);  // a prefix of the lanes
+            if (live) {
                 uint32_t at = nlog + lane;
                 R.log_path[2 * at] = p0;
                 R.log_path[2 * at + 1] = p1;
                 R.log_meta[2 * at] = depth;
                 R.log_meta[2 * at + 1] = (uint32_t)my_passes;
             }
-            nlog += k;
+            nlog += __popc(hm);
             tot_nodes += __popc(hm);
-            tot_passes += __reduce_add_sync(FULL, (unsigned)my_passes);
+            tot_passes += __reduce_add_sync(FULL, live ? (unsigned)my_passes : 0u);
         }
         // ---- Sat: the leftmost candidate wins; everything right of it goes ----
         unsigned sm = __ballot_sync(FULL, outcome == FN_SAT);
@@ -240,10 +262,13 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
         __syncwarp();  // freed entries written above are read below by other lanes
         const bool splits = outcome == FN_SPLIT && lane < limit;
         unsigned spm = __ballot_sync(FULL, splits);
+        const unsigned rpm = sm ? 0u : __ballot_sync(FULL, repush);  // (a Sat cut drops them)
         uint32_t s = __popc(spm);
+        const unsigned right = ~((2u << lane) - 1u);
+        if (repush && !sm) R.units[nunits + 2 * __popc(spm & right) + __popc(rpm & right)] = u;
         if (splits) {
             uint32_t r = __popc(spm & ((1u << lane) - 1u));        // rank from the left
-            uint32_t h = __popc(spm & ~((2u << lane) - 1u));       // splitters to my right
+            uint32_t h = 2 * __popc(spm & right) + __popc(rpm & right);  // stack slots to my right
             uint32_t e = r < nfree ? R.freel[nfree - 1 - r] : ebump + (r - nfree);
             T* env = R.e_env + (size_t)e * 2 * nv;
             L.store_env(env);
@@ -259,13 +284,13 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
             c[1] = (uint32_t)(L.clean0 >> 32);
             c[2] = (uint32_t)L.clean1;
             c[3] = (uint32_t)(L.clean1 >> 32);
-            R.units[nunits + 2 * h] = (e << 1) | 1u;      // upper half, below
-            R.units[nunits + 2 * h + 1] = (e << 1);       // lower half, on top
+            R.units[nunits + h] = (e << 1) | 1u;          // upper half, below
+            R.units[nunits + h + 1] = (e << 1);           // lower half, on top
         }
         uint32_t from_free = min(s, nfree);
         nfree -= from_free;
         ebump += s - from_free;
-        nunits += 2 * s;
+        nunits += 2 * s + __popc(rpm);
         __syncwarp();
     }
     // ---- result ----

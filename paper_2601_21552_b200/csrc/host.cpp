@@ -2014,6 +2014,16 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
     // (default 4096, 0 = off)
     a.enum_n = 0;
     a.enum_max = 0;
+    {
+        // frontier speculative-lane abort (frontier.cuh): on in fast mode (B200
+        // A/B: C4 13.4 -> 11.4 ms, C3 and C5s within noise; canonical C4 +4%,
+        // so off there); SCUBA_OOB_FRONTIER_ABORT=<factor> overrides both
+        static const int fa = [] {
+            const char* e = std::getenv("SCUBA_OOB_FRONTIER_ABORT");
+            return (e && *e) ? std::max(0, std::atoi(e)) : -1;
+        }();
+        a.fr_abort = fa >= 0 ? (uint32_t)fa : (fast ? 2u : 0u);
+    }
     if (fast && rc.mode == MODE_SOLVE && j.wide == 0 && enum_max_points() > 0) {
         uint32_t own = 0;
         while (own < n && !j.is_shadow[own]) ++own;
