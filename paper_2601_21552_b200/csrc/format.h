@@ -199,6 +199,7 @@ struct LaunchArgs {
     // frontier: speculative lanes stop after fr_abort x the leftmost lane's
     // passes (+16) once it has finished (frontier.cuh); 0 = never
     uint32_t fr_abort;
+    uint32_t fr_abort_min;
 };
 
 enum { MODE_SOLVE = 0, MODE_PROPAGATE = 1, MODE_CHECK = 2 };

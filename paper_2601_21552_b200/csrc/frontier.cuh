@@ -154,7 +154,7 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
         bool dead = false;
         // speculative lanes (right of the leftmost) stop once the leftmost
         // lane has finished and the round has run fr_abort times its passes
-        // (+16): their units go back on the stack unexpanded, so a creeping
+        // (+fr_abort_min): their units go back on the stack unexpanded, so a creeping
         // right sibling no longer holds up the leftmost path (a.fr_abort 0:
         // every lane runs to its fixpoint)
         bool aborted = false;
@@ -162,7 +162,7 @@ __device__ void frontier_query(LaneT& L, const LaunchArgs& a, FrontierRegion<typ
         for (int pin = 0; __any_sync(FULL, prop); ++pin) {
             if (a.fr_abort) {
                 if (l0_end < 0 && !__shfl_sync(FULL, prop ? 1 : 0, 0)) l0_end = pin;
-                if (l0_end >= 0 && pin >= (int)a.fr_abort * l0_end + 16 && prop) {
+                if (l0_end >= 0 && pin >= (int)a.fr_abort * l0_end + (int)a.fr_abort_min && prop) {
                     aborted = true;
                     prop = false;
                 }

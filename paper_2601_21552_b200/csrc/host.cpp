@@ -2023,6 +2023,11 @@ std::string stage(const RunCtx& rc, DevJob& j, DevicePool* P, uint32_t depth_cap
             return (e && *e) ? std::max(0, std::atoi(e)) : -1;
         }();
         a.fr_abort = fa >= 0 ? (uint32_t)fa : (fast ? 2u : 0u);
+        static const uint32_t fm = [] {
+            const char* e = std::getenv("SCUBA_OOB_FRONTIER_ABORT_MIN");
+            return (uint32_t)((e && *e) ? std::max(0, std::atoi(e)) : 16);
+        }();
+        a.fr_abort_min = fm;
     }
     if (fast && rc.mode == MODE_SOLVE && j.wide == 0 && enum_max_points() > 0) {
         uint32_t own = 0;
