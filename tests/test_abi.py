@@ -76,3 +76,11 @@ def test_side_constraint_count_matches_oracle():
     recs = load_golden("random_solver") + load_golden("crafted")
     fb = flatten(recs)
     assert np.array_equal(_lib.side_counts(fb), oracle.side_counts(fb))
+
+
+def test_option_flags_match_the_header():
+    """The shim's option flags are the header's OOB_F_* values."""
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "scuba_oob.h").read_text(), flags=re.S)
+    hdr = {m[0]: int(m[1]) for m in re.findall(r"\bOOB_F_(\w+)\s*=\s*(\d+)", text)}
+    shim = {k[2:]: v for k, v in vars(_lib).items() if re.fullmatch(r"F_[A-Z0-9_]+", k)}
+    assert hdr and hdr == shim, (hdr, shim)
