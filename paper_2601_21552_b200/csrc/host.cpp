@@ -3833,7 +3833,8 @@ int oob_plan_info(const oob_plan* p, int64_t info[9]) {
             jobs++;
             launches += 1 + (int64_t)j.jit_cls.size() + (j.tail_blocks ? 1 : 0) +
                         ((!j.slot[0].empty() || !j.slot[1].empty() || !j.slot[2].empty()) ? 1 : 0) +
-                        (j.a.certs && j.a.cert_kmax ? (j.a.cert_kmax > 1 ? 2 : 1) : 0);  // fast mode: certificates
+                        (j.a.certs && j.a.cert_kmax ? (j.a.cert_kmax > 1 ? 2 : 1) : 0) +  // fast mode: certificates
+                        (j.a.enum_n ? 1 : 0) + (j.a.chain_n ? 1 : 0);  // fast mode: enumeration, (opt-in) search
         }
     }
     info[0] = nq;
