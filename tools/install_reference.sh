@@ -8,3 +8,6 @@ cd "$(dirname "$0")/.."
 python -m pip install --no-index --no-build-isolation --find-links /opt/wheelhouse --target baseline/_ref /root/reference/pkg
 rm -rf baseline/_ref/corpus
 cp -r /root/reference/pkg/corpus baseline/_ref/corpus
+# its own test suite (run against the GPU engine by tools/ref_suite_gpu.sh on the box)
+rm -rf baseline/_ref/tests
+cp -r /root/reference/pkg/tests baseline/_ref/tests
